@@ -1,0 +1,383 @@
+// TEST INFRASTRUCTURE ONLY (oracle/_ref).  Built from the reference headers
+// where they lie (/root/reference/proj/include, read-only, compiled
+// unchanged) plus the Eigen-free shim in oracle/shim/.  Output goes only to
+// oracle/_ref/.  Three roles:
+//   1. ref_mpm_rollout: the reference's own mpm_step<double> (mpm.hpp:348-367)
+//      on reference descriptors -- pins the restatement's forward.
+//   2. ref_mpm_grad:    the reference's own mpm_step<Value> + Tape::backward
+//      (tape.hpp:124-164) -- pins the restatement's gradient.
+//   3. ref_rollout_grad: the restatement (oracle/mpm.hpp) instantiated on the
+//      reference tape, with recompute-on-backward segments via
+//      Tape::checkpoint (tape.hpp:181-255) as step_checkpointed does
+//      (algo.hpp:79-104) -- the gradient oracle for every BASELINE config,
+//      including the config-gap extensions.
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <span>
+#include <vector>
+
+#include "diffsim/linalg.hpp"
+#include "diffsim/rng.hpp"
+#include "diffsim/mpm.hpp"
+#include "diffsim/tape.hpp"
+
+// tape overload of the restatement's SVD hook (mirrors linalg.hpp:173-194)
+#include "oracle/linalg.hpp"
+namespace oracle {
+inline void svd3(const M3<diffsim::Value>& f, M3<diffsim::Value>& u, V3<diffsim::Value>& s,
+                 M3<diffsim::Value>& vt);
+}
+#include "oracle/driver.hpp"
+
+namespace oracle {
+inline void svd3(const M3<diffsim::Value>& f, M3<diffsim::Value>& u, V3<diffsim::Value>& s,
+                 M3<diffsim::Value>& vt) {
+  using diffsim::Value;
+  diffsim::Tape* tape = nullptr;
+  for (const Value& e : f.m)
+    if (e.tape) {
+      tape = e.tape;
+      break;
+    }
+  Value sv[3];
+  if (!tape) {
+    double fd[9], ud[9], sd[3], vd[9];
+    for (int i = 0; i < 9; ++i) fd[i] = f.m[i].v;
+    svd3x3_values(fd, ud, sd, vd);
+    for (int i = 0; i < 9; ++i) {
+      u.m[i] = Value(ud[i]);
+      vt.m[i] = Value(vd[i]);
+    }
+    s = {Value(sd[0]), Value(sd[1]), Value(sd[2])};
+    return;
+  }
+  tape->svd3x3(f.m.data(), u.m.data(), sv, vt.m.data());
+  s = {sv[0], sv[1], sv[2]};
+}
+}  // namespace oracle
+
+using diffsim::Tape;
+using diffsim::Value;
+
+namespace {
+
+void put_err(const char* msg, char* err, int errlen) {
+  if (err && errlen > 0) std::snprintf(err, static_cast<std::size_t>(errlen), "%s", msg);
+}
+
+// ---- reference descriptors (mpm.hpp:23-137) ----
+diffsim::mpm::MpmMaterial ref_material(const OrMat& m) {
+  diffsim::mpm::MpmMaterial o;
+  o.density = m.density;
+  o.youngs = m.youngs;
+  o.poisson = m.poisson;
+  o.yield_stress = m.yield_stress;
+  o.kind = m.kind == 3 ? diffsim::mpm::MaterialKind::kFluid : diffsim::mpm::MaterialKind::kElastoplastic;
+  o.wide_yield = m.wide_yield != 0;
+  return o;
+}
+
+template <class T>
+diffsim::mpm::SdfCollider<T> ref_collider(const OrCol& c) {
+  diffsim::mpm::SdfCollider<T> o;
+  using K = typename diffsim::mpm::SdfCollider<T>::Kind;
+  o.kind = c.kind == 0 ? K::kPlane : (c.kind == 1 ? K::kSphere : K::kBox);
+  o.center = {T(c.center[0]), T(c.center[1]), T(c.center[2])};
+  o.velocity = {T(c.velocity[0]), T(c.velocity[1]), T(c.velocity[2])};
+  o.normal = {c.normal[0], c.normal[1], c.normal[2]};
+  o.radius = c.radius;
+  o.half = {c.half[0], c.half[1], c.half[2]};
+  return o;
+}
+
+template <class T>
+diffsim::mpm::MpmState<T> ref_state(const OrMat* mats, int n, const double* x, const double* v,
+                                    const double* F, const double* C, const int* material) {
+  diffsim::mpm::MpmState<T> st;
+  for (int p = 0; p < n; ++p) {
+    st.x.push_back({T(x[3 * p]), T(x[3 * p + 1]), T(x[3 * p + 2])});
+    st.v.push_back({T(v[3 * p]), T(v[3 * p + 1]), T(v[3 * p + 2])});
+    diffsim::Mat3<T> f, c;
+    for (int i = 0; i < 9; ++i) {
+      f.m[i] = T(F[9 * p + i]);
+      c.m[i] = T(C[9 * p + i]);
+    }
+    st.F.push_back(f);
+    st.C.push_back(c);
+    const OrMat& m = mats[material[p]];
+    st.mass.push_back(m.density * m.volume);
+    st.volume0.push_back(m.volume);
+    st.material_id.push_back(material[p]);
+  }
+  return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+// (1) reference forward: n_sub substeps of mpm_step<double>, colliders fixed.
+int ref_mpm_rollout(const OrSim* sim, const OrMat* mats, int nmat, const OrCol* cols, int ncol, int n,
+                    double* x, double* v, double* F, double* C, const int* material, int n_sub,
+                    double* seconds, char* err, int errlen) {
+  try {
+    std::vector<diffsim::mpm::MpmMaterial> mt;
+    for (int i = 0; i < nmat; ++i) mt.push_back(ref_material(mats[i]));
+    std::vector<diffsim::mpm::SdfCollider<double>> cl;
+    for (int c = 0; c < ncol; ++c) cl.push_back(ref_collider<double>(cols[c]));
+    auto st = ref_state<double>(mats, n, x, v, F, C, material);
+    diffsim::mpm::MpmGrid<double> grid;
+    grid.dims = {sim->dims[0], sim->dims[1], sim->dims[2]};
+    grid.dx = sim->dx;
+    grid.clear();
+    diffsim::mpm::CouplingParams cp;
+    cp.alpha_c = sim->alpha_c;
+    cp.mu_b = sim->mu_b;
+    const auto t0 = std::chrono::steady_clock::now();
+    diffsim::mpm::mpm_step(st, grid, mt, cl, cp, {sim->gravity[0], sim->gravity[1], sim->gravity[2]},
+                           sim->dt, n_sub);
+    const auto t1 = std::chrono::steady_clock::now();
+    if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+    for (int p = 0; p < n; ++p) {
+      for (int a = 0; a < 3; ++a) {
+        x[3 * p + a] = st.x[p][a];
+        v[3 * p + a] = st.v[p][a];
+      }
+      for (int i = 0; i < 9; ++i) {
+        F[9 * p + i] = st.F[p].m[i];
+        C[9 * p + i] = st.C[p].m[i];
+      }
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(e.what(), err, errlen);
+    return 1;
+  }
+}
+
+// (2) reference gradient of L = |com(x_final) - target|^2 w.r.t. the initial
+// state, through mpm_step<Value>.  seg = 0: one tape; seg = k > 0: every k
+// substeps run inside a Tape::checkpoint segment (restated step_checkpointed).
+int ref_mpm_grad(const OrSim* sim, const OrMat* mats, int nmat, const OrCol* cols, int ncol, int n,
+                 const double* x, const double* v, const double* F, const double* C, const int* material,
+                 int n_sub, int seg, const double* target, double* loss_out, double* gx, double* gv,
+                 double* gF, double* gC, double* seconds, char* err, int errlen) {
+  try {
+    std::vector<diffsim::mpm::MpmMaterial> mt;
+    for (int i = 0; i < nmat; ++i) mt.push_back(ref_material(mats[i]));
+    std::vector<diffsim::mpm::SdfCollider<Value>> cl;
+    for (int c = 0; c < ncol; ++c) cl.push_back(ref_collider<Value>(cols[c]));
+    diffsim::mpm::CouplingParams cp;
+    cp.alpha_c = sim->alpha_c;
+    cp.mu_b = sim->mu_b;
+    const diffsim::Vec3<double> grav{sim->gravity[0], sim->gravity[1], sim->gravity[2]};
+    const auto t0 = std::chrono::steady_clock::now();
+    Tape tape;
+    auto st = ref_state<Value>(mats, n, x, v, F, C, material);
+    std::vector<Value> leaves;
+    auto visit = [&](auto&& fn) {
+      for (auto& p : st.x) { fn(p.x); fn(p.y); fn(p.z); }
+      for (auto& p : st.v) { fn(p.x); fn(p.y); fn(p.z); }
+      for (auto& m : st.F) for (int i = 0; i < 9; ++i) fn(m.m[i]);
+      for (auto& m : st.C) for (int i = 0; i < 9; ++i) fn(m.m[i]);
+    };
+    visit([&](Value& val) { val = tape.var(val.v); leaves.push_back(val); });
+    const auto shape = st;
+    auto run = [&](diffsim::mpm::MpmState<Value>& s, int k) {
+      diffsim::mpm::MpmGrid<Value> grid;
+      grid.dims = {sim->dims[0], sim->dims[1], sim->dims[2]};
+      grid.dx = sim->dx;
+      grid.clear();
+      diffsim::mpm::mpm_step(s, grid, mt, cl, cp, grav, sim->dt, k);
+    };
+    int done = 0;
+    while (done < n_sub) {
+      const int k = seg > 0 ? std::min(seg, n_sub - done) : n_sub - done;
+      if (seg > 0) {
+        std::vector<Value> in;
+        visit([&](Value& val) { in.push_back(val); });
+        auto outs = tape.checkpoint(
+            [&, k](Tape&, std::span<const Value> vin) {
+              auto s = shape;
+              std::size_t i = 0;
+              for (auto& p : s.x) { p.x = vin[i++]; p.y = vin[i++]; p.z = vin[i++]; }
+              for (auto& p : s.v) { p.x = vin[i++]; p.y = vin[i++]; p.z = vin[i++]; }
+              for (auto& m : s.F) for (int q = 0; q < 9; ++q) m.m[q] = vin[i++];
+              for (auto& m : s.C) for (int q = 0; q < 9; ++q) m.m[q] = vin[i++];
+              run(s, k);
+              std::vector<Value> out;
+              for (auto& p : s.x) { out.push_back(p.x); out.push_back(p.y); out.push_back(p.z); }
+              for (auto& p : s.v) { out.push_back(p.x); out.push_back(p.y); out.push_back(p.z); }
+              for (auto& m : s.F) for (int q = 0; q < 9; ++q) out.push_back(m.m[q]);
+              for (auto& m : s.C) for (int q = 0; q < 9; ++q) out.push_back(m.m[q]);
+              return out;
+            },
+            in);
+        std::size_t i = 0;
+        visit([&](Value& val) { val = outs[i++]; });
+      } else {
+        run(st, k);
+      }
+      done += k;
+    }
+    Value loss(0.0);
+    for (int a = 0; a < 3; ++a) {
+      Value com(0.0);
+      for (const auto& p : st.x) com += p[a] * Value(1.0 / n);
+      const Value d = com - Value(target[a]);
+      loss += d * d;
+    }
+    tape.backward(loss);
+    const auto t1 = std::chrono::steady_clock::now();
+    if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+    if (loss_out) *loss_out = loss.v;
+    std::size_t i = 0;
+    for (int p = 0; p < n; ++p)
+      for (int a = 0; a < 3; ++a) gx[3 * p + a] = tape.grad(leaves[i++]);
+    for (int p = 0; p < n; ++p)
+      for (int a = 0; a < 3; ++a) gv[3 * p + a] = tape.grad(leaves[i++]);
+    for (int p = 0; p < n; ++p)
+      for (int q = 0; q < 9; ++q) gF[9 * p + q] = tape.grad(leaves[i++]);
+    for (int p = 0; p < n; ++p)
+      for (int q = 0; q < 9; ++q) gC[9 * p + q] = tape.grad(leaves[i++]);
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(e.what(), err, errlen);
+    return 1;
+  }
+}
+
+// (3) restatement on the reference tape: loss + gradients for a rollout of
+// n_ctrl control steps x n_sub substeps.  seg = checkpoint segment length in
+// substeps (0: record everything on one tape).
+int ref_rollout_grad(const OrSim* sim, const OrMat* mats, int nmat, const OrCol* cols, int ncol,
+                     const double* cvo, const double* act, int nact, int n, const double* x,
+                     const double* v, const double* F, const double* C, const int* material,
+                     const int* group, int n_ctrl, int n_sub, const OrLoss* loss, int seg,
+                     double* loss_out, double* obs, double* gx, double* gv, double* gF, double* gC,
+                     double* gcvo, double* gact, double* gE, double* seconds, char* err, int errlen) {
+  using namespace oracle;
+  try {
+    const SimParams sp = sim_from(*sim);
+    const auto t0 = std::chrono::steady_clock::now();
+    Tape tape;
+    std::vector<double> st0;
+    st0.reserve(24 * static_cast<std::size_t>(n));
+    st0.insert(st0.end(), x, x + 3 * n);
+    st0.insert(st0.end(), v, v + 3 * n);
+    st0.insert(st0.end(), F, F + 9 * n);
+    st0.insert(st0.end(), C, C + 9 * n);
+    std::vector<Value> s_leaves, c_leaves, a_leaves, e_leaves;
+    for (double val : st0) s_leaves.push_back(tape.var(val));
+    for (int i = 0; i < n_ctrl * ncol * 9; ++i) c_leaves.push_back(tape.var(cvo[i]));
+    for (int i = 0; i < n_ctrl * nact; ++i) a_leaves.push_back(tape.var(act[i]));
+    for (int i = 0; i < nmat; ++i) e_leaves.push_back(tape.var(mats[i].youngs));
+    const std::vector<int> mat_ids(material, material + n);
+    std::vector<int> grp(n, 0);
+    if (group) grp.assign(group, group + n);
+
+    // substeps k from flattened (state, colliders, act, E) -> flattened state
+    auto body = [&, n](std::span<const Value> in, int k) {
+      const Value* s = in.data();
+      State<Value> stt = state_from<Value>(n, s, s + 3 * n, s + 6 * n, s + 15 * n, mat_ids.data(), grp.data());
+      const Value* cp = s + 24 * n;
+      std::vector<Collider<Value>> cl;
+      for (int c = 0; c < ncol; ++c) cl.push_back(collider_from<Value>(cols[c], cp + 9 * c));
+      const Value* ap = cp + 9 * ncol;
+      std::vector<Value> a(ap, ap + nact);
+      const Value* ep = ap + nact;
+      std::vector<Material<Value>> mt;
+      for (int i = 0; i < nmat; ++i) mt.push_back(material_from<Value>(mats[i], ep[i]));
+      Grid<Value> g;
+      for (int q = 0; q < k; ++q) substep(sp, stt, g, mt, cl, a);
+      std::vector<Value> out(24 * static_cast<std::size_t>(n));
+      for (int p = 0; p < n; ++p) {
+        for (int d = 0; d < 3; ++d) {
+          out[3 * p + d] = stt.x[p][d];
+          out[3 * n + 3 * p + d] = stt.v[p][d];
+        }
+        for (int q = 0; q < 9; ++q) {
+          out[6 * n + 9 * p + q] = stt.F[p].m[q];
+          out[15 * n + 9 * p + q] = stt.C[p].m[q];
+        }
+      }
+      return out;
+    };
+
+    std::vector<Value> cur = s_leaves;
+    Value total(0.0);
+    for (int t = 0; t < n_ctrl; ++t) {
+      std::vector<Value> extra;
+      for (int i = 0; i < ncol * 9; ++i) extra.push_back(c_leaves[t * ncol * 9 + i]);
+      for (int i = 0; i < nact; ++i) extra.push_back(a_leaves[t * nact + i]);
+      for (int i = 0; i < nmat; ++i) extra.push_back(e_leaves[i]);
+      int done = 0;
+      while (done < n_sub) {
+        const int k = seg > 0 ? std::min(seg, n_sub - done) : n_sub - done;
+        std::vector<Value> in = cur;
+        in.insert(in.end(), extra.begin(), extra.end());
+        if (seg > 0) {
+          auto outs = tape.checkpoint([&, k](Tape&, std::span<const Value> vin) { return body(vin, k); }, in);
+          cur = outs;
+        } else {
+          cur = body(std::span<const Value>(in), k);
+        }
+        done += k;
+      }
+      // observables on the main tape
+      State<Value> stt = state_from<Value>(n, cur.data(), cur.data() + 3 * n, cur.data() + 6 * n,
+                                           cur.data() + 15 * n, mat_ids.data(), grp.data());
+      Value o[kObsDim];
+      if (ncol > 0) {
+        const Collider<Value> c0 = collider_from<Value>(cols[0], &c_leaves[t * ncol * 9]);
+        observe(stt, &c0, *loss, o);
+      } else {
+        observe<Value>(stt, nullptr, *loss, o);
+      }
+      if (obs)
+        for (int i = 0; i < kObsDim; ++i) obs[t * kObsDim + i] = o[i].v;
+      total = total + step_loss(*loss, o, t == n_ctrl - 1);
+    }
+    if (total.is_const()) throw std::runtime_error("ref_rollout_grad: loss does not depend on inputs");
+    tape.backward(total);
+    const auto t1 = std::chrono::steady_clock::now();
+    if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+    if (loss_out) *loss_out = total.v;
+    for (int i = 0; i < 3 * n; ++i) {
+      gx[i] = tape.grad(s_leaves[i]);
+      gv[i] = tape.grad(s_leaves[3 * n + i]);
+    }
+    for (int i = 0; i < 9 * n; ++i) {
+      gF[i] = tape.grad(s_leaves[6 * n + i]);
+      gC[i] = tape.grad(s_leaves[15 * n + i]);
+    }
+    if (gcvo)
+      for (int i = 0; i < n_ctrl * ncol * 9; ++i) gcvo[i] = tape.grad(c_leaves[i]);
+    if (gact)
+      for (int i = 0; i < n_ctrl * nact; ++i) gact[i] = tape.grad(a_leaves[i]);
+    if (gE)
+      for (int i = 0; i < nmat; ++i) gE[i] = tape.grad(e_leaves[i]);
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(e.what(), err, errlen);
+    return 1;
+  }
+}
+
+// reference RngStream draws (rng.hpp:11-55): kind 0 u64, 1 double, 2 normal
+void ref_rng_draws(unsigned long long seed, unsigned long long stream, int n, int kind, double* out,
+                   unsigned long long* out_u64) {
+  diffsim::RngStream r(seed, stream);
+  for (int i = 0; i < n; ++i) {
+    if (kind == 0)
+      out_u64[i] = r.next_u64();
+    else if (kind == 1)
+      out[i] = r.next_double();
+    else
+      out[i] = r.normal();
+  }
+}
+
+}  // extern "C"
