@@ -1,0 +1,253 @@
+// Per-particle MLS-MPM transfers (quadratic B-spline APIC) and their adjoints.
+// Restates p2g (mpm.hpp:219-254) and g2p (mpm.hpp:307-346); node access goes
+// through a functor so the same code serves the shared-memory tile kernels
+// and the host fp64 adjoint check.
+#pragma once
+
+#include "dm_physics.cuh"
+
+namespace dm {
+
+// fp32 products/differences that must not be contracted into FMAs, so the
+// stencil base (and therefore the bin key) is bit-reproducible on host and
+// device (SURVEY.md 8(d) "Binning").
+DM_HD float mul_rn(float a, float b) {
+#ifdef __CUDA_ARCH__
+  return __fmul_rn(a, b);
+#else
+  volatile float r = a * b;
+  return r;
+#endif
+}
+DM_HD float sub_rn(float a, float b) {
+#ifdef __CUDA_ARCH__
+  return __fsub_rn(a, b);
+#else
+  volatile float r = a - b;
+  return r;
+#endif
+}
+
+template <class R>
+struct Stencil {
+  int base[3];
+  R fx[3];
+  R w[3][3];   // w[axis][offset]
+  R dw[3][3];  // d w / d fx
+};
+
+// Base cell + fractional offset.  fp32: gx = fl(x * inv_dx),
+// base = floor(fl(gx - 0.5)), fx = fl(gx - base).  fp64 (host check): the
+// reference's double division for base (mpm.hpp:153-154) and multiplication
+// for fx (mpm.hpp:159).  Returns the first failing axis or -1.
+DM_HD int stencil_base(const float x[3], float inv_dx, double dx, const int dims[3], int base[3], float fx[3]) {
+  int bad = -1;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float gx = mul_rn(x[a], inv_dx);
+    const float b = floorf(sub_rn(gx, 0.5f));
+    base[a] = static_cast<int>(b);
+    fx[a] = sub_rn(gx, b);
+    if ((base[a] < 1 || base[a] + 2 > dims[a] - 2) && bad < 0) bad = a;
+  }
+  return bad;
+}
+DM_HD int stencil_base(const double x[3], double inv_dx, double dx, const int dims[3], int base[3], double fx[3]) {
+  int bad = -1;
+  for (int a = 0; a < 3; ++a) {
+    base[a] = static_cast<int>(floor(x[a] / dx - 0.5));
+    fx[a] = x[a] * inv_dx - static_cast<double>(base[a]);
+    if ((base[a] < 1 || base[a] + 2 > dims[a] - 2) && bad < 0) bad = a;
+  }
+  return bad;
+}
+
+template <class R>
+DM_HD int make_stencil(const R x[3], R inv_dx, double dx, const int dims[3], Stencil<R>& s) {
+  const int bad = stencil_base(x, inv_dx, dx, dims, s.base, s.fx);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    bspline(s.fx[a], s.w[a]);
+    bspline_d(s.fx[a], s.dw[a]);
+  }
+  return bad;
+}
+
+template <class R>
+struct TransferCtx {
+  int dims[3];
+  R dx, inv_dx, dt;
+  double dx64;
+};
+
+// ---------------- P2G ----------------
+// Affine momentum matrix A = -dt V0 4/dx^2 (P F^T + J eta (C + C^T)) + m C
+// (mpm.hpp:236-239 + viscosity extension).  The node at offset o receives
+//   mass: w_o m,   momentum: w_o (m v + A dpos_o),  dpos_o = (o - fx) dx
+// written as w_o (q + Ad o) with q = m v - A fx dx and Ad = A dx.
+template <class R>
+DM_HD m3<R> p2g_affine(const Law<R>& L, const TransferCtx<R>& t, const m3<R>& F, const m3<R>& C, R act, bool* bad) {
+  const m3<R> P = law_stress(L, F, act, bad);
+  m3<R> tau = mul_bt(P, F);
+  if (L.kind == kFluid && L.visc != R(0)) {
+    const R jv = det(F) * L.visc;
+    tau += (C + transpose(C)) * jv;
+  }
+  const R kA = -t.dt * L.vol * R(4) * t.inv_dx * t.inv_dx;
+  return tau * kA + C * L.mass;
+}
+
+template <class R>
+DM_HD void p2g_payload(const m3<R>& A, R mass, v3<R> v, const Stencil<R>& s, R dx, v3<R>& q, m3<R>& Ad) {
+  const v3<R> f = mk3(s.fx[0] * dx, s.fx[1] * dx, s.fx[2] * dx);
+  q = v * mass - A * f;
+  Ad = A * dx;
+}
+
+// ---------------- G2P ----------------
+template <class R, class GetV>
+DM_HD void g2p_gather(const Stencil<R>& s, R dx, GetV getv, v3<R>& vnew, m3<R>& B) {
+  vnew = zero3<R>();
+  B = mzero<R>();
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const R w = s.w[0][i] * s.w[1][j] * s.w[2][k];
+        const v3<R> vw = getv(i, j, k) * w;
+        const v3<R> dpos = mk3((R(i) - s.fx[0]) * dx, (R(j) - s.fx[1]) * dx, (R(k) - s.fx[2]) * dx);
+        vnew += vw;
+        B += outer(vw, dpos);
+      }
+}
+
+// Forward G2P for one particle: returns new (x, v, C, F); *bad_adv when the
+// advected particle leaves [1.5, dims-2.5] cells (mpm.hpp:335-340).
+template <class R, class GetV>
+DM_HD void g2p_particle(const Law<R>& L, const TransferCtx<R>& t, const Stencil<R>& s, GetV getv, v3<R>& x, v3<R>& v,
+                        m3<R>& C, m3<R>& F, bool* bad_adv, bool* bad_det) {
+  m3<R> B;
+  g2p_gather(s, t.dx, getv, v, B);
+  C = B * (R(4) * t.inv_dx * t.inv_dx);
+  x.x += t.dt * v.x;
+  x.y += t.dt * v.y;
+  x.z += t.dt * v.z;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const R gx = x[a] / t.dx;
+    if (gx < R(1.5) || gx > R(t.dims[a]) - R(2.5)) *bad_adv = true;
+  }
+  const m3<R> Fnew = (meye<R>() + C * t.dt) * F;
+  F = law_project(L, Fnew, bad_det);
+}
+
+// Adjoint of g2p_particle.  Inputs: start-of-substep x (via stencil s), F;
+// output cotangents xb', vb', Cb', Fb'.  Produces the particle-side partial
+// cotangents (xb_part, Fb_part) and the node-scatter payload:
+//   vbar_node(o) += w_o (gq + Bd o)   with gq = gbar - Bbar fx dx, Bd = Bbar dx.
+template <class R, class GetV>
+DM_HD void g2p_vjp(const Law<R>& L, const TransferCtx<R>& t, const Stencil<R>& s, GetV getv, const m3<R>& F,
+                   v3<R> xb_o, v3<R> vb_o, const m3<R>& Cb_o, const m3<R>& Fb_o, v3<R>& xb_part, m3<R>& Fb_part,
+                   v3<R>& gq, m3<R>& Bd, R& mubar) {
+  // recompute forward
+  v3<R> vnew;
+  m3<R> B;
+  g2p_gather(s, t.dx, getv, vnew, B);
+  const R c4 = R(4) * t.inv_dx * t.inv_dx;
+  const m3<R> Cn = B * c4;
+  const m3<R> Ad = meye<R>() + Cn * t.dt;
+  const m3<R> Fnew = Ad * F;
+  const m3<R> Fnb = law_project_vjp(L, Fnew, Fb_o, mubar);
+  // Fnew = (I + dt C) F
+  const m3<R> Cb = Cb_o + mul_bt(Fnb, F) * t.dt;
+  Fb_part = mul_at(Ad, Fnb);
+  // x' = x + dt v' ;  C = c4 B
+  const v3<R> gb = vb_o + xb_o * t.dt;
+  const m3<R> Bb = Cb * c4;
+  // per node: u = gb + Bb dpos; vbar_n += w u; wbar = v_n . u; dposbar = w Bb^T v_n
+  R fxb[3] = {R(0), R(0), R(0)};
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const R w = s.w[0][i] * s.w[1][j] * s.w[2][k];
+        const v3<R> vn = getv(i, j, k);
+        const v3<R> dpos = mk3((R(i) - s.fx[0]) * t.dx, (R(j) - s.fx[1]) * t.dx, (R(k) - s.fx[2]) * t.dx);
+        const v3<R> u = gb + Bb * dpos;
+        const R wb = dot(vn, u);
+        fxb[0] += wb * s.dw[0][i] * s.w[1][j] * s.w[2][k];
+        fxb[1] += wb * s.w[0][i] * s.dw[1][j] * s.w[2][k];
+        fxb[2] += wb * s.w[0][i] * s.w[1][j] * s.dw[2][k];
+        const v3<R> dpb = tmul(Bb, vn) * w;
+        fxb[0] -= t.dx * dpb.x;
+        fxb[1] -= t.dx * dpb.y;
+        fxb[2] -= t.dx * dpb.z;
+      }
+  xb_part = mk3(xb_o.x + fxb[0] * t.inv_dx, xb_o.y + fxb[1] * t.inv_dx, xb_o.z + fxb[2] * t.inv_dx);
+  const v3<R> f = mk3(s.fx[0] * t.dx, s.fx[1] * t.dx, s.fx[2] * t.dx);
+  gq = gb - Bb * f;
+  Bd = Bb * t.dx;
+}
+
+// Adjoint of the P2G for one particle, given node cotangents (mass_bar,
+// mom_bar) through getmb(i,j,k, mb, pb).  Adds into xb, vb, Fb, Cb, and the
+// material / actuation cotangents.
+template <class R, class GetMB>
+DM_HD void p2g_vjp(const Law<R>& L, const TransferCtx<R>& t, const Stencil<R>& s, GetMB getmb, v3<R> v, const m3<R>& F,
+                   const m3<R>& C, R act, v3<R>& xb, v3<R>& vb, m3<R>& Fb, m3<R>& Cb, R& mubar, R& lambar, R& actbar) {
+  bool bad = false;
+  const m3<R> P = law_stress(L, F, act, &bad);
+  m3<R> tau = mul_bt(P, F);
+  const bool visc = L.kind == kFluid && L.visc != R(0);
+  const m3<R> Cs = C + transpose(C);
+  const R J = det(F);
+  if (visc) tau += Cs * (J * L.visc);
+  const R kA = -t.dt * L.vol * R(4) * t.inv_dx * t.inv_dx;
+  const m3<R> A = tau * kA + C * L.mass;
+  const v3<R> mv = v * L.mass;
+  R fxb[3] = {R(0), R(0), R(0)};
+  v3<R> S = zero3<R>();
+  m3<R> Ab = mzero<R>();
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const R w = s.w[0][i] * s.w[1][j] * s.w[2][k];
+        R mb;
+        v3<R> pb;
+        getmb(i, j, k, mb, pb);
+        const v3<R> dpos = mk3((R(i) - s.fx[0]) * t.dx, (R(j) - s.fx[1]) * t.dx, (R(k) - s.fx[2]) * t.dx);
+        const v3<R> u = mv + A * dpos;
+        const R wb = mb * L.mass + dot(pb, u);
+        fxb[0] += wb * s.dw[0][i] * s.w[1][j] * s.w[2][k];
+        fxb[1] += wb * s.w[0][i] * s.dw[1][j] * s.w[2][k];
+        fxb[2] += wb * s.w[0][i] * s.w[1][j] * s.dw[2][k];
+        const v3<R> ub = pb * w;
+        S += ub;
+        Ab += outer(ub, dpos);
+        const v3<R> dpb = tmul(A, ub);
+        fxb[0] -= t.dx * dpb.x;
+        fxb[1] -= t.dx * dpb.y;
+        fxb[2] -= t.dx * dpb.z;
+      }
+  xb += mk3(fxb[0] * t.inv_dx, fxb[1] * t.inv_dx, fxb[2] * t.inv_dx);
+  vb += S * L.mass;
+  Cb += Ab * L.mass;
+  const m3<R> taub = Ab * kA;
+  if (visc) {
+    Cb += (taub + transpose(taub)) * (J * L.visc);
+    Fb += cofactor(F) * (L.visc * ddot(Cs, taub));
+  }
+  // tau = P F^T
+  const m3<R> Pb = taub * F;
+  Fb += mul_at(taub, P);
+  law_stress_vjp(L, F, act, Pb, Fb, mubar, lambar, actbar);
+}
+
+}  // namespace dm
