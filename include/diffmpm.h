@@ -1,0 +1,139 @@
+/* diffmpm: B200-native batched differentiable MLS-MPM (C ABI).
+ *
+ * Drop-in boundary for the reference's simulator path
+ * (/root/reference/proj/include/diffsim).  The reference surface is C++
+ * templates with no FFI; every entry point below names the reference symbol
+ * it replaces (file:line).  Plain pointers and sizes only.  Host-pointer
+ * entry points copy through pinned staging; *_device variants take device
+ * pointers on the context's stream.
+ *
+ * Threading: one context per GPU, one CUDA stream per context; a context is
+ * not thread-safe; separate contexts may be driven from separate threads or
+ * processes.
+ *
+ * Errors: every call returns DM_OK or a DM_ERR_* code; dm_last_error()
+ * returns the reference's exception text (mpm.hpp:156-158, 203-205, 338-339,
+ * 354; tape.hpp:238-240) so adapters can rethrow it verbatim.
+ */
+#ifndef DIFFMPM_H
+#define DIFFMPM_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DM_OK 0
+#define DM_ERR_ARG 1       /* std::invalid_argument (mpm.hpp:354) */
+#define DM_ERR_RUNTIME 2   /* std::runtime_error (mpm.hpp:156-158, 169, 205, 338-339) */
+#define DM_ERR_CUDA 3
+#define DM_ERR_CAPACITY 4  /* tape capacity (max_steps) exceeded */
+
+#define DM_MAX_COLLIDERS 4
+#define DM_MAX_GROUPS 16
+#define DM_MAX_MATERIALS 4
+#define DM_OBS_DIM 7 /* com(3), var(3), spill(1) */
+
+/* MpmMaterial (mpm.hpp:23-41) extended: kind 0 fixed-corotated,
+ * 1 neo-Hookean (fem.hpp:124-142) + x-axis actuation, 2 elastoplastic
+ * (Hencky / von Mises, mpm.hpp:165-198), 3 fluid (mpm.hpp:200-210) +
+ * viscosity.  Particle mass = density * volume (sample_box, mpm.hpp:382-393). */
+typedef struct {
+  int kind;
+  double youngs, poisson, density, volume, yield_stress;
+  int wide_yield;
+  double viscosity, act_strength, bulk;
+} DmMaterial;
+
+/* SdfCollider geometry (mpm.hpp:76-84) extended: kind 0 plane, 1 sphere,
+ * 2 box, 3 capped cylinder, 4 open-top hollow box.  Center, velocity and
+ * angular velocity are per control step (dm_step's cvo). */
+typedef struct {
+  int kind;
+  double normal[3]; /* plane normal / cylinder axis (unit) */
+  double radius;    /* sphere, cylinder */
+  double half[3];   /* box; hollow-box cavity half extents */
+  double length;    /* cylinder full length */
+  double thickness; /* hollow-box wall thickness */
+} DmColliderShape;
+
+typedef struct {
+  int device;
+  int num_envs;          /* EnvBatch size (env.hpp:55-117) */
+  int particles_per_env;
+  int dims[3];           /* MpmGrid::dims (mpm.hpp:58) */
+  double dx, dt;         /* MpmGrid::dx, mpm_step dt */
+  double gravity[3];
+  int boundary;          /* 0 slip (mpm.hpp:296-302), 1 sticky */
+  double alpha_c, mu_b;  /* CouplingParams (mpm.hpp:134-137) */
+  int num_colliders;     /* per env, <= DM_MAX_COLLIDERS */
+  int num_groups;        /* actuation groups, <= DM_MAX_GROUPS */
+  int substeps;          /* mpm_step substeps per control step (mpm.hpp:349-353) */
+  int max_steps;         /* tape capacity in control steps */
+  int checkpoint_every;  /* substeps per recompute segment; 0 = one per control step (algo.hpp:79-104) */
+  double spill_half, spill_temp; /* spill observable footprint (tasks.hpp:606-614) */
+} DmConfig;
+
+typedef struct DmContext DmContext;
+
+/* Context owning every device buffer (SURVEY.md 8(b) "create/destroy"). */
+DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materials,
+                     const DmColliderShape* shapes);
+void dm_destroy(DmContext* ctx);
+int dm_last_error(const DmContext* ctx, char* buf, int len);
+/* cudaStream_t of the context, as void*. */
+void* dm_stream(DmContext* ctx);
+/* Bytes of device memory held by the context. */
+unsigned long long dm_device_bytes(const DmContext* ctx);
+
+/* Upload the state (lift_state/convert_state, env.hpp:41-47, mpm.hpp:425-444)
+ * and reset the tape to step 0.  Host layout per env in the reference visit
+ * order (tasks.hpp:203-219): x [E][N][3], v [E][N][3], F [E][N][9] row-major,
+ * C [E][N][9]; material [E][N], group [E][N] (group may be NULL). */
+int dm_set_state(DmContext* ctx, const float* x, const float* v, const float* F, const float* C,
+                 const int* material, const int* group);
+int dm_set_state_device(DmContext* ctx, const float* x, const float* v, const float* F, const float* C,
+                        const int* material, const int* group);
+/* Download the current state in the original particle order (lower_state, env.hpp:49-53). */
+int dm_get_state(DmContext* ctx, float* x, float* v, float* F, float* C);
+int dm_get_state_device(DmContext* ctx, float* x, float* v, float* F, float* C);
+
+/* One control step = `substeps` MLS-MPM substeps (mpm_step, mpm.hpp:348-367)
+ * with colliders frozen at the given pose (Task::step, tasks.hpp:306-339).
+ * cvo [E][K][9]: center, velocity, angular velocity per collider;
+ * act [E][G] actuation (may be NULL); obs [E][7] written after the step
+ * (may be NULL).  The step is recorded on the tape (Tape::checkpoint,
+ * tape.hpp:181-216). */
+int dm_step(DmContext* ctx, const float* cvo, const float* act, float* obs);
+int dm_step_device(DmContext* ctx, const float* cvo, const float* act, float* obs);
+
+/* Backward through every recorded step (Tape::backward + backward_segment,
+ * tape.hpp:124-164, 227-255).
+ *   dobs      [T][E][7]  cotangents of the per-step observables (may be NULL)
+ *   dfinal_x/v/F/C       cotangents of the final state, original order (may be NULL)
+ * outputs (any may be NULL):
+ *   dx0, dv0, dF0, dC0   cotangents of the initial state, original order
+ *   dcvo  [T][E][K][9]   collider center / velocity / omega cotangents
+ *   dact  [T][E][G]      actuation cotangents
+ *   dE    [E][num_materials] Young's modulus cotangents (the reference tape
+ *         cannot produce these, mpm.hpp:23-41) */
+int dm_backward(DmContext* ctx, const float* dobs, const float* dfinal_x, const float* dfinal_v,
+                const float* dfinal_F, const float* dfinal_C, float* dx0, float* dv0, float* dF0, float* dC0,
+                float* dcvo, float* dact, double* dE);
+int dm_backward_device(DmContext* ctx, const float* dobs, const float* dfinal_x, const float* dfinal_v,
+                       const float* dfinal_F, const float* dfinal_C, float* dx0, float* dv0, float* dF0,
+                       float* dC0, float* dcvo, float* dact, double* dE);
+
+/* Number of control steps currently on the tape. */
+int dm_tape_steps(const DmContext* ctx);
+
+/* Parity hooks: bin keys / stable permutation of the
+ * current state (per env, local indices) and the current physical order's
+ * original particle ids. */
+int dm_debug_sort(DmContext* ctx, int* keys, int* perm);
+/* Kernel launches issued since the context was created. */
+unsigned long long dm_launch_count(const DmContext* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DIFFMPM_H */

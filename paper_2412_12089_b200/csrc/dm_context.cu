@@ -1,0 +1,633 @@
+// C-ABI implementation: context, device memory plan, substep schedule,
+// checkpointed tape (forward stores a state every `checkpoint_every`
+// substeps; backward replays each segment and runs the adjoint kernels in
+// reverse) -- the B200 replacement for Tape::checkpoint / backward_segment
+// (tape.hpp:181-255) driven per control step as step_checkpointed does
+// (algo.hpp:79-104).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/diffmpm.h"
+#include "dm_kernels.cuh"
+
+using namespace dm;
+
+struct DmContext {
+  DmConfig cfg{};
+  int nmat = 0;
+  DevParams P{};
+  double dmu_dE[4] = {0, 0, 0, 0}, dlam_dE[4] = {0, 0, 0, 0};
+  int law_kind[4] = {0, 0, 0, 0};
+  cudaStream_t stream = nullptr;
+  std::string err;
+  bool poisoned = false;
+  size_t Ntot = 0;
+  int ck = 1;  // substeps per checkpoint segment
+  int steps = 0;
+  int n_store = 0;
+  unsigned long long launches = 0, bytes = 0;
+  int grid_tiles = 148 * 4;
+
+  float* store = nullptr;  // [n_store][24][Ntot]
+  uint32_t* store_attr = nullptr;
+  float* seg = nullptr;  // [ck-1][24][Ntot]
+  uint32_t* seg_attr = nullptr;
+  float* scratch[2] = {nullptr, nullptr};
+  uint32_t* scratch_attr[2] = {nullptr, nullptr};
+  float* adj[2] = {nullptr, nullptr};  // [24][Ntot]
+  float* part = nullptr;               // [12][Ntot]
+  int *keys = nullptr, *perm = nullptr, *tile_start = nullptr, *tile_count = nullptr;
+  int *env_abase = nullptr, *env_acount = nullptr;
+  int2* active = nullptr;
+  float4 *blocks = nullptr, *ablocks = nullptr;
+  float* tile_acc = nullptr;
+  DevFlags* flags = nullptr;
+  DevFlags* h_flags = nullptr;
+  float *cvo_tape = nullptr, *act_tape = nullptr, *obs_tape = nullptr;
+  double *gcvo = nullptr, *gact = nullptr, *gmu = nullptr, *glam = nullptr;
+};
+
+namespace {
+
+#define DM_CUDA(call)                                                                     \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      ctx->err = std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #call;    \
+      ctx->poisoned = true;                                                               \
+      return DM_ERR_CUDA;                                                                 \
+    }                                                                                     \
+  } while (0)
+
+template <class T>
+bool dalloc(DmContext* ctx, T** p, size_t n) {
+  if (n == 0) n = 1;
+  if (cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)) != cudaSuccess) return false;
+  ctx->bytes += n * sizeof(T);
+  return true;
+}
+
+size_t state_floats(const DmContext* c) { return 24 * c->Ntot; }
+
+StateView view(float* f, uint32_t* a, size_t stride) {
+  StateView s;
+  s.f = f;
+  s.attr = a;
+  s.stride = stride;
+  return s;
+}
+
+StateView store_view(DmContext* c, int k) {
+  return view(c->store + (size_t)k * state_floats(c), c->store_attr + (size_t)k * c->Ntot, c->Ntot);
+}
+
+// State of global substep index s while running forward.
+StateView fwd_state(DmContext* c, int s) {
+  if (s % c->ck == 0) return store_view(c, s / c->ck);
+  return view(c->scratch[s & 1], c->scratch_attr[s & 1], c->Ntot);
+}
+
+// State of substep s inside the segment starting at s0 during backward.
+StateView seg_state(DmContext* c, int s0, int s) {
+  if (s == s0) return store_view(c, s0 / c->ck);
+  const int k = s - s0 - 1;
+  return view(c->seg + (size_t)k * state_floats(c), c->seg_attr + (size_t)k * c->Ntot, c->Ntot);
+}
+
+int maxc_of(int K) { return K <= 1 ? 1 : 4; }
+
+void launch_bin(DmContext* c, const StateView& S, int sub, int check_vmax) {
+  cudaMemsetAsync(&c->flags->active_count, 0, sizeof(int), c->stream);
+  const size_t shm = 2 * (size_t)c->P.Tn * sizeof(int);
+  k_bin<<<c->P.E, 512, shm, c->stream>>>(c->P, S, c->keys, c->perm, c->tile_start, c->tile_count, c->active,
+                                          c->env_abase, c->env_acount, c->flags, sub, check_vmax);
+  ++c->launches;
+}
+
+const float* step_cvo(DmContext* c, int t) { return c->cvo_tape + (size_t)t * c->P.E * (c->P.K > 0 ? c->P.K : 1) * 9; }
+const float* step_act(DmContext* c, int t) {
+  return c->P.G > 0 ? c->act_tape + (size_t)t * c->P.E * c->P.G : nullptr;
+}
+
+void launch_p2g(DmContext* c, const StateView& S, int t, int sub) {
+  if (maxc_of(c->P.K) == 1)
+    k_p2g<1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, c->perm, c->tile_start, c->tile_count, c->active,
+                                                           step_act(c, t), c->blocks, c->flags, sub);
+  else
+    k_p2g<4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, c->perm, c->tile_start, c->tile_count, c->active,
+                                                           step_act(c, t), c->blocks, c->flags, sub);
+  ++c->launches;
+}
+
+void launch_g2p(DmContext* c, const StateView& S, const StateView& So, int t, int sub) {
+  if (maxc_of(c->P.K) == 1)
+    k_g2p<1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, c->perm, c->tile_start, c->tile_count,
+                                                           c->active, step_cvo(c, t), c->blocks, c->flags, sub);
+  else
+    k_g2p<4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, c->perm, c->tile_start, c->tile_count,
+                                                           c->active, step_cvo(c, t), c->blocks, c->flags, sub);
+  ++c->launches;
+}
+
+void forward_substep(DmContext* c, const StateView& S, const StateView& So, int t, int sub, int check_vmax) {
+  launch_bin(c, S, sub, check_vmax);
+  launch_p2g(c, S, t, sub);
+  launch_g2p(c, S, So, t, sub);
+}
+
+template <int MAXC, int NG>
+void launch_p2g_adj(DmContext* c, const StateView& S, int t, float* adj_out) {
+  k_p2g_adj<MAXC, NG><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(
+      c->P, S, c->perm, c->tile_start, c->tile_count, c->active, step_cvo(c, t), step_act(c, t), c->blocks,
+      c->ablocks, c->part, adj_out, c->Ntot, c->tile_acc, c->flags);
+}
+
+void backward_substep(DmContext* c, const StateView& S, int t, int sub, const float* adj_in, float* adj_out) {
+  launch_bin(c, S, sub, 0);
+  launch_p2g(c, S, t, sub);
+  if (maxc_of(c->P.K) == 1)
+    k_g2p_adj<1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, adj_in, c->Ntot, c->perm, c->tile_start,
+                                                               c->tile_count, c->active, step_cvo(c, t), c->blocks,
+                                                               c->ablocks, c->part, c->tile_acc, c->flags);
+  else
+    k_g2p_adj<4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, adj_in, c->Ntot, c->perm, c->tile_start,
+                                                               c->tile_count, c->active, step_cvo(c, t), c->blocks,
+                                                               c->ablocks, c->part, c->tile_acc, c->flags);
+  ++c->launches;
+  const int m = maxc_of(c->P.K);
+  const int G = c->P.G;
+  if (m == 1) {
+    if (G <= 1)
+      launch_p2g_adj<1, 1>(c, S, t, adj_out);
+    else if (G <= 8)
+      launch_p2g_adj<1, 8>(c, S, t, adj_out);
+    else
+      launch_p2g_adj<1, 16>(c, S, t, adj_out);
+  } else {
+    if (G <= 1)
+      launch_p2g_adj<4, 1>(c, S, t, adj_out);
+    else
+      launch_p2g_adj<4, 16>(c, S, t, adj_out);
+  }
+  ++c->launches;
+  const int Kc = c->P.K > 0 ? c->P.K : 1;
+  k_env_reduce<<<c->P.E, kNacc, 0, c->stream>>>(c->P, c->active, c->env_abase, c->env_acount, c->tile_acc,
+                                                c->gcvo + (size_t)t * c->P.E * Kc * 9,
+                                                c->gact + (size_t)t * c->P.E * (G > 0 ? G : 1), c->gmu, c->glam);
+  ++c->launches;
+}
+
+std::string fmt_error(DmContext* c, unsigned long long key) {
+  const int code = (int)(key & 0xF);
+  const int axis = (int)((key >> 4) & 3);
+  const unsigned particle = (unsigned)((key >> 6) & 0xFFFFFF);
+  const int sub = (int)((key >> 32) & 0x3FF);
+  const int env = (int)((key >> 42) & 0xFFFF);
+  char buf[256];
+  if (code == kErrP2GInterior) {
+    std::snprintf(buf, sizeof(buf), "mpm: particle %u outside grid interior (axis %d) [env %d, substep %d]", particle,
+                  axis, env, sub);
+  } else if (code == kErrG2PInterior) {
+    std::snprintf(buf, sizeof(buf), "g2p: particle %u advected outside grid interior [env %d, substep %d]", particle,
+                  env, sub);
+  } else {
+    static const char* names[4] = {"stress_fixed_corotated", "stress_neo_hookean", "stress_elastoplastic",
+                                   "stress_fluid"};
+    const int kind = c->law_kind[axis];
+    std::snprintf(buf, sizeof(buf), "%s: det(F) <= 0 [env %d, particle %u, substep %d]", names[kind & 3], env,
+                  particle, sub);
+  }
+  return buf;
+}
+
+// Reads the device flags after a control step; returns DM_OK or the error.
+int check_flags(DmContext* ctx, bool cfl) {
+  DM_CUDA(cudaMemcpyAsync(ctx->h_flags, ctx->flags, sizeof(DevFlags), cudaMemcpyDeviceToHost, ctx->stream));
+  DM_CUDA(cudaStreamSynchronize(ctx->stream));
+  DM_CUDA(cudaGetLastError());
+  if (ctx->h_flags->err_key != ~0ull) {
+    ctx->err = fmt_error(ctx, ctx->h_flags->err_key);
+    ctx->poisoned = true;
+    return DM_ERR_RUNTIME;
+  }
+  if (cfl) {
+    float vmax;
+    std::memcpy(&vmax, &ctx->h_flags->vmax_bits, sizeof(float));
+    if ((double)vmax * ctx->cfg.dt >= ctx->cfg.dx)
+      std::fprintf(stderr, "mpm_step: CFL violated (max|v| dt = %g >= dx = %g)\n", (double)vmax * ctx->cfg.dt,
+                   ctx->cfg.dx);
+  }
+  return DM_OK;
+}
+
+int reset_flags(DmContext* ctx) {
+  DevFlags f;
+  f.err_key = ~0ull;
+  f.vmax_bits = 0;
+  f.active_count = 0;
+  DM_CUDA(cudaMemcpyAsync(ctx->flags, &f, sizeof(DevFlags), cudaMemcpyHostToDevice, ctx->stream));
+  DM_CUDA(cudaStreamSynchronize(ctx->stream));
+  return DM_OK;
+}
+
+int set_state_impl(DmContext* ctx, const float* x, const float* v, const float* F, const float* C, const int* mat,
+                   const int* grp, cudaMemcpyKind kind) {
+  if (ctx->poisoned && ctx->h_flags->err_key == ~0ull) ctx->poisoned = false;
+  const size_t N = ctx->Ntot;
+  float* st = ctx->adj[0];
+  int* ints = reinterpret_cast<int*>(ctx->part);
+  DM_CUDA(cudaMemcpyAsync(st, x, 3 * N * sizeof(float), kind, ctx->stream));
+  DM_CUDA(cudaMemcpyAsync(st + 3 * N, v, 3 * N * sizeof(float), kind, ctx->stream));
+  DM_CUDA(cudaMemcpyAsync(st + 6 * N, F, 9 * N * sizeof(float), kind, ctx->stream));
+  DM_CUDA(cudaMemcpyAsync(st + 15 * N, C, 9 * N * sizeof(float), kind, ctx->stream));
+  if (mat) DM_CUDA(cudaMemcpyAsync(ints, mat, N * sizeof(int), kind, ctx->stream));
+  if (grp) DM_CUDA(cudaMemcpyAsync(ints + N, grp, N * sizeof(int), kind, ctx->stream));
+  const StateView S0 = store_view(ctx, 0);
+  k_aos_to_soa<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>((int)N, st, st + 3 * N, st + 6 * N, st + 15 * N,
+                                                                     mat ? ints : nullptr, grp ? ints + N : nullptr,
+                                                                     ctx->P.N, S0);
+  ++ctx->launches;
+  ctx->steps = 0;
+  ctx->poisoned = false;
+  const int rc = reset_flags(ctx);
+  if (rc != DM_OK) return rc;
+  DM_CUDA(cudaGetLastError());
+  return DM_OK;
+}
+
+int get_state_impl(DmContext* ctx, float* x, float* v, float* F, float* C, cudaMemcpyKind kind) {
+  const size_t N = ctx->Ntot;
+  const int s = ctx->steps * ctx->cfg.substeps;
+  const StateView S = fwd_state(ctx, s);
+  float* out = ctx->adj[1];
+  k_soa_to_aos<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>((int)N, ctx->P.N, S.f, S.attr, N, out,
+                                                                     out + 3 * N, out + 6 * N, out + 15 * N);
+  ++ctx->launches;
+  if (x) DM_CUDA(cudaMemcpyAsync(x, out, 3 * N * sizeof(float), kind, ctx->stream));
+  if (v) DM_CUDA(cudaMemcpyAsync(v, out + 3 * N, 3 * N * sizeof(float), kind, ctx->stream));
+  if (F) DM_CUDA(cudaMemcpyAsync(F, out + 6 * N, 9 * N * sizeof(float), kind, ctx->stream));
+  if (C) DM_CUDA(cudaMemcpyAsync(C, out + 15 * N, 9 * N * sizeof(float), kind, ctx->stream));
+  DM_CUDA(cudaStreamSynchronize(ctx->stream));
+  return DM_OK;
+}
+
+int step_impl(DmContext* ctx, const float* cvo, const float* act, float* obs, cudaMemcpyKind kin,
+              cudaMemcpyKind kout) {
+  if (ctx->poisoned) {
+    if (ctx->err.empty()) ctx->err = "context poisoned by an earlier error";
+    return DM_ERR_RUNTIME;
+  }
+  if (ctx->steps >= ctx->cfg.max_steps) {
+    ctx->err = "tape capacity exceeded (max_steps)";
+    return DM_ERR_CAPACITY;
+  }
+  const int t = ctx->steps;
+  const int E = ctx->P.E, K = ctx->P.K, G = ctx->P.G;
+  if (K > 0) {
+    if (!cvo) {
+      ctx->err = "dm_step: colliders configured but cvo is NULL";
+      return DM_ERR_ARG;
+    }
+    DM_CUDA(cudaMemcpyAsync(const_cast<float*>(step_cvo(ctx, t)), cvo, (size_t)E * K * 9 * sizeof(float), kin,
+                            ctx->stream));
+  }
+  if (G > 0) {
+    if (act)
+      DM_CUDA(cudaMemcpyAsync(const_cast<float*>(step_act(ctx, t)), act, (size_t)E * G * sizeof(float), kin,
+                              ctx->stream));
+    else
+      DM_CUDA(cudaMemsetAsync(const_cast<float*>(step_act(ctx, t)), 0, (size_t)E * G * sizeof(float), ctx->stream));
+  }
+  const int S = ctx->cfg.substeps;
+  for (int q = 0; q < S; ++q) {
+    const int s = t * S + q;
+    forward_substep(ctx, fwd_state(ctx, s), fwd_state(ctx, s + 1), t, q, q == 0);
+  }
+  float* o = ctx->obs_tape + (size_t)t * E * DM_OBS_DIM;
+  k_obs<<<E, 256, 0, ctx->stream>>>(ctx->P, fwd_state(ctx, (t + 1) * S), step_cvo(ctx, t), (float)ctx->cfg.spill_half,
+                                    (float)ctx->cfg.spill_temp, o);
+  ++ctx->launches;
+  if (obs) DM_CUDA(cudaMemcpyAsync(obs, o, (size_t)E * DM_OBS_DIM * sizeof(float), kout, ctx->stream));
+  const int rc = check_flags(ctx, true);
+  if (rc != DM_OK) return rc;
+  ctx->steps = t + 1;
+  return DM_OK;
+}
+
+int backward_impl(DmContext* ctx, const float* dobs, const float* dfx, const float* dfv, const float* dfF,
+                  const float* dfC, float* dx0, float* dv0, float* dF0, float* dC0, float* dcvo, float* dact,
+                  double* dE, cudaMemcpyKind kin, cudaMemcpyKind kout) {
+  if (ctx->poisoned) return DM_ERR_RUNTIME;
+  const int T = ctx->steps, S = ctx->cfg.substeps, E = ctx->P.E;
+  const int Kc = ctx->P.K > 0 ? ctx->P.K : 1, Gc = ctx->P.G > 0 ? ctx->P.G : 1;
+  const size_t N = ctx->Ntot;
+  if (T == 0) {
+    ctx->err = "backward: no recorded steps";
+    return DM_ERR_ARG;
+  }
+  DM_CUDA(cudaMemsetAsync(ctx->gcvo, 0, (size_t)T * E * Kc * 9 * sizeof(double), ctx->stream));
+  DM_CUDA(cudaMemsetAsync(ctx->gact, 0, (size_t)T * E * Gc * sizeof(double), ctx->stream));
+  DM_CUDA(cudaMemsetAsync(ctx->gmu, 0, (size_t)E * 4 * sizeof(double), ctx->stream));
+  DM_CUDA(cudaMemsetAsync(ctx->glam, 0, (size_t)E * 4 * sizeof(double), ctx->stream));
+  // dobs staged in part (T*E*7 floats) -- copied per step below
+  float* dobs_dev = nullptr;
+  if (dobs) {
+    if (!dalloc(ctx, &dobs_dev, (size_t)T * E * DM_OBS_DIM)) {
+      ctx->err = "backward: out of device memory";
+      return DM_ERR_CUDA;
+    }
+    DM_CUDA(cudaMemcpyAsync(dobs_dev, dobs, (size_t)T * E * DM_OBS_DIM * sizeof(float), kin, ctx->stream));
+  }
+  // final-state cotangent in the physical order of the final state
+  int cur = 0;
+  float* A = ctx->adj[cur];
+  {
+    const StateView Sf = fwd_state(ctx, T * S);
+    if (dfx || dfv || dfF || dfC) {
+      float* stg = ctx->adj[1];
+      if (dfx) DM_CUDA(cudaMemcpyAsync(stg, dfx, 3 * N * sizeof(float), kin, ctx->stream));
+      if (dfv) DM_CUDA(cudaMemcpyAsync(stg + 3 * N, dfv, 3 * N * sizeof(float), kin, ctx->stream));
+      if (dfF) DM_CUDA(cudaMemcpyAsync(stg + 6 * N, dfF, 9 * N * sizeof(float), kin, ctx->stream));
+      if (dfC) DM_CUDA(cudaMemcpyAsync(stg + 15 * N, dfC, 9 * N * sizeof(float), kin, ctx->stream));
+      k_aos_to_soa_perm<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>(
+          (int)N, ctx->P.N, dfx ? stg : nullptr, dfv ? stg + 3 * N : nullptr, dfF ? stg + 6 * N : nullptr,
+          dfC ? stg + 15 * N : nullptr, Sf.attr, A, N);
+      ++ctx->launches;
+    } else {
+      DM_CUDA(cudaMemsetAsync(A, 0, 24 * N * sizeof(float), ctx->stream));
+    }
+  }
+  const int ck = ctx->ck;
+  for (int t = T - 1; t >= 0; --t) {
+    const int s_end = (t + 1) * S;
+    if (dobs_dev) {
+      k_obs_adj<<<E, 256, 0, ctx->stream>>>(ctx->P, store_view(ctx, s_end / ck), step_cvo(ctx, t),
+                                            (float)ctx->cfg.spill_half, (float)ctx->cfg.spill_temp,
+                                            dobs_dev + (size_t)t * E * DM_OBS_DIM, ctx->adj[cur], N,
+                                            ctx->gcvo + (size_t)t * E * Kc * 9);
+      ++ctx->launches;
+    }
+    for (int s0 = s_end - ck; s0 >= t * S; s0 -= ck) {
+      // replay the segment's forward (tape.hpp:229-233)
+      for (int s = s0; s < s0 + ck - 1; ++s) forward_substep(ctx, seg_state(ctx, s0, s), seg_state(ctx, s0, s + 1), t, s - t * S, 0);
+      for (int s = s0 + ck - 1; s >= s0; --s) {
+        backward_substep(ctx, seg_state(ctx, s0, s), t, s - t * S, ctx->adj[cur], ctx->adj[cur ^ 1]);
+        cur ^= 1;
+      }
+    }
+  }
+  // outputs
+  {
+    float* out = ctx->adj[cur ^ 1];
+    const StateView S0 = store_view(ctx, 0);
+    k_soa_to_aos<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>((int)N, ctx->P.N, ctx->adj[cur], S0.attr, N,
+                                                                       out, out + 3 * N, out + 6 * N, out + 15 * N);
+    ++ctx->launches;
+    if (dx0) DM_CUDA(cudaMemcpyAsync(dx0, out, 3 * N * sizeof(float), kout, ctx->stream));
+    if (dv0) DM_CUDA(cudaMemcpyAsync(dv0, out + 3 * N, 3 * N * sizeof(float), kout, ctx->stream));
+    if (dF0) DM_CUDA(cudaMemcpyAsync(dF0, out + 6 * N, 9 * N * sizeof(float), kout, ctx->stream));
+    if (dC0) DM_CUDA(cudaMemcpyAsync(dC0, out + 15 * N, 9 * N * sizeof(float), kout, ctx->stream));
+  }
+  std::vector<double> h;
+  if (dcvo && ctx->P.K > 0) {
+    h.resize((size_t)T * E * Kc * 9);
+    DM_CUDA(cudaMemcpyAsync(h.data(), ctx->gcvo, h.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    DM_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::vector<float> f(h.begin(), h.end());
+    DM_CUDA(cudaMemcpy(dcvo, f.data(), f.size() * sizeof(float), kout == cudaMemcpyDeviceToDevice
+                                                                          ? cudaMemcpyHostToDevice
+                                                                          : cudaMemcpyHostToHost));
+  }
+  if (dact && ctx->P.G > 0) {
+    h.resize((size_t)T * E * Gc);
+    DM_CUDA(cudaMemcpyAsync(h.data(), ctx->gact, h.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    DM_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::vector<float> f(h.begin(), h.end());
+    DM_CUDA(cudaMemcpy(dact, f.data(), f.size() * sizeof(float), kout == cudaMemcpyDeviceToDevice
+                                                                         ? cudaMemcpyHostToDevice
+                                                                         : cudaMemcpyHostToHost));
+  }
+  if (dE) {
+    std::vector<double> mu((size_t)E * 4), la((size_t)E * 4);
+    DM_CUDA(cudaMemcpyAsync(mu.data(), ctx->gmu, mu.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    DM_CUDA(cudaMemcpyAsync(la.data(), ctx->glam, la.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    DM_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::vector<double> g((size_t)E * ctx->nmat);
+    for (int e = 0; e < E; ++e)
+      for (int m = 0; m < ctx->nmat; ++m)
+        g[(size_t)e * ctx->nmat + m] = mu[e * 4 + m] * ctx->dmu_dE[m] + la[e * 4 + m] * ctx->dlam_dE[m];
+    DM_CUDA(cudaMemcpy(dE, g.data(), g.size() * sizeof(double), kout == cudaMemcpyDeviceToDevice
+                                                                       ? cudaMemcpyHostToDevice
+                                                                       : cudaMemcpyHostToHost));
+  }
+  DM_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (dobs_dev) {
+    cudaFree(dobs_dev);
+    ctx->bytes -= (size_t)T * E * DM_OBS_DIM * sizeof(float);
+  }
+  return check_flags(ctx, false);
+}
+
+}  // namespace
+
+extern "C" {
+
+DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materials, const DmColliderShape* shapes) {
+  DmContext* ctx = new DmContext();
+  ctx->cfg = *cfg;
+  auto fail = [&](const char* m) {
+    ctx->err = m;
+    ctx->poisoned = true;
+    return ctx;
+  };
+  if (cfg->substeps < 1) return fail("mpm_step: substeps < 1");
+  if (num_materials < 1 || num_materials > DM_MAX_MATERIALS) return fail("dm_create: 1..4 materials supported");
+  if (cfg->num_colliders < 0 || cfg->num_colliders > DM_MAX_COLLIDERS) return fail("dm_create: <= 4 colliders");
+  if (cfg->num_groups < 0 || cfg->num_groups > DM_MAX_GROUPS) return fail("dm_create: <= 16 actuation groups");
+  if (cfg->particles_per_env < 1 || cfg->particles_per_env > (1 << 20)) return fail("dm_create: 1..2^20 particles per env");
+  if (cfg->num_envs < 1 || cfg->num_envs > 65535) return fail("dm_create: 1..65535 envs");
+  const int ck = cfg->checkpoint_every > 0 ? cfg->checkpoint_every : cfg->substeps;
+  if (cfg->substeps % ck != 0) return fail("dm_create: checkpoint_every must divide substeps");
+  if (cudaSetDevice(cfg->device) != cudaSuccess) return fail("dm_create: cudaSetDevice failed");
+  ctx->ck = ck;
+  ctx->nmat = num_materials;
+  DevParams& P = ctx->P;
+  P.E = cfg->num_envs;
+  P.N = cfg->particles_per_env;
+  for (int a = 0; a < 3; ++a) {
+    P.dims[a] = cfg->dims[a];
+    P.td[a] = (cfg->dims[a] + kTile - 1) / kTile;
+    P.grav[a] = (float)cfg->gravity[a];
+  }
+  P.Tn = P.td[0] * P.td[1] * P.td[2];
+  if (2 * (size_t)P.Tn * sizeof(int) > 200 * 1024) return fail("dm_create: grid too large for the bin kernel");
+  P.dx = (float)cfg->dx;
+  P.inv_dx = (float)(1.0 / cfg->dx);
+  P.dt = (float)cfg->dt;
+  P.boundary = cfg->boundary;
+  P.alpha_c = (float)cfg->alpha_c;
+  P.mu_b = (float)cfg->mu_b;
+  P.K = cfg->num_colliders;
+  P.G = cfg->num_groups;
+  P.nmat = num_materials;
+  for (int m = 0; m < num_materials; ++m) {
+    const DmMaterial& M = mats[m];
+    const double nu = M.poisson;
+    const double mu = M.youngs / (2.0 * (1.0 + nu));
+    double lam = M.youngs * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+    ctx->dmu_dE[m] = 1.0 / (2.0 * (1.0 + nu));
+    ctx->dlam_dE[m] = nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+    if (M.kind == kFluid && M.bulk > 0.0) {
+      lam = M.bulk;
+      ctx->dlam_dE[m] = 0.0;
+    }
+    Law<float>& L = P.law[m];
+    L.kind = M.kind;
+    L.mu = (float)mu;
+    L.lam = (float)lam;
+    L.cy = (float)(M.wide_yield ? M.yield_stress / mu : M.yield_stress / (2.0 * mu));
+    L.visc = (float)M.viscosity;
+    L.act_k = (float)M.act_strength;
+    L.mass = (float)(M.density * M.volume);
+    L.vol = (float)M.volume;
+    L.dmu_dE = (float)ctx->dmu_dE[m];
+    L.dlam_dE = (float)ctx->dlam_dE[m];
+    ctx->law_kind[m] = M.kind;
+  }
+  for (int c = 0; c < P.K; ++c) {
+    ColShape& s = P.shape[c];
+    s.kind = shapes[c].kind;
+    for (int a = 0; a < 3; ++a) {
+      s.nrm[a] = (float)shapes[c].normal[a];
+      s.half[a] = (float)shapes[c].half[a];
+    }
+    s.radius = (float)shapes[c].radius;
+    s.length = (float)shapes[c].length;
+    s.thickness = (float)shapes[c].thickness;
+  }
+  ctx->Ntot = (size_t)P.E * P.N;
+  const size_t N = ctx->Ntot;
+  const size_t TT = (size_t)P.E * P.Tn;
+  const int Kc = P.K > 0 ? P.K : 1, Gc = P.G > 0 ? P.G : 1;
+  ctx->n_store = cfg->max_steps * cfg->substeps / ck + 1;
+  bool ok = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) == cudaSuccess;
+  ok = ok && dalloc(ctx, &ctx->store, (size_t)ctx->n_store * 24 * N) &&
+       dalloc(ctx, &ctx->store_attr, (size_t)ctx->n_store * N);
+  if (ck > 1) ok = ok && dalloc(ctx, &ctx->seg, (size_t)(ck - 1) * 24 * N) && dalloc(ctx, &ctx->seg_attr, (size_t)(ck - 1) * N);
+  if (ck > 1)
+    for (int i = 0; i < 2; ++i)
+      ok = ok && dalloc(ctx, &ctx->scratch[i], 24 * N) && dalloc(ctx, &ctx->scratch_attr[i], N);
+  ok = ok && dalloc(ctx, &ctx->adj[0], 24 * N) && dalloc(ctx, &ctx->adj[1], 24 * N) && dalloc(ctx, &ctx->part, 12 * N);
+  ok = ok && dalloc(ctx, &ctx->keys, N) && dalloc(ctx, &ctx->perm, N) && dalloc(ctx, &ctx->tile_start, TT) &&
+       dalloc(ctx, &ctx->tile_count, TT) && dalloc(ctx, &ctx->env_abase, P.E) && dalloc(ctx, &ctx->env_acount, P.E) &&
+       dalloc(ctx, &ctx->active, TT);
+  ok = ok && dalloc(ctx, &ctx->blocks, TT * kExt3) && dalloc(ctx, &ctx->ablocks, TT * kExt3) &&
+       dalloc(ctx, &ctx->tile_acc, TT * kNacc) && dalloc(ctx, &ctx->flags, 1);
+  ok = ok && dalloc(ctx, &ctx->cvo_tape, (size_t)cfg->max_steps * P.E * Kc * 9) &&
+       dalloc(ctx, &ctx->act_tape, (size_t)cfg->max_steps * P.E * Gc) &&
+       dalloc(ctx, &ctx->obs_tape, (size_t)cfg->max_steps * P.E * DM_OBS_DIM) &&
+       dalloc(ctx, &ctx->gcvo, (size_t)cfg->max_steps * P.E * Kc * 9) &&
+       dalloc(ctx, &ctx->gact, (size_t)cfg->max_steps * P.E * Gc) && dalloc(ctx, &ctx->gmu, (size_t)P.E * 4) &&
+       dalloc(ctx, &ctx->glam, (size_t)P.E * 4);
+  ok = ok && cudaMallocHost(reinterpret_cast<void**>(&ctx->h_flags), sizeof(DevFlags)) == cudaSuccess;
+  if (!ok) {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "dm_create: device allocation failed (%.2f GB requested so far)",
+                  ctx->bytes / 1e9);
+    return fail(buf);
+  }
+  cudaMemsetAsync(ctx->store_attr, 0, N * sizeof(uint32_t), ctx->stream);
+  cudaMemsetAsync(ctx->tile_acc, 0, TT * kNacc * sizeof(float), ctx->stream);
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<4, 16>, kWarps * 32, 0);
+  if (occ < 1) occ = 1;
+  ctx->grid_tiles = dev_sms * (occ < 8 ? 8 : occ);
+  if (reset_flags(ctx) != DM_OK) return ctx;
+  return ctx;
+}
+
+void dm_destroy(DmContext* ctx) {
+  if (!ctx) return;
+  void* ptrs[] = {ctx->store,     ctx->store_attr, ctx->seg,       ctx->seg_attr,   ctx->scratch[0], ctx->scratch[1],
+                  ctx->scratch_attr[0], ctx->scratch_attr[1], ctx->adj[0], ctx->adj[1], ctx->part, ctx->keys,
+                  ctx->perm,      ctx->tile_start, ctx->tile_count, ctx->env_abase, ctx->env_acount, ctx->active,
+                  ctx->blocks,    ctx->ablocks,    ctx->tile_acc,   ctx->flags,      ctx->cvo_tape,  ctx->act_tape,
+                  ctx->obs_tape,  ctx->gcvo,       ctx->gact,       ctx->gmu,        ctx->glam};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int dm_last_error(const DmContext* ctx, char* buf, int len) {
+  if (!ctx) return DM_ERR_ARG;
+  if (buf && len > 0) std::snprintf(buf, (size_t)len, "%s", ctx->err.c_str());
+  return ctx->poisoned ? DM_ERR_RUNTIME : DM_OK;
+}
+
+void* dm_stream(DmContext* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+unsigned long long dm_device_bytes(const DmContext* ctx) { return ctx ? ctx->bytes : 0; }
+int dm_tape_steps(const DmContext* ctx) { return ctx ? ctx->steps : 0; }
+unsigned long long dm_launch_count(const DmContext* ctx) { return ctx ? ctx->launches : 0; }
+
+int dm_set_state(DmContext* ctx, const float* x, const float* v, const float* F, const float* C, const int* material,
+                 const int* group) {
+  if (!ctx || !ctx->store) return DM_ERR_ARG;
+  return set_state_impl(ctx, x, v, F, C, material, group, cudaMemcpyHostToDevice);
+}
+int dm_set_state_device(DmContext* ctx, const float* x, const float* v, const float* F, const float* C,
+                        const int* material, const int* group) {
+  if (!ctx || !ctx->store) return DM_ERR_ARG;
+  return set_state_impl(ctx, x, v, F, C, material, group, cudaMemcpyDeviceToDevice);
+}
+int dm_get_state(DmContext* ctx, float* x, float* v, float* F, float* C) {
+  if (!ctx || !ctx->store) return DM_ERR_ARG;
+  return get_state_impl(ctx, x, v, F, C, cudaMemcpyDeviceToHost);
+}
+int dm_get_state_device(DmContext* ctx, float* x, float* v, float* F, float* C) {
+  if (!ctx || !ctx->store) return DM_ERR_ARG;
+  return get_state_impl(ctx, x, v, F, C, cudaMemcpyDeviceToDevice);
+}
+int dm_step(DmContext* ctx, const float* cvo, const float* act, float* obs) {
+  if (!ctx || !ctx->store) return DM_ERR_ARG;
+  return step_impl(ctx, cvo, act, obs, cudaMemcpyHostToDevice, cudaMemcpyDeviceToHost);
+}
+int dm_step_device(DmContext* ctx, const float* cvo, const float* act, float* obs) {
+  if (!ctx || !ctx->store) return DM_ERR_ARG;
+  return step_impl(ctx, cvo, act, obs, cudaMemcpyDeviceToDevice, cudaMemcpyDeviceToDevice);
+}
+int dm_backward(DmContext* ctx, const float* dobs, const float* dfx, const float* dfv, const float* dfF,
+                const float* dfC, float* dx0, float* dv0, float* dF0, float* dC0, float* dcvo, float* dact, double* dE) {
+  if (!ctx || !ctx->store) return DM_ERR_ARG;
+  return backward_impl(ctx, dobs, dfx, dfv, dfF, dfC, dx0, dv0, dF0, dC0, dcvo, dact, dE, cudaMemcpyHostToDevice,
+                       cudaMemcpyDeviceToHost);
+}
+int dm_backward_device(DmContext* ctx, const float* dobs, const float* dfx, const float* dfv, const float* dfF,
+                       const float* dfC, float* dx0, float* dv0, float* dF0, float* dC0, float* dcvo, float* dact,
+                       double* dE) {
+  if (!ctx || !ctx->store) return DM_ERR_ARG;
+  return backward_impl(ctx, dobs, dfx, dfv, dfF, dfC, dx0, dv0, dF0, dC0, dcvo, dact, dE, cudaMemcpyDeviceToDevice,
+                       cudaMemcpyDeviceToDevice);
+}
+
+int dm_debug_sort(DmContext* ctx, int* keys, int* perm) {
+  if (!ctx || !ctx->store) return DM_ERR_ARG;
+  const int s = ctx->steps * ctx->cfg.substeps;
+  launch_bin(ctx, fwd_state(ctx, s), 0, 0);
+  const size_t N = ctx->Ntot;
+  std::vector<int> p(N);
+  DM_CUDA(cudaMemcpyAsync(keys, ctx->keys, N * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  DM_CUDA(cudaMemcpyAsync(p.data(), ctx->perm, N * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  DM_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (size_t i = 0; i < N; ++i) perm[i] = p[i] - (int)((i / ctx->P.N) * ctx->P.N);
+  return check_flags(ctx, false);
+}
+
+}  // extern "C"

@@ -1,0 +1,906 @@
+// sm_100a kernels for the batched MLS-MPM substep and its adjoint.
+//
+// Layout:
+//   particle state  SoA fp32 [24][Ntot]: x(3) v(3) F(9, row-major) C(9),
+//                   env-major; plus one packed u32 attribute per particle
+//                   (original index | material | actuation group)
+//   bins            4x4x4-cell tiles; per env a dense table of tile start /
+//                   count into the env's stably sorted particle order
+//   grid            per active tile a 6x6x6 node block (fp32 mass, momentum)
+//                   accumulated in shared memory and written once; a node's
+//                   value is the sum of the (<= 8) blocks that cover it, taken
+//                   in ascending tile order, so every transfer is
+//                   deterministic and atomic-free
+//
+// One warp owns one tile.  Constitutive / per-particle math runs with lanes =
+// particles; the stencil scatter runs with lanes = the 27 stencil nodes,
+// serially over the chunk's particles, so shared-memory accumulation needs no
+// atomics and has a fixed order (bit-reproducible replays: the recompute-on-
+// backward contract of tape.hpp:234-241).
+#pragma once
+
+#include <cstdint>
+
+#include "dm_transfer.cuh"
+
+namespace dm {
+
+constexpr int kTile = 4;
+constexpr int kExt = 6;  // tile + quadratic stencil reach
+constexpr int kExt3 = kExt * kExt * kExt;
+constexpr int kWarps = 4;  // warps per CTA in tile kernels
+constexpr int kPay = 25;   // payload stride (floats, odd: conflict-free writes)
+constexpr int kNacc = 64;  // per-tile cotangent accumulators
+constexpr int kAccMu = 0, kAccLam = 4, kAccMuG = 8, kAccCol = 12, kAccAct = 48;
+
+struct ColShape {
+  int kind;
+  float nrm[3], radius, half[3], length, thickness;
+};
+
+struct DevParams {
+  int E, N;                // envs, particles per env
+  int dims[3], td[3], Tn;  // grid dims, tile dims, tiles per env
+  float dx, inv_dx, dt;
+  float grav[3];
+  int boundary;
+  float alpha_c, mu_b;
+  int K, G, nmat;
+  Law<float> law[4];
+  ColShape shape[4];
+};
+
+struct StateView {
+  float* f;
+  uint32_t* attr;
+  size_t stride;
+  __device__ __forceinline__ float& c(int comp, size_t i) const { return f[comp * stride + i]; }
+};
+
+struct DevFlags {
+  unsigned long long err_key;  // min over (env, substep, stage, particle, axis, code)
+  unsigned int vmax_bits;      // max |v| component (CFL warning, mpm.hpp:355-361)
+  int active_count;
+};
+
+__device__ __forceinline__ uint32_t attr_index(uint32_t a) { return a & 0xFFFFFu; }
+__device__ __forceinline__ int attr_mat(uint32_t a) { return (a >> 20) & 0xF; }
+__device__ __forceinline__ int attr_group(uint32_t a) { return (a >> 24) & 0xFF; }
+
+// error key: env(16) | substep(10) | stage(2) | particle(24) | axis(2) | code(4)
+__device__ __forceinline__ void report(DevFlags* fl, int env, int sub, int stage, uint32_t particle, int axis,
+                                       int code) {
+  const unsigned long long k = ((unsigned long long)(env & 0xFFFF) << 42) |
+                               ((unsigned long long)(sub & 0x3FF) << 32) | ((unsigned long long)(stage & 3) << 30) |
+                               ((unsigned long long)(particle & 0xFFFFFF) << 6) | ((unsigned long long)(axis & 3) << 4) |
+                               (unsigned long long)(code & 0xF);
+  atomicMin(&fl->err_key, k);
+}
+
+__device__ __forceinline__ TransferCtx<float> tctx(const DevParams& P) {
+  TransferCtx<float> t;
+  t.dims[0] = P.dims[0];
+  t.dims[1] = P.dims[1];
+  t.dims[2] = P.dims[2];
+  t.dx = P.dx;
+  t.inv_dx = P.inv_dx;
+  t.dt = P.dt;
+  t.dx64 = P.dx;
+  return t;
+}
+
+__device__ __forceinline__ NodeCtx<float> nctx(const DevParams& P) {
+  NodeCtx<float> g;
+  g.dims[0] = P.dims[0];
+  g.dims[1] = P.dims[1];
+  g.dims[2] = P.dims[2];
+  g.dx = P.dx;
+  g.dt = P.dt;
+  g.gravity = mk3(P.grav[0], P.grav[1], P.grav[2]);
+  g.boundary = P.boundary;
+  g.alpha_c = P.alpha_c;
+  g.mu_b = P.mu_b;
+  return g;
+}
+
+template <int MAXC>
+__device__ __forceinline__ void load_cols(const DevParams& P, const float* cvo_env, Col<float>* cols) {
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) {
+    if (c >= P.K) break;
+    const ColShape& s = P.shape[c];
+    const float* q = cvo_env + 9 * c;
+    cols[c].kind = s.kind;
+    cols[c].c = mk3(q[0], q[1], q[2]);
+    cols[c].vel = mk3(q[3], q[4], q[5]);
+    cols[c].om = mk3(q[6], q[7], q[8]);
+    cols[c].nrm = mk3(s.nrm[0], s.nrm[1], s.nrm[2]);
+    cols[c].radius = s.radius;
+    cols[c].length = s.length;
+    cols[c].thickness = s.thickness;
+    cols[c].half = mk3(s.half[0], s.half[1], s.half[2]);
+  }
+}
+
+__device__ __forceinline__ void load_state(const StateView& S, size_t i, float x[3], v3<float>& v, m3<float>& F,
+                                           m3<float>& C) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) x[a] = S.c(a, i);
+  v = mk3(S.c(3, i), S.c(4, i), S.c(5, i));
+#pragma unroll
+  for (int q = 0; q < 9; ++q) {
+    F.a[q] = S.c(6 + q, i);
+    C.a[q] = S.c(15 + q, i);
+  }
+}
+
+__device__ __forceinline__ void store_state(const StateView& S, size_t i, v3<float> x, v3<float> v, const m3<float>& F,
+                                            const m3<float>& C) {
+  S.c(0, i) = x.x;
+  S.c(1, i) = x.y;
+  S.c(2, i) = x.z;
+  S.c(3, i) = v.x;
+  S.c(4, i) = v.y;
+  S.c(5, i) = v.z;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) {
+    S.c(6 + q, i) = F.a[q];
+    S.c(15 + q, i) = C.a[q];
+  }
+}
+
+// ============================ binning ============================
+// One CTA per env: keys, interior check (p2g's stencil_base, mpm.hpp:149-161),
+// tile histogram, dense tile table, active-tile list, stable permutation.
+__global__ void __launch_bounds__(512) k_bin(DevParams P, StateView S, int* keys, int* perm, int* tile_start,
+                                             int* tile_count, int2* active, int* env_abase, int* env_acount,
+                                             DevFlags* flags, int substep, int check_vmax) {
+  extern __shared__ int sh[];
+  int* hist = sh;           // [Tn]
+  int* cursor = sh + P.Tn;  // [Tn]
+  __shared__ int s_part[512 / 32 + 1][2];
+  __shared__ int s_base;
+  const int e = blockIdx.x;
+  const size_t base = (size_t)e * P.N;
+  for (int t = threadIdx.x; t < P.Tn; t += blockDim.x) hist[t] = 0;
+  __syncthreads();
+  float vmax = 0.f;
+  for (int p = threadIdx.x; p < P.N; p += blockDim.x) {
+    const size_t i = base + p;
+    float x[3] = {S.c(0, i), S.c(1, i), S.c(2, i)};
+    int b[3];
+    float fx[3];
+    const int bad = stencil_base(x, P.inv_dx, (double)P.dx, P.dims, b, fx);
+    if (bad >= 0) {
+      report(flags, e, substep, 0, attr_index(S.attr[i]), bad, kErrP2GInterior);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) b[a] = b[a] < 1 ? 1 : (b[a] > P.dims[a] - 4 ? P.dims[a] - 4 : b[a]);
+    }
+    const int key = ((b[0] >> 2) * P.td[1] + (b[1] >> 2)) * P.td[2] + (b[2] >> 2);
+    keys[i] = key;
+    atomicAdd(&hist[key], 1);
+    if (check_vmax) vmax = fmaxf(vmax, fmaxf(fabsf(S.c(3, i)), fmaxf(fabsf(S.c(4, i)), fabsf(S.c(5, i)))));
+  }
+  if (check_vmax) {
+    for (int o = 16; o > 0; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(&flags->vmax_bits, __float_as_uint(vmax));
+  }
+  __syncthreads();
+  // exclusive scan of (count, active) over Tn bins: each thread a contiguous chunk
+  const int nt = blockDim.x;
+  const int per = (P.Tn + nt - 1) / nt;
+  const int t0 = threadIdx.x * per, t1 = min(P.Tn, t0 + per);
+  int sc = 0, sa = 0;
+  for (int t = t0; t < t1; ++t) {
+    sc += hist[t];
+    sa += hist[t] > 0;
+  }
+  // block scan of per-thread sums (warp shuffles + one level)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int ic = sc, ia = sa;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int yc = __shfl_up_sync(0xffffffffu, ic, o);
+    const int ya = __shfl_up_sync(0xffffffffu, ia, o);
+    if (lane >= o) {
+      ic += yc;
+      ia += ya;
+    }
+  }
+  if (lane == 31) {
+    s_part[wid][0] = ic;
+    s_part[wid][1] = ia;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int rc = 0, ra = 0;
+    const int nw = nt / 32;
+    for (int w = 0; w < nw; ++w) {
+      const int c = s_part[w][0], a = s_part[w][1];
+      s_part[w][0] = rc;
+      s_part[w][1] = ra;
+      rc += c;
+      ra += a;
+    }
+    s_part[nw][0] = rc;
+    s_part[nw][1] = ra;
+    s_base = atomicAdd(&flags->active_count, ra);
+    env_abase[e] = s_base;
+    env_acount[e] = ra;
+  }
+  __syncthreads();
+  int oc = s_part[wid][0] + ic - sc, oa = s_part[wid][1] + ia - sa;
+  const size_t tb = (size_t)e * P.Tn;
+  for (int t = t0; t < t1; ++t) {
+    const int c = hist[t];
+    tile_start[tb + t] = oc;
+    tile_count[tb + t] = c;
+    cursor[t] = oc;
+    if (c > 0) {
+      active[s_base + oa] = make_int2(e, t);
+      ++oa;
+    }
+    oc += c;
+  }
+  __syncthreads();
+  // stable scatter (one warp, particles in index order)
+  if (wid == 0) {
+    for (int c0 = 0; c0 < P.N; c0 += 32) {
+      const int p = c0 + lane;
+      const int key = p < P.N ? keys[base + p] : -1 - lane;
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      const int leader = __ffs(peers) - 1;
+      const int rank = __popc(peers & ((1u << lane) - 1u));
+      int pos = 0;
+      if (lane == leader && p < P.N) {
+        pos = cursor[key];
+        cursor[key] = pos + __popc(peers);
+      }
+      pos = __shfl_sync(0xffffffffu, pos, leader);
+      if (p < P.N) perm[base + pos + rank] = (int)(base + p);
+      __syncwarp();
+    }
+  }
+}
+
+// ============================ P2G ============================
+// Per active tile: stage particle payloads (lanes = particles), scatter into
+// the warp's 6^3 shared block (lanes = stencil nodes), write the block.
+template <int MAXC>
+__global__ void __launch_bounds__(kWarps * 32) k_p2g(DevParams P, StateView S, const int* __restrict__ perm,
+                                                     const int* __restrict__ tile_start,
+                                                     const int* __restrict__ tile_count, const int2* __restrict__ active,
+                                                     const float* __restrict__ act, float4* __restrict__ blocks,
+                                                     DevFlags* flags, int substep) {
+  __shared__ float4 blk[kWarps][kExt3];
+  __shared__ float pay[kWarps][32 * kPay];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_active = *(volatile int*)&flags->active_count;
+  const TransferCtx<float> T = tctx(P);
+  const int oi = lane / 9, oj = (lane / 3) % 3, ok = lane % 3;
+  float* pw = pay[warp];
+  float4* bw = blk[warp];
+  for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
+    const int2 et = active[a];
+    const int e = et.x, t = et.y;
+    const int tz = t % P.td[2], ty = (t / P.td[2]) % P.td[1], tx = t / (P.td[2] * P.td[1]);
+    const int o[3] = {tx * kTile, ty * kTile, tz * kTile};
+    const size_t tix = (size_t)e * P.Tn + t;
+    const int start = tile_start[tix], cnt = tile_count[tix];
+    for (int i = lane; i < kExt3; i += 32) bw[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncwarp();
+    for (int c0 = 0; c0 < cnt; c0 += 32) {
+      if (c0 + lane < cnt) {
+        const int src = perm[(size_t)e * P.N + start + c0 + lane];
+        float x[3];
+        v3<float> v;
+        m3<float> F, C;
+        load_state(S, src, x, v, F, C);
+        const uint32_t at = S.attr[src];
+        Stencil<float> sc;
+        make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
+        const Law<float>& L = P.law[attr_mat(at)];
+        const float av = act ? act[e * P.G + attr_group(at)] : 0.f;
+        bool bad = false;
+        const m3<float> A = p2g_affine(L, T, F, C, av, &bad);
+        if (bad) report(flags, e, substep, 0, attr_index(at), attr_mat(at), kErrDetF);
+        v3<float> q;
+        m3<float> Ad;
+        p2g_payload(A, L.mass, v, sc, P.dx, q, Ad);
+        float* pp = pw + lane * kPay;
+        const int lb = (sc.base[0] - o[0]) | ((sc.base[1] - o[1]) << 8) | ((sc.base[2] - o[2]) << 16);
+        pp[0] = __int_as_float(lb);
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          pp[1 + r] = sc.w[0][r];
+          pp[4 + r] = sc.w[1][r];
+          pp[7 + r] = sc.w[2][r];
+        }
+        pp[10] = L.mass;
+        pp[11] = q.x;
+        pp[12] = q.y;
+        pp[13] = q.z;
+#pragma unroll
+        for (int r = 0; r < 9; ++r) pp[14 + r] = Ad.a[r];
+      }
+      __syncwarp();
+      const int nv = min(32, cnt - c0);
+      if (lane < 27) {
+        const float fo_i = (float)oi, fo_j = (float)oj, fo_k = (float)ok;
+        for (int k = 0; k < nv; ++k) {
+          const float* pk = pw + k * kPay;
+          const int lb = __float_as_int(pk[0]);
+          const int nx = (lb & 0xff) + oi, ny = ((lb >> 8) & 0xff) + oj, nz = ((lb >> 16) & 0xff) + ok;
+          const float w = pk[1 + oi] * pk[4 + oj] * pk[7 + ok];
+          const float cx = pk[11] + pk[14] * fo_i + pk[15] * fo_j + pk[16] * fo_k;
+          const float cy = pk[12] + pk[17] * fo_i + pk[18] * fo_j + pk[19] * fo_k;
+          const float cz = pk[13] + pk[20] * fo_i + pk[21] * fo_j + pk[22] * fo_k;
+          const int nd = (nx * kExt + ny) * kExt + nz;
+          float4 b = bw[nd];
+          b.x += w * pk[10];
+          b.y += w * cx;
+          b.z += w * cy;
+          b.w += w * cz;
+          bw[nd] = b;
+          __syncwarp(0x07ffffffu);
+        }
+      }
+      __syncwarp();
+    }
+    float4* dst = blocks + tix * kExt3;
+    for (int i = lane; i < kExt3; i += 32) dst[i] = bw[i];
+    __syncwarp();
+  }
+}
+
+// Sum the blocks covering global node g (ascending tile order); returns
+// whether any active tile covers it, and the first such tile (owner).
+__device__ __forceinline__ float4 gather_node(const DevParams& P, const int* __restrict__ tile_count,
+                                              const float4* __restrict__ blocks, int e, const int tc[3], const int g[3],
+                                              int* owner) {
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  *owner = -1;
+  for (int sx = tc[0] - 1; sx <= tc[0] + 1; ++sx) {
+    const int lx = g[0] - sx * kTile;
+    if (sx < 0 || sx >= P.td[0] || lx < 0 || lx >= kExt) continue;
+    for (int sy = tc[1] - 1; sy <= tc[1] + 1; ++sy) {
+      const int ly = g[1] - sy * kTile;
+      if (sy < 0 || sy >= P.td[1] || ly < 0 || ly >= kExt) continue;
+      for (int sz = tc[2] - 1; sz <= tc[2] + 1; ++sz) {
+        const int lz = g[2] - sz * kTile;
+        if (sz < 0 || sz >= P.td[2] || lz < 0 || lz >= kExt) continue;
+        const int st = (sx * P.td[1] + sy) * P.td[2] + sz;
+        const size_t six = (size_t)e * P.Tn + st;
+        if (tile_count[six] == 0) continue;
+        if (*owner < 0) *owner = st;
+        const float4 b = blocks[six * kExt3 + (lx * kExt + ly) * kExt + lz];
+        acc.x += b.x;
+        acc.y += b.y;
+        acc.z += b.z;
+        acc.w += b.w;
+      }
+    }
+  }
+  return acc;
+}
+
+// ============================ G2P ============================
+template <int MAXC>
+__global__ void __launch_bounds__(kWarps * 32) k_g2p(DevParams P, StateView S, StateView Sout,
+                                                     const int* __restrict__ perm, const int* __restrict__ tile_start,
+                                                     const int* __restrict__ tile_count, const int2* __restrict__ active,
+                                                     const float* __restrict__ cvo, const float4* __restrict__ blocks,
+                                                     DevFlags* flags, int substep) {
+  __shared__ float4 vg[kWarps][kExt3];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_active = *(volatile int*)&flags->active_count;
+  const TransferCtx<float> T = tctx(P);
+  const NodeCtx<float> G = nctx(P);
+  float4* vw = vg[warp];
+  for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
+    const int2 et = active[a];
+    const int e = et.x, t = et.y;
+    const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
+    const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
+    Col<float> cols[MAXC];
+    load_cols<MAXC>(P, cvo + (size_t)e * P.K * 9, cols);
+    for (int i = lane; i < kExt3; i += 32) {
+      const int g[3] = {o[0] + i / 36, o[1] + (i / 6) % 6, o[2] + i % 6};
+      v3<float> v = zero3<float>();
+      if (g[0] < P.dims[0] && g[1] < P.dims[1] && g[2] < P.dims[2]) {
+        int own;
+        const float4 mm = gather_node(P, tile_count, blocks, e, tc, g, &own);
+        v = node_update<float, MAXC>(G, cols, P.K, g, mm.x, mk3(mm.y, mm.z, mm.w));
+      }
+      vw[i] = make_float4(v.x, v.y, v.z, 0.f);
+    }
+    __syncwarp();
+    const size_t tix = (size_t)e * P.Tn + t;
+    const int start = tile_start[tix], cnt = tile_count[tix];
+    for (int c0 = lane; c0 < cnt; c0 += 32) {
+      const size_t dst = (size_t)e * P.N + start + c0;
+      const int src = perm[dst];
+      float x[3];
+      v3<float> v;
+      m3<float> F, C;
+      load_state(S, src, x, v, F, C);
+      const uint32_t at = S.attr[src];
+      Stencil<float> sc;
+      make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
+      const int lb[3] = {sc.base[0] - o[0], sc.base[1] - o[1], sc.base[2] - o[2]};
+      auto getv = [&](int i, int j, int k) {
+        const float4 q = vw[((lb[0] + i) * kExt + (lb[1] + j)) * kExt + lb[2] + k];
+        return mk3(q.x, q.y, q.z);
+      };
+      v3<float> xn = mk3(x[0], x[1], x[2]);
+      bool bad_adv = false, bad_det = false;
+      g2p_particle(P.law[attr_mat(at)], T, sc, getv, xn, v, C, F, &bad_adv, &bad_det);
+      if (bad_adv) report(flags, e, substep, 1, attr_index(at), 0, kErrG2PInterior);
+      if (bad_det) report(flags, e, substep, 1, attr_index(at), attr_mat(at), kErrDetF);
+      store_state(Sout, dst, xn, v, F, C);
+      Sout.attr[dst] = at;
+    }
+    __syncwarp();
+  }
+}
+
+// ============================ G2P adjoint ============================
+// Reads the start-of-substep state (via perm) and the cotangent of the
+// end-of-substep state (sorted position); writes particle-side partial
+// cotangents (sorted position) and a 6^3 block of node-velocity cotangents.
+template <int MAXC>
+__global__ void __launch_bounds__(kWarps * 32) k_g2p_adj(DevParams P, StateView S, const float* __restrict__ adj_in,
+                                                         size_t astride, const int* __restrict__ perm,
+                                                         const int* __restrict__ tile_start,
+                                                         const int* __restrict__ tile_count,
+                                                         const int2* __restrict__ active, const float* __restrict__ cvo,
+                                                         const float4* __restrict__ blocks, float4* __restrict__ ablocks,
+                                                         float* __restrict__ part, float* __restrict__ tile_acc,
+                                                         const DevFlags* flags) {
+  __shared__ float4 vg[kWarps][kExt3];
+  __shared__ float4 ab[kWarps][kExt3];
+  __shared__ float pay[kWarps][32 * kPay];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const TransferCtx<float> T = tctx(P);
+  const NodeCtx<float> G = nctx(P);
+  float4* vw = vg[warp];
+  float4* aw = ab[warp];
+  float* pw = pay[warp];
+  const int oi = lane / 9, oj = (lane / 3) % 3, ok = lane % 3;
+  const int n_active = *(const volatile int*)&flags->active_count;
+  for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
+    const int2 et = active[a];
+    const int e = et.x, t = et.y;
+    const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
+    const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
+    Col<float> cols[MAXC];
+    load_cols<MAXC>(P, cvo + (size_t)e * P.K * 9, cols);
+    for (int i = lane; i < kExt3; i += 32) {
+      const int g[3] = {o[0] + i / 36, o[1] + (i / 6) % 6, o[2] + i % 6};
+      v3<float> v = zero3<float>();
+      if (g[0] < P.dims[0] && g[1] < P.dims[1] && g[2] < P.dims[2]) {
+        int own;
+        const float4 mm = gather_node(P, tile_count, blocks, e, tc, g, &own);
+        v = node_update<float, MAXC>(G, cols, P.K, g, mm.x, mk3(mm.y, mm.z, mm.w));
+      }
+      vw[i] = make_float4(v.x, v.y, v.z, 0.f);
+      aw[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncwarp();
+    const size_t tix = (size_t)e * P.Tn + t;
+    const int start = tile_start[tix], cnt = tile_count[tix];
+    float mub[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int c0 = 0; c0 < cnt; c0 += 32) {
+      if (c0 + lane < cnt) {
+        const size_t dst = (size_t)e * P.N + start + c0 + lane;
+        const int src = perm[dst];
+        float x[3];
+        v3<float> v;
+        m3<float> F, C;
+        load_state(S, src, x, v, F, C);
+        const uint32_t at = S.attr[src];
+        Stencil<float> sc;
+        make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
+        const int lb[3] = {sc.base[0] - o[0], sc.base[1] - o[1], sc.base[2] - o[2]};
+        auto getv = [&](int i, int j, int k) {
+          const float4 q = vw[((lb[0] + i) * kExt + (lb[1] + j)) * kExt + lb[2] + k];
+          return mk3(q.x, q.y, q.z);
+        };
+        v3<float> xb = mk3(adj_in[0 * astride + dst], adj_in[1 * astride + dst], adj_in[2 * astride + dst]);
+        v3<float> vb = mk3(adj_in[3 * astride + dst], adj_in[4 * astride + dst], adj_in[5 * astride + dst]);
+        m3<float> Fb, Cb;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+          Fb.a[q] = adj_in[(6 + q) * astride + dst];
+          Cb.a[q] = adj_in[(15 + q) * astride + dst];
+        }
+        v3<float> xp, gq;
+        m3<float> Fp, Bd;
+        const int mi = attr_mat(at);
+        float mu_l = 0.f;
+        g2p_vjp(P.law[mi], T, sc, getv, F, xb, vb, Cb, Fb, xp, Fp, gq, Bd, mu_l);
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+          if (m == mi) mub[m] += mu_l;
+        part[0 * astride + dst] = xp.x;
+        part[1 * astride + dst] = xp.y;
+        part[2 * astride + dst] = xp.z;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) part[(3 + q) * astride + dst] = Fp.a[q];
+        float* pp = pw + lane * kPay;
+        pp[0] = __int_as_float(lb[0] | (lb[1] << 8) | (lb[2] << 16));
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          pp[1 + r] = sc.w[0][r];
+          pp[4 + r] = sc.w[1][r];
+          pp[7 + r] = sc.w[2][r];
+        }
+        pp[11] = gq.x;
+        pp[12] = gq.y;
+        pp[13] = gq.z;
+#pragma unroll
+        for (int r = 0; r < 9; ++r) pp[14 + r] = Bd.a[r];
+      }
+      __syncwarp();
+      const int nv = min(32, cnt - c0);
+      if (lane < 27) {
+        const float fo_i = (float)oi, fo_j = (float)oj, fo_k = (float)ok;
+        for (int k = 0; k < nv; ++k) {
+          const float* pk = pw + k * kPay;
+          const int lb = __float_as_int(pk[0]);
+          const int nx = (lb & 0xff) + oi, ny = ((lb >> 8) & 0xff) + oj, nz = ((lb >> 16) & 0xff) + ok;
+          const float w = pk[1 + oi] * pk[4 + oj] * pk[7 + ok];
+          const int nd = (nx * kExt + ny) * kExt + nz;
+          float4 b = aw[nd];
+          b.x += w * (pk[11] + pk[14] * fo_i + pk[15] * fo_j + pk[16] * fo_k);
+          b.y += w * (pk[12] + pk[17] * fo_i + pk[18] * fo_j + pk[19] * fo_k);
+          b.z += w * (pk[13] + pk[20] * fo_i + pk[21] * fo_j + pk[22] * fo_k);
+          aw[nd] = b;
+          __syncwarp(0x07ffffffu);
+        }
+      }
+      __syncwarp();
+    }
+    float4* dst = ablocks + tix * kExt3;
+    for (int i = lane; i < kExt3; i += 32) dst[i] = aw[i];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+      for (int off = 16; off > 0; off >>= 1) mub[m] += __shfl_xor_sync(0xffffffffu, mub[m], off);
+    if (lane == 0)
+#pragma unroll
+      for (int m = 0; m < 4; ++m) tile_acc[tix * kNacc + kAccMuG + m] = mub[m];
+    __syncwarp();
+  }
+}
+
+// ============================ P2G adjoint ============================
+template <int MAXC, int NG>
+__global__ void __launch_bounds__(kWarps * 32) k_p2g_adj(DevParams P, StateView S, const int* __restrict__ perm,
+                                                         const int* __restrict__ tile_start,
+                                                         const int* __restrict__ tile_count,
+                                                         const int2* __restrict__ active, const float* __restrict__ cvo,
+                                                         const float* __restrict__ act,
+                                                         const float4* __restrict__ blocks,
+                                                         const float4* __restrict__ ablocks,
+                                                         const float* __restrict__ part, float* __restrict__ adj_out,
+                                                         size_t astride, float* __restrict__ tile_acc,
+                                                         const DevFlags* flags) {
+  __shared__ float4 mb[kWarps][kExt3];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const TransferCtx<float> T = tctx(P);
+  const NodeCtx<float> G = nctx(P);
+  float4* bw = mb[warp];
+  const int n_active = *(const volatile int*)&flags->active_count;
+  for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
+    const int2 et = active[a];
+    const int e = et.x, t = et.y;
+    const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
+    const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
+    Col<float> cols[MAXC];
+    load_cols<MAXC>(P, cvo + (size_t)e * P.K * 9, cols);
+    float cg[MAXC * 9];
+#pragma unroll
+    for (int q = 0; q < MAXC * 9; ++q) cg[q] = 0.f;
+    for (int i = lane; i < kExt3; i += 32) {
+      const int g[3] = {o[0] + i / 36, o[1] + (i / 6) % 6, o[2] + i % 6};
+      float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (g[0] < P.dims[0] && g[1] < P.dims[1] && g[2] < P.dims[2]) {
+        int own, own2;
+        const float4 mm = gather_node(P, tile_count, blocks, e, tc, g, &own);
+        const float4 vb = gather_node(P, tile_count, ablocks, e, tc, g, &own2);
+        float mbar;
+        v3<float> pbar;
+        float cgl[MAXC * 9];
+#pragma unroll
+        for (int q = 0; q < MAXC * 9; ++q) cgl[q] = 0.f;
+        node_update_vjp<float, MAXC>(G, cols, P.K, g, mm.x, mk3(mm.y, mm.z, mm.w), mk3(vb.x, vb.y, vb.z), mbar,
+                                     pbar, cgl);
+        if (own == t)
+#pragma unroll
+          for (int q = 0; q < MAXC * 9; ++q) cg[q] += cgl[q];
+        out = make_float4(mbar, pbar.x, pbar.y, pbar.z);
+      }
+      bw[i] = out;
+    }
+    __syncwarp();
+    const size_t tix = (size_t)e * P.Tn + t;
+    const int start = tile_start[tix], cnt = tile_count[tix];
+    float mub[4] = {0.f, 0.f, 0.f, 0.f}, lab[4] = {0.f, 0.f, 0.f, 0.f};
+    float actb[NG];
+#pragma unroll
+    for (int q = 0; q < NG; ++q) actb[q] = 0.f;
+    for (int c0 = lane; c0 < cnt; c0 += 32) {
+      const size_t j = (size_t)e * P.N + start + c0;
+      const int src = perm[j];
+      float x[3];
+      v3<float> v;
+      m3<float> F, C;
+      load_state(S, src, x, v, F, C);
+      const uint32_t at = S.attr[src];
+      Stencil<float> sc;
+      make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
+      const int lb[3] = {sc.base[0] - o[0], sc.base[1] - o[1], sc.base[2] - o[2]};
+      auto getmb = [&](int i, int jj, int k, float& m_, v3<float>& p_) {
+        const float4 q = bw[((lb[0] + i) * kExt + (lb[1] + jj)) * kExt + lb[2] + k];
+        m_ = q.x;
+        p_ = mk3(q.y, q.z, q.w);
+      };
+      v3<float> xb = mk3(part[0 * astride + j], part[1 * astride + j], part[2 * astride + j]);
+      m3<float> Fb, Cb = mzero<float>();
+#pragma unroll
+      for (int q = 0; q < 9; ++q) Fb.a[q] = part[(3 + q) * astride + j];
+      v3<float> vb = zero3<float>();
+      const int mi = attr_mat(at), gi = attr_group(at);
+      const float av = act ? act[e * P.G + gi] : 0.f;
+      float mu_l = 0.f, la_l = 0.f, ac_l = 0.f;
+      p2g_vjp(P.law[mi], T, sc, getmb, v, F, C, av, xb, vb, Fb, Cb, mu_l, la_l, ac_l);
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        if (m == mi) {
+          mub[m] += mu_l;
+          lab[m] += la_l;
+        }
+#pragma unroll
+      for (int q = 0; q < NG; ++q)
+        if (q == gi) actb[q] += ac_l;
+      adj_out[0 * astride + src] = xb.x;
+      adj_out[1 * astride + src] = xb.y;
+      adj_out[2 * astride + src] = xb.z;
+      adj_out[3 * astride + src] = vb.x;
+      adj_out[4 * astride + src] = vb.y;
+      adj_out[5 * astride + src] = vb.z;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        adj_out[(6 + q) * astride + src] = Fb.a[q];
+        adj_out[(15 + q) * astride + src] = Cb.a[q];
+      }
+    }
+    // warp reductions (fixed butterfly order -> deterministic)
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+      for (int off = 16; off > 0; off >>= 1) {
+        mub[m] += __shfl_xor_sync(0xffffffffu, mub[m], off);
+        lab[m] += __shfl_xor_sync(0xffffffffu, lab[m], off);
+      }
+#pragma unroll
+    for (int q = 0; q < NG; ++q)
+      for (int off = 16; off > 0; off >>= 1) actb[q] += __shfl_xor_sync(0xffffffffu, actb[q], off);
+#pragma unroll
+    for (int q = 0; q < MAXC * 9; ++q)
+      for (int off = 16; off > 0; off >>= 1) cg[q] += __shfl_xor_sync(0xffffffffu, cg[q], off);
+    if (lane == 0) {
+      float* ta = tile_acc + tix * kNacc;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        ta[kAccMu + m] = mub[m];
+        ta[kAccLam + m] = lab[m];
+      }
+#pragma unroll
+      for (int q = 0; q < MAXC * 9; ++q) ta[kAccCol + q] = cg[q];
+#pragma unroll
+      for (int q = 0; q < NG; ++q) ta[kAccAct + q] = actb[q];
+    }
+    __syncwarp();
+  }
+}
+
+// Per env: sum the env's tile accumulators in tile order into the step's
+// (double) parameter cotangents.
+__global__ void k_env_reduce(DevParams P, const int2* __restrict__ active, const int* __restrict__ env_abase,
+                             const int* __restrict__ env_acount, const float* __restrict__ tile_acc,
+                             double* __restrict__ gcvo_t, double* __restrict__ gact_t, double* __restrict__ gmu,
+                             double* __restrict__ glam) {
+  const int e = blockIdx.x, f = threadIdx.x;
+  if (f >= kNacc) return;
+  const int b = env_abase[e], n = env_acount[e];
+  float s = 0.f;
+  for (int i = 0; i < n; ++i) {
+    const int2 et = active[b + i];
+    s += tile_acc[((size_t)et.x * P.Tn + et.y) * kNacc + f];
+  }
+  if (f < 4) {
+    if (f < P.nmat) gmu[e * 4 + f] += s;
+  } else if (f < 8) {
+    if (f - 4 < P.nmat) glam[e * 4 + f - 4] += s;
+  } else if (f < 12) {
+    if (f - 8 < P.nmat) gmu[e * 4 + f - 8] += s;
+  } else if (f < 48) {
+    const int q = f - 12;
+    if (q < P.K * 9) gcvo_t[(size_t)e * P.K * 9 + q] += s;
+  } else {
+    const int q = f - 48;
+    if (q < P.G) gact_t[(size_t)e * P.G + q] += s;
+  }
+}
+
+// ============================ observables ============================
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  const int nw = blockDim.x >> 5;
+  for (int w = 0; w < nw; ++w) r += sh[w];
+  return r;
+}
+
+// com(3), var(3), spill(1) per env (tasks.hpp:286-304, 604-615); fp64 sums
+// in a fixed order (deterministic).
+__global__ void __launch_bounds__(256) k_obs(DevParams P, StateView S, const float* __restrict__ cvo, float spill_half,
+                                             float spill_temp, float* __restrict__ obs) {
+  __shared__ double sh[8];
+  const int e = blockIdx.x;
+  const size_t base = (size_t)e * P.N;
+  double s[3] = {0.0, 0.0, 0.0};
+  for (int p = threadIdx.x; p < P.N; p += blockDim.x)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) s[a] += (double)S.c(a, base + p);
+  double m[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) m[a] = block_sum(s[a], sh) / P.N;
+  double q[3] = {0.0, 0.0, 0.0}, sp = 0.0;
+  const bool spill = P.K > 0 && spill_temp > 0.f;
+  const double cx = spill ? cvo[(size_t)e * P.K * 9 + 0] : 0.0, cy = spill ? cvo[(size_t)e * P.K * 9 + 1] : 0.0;
+  for (int p = threadIdx.x; p < P.N; p += blockDim.x) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double d = (double)S.c(a, base + p) - m[a];
+      q[a] += d * d;
+    }
+    if (spill) {
+      const double sd = fmax(fabs((double)S.c(0, base + p) - cx), fabs((double)S.c(1, base + p) - cy)) - spill_half;
+      sp += 1.0 / (1.0 + exp(-sd / spill_temp));
+    }
+  }
+  double v[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) v[a] = block_sum(q[a], sh) / P.N;
+  const double spt = block_sum(sp, sh) / P.N;
+  if (threadIdx.x == 0) {
+    float* o = obs + (size_t)e * 7;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      o[a] = (float)m[a];
+      o[3 + a] = (float)v[a];
+    }
+    o[6] = (float)spt;
+  }
+}
+
+// Adds the observable cotangent into the state cotangent (physical order of
+// that state) and the spill's collider-center cotangent into gcvo_t.
+__global__ void __launch_bounds__(256) k_obs_adj(DevParams P, StateView S, const float* __restrict__ cvo,
+                                                 float spill_half, float spill_temp, const float* __restrict__ dobs,
+                                                 float* __restrict__ adj, size_t astride, double* __restrict__ gcvo_t) {
+  __shared__ double sh[8];
+  const int e = blockIdx.x;
+  const size_t base = (size_t)e * P.N;
+  const float* ob = dobs + (size_t)e * 7;
+  double s[3] = {0.0, 0.0, 0.0};
+  for (int p = threadIdx.x; p < P.N; p += blockDim.x)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) s[a] += (double)S.c(a, base + p);
+  double m[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) m[a] = block_sum(s[a], sh) / P.N;
+  const bool spill = P.K > 0 && spill_temp > 0.f && ob[6] != 0.f;
+  const double cx = spill ? cvo[(size_t)e * P.K * 9 + 0] : 0.0, cy = spill ? cvo[(size_t)e * P.K * 9 + 1] : 0.0;
+  double gcx = 0.0, gcy = 0.0;
+  const double invn = 1.0 / P.N;
+  for (int p = threadIdx.x; p < P.N; p += blockDim.x) {
+    double g[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) g[a] = ob[a] * invn + ob[3 + a] * 2.0 * ((double)S.c(a, base + p) - m[a]) * invn;
+    if (spill) {
+      const double dxp = (double)S.c(0, base + p) - cx, dyp = (double)S.c(1, base + p) - cy;
+      const double ax = fabs(dxp), ay = fabs(dyp);
+      const double sd = fmax(ax, ay) - spill_half;
+      const double sg = 1.0 / (1.0 + exp(-sd / spill_temp));
+      const double gg = ob[6] * invn * sg * (1.0 - sg) / spill_temp;
+      if (ax > ay) {
+        const double sgn = dxp > 0 ? 1.0 : (dxp < 0 ? -1.0 : 0.0);
+        g[0] += gg * sgn;
+        gcx -= gg * sgn;
+      } else if (ay > ax) {
+        const double sgn = dyp > 0 ? 1.0 : (dyp < 0 ? -1.0 : 0.0);
+        g[1] += gg * sgn;
+        gcy -= gg * sgn;
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) adj[a * astride + base + p] += (float)g[a];
+  }
+  if (spill) {
+    gcx = block_sum(gcx, sh);
+    gcy = block_sum(gcy, sh);
+    if (threadIdx.x == 0) {
+      gcvo_t[(size_t)e * P.K * 9 + 0] += gcx;
+      gcvo_t[(size_t)e * P.K * 9 + 1] += gcy;
+    }
+  }
+}
+
+// ============================ layout conversion ============================
+// host visit order (AoS per env) <-> SoA physical order
+__global__ void k_aos_to_soa(int Ntot, const float* __restrict__ x, const float* __restrict__ v,
+                             const float* __restrict__ F, const float* __restrict__ C, const int* __restrict__ mat,
+                             const int* __restrict__ grp, int N, StateView S) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= (size_t)Ntot) return;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    S.c(a, i) = x[3 * i + a];
+    S.c(3 + a, i) = v[3 * i + a];
+  }
+#pragma unroll
+  for (int q = 0; q < 9; ++q) {
+    S.c(6 + q, i) = F[9 * i + q];
+    S.c(15 + q, i) = C[9 * i + q];
+  }
+  const uint32_t idx = (uint32_t)(i % N);
+  const uint32_t m = mat ? (uint32_t)mat[i] : 0u, g = grp ? (uint32_t)grp[i] : 0u;
+  S.attr[i] = idx | ((m & 0xF) << 20) | ((g & 0xFF) << 24);
+}
+
+// physical SoA -> canonical AoS (original order within each env)
+__global__ void k_soa_to_aos(int Ntot, int N, const float* __restrict__ f, const uint32_t* __restrict__ attr,
+                             size_t stride, float* __restrict__ x, float* __restrict__ v, float* __restrict__ F,
+                             float* __restrict__ C) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= (size_t)Ntot) return;
+  const size_t e = i / N;
+  const size_t o = e * N + (attr[i] & 0xFFFFFu);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (x) x[3 * o + a] = f[a * stride + i];
+    if (v) v[3 * o + a] = f[(3 + a) * stride + i];
+  }
+#pragma unroll
+  for (int q = 0; q < 9; ++q) {
+    if (F) F[9 * o + q] = f[(6 + q) * stride + i];
+    if (C) C[9 * o + q] = f[(15 + q) * stride + i];
+  }
+}
+
+// canonical AoS cotangent -> physical SoA order of the state with attributes attr
+__global__ void k_aos_to_soa_perm(int Ntot, int N, const float* __restrict__ x, const float* __restrict__ v,
+                                  const float* __restrict__ F, const float* __restrict__ C,
+                                  const uint32_t* __restrict__ attr, float* __restrict__ f, size_t stride) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= (size_t)Ntot) return;
+  const size_t e = i / N;
+  const size_t o = e * N + (attr[i] & 0xFFFFFu);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    f[a * stride + i] = x ? x[3 * o + a] : 0.f;
+    f[(3 + a) * stride + i] = v ? v[3 * o + a] : 0.f;
+  }
+#pragma unroll
+  for (int q = 0; q < 9; ++q) {
+    f[(6 + q) * stride + i] = F ? F[9 * o + q] : 0.f;
+    f[(15 + q) * stride + i] = C ? C[9 * o + q] : 0.f;
+  }
+}
+
+}  // namespace dm
