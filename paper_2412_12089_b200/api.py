@@ -211,6 +211,10 @@ class MpmBatch:
                                                     _ptr(group)))
             return
         arrs = [_f32(x), _f32(v), _f32(F), _f32(C_), _i32(material), _i32(group)]
+        if arrs[4] is not None and (arrs[4].min() < 0 or arrs[4].max() >= self.n_materials):
+            raise ValueError("set_state: material id out of range")
+        if arrs[5] is not None and self.G > 0 and (arrs[5].min() < 0 or arrs[5].max() >= self.G):
+            raise ValueError("set_state: actuation group out of range")
         self._keep = arrs
         self._check(self._L.dm_set_state(self._h, *(_ptr(a) for a in arrs)))
 

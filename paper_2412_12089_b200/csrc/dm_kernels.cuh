@@ -64,7 +64,7 @@ struct DevFlags {
 };
 
 __device__ __forceinline__ uint32_t attr_index(uint32_t a) { return a & 0xFFFFFu; }
-__device__ __forceinline__ int attr_mat(uint32_t a) { return (a >> 20) & 0xF; }
+__device__ __forceinline__ int attr_mat(uint32_t a) { return (a >> 20) & 0x3; }
 __device__ __forceinline__ int attr_group(uint32_t a) { return (a >> 24) & 0xFF; }
 
 // error key: env(16) | substep(10) | stage(2) | particle(24) | axis(2) | code(4)
@@ -75,6 +75,14 @@ __device__ __forceinline__ void report(DevFlags* fl, int env, int sub, int stage
                                ((unsigned long long)(particle & 0xFFFFFF) << 6) | ((unsigned long long)(axis & 3) << 4) |
                                (unsigned long long)(code & 0xF);
   atomicMin(&fl->err_key, k);
+}
+
+// Local base inside the tile, in [0, 4).  Always in range for valid particles
+// (the bin key comes from the same fp32 base); clamped for particles already
+// reported outside the interior so shared-memory indices stay in bounds.
+__device__ __forceinline__ int tile_local(int base, int origin) {
+  const int l = base - origin;
+  return l < 0 ? 0 : (l > kTile - 1 ? kTile - 1 : l);
 }
 
 __device__ __forceinline__ TransferCtx<float> tctx(const DevParams& P) {
@@ -299,7 +307,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_p2g(DevParams P, StateView S, c
         Stencil<float> sc;
         make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
         const Law<float>& L = P.law[attr_mat(at)];
-        const float av = act ? act[e * P.G + attr_group(at)] : 0.f;
+        const float av = act ? act[e * P.G + min(attr_group(at), P.G - 1)] : 0.f;
         bool bad = false;
         const m3<float> A = p2g_affine(L, T, F, C, av, &bad);
         if (bad) report(flags, e, substep, 0, attr_index(at), attr_mat(at), kErrDetF);
@@ -307,7 +315,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_p2g(DevParams P, StateView S, c
         m3<float> Ad;
         p2g_payload(A, L.mass, v, sc, P.dx, q, Ad);
         float* pp = pw + lane * kPay;
-        const int lb = (sc.base[0] - o[0]) | ((sc.base[1] - o[1]) << 8) | ((sc.base[2] - o[2]) << 16);
+        const int lb = tile_local(sc.base[0], o[0]) | (tile_local(sc.base[1], o[1]) << 8) | (tile_local(sc.base[2], o[2]) << 16);
         pp[0] = __int_as_float(lb);
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
@@ -426,7 +434,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_g2p(DevParams P, StateView S, S
       const uint32_t at = S.attr[src];
       Stencil<float> sc;
       make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
-      const int lb[3] = {sc.base[0] - o[0], sc.base[1] - o[1], sc.base[2] - o[2]};
+      const int lb[3] = {tile_local(sc.base[0], o[0]), tile_local(sc.base[1], o[1]), tile_local(sc.base[2], o[2])};
       auto getv = [&](int i, int j, int k) {
         const float4 q = vw[((lb[0] + i) * kExt + (lb[1] + j)) * kExt + lb[2] + k];
         return mk3(q.x, q.y, q.z);
@@ -500,7 +508,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_g2p_adj(DevParams P, StateView 
         const uint32_t at = S.attr[src];
         Stencil<float> sc;
         make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
-        const int lb[3] = {sc.base[0] - o[0], sc.base[1] - o[1], sc.base[2] - o[2]};
+        const int lb[3] = {tile_local(sc.base[0], o[0]), tile_local(sc.base[1], o[1]), tile_local(sc.base[2], o[2])};
         auto getv = [&](int i, int j, int k) {
           const float4 q = vw[((lb[0] + i) * kExt + (lb[1] + j)) * kExt + lb[2] + k];
           return mk3(q.x, q.y, q.z);
@@ -638,7 +646,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_p2g_adj(DevParams P, StateView 
       const uint32_t at = S.attr[src];
       Stencil<float> sc;
       make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
-      const int lb[3] = {sc.base[0] - o[0], sc.base[1] - o[1], sc.base[2] - o[2]};
+      const int lb[3] = {tile_local(sc.base[0], o[0]), tile_local(sc.base[1], o[1]), tile_local(sc.base[2], o[2])};
       auto getmb = [&](int i, int jj, int k, float& m_, v3<float>& p_) {
         const float4 q = bw[((lb[0] + i) * kExt + (lb[1] + jj)) * kExt + lb[2] + k];
         m_ = q.x;
@@ -649,7 +657,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_p2g_adj(DevParams P, StateView 
 #pragma unroll
       for (int q = 0; q < 9; ++q) Fb.a[q] = part[(3 + q) * astride + j];
       v3<float> vb = zero3<float>();
-      const int mi = attr_mat(at), gi = attr_group(at);
+      const int mi = attr_mat(at), gi = min(attr_group(at), P.G > 0 ? P.G - 1 : 0);
       const float av = act ? act[e * P.G + gi] : 0.f;
       float mu_l = 0.f, la_l = 0.f, ac_l = 0.f;
       p2g_vjp(P.law[mi], T, sc, getmb, v, F, C, av, xb, vb, Fb, Cb, mu_l, la_l, ac_l);

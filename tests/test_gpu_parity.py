@@ -31,11 +31,14 @@ COLS = {
     "none": [],
     "plane": [{"kind": "plane", "center": (0, 0, 0.42), "normal": (0, 0, 1), "velocity": (0, 0, 0.1)}],
     "sphere": [{"kind": "sphere", "center": (0.5, 0.5, 0.66), "radius": 0.08, "velocity": (0.1, 0, -0.3)}],
-    "box": [{"kind": "box", "center": (0.35, 0.5, 0.5), "half": (0.05, 0.1, 0.05), "velocity": (0.3, 0, 0)}],
-    "cylinder": [{"kind": "cylinder", "normal": (0, 1, 0), "radius": 0.05, "length": 0.3,
-                  "center": (0.5, 0.5, 0.6), "velocity": (0.1, 0, -0.3), "omega": (0, 5, 0)}],
-    "hollow_box": [{"kind": "hollow_box", "half": (0.1, 0.1, 0.1), "thickness": 0.1, "center": (0.5, 0.5, 0.45),
-                    "velocity": (0.2, -0.1, 0.05)}],
+    "box": [{"kind": "box", "center": (0.3513, 0.5021, 0.4987), "half": (0.0511, 0.1013, 0.0493),
+             "velocity": (0.3, 0, 0)}],
+    # off-lattice geometry: no grid node sits on an SDF branch tie (the
+    # inside-normal switch is discontinuous by design, mpm.hpp:114-122)
+    "cylinder": [{"kind": "cylinder", "normal": (0, 1, 0), "radius": 0.0513, "length": 0.3107,
+                  "center": (0.5031, 0.4987, 0.6029), "velocity": (0.1, 0, -0.3), "omega": (0, 5, 0)}],
+    "hollow_box": [{"kind": "hollow_box", "half": (0.1013, 0.0987, 0.1021), "thickness": 0.0911,
+                    "center": (0.5017, 0.4983, 0.4529), "velocity": (0.2, -0.1, 0.05)}],
 }
 
 
