@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""Benchmark: batched differentiable MLS-MPM, forward + backward.
+
+Metric (BASELINE.json): particle-substeps/s of forward + full adjoint over a
+checkpointed substep tape.  Default workload = config 4 (FluidMove-like:
+1,024 envs x 16,384 particles, 48^3 grid, 16 control steps x 32 substeps),
+the configuration BASELINE.json shards over 1/2/4/8 GPUs (strong scaling:
+the 1,024 envs are split across ranks, no simulator collective).
+
+One step = one whole rollout: set the initial state, 16 recorded control
+steps (512 substeps), loss over the per-step observables, backward through
+all 512 substeps (per-control-step recompute segments, algo.hpp:79-104)
+down to the initial state, collider kinematics and Young's modulus.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`value`  : device-resident inputs (torch CUDA tensors through the *_device ABI).
+`e2e`    : the same rollout through the host-pointer C ABI from pinned host
+           memory, H2D of the initial state / per-step kinematics / dobs and
+           D2H of observations and all cotangents inside the timed region.
+`--impl reference`: the reference's own CPU implementation
+           (oracle/_ref/libref.so = /root/reference headers compiled
+           unchanged: mpm_step<Value> + Tape with per-substep checkpoint
+           segments) on a bounded sample of the same workload, all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle-substeps/s fwd+bwd"
+UNIT = "particle-substeps/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", type=int, default=4)
+    p.add_argument("--envs", type=int, default=0, help="override total envs (default: the config's)")
+    p.add_argument("--ctrl", type=int, default=0, help="override control steps")
+    p.add_argument("--checkpoint-every", type=int, default=-1)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--profile-out", default="")
+    return p.parse_args()
+
+
+# ---------------- distributed plumbing ----------------
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def init_dist(world, local):
+    if world <= 1:
+        return None
+    import torch
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    backend = "nccl" if torch.cuda.is_available() else "gloo"
+    if backend == "nccl":
+        torch.cuda.set_device(local)
+    dist.init_process_group(backend)
+    return dist
+
+
+def max_over_ranks(dist, value: float) -> float:
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+# ---------------- clocks ----------------
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([c.strip() for c in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------- reference CPU arm ----------------
+
+def reference_sample(scene, n_threads: int, n_sub: int = 1):
+    """The reference's own CPU path (mpm_step<Value> + Tape, per-substep
+    checkpoint segments, restated step_checkpointed) on n_threads envs of the
+    scene in parallel (one tape per worker, tape.hpp:78-79).  Fluid law with
+    lambda = the config's bulk modulus and the container as plane walls +
+    floor (the reference has no hollow-box SDF or viscosity; the
+    particle-substep cost is the same transfer/tape work).
+    Returns (particle-substeps, wall seconds, sample description)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as O
+    mat = dict(scene.materials[0])
+    if mat["kind"] == "fluid":
+        nu = mat.get("nu", 0.3)
+        lam = mat.get("bulk", 0.0) or mat["E"] * nu / ((1 + nu) * (1 - 2 * nu))
+        mat = dict(mat, E=lam * (1 + nu) * (1 - 2 * nu) / nu, bulk=0.0, viscosity=0.0)
+    elif mat["kind"] not in ("elastoplastic", "fluid"):
+        mat = dict(mat, kind="elastoplastic", yield_stress=1e9)
+    cvo, _ = scene.cvo_act()
+    results = [None] * n_threads
+    sim = dict(scene.sim, boundary="slip")
+
+    def work(i):
+        e = i % scene.n_envs
+        c = cvo[e, 0, 0, 0:3] if scene.colliders else np.array([0.5, 0.5, 0.3])
+        h = scene.colliders[0].get("half", (0.15, 0.15, 0.15)) if scene.colliders else (0.15, 0.15, 0.15)
+        cols = [{"kind": "plane", "center": (c[0] - h[0], 0, 0), "normal": (1, 0, 0)},
+                {"kind": "plane", "center": (c[0] + h[0], 0, 0), "normal": (-1, 0, 0)},
+                {"kind": "plane", "center": (0, c[1] - h[1], 0), "normal": (0, 1, 0)},
+                {"kind": "plane", "center": (0, c[1] + h[1], 0), "normal": (0, -1, 0)}]
+        st = scene.env_state(e)
+        t0 = time.perf_counter()
+        O.ref_grad(sim, [mat], cols, st, n_sub, (0.55, 0.5, 0.2), seg=1)
+        results[i] = time.perf_counter() - t0
+
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(n_threads)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    wall = time.perf_counter() - t0
+    units = n_threads * scene.n_per_env * n_sub
+    desc = (f"{n_threads} env(s) x {scene.n_per_env} particles x {n_sub} substep(s) fwd+bwd, reference "
+            f"mpm_step<Value> + Tape (per-substep checkpoint segments), fp64, {n_threads} thread(s)")
+    return units, wall, desc
+
+
+def cpu_threads():
+    try:
+        return max(1, min(len(os.sched_getaffinity(0)), 16))
+    except Exception:
+        return max(1, min(os.cpu_count() or 1, 16))
+
+
+def run_reference(args, scene, rank, dist):
+    if rank != 0:
+        return
+    nt = cpu_threads()
+    vals = []
+    for i in range(args.warmup + args.steps):
+        units, wall, desc = reference_sample(scene, nt, 1)
+        if i >= args.warmup:
+            vals.append(units / wall)
+    v = float(np.mean(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * scene.n_per_env * nt / v,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": scene.name, "sample": desc},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": nt, "kind": "reference", "sample": desc},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------- our arm ----------------
+
+ALG_BYTES = {  # algorithmic HBM bytes per particle per launch
+    "bin": 12, "p2g": 96, "g2p": 48 + 96, "g2p_adj": 48 + 96 + 48, "p2g_adj": 96 + 48 + 96,
+}
+
+
+def run_ours(args, scene, rank, world, local, dist):
+    import torch
+    from paper_2412_12089_b200 import api
+    from paper_2412_12089_b200.losses import loss_and_dobs, loss_and_dobs_torch
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    E, N, T, S = scene.n_envs, scene.n_per_env, scene.n_ctrl, scene.n_sub
+    ck = scene.checkpoint_every if args.checkpoint_every < 0 else args.checkpoint_every
+    batch = api.from_scene(scene, checkpoint_every=ck, device=local)
+    K, G = batch.K, batch.G
+    cvo, act = scene.cvo_act()
+    f32 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float32), device=dev)
+    x0, v0, F0, C0 = f32(scene.x), f32(scene.v), f32(scene.F), f32(scene.C)
+    mat = torch.as_tensor(scene.material, dtype=torch.int32, device=dev)
+    grp = torch.as_tensor(scene.group, dtype=torch.int32, device=dev)
+    cvo_d = f32(np.transpose(cvo[:, :, :max(K, 1)], (1, 0, 2, 3))) if K else None  # [T,E,K,9]
+    act_d = f32(np.transpose(act[:, :, :max(G, 1)], (1, 0, 2))) if G else None      # [T,E,G]
+    obs_d = torch.zeros((T, E, 7), dtype=torch.float32, device=dev)
+    out = {"x": torch.empty((E, N, 3), device=dev), "v": torch.empty((E, N, 3), device=dev),
+           "F": torch.empty((E, N, 9), device=dev), "C": torch.empty((E, N, 9), device=dev),
+           "cvo": torch.empty((T, E, max(K, 1), 9), device=dev) if K else None,
+           "act": torch.empty((T, E, max(G, 1)), device=dev) if G else None,
+           "E": torch.empty((E, batch.n_materials), dtype=torch.float64, device=dev)}
+    torch.cuda.synchronize()
+
+    def rollout_device():
+        batch.set_state(x0, v0, F0, C0, mat, grp)
+        for t in range(T):
+            batch.step(None if cvo_d is None else cvo_d[t], None if act_d is None else act_d[t], obs_d[t])
+        _, dobs = loss_and_dobs_torch(scene.loss, obs_d.transpose(0, 1))
+        batch.backward(dobs=dobs.transpose(0, 1).contiguous(), out=out)
+
+    # host (pinned) buffers for the end-to-end arm
+    def pinned(a, dtype=np.float32):
+        t = torch.empty(a.shape, dtype=torch.float32 if dtype == np.float32 else torch.int32).pin_memory()
+        t.numpy()[...] = a
+        return t.numpy()
+
+    hx, hv, hF, hC = (pinned(scene.x), pinned(scene.v), pinned(scene.F), pinned(scene.C))
+    hmat, hgrp = pinned(scene.material, np.int32), pinned(scene.group, np.int32)
+    hcvo = [np.ascontiguousarray(pinned(cvo[:, t, :K])) for t in range(T)] if K else None
+    hact = [np.ascontiguousarray(pinned(act[:, t, :G])) for t in range(T)] if G else None
+
+    def rollout_host():
+        batch.set_state(hx, hv, hF, hC, hmat, hgrp)
+        obs = np.zeros((T, E, 7), np.float32)
+        for t in range(T):
+            obs[t] = batch.step(hcvo[t] if K else None, hact[t] if G else None)
+        _, dobs = loss_and_dobs(scene.loss, np.transpose(obs, (1, 0, 2)))
+        return batch.backward(dobs=np.ascontiguousarray(np.transpose(dobs, (1, 0, 2)), dtype=np.float32))
+
+    h2d = (hx.nbytes + hv.nbytes + hF.nbytes + hC.nbytes + hmat.nbytes + hgrp.nbytes +
+           (sum(a.nbytes for a in hcvo) if K else 0) + (sum(a.nbytes for a in hact) if G else 0) + T * E * 7 * 4)
+    d2h = T * E * 7 * 4 + E * N * 24 * 4 + (T * E * K * 9 * 4 if K else 0) + (T * E * G * 4 if G else 0) + E * 8 * batch.n_materials
+
+    stream = torch.cuda.ExternalStream(batch.stream_ptr, device=dev)
+    units_rank = E * N * T * S
+    # warm-up
+    for _ in range(args.warmup):
+        rollout_device()
+    torch.cuda.synchronize()
+    launches0 = batch.launches
+    batch.profile(True)
+    barrier(dist)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            rollout_device()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier(dist)
+    prof = batch.profile(False)
+    ms_rank = ev0.elapsed_time(ev1) / args.steps
+    launches = (batch.launches - launches0) // args.steps
+    ms = max_over_ranks(dist, ms_rank)
+    value = units_rank * world / (ms / 1e3)
+
+    e2e = None
+    if not args.no_e2e:
+        rollout_host()
+        torch.cuda.synchronize()
+        barrier(dist)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            rollout_host()
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(dist, (time.perf_counter() - t0) * 1e3 / args.steps)
+        barrier(dist)
+        e2e = {"value": units_rank * world / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms}
+
+    if rank != 0:
+        return
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+        hbm, peak_src = float(peaks["hbm_gbs"]), "measured"
+    except Exception:
+        hbm, peak_src = 6650.0, "fallback"
+    # dominant kernel (largest total time in the timed region)
+    kern = {k: v for k, v in prof.items() if k in ALG_BYTES and v[1] > 0}
+    dom = max(kern, key=lambda k: kern[k][0])
+    dom_ms, dom_n = kern[dom]
+    per_launch_units = E * N  # every launch of these kernels sweeps all particles once
+    achieved = ALG_BYTES[dom] * per_launch_units / (dom_ms / dom_n / 1e3) / 1e9
+    total_prof = sum(v[0] for v in prof.values())
+    path_gbs = 480.0 * units_rank / (ms_rank / 1e3) / 1e9
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        nt = cpu_threads()
+        units, wall, desc = reference_sample(scene, nt, 1)
+        cpu = {"value": units / wall, "unit": UNIT, "cores": nt, "kind": "reference", "sample": desc}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": scene.name, "envs": E * world, "particles_per_env": N, "control_steps": T,
+                   "substeps_per_step": S, "grid": list(scene.sim["dims"]), "checkpoint_every": ck or S,
+                   "particle_substeps_per_step": units_rank * world,
+                   "l2": "inputs larger than L2 (state %.2f GB per rank)" % (E * N * 96 / 1e9)},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
+                     "alg_bytes_per_particle": ALG_BYTES[dom], "kernel_share": dom_ms / total_prof,
+                     "path_alg_gbs": path_gbs, "path_frac": path_gbs / hbm},
+        "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+    }
+    print(json.dumps(line), flush=True)
+    if args.profile_out:
+        with open(args.profile_out, "w") as f:
+            json.dump(line, f, indent=1)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference" and rank != 0:
+        return
+    dist = init_dist(world, local) if args.impl == "ours" else None
+    from paper_2412_12089_b200 import scenes
+    total = args.envs or {1: 1, 2: 32, 3: 256, 4: 1024}[args.config]
+    per = total // world if args.impl == "ours" else min(total, cpu_threads())
+    kw = {"n_envs": per, "env_offset": rank * per if args.impl == "ours" else 0}
+    if args.ctrl:
+        kw["n_ctrl"] = args.ctrl
+    scene = scenes.CONFIGS[args.config](seed=0, **kw)
+    if args.impl == "reference":
+        run_reference(args, scene, rank, dist)
+    else:
+        run_ours(args, scene, rank, world, local, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

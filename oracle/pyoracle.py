@@ -84,7 +84,7 @@ def make_sim(spec) -> OrSim:
     s = OrSim()
     s.dims[:] = list(spec["dims"])
     s.dx = spec["dx"]
-    s.dt = spec["dt"]
+    s.dt = spec.get("dt", 1e-4)
     s.gravity[:] = list(spec.get("gravity", (0.0, 0.0, -9.8)))
     s.boundary = {"slip": 0, "sticky": 1}[spec.get("boundary", "slip")]
     s.alpha_c = spec.get("alpha_c", 100.0)

@@ -66,7 +66,10 @@ _SIGS = {
     "dm_tape_steps": (C.c_int, [_P]),
     "dm_debug_sort": (C.c_int, [_P, _P, _P]),
     "dm_launch_count": (C.c_ulonglong, [_P]),
+    "dm_profile": (C.c_int, [_P, C.c_int, _P, _P]),
 }
+
+PROF_CLASSES = ("bin", "p2g", "g2p", "g2p_adj", "p2g_adj", "env_reduce", "obs", "obs_adj", "layout")
 
 
 def lib():
@@ -273,6 +276,14 @@ class MpmBatch:
         self._check(self._L.dm_backward(self._h, _ptr(d), *(_ptr(a) for a in fin),
                                         *(_ptr(res.get(k)) for k in ("x", "v", "F", "C", "cvo", "act", "E"))))
         return res
+
+    def profile(self, enable: bool = True):
+        """Returns {class: (ms, launches)} accumulated since the last call and
+        switches per-kernel CUDA-event timing on/off."""
+        ms = np.zeros(9, np.float64)
+        n = np.zeros(9, np.int64)
+        self._check(self._L.dm_profile(self._h, int(enable), _ptr(ms), _ptr(n)))
+        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(PROF_CLASSES)}
 
     def debug_sort(self):
         """(keys, perm) of the current state per env: bin key per particle (in

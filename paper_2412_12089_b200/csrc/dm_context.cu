@@ -16,6 +16,10 @@
 
 using namespace dm;
 
+// kernel classes for dm_profile: bin, p2g, g2p, g2p_adj, p2g_adj, env_reduce,
+// obs, obs_adj, layout
+constexpr int kProfClasses = 9;
+
 struct DmContext {
   DmConfig cfg{};
   int nmat = 0;
@@ -49,6 +53,13 @@ struct DmContext {
   DevFlags* h_flags = nullptr;
   float *cvo_tape = nullptr, *act_tape = nullptr, *obs_tape = nullptr;
   double *gcvo = nullptr, *gact = nullptr, *gmu = nullptr, *glam = nullptr;
+  // optional per-kernel-class CUDA-event timing (bench roofline)
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<int> ev_class;
+  std::vector<double> prof_ms = std::vector<double>(kProfClasses, 0.0);
+  std::vector<long long> prof_n = std::vector<long long>(kProfClasses, 0);
 };
 
 namespace {
@@ -100,11 +111,42 @@ StateView seg_state(DmContext* c, int s0, int s) {
 
 int maxc_of(int K) { return K <= 1 ? 1 : 4; }
 
+cudaEvent_t next_event(DmContext* c) {
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[c->ev_used++];
+}
+void prof_mark(DmContext* c, int cls) {
+  if (!c->prof) return;
+  cudaEventRecord(next_event(c), c->stream);
+  c->ev_class.push_back(cls);
+}
+// Sum (end - start) per class; events are recorded in begin/end pairs.
+void prof_flush(DmContext* c) {
+  if (!c->prof || c->ev_used == 0) return;
+  cudaStreamSynchronize(c->stream);
+  for (size_t i = 0; i + 1 < c->ev_used; i += 2) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev_pool[i], c->ev_pool[i + 1]);
+    c->prof_ms[c->ev_class[i]] += ms;
+    c->prof_n[c->ev_class[i]] += 1;
+  }
+  c->ev_used = 0;
+  c->ev_class.clear();
+}
+#define PROF_BEGIN(c, cls) prof_mark(c, cls)
+#define PROF_END(c, cls) prof_mark(c, cls)
+
 void launch_bin(DmContext* c, const StateView& S, int sub, int check_vmax) {
   cudaMemsetAsync(&c->flags->active_count, 0, sizeof(int), c->stream);
   const size_t shm = 2 * (size_t)c->P.Tn * sizeof(int);
+  PROF_BEGIN(c, 0);
   k_bin<<<c->P.E, 512, shm, c->stream>>>(c->P, S, c->keys, c->perm, c->tile_start, c->tile_count, c->active,
                                           c->env_abase, c->env_acount, c->flags, sub, check_vmax);
+  PROF_END(c, 0);
   ++c->launches;
 }
 
@@ -114,22 +156,26 @@ const float* step_act(DmContext* c, int t) {
 }
 
 void launch_p2g(DmContext* c, const StateView& S, int t, int sub) {
+  PROF_BEGIN(c, 1);
   if (maxc_of(c->P.K) == 1)
     k_p2g<1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, c->perm, c->tile_start, c->tile_count, c->active,
                                                            step_act(c, t), c->blocks, c->flags, sub);
   else
     k_p2g<4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, c->perm, c->tile_start, c->tile_count, c->active,
                                                            step_act(c, t), c->blocks, c->flags, sub);
+  PROF_END(c, 1);
   ++c->launches;
 }
 
 void launch_g2p(DmContext* c, const StateView& S, const StateView& So, int t, int sub) {
+  PROF_BEGIN(c, 2);
   if (maxc_of(c->P.K) == 1)
     k_g2p<1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, c->perm, c->tile_start, c->tile_count,
                                                            c->active, step_cvo(c, t), c->blocks, c->flags, sub);
   else
     k_g2p<4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, c->perm, c->tile_start, c->tile_count,
                                                            c->active, step_cvo(c, t), c->blocks, c->flags, sub);
+  PROF_END(c, 2);
   ++c->launches;
 }
 
@@ -149,6 +195,7 @@ void launch_p2g_adj(DmContext* c, const StateView& S, int t, float* adj_out) {
 void backward_substep(DmContext* c, const StateView& S, int t, int sub, const float* adj_in, float* adj_out) {
   launch_bin(c, S, sub, 0);
   launch_p2g(c, S, t, sub);
+  PROF_BEGIN(c, 3);
   if (maxc_of(c->P.K) == 1)
     k_g2p_adj<1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, adj_in, c->Ntot, c->perm, c->tile_start,
                                                                c->tile_count, c->active, step_cvo(c, t), c->blocks,
@@ -157,9 +204,11 @@ void backward_substep(DmContext* c, const StateView& S, int t, int sub, const fl
     k_g2p_adj<4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, adj_in, c->Ntot, c->perm, c->tile_start,
                                                                c->tile_count, c->active, step_cvo(c, t), c->blocks,
                                                                c->ablocks, c->part, c->tile_acc, c->flags);
+  PROF_END(c, 3);
   ++c->launches;
   const int m = maxc_of(c->P.K);
   const int G = c->P.G;
+  PROF_BEGIN(c, 4);
   if (m == 1) {
     if (G <= 1)
       launch_p2g_adj<1, 1>(c, S, t, adj_out);
@@ -173,11 +222,14 @@ void backward_substep(DmContext* c, const StateView& S, int t, int sub, const fl
     else
       launch_p2g_adj<4, 16>(c, S, t, adj_out);
   }
+  PROF_END(c, 4);
   ++c->launches;
   const int Kc = c->P.K > 0 ? c->P.K : 1;
+  PROF_BEGIN(c, 5);
   k_env_reduce<<<c->P.E, kNacc, 0, c->stream>>>(c->P, c->active, c->env_abase, c->env_acount, c->tile_acc,
                                                 c->gcvo + (size_t)t * c->P.E * Kc * 9,
                                                 c->gact + (size_t)t * c->P.E * (G > 0 ? G : 1), c->gmu, c->glam);
+  PROF_END(c, 5);
   ++c->launches;
 }
 
@@ -206,6 +258,7 @@ std::string fmt_error(DmContext* c, unsigned long long key) {
 
 // Reads the device flags after a control step; returns DM_OK or the error.
 int check_flags(DmContext* ctx, bool cfl) {
+  prof_flush(ctx);
   DM_CUDA(cudaMemcpyAsync(ctx->h_flags, ctx->flags, sizeof(DevFlags), cudaMemcpyDeviceToHost, ctx->stream));
   DM_CUDA(cudaStreamSynchronize(ctx->stream));
   DM_CUDA(cudaGetLastError());
@@ -308,8 +361,10 @@ int step_impl(DmContext* ctx, const float* cvo, const float* act, float* obs, cu
     forward_substep(ctx, fwd_state(ctx, s), fwd_state(ctx, s + 1), t, q, q == 0);
   }
   float* o = ctx->obs_tape + (size_t)t * E * DM_OBS_DIM;
+  PROF_BEGIN(ctx, 6);
   k_obs<<<E, 256, 0, ctx->stream>>>(ctx->P, fwd_state(ctx, (t + 1) * S), step_cvo(ctx, t), (float)ctx->cfg.spill_half,
                                     (float)ctx->cfg.spill_temp, o);
+  PROF_END(ctx, 6);
   ++ctx->launches;
   if (obs) DM_CUDA(cudaMemcpyAsync(obs, o, (size_t)E * DM_OBS_DIM * sizeof(float), kout, ctx->stream));
   const int rc = check_flags(ctx, true);
@@ -365,10 +420,12 @@ int backward_impl(DmContext* ctx, const float* dobs, const float* dfx, const flo
   for (int t = T - 1; t >= 0; --t) {
     const int s_end = (t + 1) * S;
     if (dobs_dev) {
+      PROF_BEGIN(ctx, 7);
       k_obs_adj<<<E, 256, 0, ctx->stream>>>(ctx->P, store_view(ctx, s_end / ck), step_cvo(ctx, t),
                                             (float)ctx->cfg.spill_half, (float)ctx->cfg.spill_temp,
                                             dobs_dev + (size_t)t * E * DM_OBS_DIM, ctx->adj[cur], N,
                                             ctx->gcvo + (size_t)t * E * Kc * 9);
+      PROF_END(ctx, 7);
       ++ctx->launches;
     }
     for (int s0 = s_end - ck; s0 >= t * S; s0 -= ck) {
@@ -562,6 +619,7 @@ void dm_destroy(DmContext* ctx) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
+  for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -615,6 +673,19 @@ int dm_backward_device(DmContext* ctx, const float* dobs, const float* dfx, cons
   if (!ctx || !ctx->store) return DM_ERR_ARG;
   return backward_impl(ctx, dobs, dfx, dfv, dfF, dfC, dx0, dv0, dF0, dC0, dcvo, dact, dE, cudaMemcpyDeviceToDevice,
                        cudaMemcpyDeviceToDevice);
+}
+
+int dm_profile(DmContext* ctx, int enable, double* ms, long long* counts) {
+  if (!ctx) return DM_ERR_ARG;
+  prof_flush(ctx);
+  for (int i = 0; i < kProfClasses; ++i) {
+    if (ms) ms[i] = ctx->prof_ms[i];
+    if (counts) counts[i] = ctx->prof_n[i];
+    ctx->prof_ms[i] = 0.0;
+    ctx->prof_n[i] = 0;
+  }
+  ctx->prof = enable != 0;
+  return DM_OK;
 }
 
 int dm_debug_sort(DmContext* ctx, int* keys, int* perm) {

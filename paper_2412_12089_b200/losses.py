@@ -49,3 +49,36 @@ def loss_and_dobs(spec: dict, obs: np.ndarray):
     else:
         raise ValueError(f"unknown loss kind {kind!r}")
     return L, d
+
+
+def loss_and_dobs_torch(spec: dict, obs):
+    """Same as loss_and_dobs for a torch tensor obs [..., T, 7] (device-side)."""
+    import torch
+    o = obs.double()
+    d = torch.zeros_like(o)
+    kind = spec["kind"]
+    if kind == "com_target":
+        tgt = torch.tensor(spec.get("target", (0.5, 0.4, 0.5)), dtype=o.dtype, device=o.device)
+        diff = o[..., -1, 0:3] - tgt
+        L = (diff ** 2).sum(-1)
+        d[..., -1, 0:3] = 2.0 * diff
+    elif kind == "neg_mean_z":
+        L = -o[..., :, 2].sum(-1)
+        d[..., :, 2] = -1.0
+    elif kind == "var_z":
+        L = o[..., :, 5].sum(-1)
+        d[..., :, 5] = 1.0
+    elif kind == "fluid_move":
+        tgt = torch.tensor(spec["target"], dtype=o.dtype, device=o.device)
+        diff = o[..., 0:3] - tgt
+        dist = torch.sqrt((diff ** 2).sum(-1) + 1e-12)
+        thr, lo, hi = spec.get("tier_threshold", 0.02), spec.get("tier_low", 1.0), spec.get("tier_high", 2.0)
+        mult = torch.where(dist > thr, torch.full_like(dist, lo), torch.full_like(dist, hi))
+        r = mult / (1.0 + dist) ** 2
+        L = (-(r - o[..., 6])).sum(-1)
+        dr = -2.0 * mult / (1.0 + dist) ** 3
+        d[..., 0:3] = (-dr / dist).unsqueeze(-1) * diff
+        d[..., 6] = 1.0
+    else:
+        raise ValueError(f"unknown loss kind {kind!r}")
+    return L, d.float()

@@ -1,0 +1,98 @@
+"""CPU: seeded synthetic inputs, task action maps and losses."""
+import numpy as np
+import pytest
+
+from paper_2412_12089_b200 import scenes
+from paper_2412_12089_b200.losses import loss_and_dobs
+
+
+def interior_ok(sc):
+    dx = sc.sim["dx"]
+    b = np.floor(sc.x / dx - 0.5)
+    return (b >= 1).all() and (b + 2 <= np.array(sc.sim["dims"]) - 2).all()
+
+
+@pytest.mark.parametrize("cfg,kw", [(1, {}), (2, {"n_envs": 2}), (3, {"n_envs": 2, "n_per_env": 3000}),
+                                     (4, {"n_envs": 2})])
+def test_configs_build(cfg, kw):
+    sc = scenes.CONFIGS[cfg](seed=0, **kw)
+    E, N = sc.n_envs, sc.n_per_env
+    assert sc.x.shape == (E, N, 3) and sc.F.shape == (E, N, 9)
+    assert interior_ok(sc)
+    cvo, act = sc.cvo_act()
+    assert cvo.shape[:2] == (E, sc.n_ctrl)
+    assert np.isfinite(sc.x).all()
+
+
+def test_config_sizes_match_baseline():
+    assert scenes.config1().n_per_env == 4096
+    assert scenes.config2(n_envs=1).n_per_env == 20480
+    assert scenes.config4(n_envs=1).n_per_env == 16384
+    sc = scenes.config4(n_envs=1)
+    assert (sc.n_ctrl, sc.n_sub) == (16, 32) and tuple(sc.sim["dims"]) == (48, 48, 48)
+    sc = scenes.config3(n_envs=1, n_per_env=30000)
+    assert (sc.n_ctrl, sc.n_sub, sc.checkpoint_every) == (24, 20, 4)
+
+
+@pytest.mark.parametrize("cfg", [1, 3, 4])
+def test_sharding_is_input_invariant(cfg):
+    kw = {"n_per_env": 500} if cfg == 3 else {}
+    full = scenes.CONFIGS[cfg](seed=5, n_envs=4, **kw)
+    part = scenes.CONFIGS[cfg](seed=5, n_envs=2, env_offset=2, **kw)
+    assert np.array_equal(full.x[2:], part.x)
+    assert np.array_equal(full.v[2:], part.v)
+    assert np.array_equal(full.actions[2:], part.actions)
+
+
+def test_seeded_determinism():
+    a = scenes.config1(seed=3)
+    b = scenes.config1(seed=3)
+    c = scenes.config1(seed=4)
+    assert np.array_equal(a.v, b.v) and not np.array_equal(a.v, c.v)
+    assert abs(a.v.std() - 0.5) < 0.02
+
+
+def test_kmeans_groups_cover():
+    sc = scenes.config2(n_envs=1)
+    g = sc.group[0]
+    assert set(np.unique(g)) == set(range(8))
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_task_vjp_matches_fd(cfg):
+    kw = {"n_per_env": 200} if cfg == 3 else {"lattice_counts": (4, 4, 2)}
+    sc = scenes.CONFIGS[cfg](seed=1, n_envs=2, n_ctrl=5, **kw)
+    rng = np.random.default_rng(0)
+    cvo, _ = sc.task.forward(sc.actions)
+    g = rng.standard_normal(cvo.shape)
+    ga = sc.task.vjp(sc.actions, g, None)
+    h = 1e-6
+    for idx in [(0, 0, 0), (1, 2, 1), (0, 4, 2)]:
+        ap = sc.actions.copy()
+        am = sc.actions.copy()
+        ap[idx] += h
+        am[idx] -= h
+        fd = ((sc.task.forward(ap)[0] - sc.task.forward(am)[0]) * g).sum() / (2 * h)
+        assert abs(ga[idx] - fd) < 1e-6 * max(1, abs(fd))
+
+
+@pytest.mark.parametrize("spec", [{"kind": "com_target", "target": (0.5, 0.4, 0.5)}, {"kind": "neg_mean_z"},
+                                  {"kind": "var_z"},
+                                  {"kind": "fluid_move", "target": (0.55, 0.5, 0.2), "spill_half": 0.15,
+                                   "spill_temp": 0.01}])
+def test_loss_gradient_fd_and_torch(spec):
+    import torch
+    from paper_2412_12089_b200.losses import loss_and_dobs_torch
+    rng = np.random.default_rng(2)
+    obs = rng.random((3, 4, 7))
+    L, d = loss_and_dobs(spec, obs)
+    h = 1e-7
+    for idx in [(0, 0, 0), (1, 3, 2), (2, 1, 5), (0, 2, 6)]:
+        op = obs.copy()
+        om = obs.copy()
+        op[idx] += h
+        om[idx] -= h
+        fd = (loss_and_dobs(spec, op)[0][idx[0]] - loss_and_dobs(spec, om)[0][idx[0]]) / (2 * h)
+        assert abs(d[idx] - fd) < 1e-5 * max(1, abs(fd))
+    Lt, dt = loss_and_dobs_torch(spec, torch.tensor(obs))
+    assert np.allclose(Lt.numpy(), L) and np.allclose(dt.numpy(), d, atol=1e-6)

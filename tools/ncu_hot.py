@@ -1,0 +1,45 @@
+"""Summarise an ncu report's SASS source page: stall samples by opcode and
+the hottest instructions.  usage: python tools/ncu_hot.py report.ncu-rep [N]"""
+import csv
+import io
+import subprocess
+import sys
+from collections import defaultdict
+
+rep = sys.argv[1]
+topn = int(sys.argv[2]) if len(sys.argv) > 2 else 25
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                     capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+hi = next(i for i, r in enumerate(rows) if len(r) > 3 and r[0] == "Address")
+h = rows[hi]
+idx = {k: i for i, k in enumerate(h)}
+samp = idx["Warp Stall Sampling (All Samples)"]
+execd = idx["Instructions Executed"]
+src = idx["Source"]
+tot = 0
+by_op = defaultdict(int)
+by_op_n = defaultdict(int)
+agg = []
+for r in rows[hi + 1:]:
+    if len(r) <= samp:
+        continue
+    try:
+        s = int(r[samp])
+        n = int(r[execd])
+    except ValueError:
+        continue
+    tot += s
+    op = r[src].split()[0] if r[src].split() else "?"
+    if op.startswith("@"):
+        op = r[src].split()[1]
+    op = op.split(".")[0]
+    by_op[op] += s
+    by_op_n[op] += n
+    agg.append((s, r[0], r[src][:110]))
+print("total samples", tot, " total warp-instructions", sum(by_op_n.values()))
+for op, s in sorted(by_op.items(), key=lambda x: -x[1])[:15]:
+    print(f"  {op:10s} {100*s/tot:5.1f}% samples   {by_op_n[op]:>12d} instr")
+agg.sort(reverse=True)
+for s, a, t in agg[:topn]:
+    print(f"{s:7d} {100*s/max(tot,1):5.1f}%  {a[-5:]}  {t}")
