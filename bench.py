@@ -220,6 +220,7 @@ def run_reference(args, scene, rank, dist):
 ALG_BYTES = {  # algorithmic HBM bytes per particle per launch
     "bin": 12, "p2g": 96, "g2p": 48 + 96, "g2p_adj": 48 + 96 + 48, "p2g_adj": 96 + 48 + 96,
 }
+# grid / grid_adj / env_reduce / obs are per-node or per-env work (reported in kernel_ms_per_step)
 
 
 def run_ours(args, scene, rank, world, local, dist):

@@ -132,8 +132,9 @@ int dm_tape_steps(const DmContext* ctx);
 int dm_debug_sort(DmContext* ctx, int* keys, int* perm);
 /* Per-kernel-class CUDA-event timing on the context stream.  Classes:
  * 0 bin, 1 p2g, 2 g2p, 3 g2p_adj, 4 p2g_adj, 5 env_reduce, 6 obs, 7 obs_adj,
- * 8 layout.  Returns (and clears) the accumulated ms / launch counts and sets
- * whether timing is recorded from now on.  ms, counts: 9 entries or NULL. */
+ * 8 layout, 9 grid, 10 grid_adj.  Returns (and clears) the accumulated ms /
+ * launch counts and sets whether timing is recorded from now on.  ms, counts:
+ * 11 entries or NULL. */
 int dm_profile(DmContext* ctx, int enable, double* ms, long long* counts);
 /* Kernel launches issued since the context was created. */
 unsigned long long dm_launch_count(const DmContext* ctx);

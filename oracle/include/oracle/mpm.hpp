@@ -490,23 +490,26 @@ void substep(const SimParams& sp, State<T>& st, Grid<T>& g, const std::vector<Ma
 }
 
 // ---- binning / stable sort (build-defined; SURVEY 8(a) a7, 8(d) "Binning") ----
-// Key = linear index of the 4x4x4-cell tile that holds the particle's stencil
-// base, computed with the same fp32 operations as the device:
-//   gx = fl(x * inv_dx); base = floor(fl(gx - 0.5)); tile = base >> 2.
+// Key = (linear index of the 4x4x4-cell tile holding the particle's stencil
+// base) * 64 + (linear index of the base cell inside the tile), computed with
+// the same fp32 operations as the device:
+//   gx = fl(x * inv_dx); base = floor(fl(gx - 0.5)); tile = base >> 2; cell = base & 3.
 inline int tile_dim(int dim) { return (dim + 3) / 4; }
 
 inline void bin_keys_f32(const SimParams& sp, const float* x /* N x 3 */, std::size_t n, int* keys) {
   const float inv_dx = static_cast<float>(1.0 / sp.dx);
   const int td[3] = {tile_dim(sp.dims[0]), tile_dim(sp.dims[1]), tile_dim(sp.dims[2])};
   for (std::size_t p = 0; p < n; ++p) {
-    int t[3];
+    int t[3], c[3];
     for (int a = 0; a < 3; ++a) {
       volatile float gx = x[3 * p + a] * inv_dx;  // volatile: no contraction
       volatile float gm = gx - 0.5f;
-      const int base = static_cast<int>(std::floor(static_cast<float>(gm)));
+      int base = static_cast<int>(std::floor(static_cast<float>(gm)));
+      base = base < 1 ? 1 : (base > sp.dims[a] - 4 ? sp.dims[a] - 4 : base);  // reported outside anyway
       t[a] = base >> 2;
+      c[a] = base & 3;
     }
-    keys[p] = (t[0] * td[1] + t[1]) * td[2] + t[2];
+    keys[p] = ((t[0] * td[1] + t[1]) * td[2] + t[2]) * 64 + (c[0] * 4 + c[1]) * 4 + c[2];
   }
 }
 

@@ -69,15 +69,16 @@ _SIGS = {
     "dm_profile": (C.c_int, [_P, C.c_int, _P, _P]),
 }
 
-PROF_CLASSES = ("bin", "p2g", "g2p", "g2p_adj", "p2g_adj", "env_reduce", "obs", "obs_adj", "layout")
+PROF_CLASSES = ("bin", "p2g", "g2p", "g2p_adj", "p2g_adj", "env_reduce", "obs", "obs_adj", "layout", "grid",
+                "grid_adj")
 
 
 def lib():
     """Load the in-tree sm_100a library (building it if sources changed)."""
     global _LIB
     if _LIB is None:
-        so = _build.SO
-        if not os.path.exists(so) or _build.needs_build():
+        so = os.environ.get("DIFFMPM_SO") or _build.SO  # DIFFMPM_SO: A/B variants of the same ABI
+        if so == _build.SO and (not os.path.exists(so) or _build.needs_build()):
             _build.build()
         L = C.CDLL(so)
         for name, (res, args) in _SIGS.items():
@@ -280,8 +281,8 @@ class MpmBatch:
     def profile(self, enable: bool = True):
         """Returns {class: (ms, launches)} accumulated since the last call and
         switches per-kernel CUDA-event timing on/off."""
-        ms = np.zeros(9, np.float64)
-        n = np.zeros(9, np.int64)
+        ms = np.zeros(len(PROF_CLASSES), np.float64)
+        n = np.zeros(len(PROF_CLASSES), np.int64)
         self._check(self._L.dm_profile(self._h, int(enable), _ptr(ms), _ptr(n)))
         return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(PROF_CLASSES)}
 

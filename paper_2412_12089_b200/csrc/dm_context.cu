@@ -17,8 +17,8 @@
 using namespace dm;
 
 // kernel classes for dm_profile: bin, p2g, g2p, g2p_adj, p2g_adj, env_reduce,
-// obs, obs_adj, layout
-constexpr int kProfClasses = 9;
+// obs, obs_adj, layout, grid, grid_adj
+constexpr int kProfClasses = 11;
 
 struct DmContext {
   DmConfig cfg{};
@@ -44,10 +44,12 @@ struct DmContext {
   uint32_t* scratch_attr[2] = {nullptr, nullptr};
   float* adj[2] = {nullptr, nullptr};  // [24][Ntot]
   float* part = nullptr;               // [12][Ntot]
-  int *keys = nullptr, *perm = nullptr, *tile_start = nullptr, *tile_count = nullptr;
+  int *keys = nullptr, *perm = nullptr, *ptile = nullptr, *tile_start = nullptr, *tile_count = nullptr;
   int *env_abase = nullptr, *env_acount = nullptr;
   int2* active = nullptr;
   float4 *blocks = nullptr, *ablocks = nullptr;
+  float4 *gmp = nullptr, *gv = nullptr, *gmb = nullptr;  // dense per-env grids
+  int bin_warps = 16;
   float* tile_acc = nullptr;
   DevFlags* flags = nullptr;
   DevFlags* h_flags = nullptr;
@@ -142,10 +144,13 @@ void prof_flush(DmContext* c) {
 
 void launch_bin(DmContext* c, const StateView& S, int sub, int check_vmax) {
   cudaMemsetAsync(&c->flags->active_count, 0, sizeof(int), c->stream);
-  const size_t shm = 2 * (size_t)c->P.Tn * sizeof(int);
+  const size_t shm = (size_t)c->bin_warps * c->P.Tn * sizeof(int);
   PROF_BEGIN(c, 0);
-  k_bin<<<c->P.E, 512, shm, c->stream>>>(c->P, S, c->keys, c->perm, c->tile_start, c->tile_count, c->active,
-                                          c->env_abase, c->env_acount, c->flags, sub, check_vmax);
+  k_bin<<<c->P.E, 32 * c->bin_warps, shm, c->stream>>>(c->P, S, c->keys, c->ptile, c->tile_start, c->tile_count,
+                                                       c->active, c->env_abase, c->env_acount, c->flags, sub, check_vmax);
+  k_cellsort<<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, c->ptile, c->perm, c->keys, c->tile_start,
+                                                           c->tile_count, c->active, c->flags);
+  ++c->launches;
   PROF_END(c, 0);
   ++c->launches;
 }
@@ -167,14 +172,22 @@ void launch_p2g(DmContext* c, const StateView& S, int t, int sub) {
   ++c->launches;
 }
 
+void launch_grid(DmContext* c, int t) {
+  PROF_BEGIN(c, 9);
+  if (maxc_of(c->P.K) == 1)
+    k_grid<1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, c->tile_count, c->active, step_cvo(c, t), c->blocks,
+                                                            c->gmp, c->gv, c->flags);
+  else
+    k_grid<4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, c->tile_count, c->active, step_cvo(c, t), c->blocks,
+                                                            c->gmp, c->gv, c->flags);
+  PROF_END(c, 9);
+  ++c->launches;
+}
+
 void launch_g2p(DmContext* c, const StateView& S, const StateView& So, int t, int sub) {
   PROF_BEGIN(c, 2);
-  if (maxc_of(c->P.K) == 1)
-    k_g2p<1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, c->perm, c->tile_start, c->tile_count,
-                                                           c->active, step_cvo(c, t), c->blocks, c->flags, sub);
-  else
-    k_g2p<4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, c->perm, c->tile_start, c->tile_count,
-                                                           c->active, step_cvo(c, t), c->blocks, c->flags, sub);
+  k_g2p<<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, c->perm, c->tile_start, c->tile_count, c->active,
+                                                      c->gv, c->flags, sub);
   PROF_END(c, 2);
   ++c->launches;
 }
@@ -182,46 +195,44 @@ void launch_g2p(DmContext* c, const StateView& S, const StateView& So, int t, in
 void forward_substep(DmContext* c, const StateView& S, const StateView& So, int t, int sub, int check_vmax) {
   launch_bin(c, S, sub, check_vmax);
   launch_p2g(c, S, t, sub);
+  launch_grid(c, t);
   launch_g2p(c, S, So, t, sub);
 }
 
-template <int MAXC, int NG>
+template <int NG>
 void launch_p2g_adj(DmContext* c, const StateView& S, int t, float* adj_out) {
-  k_p2g_adj<MAXC, NG><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(
-      c->P, S, c->perm, c->tile_start, c->tile_count, c->active, step_cvo(c, t), step_act(c, t), c->blocks,
-      c->ablocks, c->part, adj_out, c->Ntot, c->tile_acc, c->flags);
+  k_p2g_adj<NG><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, c->perm, c->tile_start, c->tile_count,
+                                                              c->active, step_act(c, t), c->gmb, c->part, adj_out,
+                                                              c->Ntot, c->tile_acc, c->flags);
 }
 
 void backward_substep(DmContext* c, const StateView& S, int t, int sub, const float* adj_in, float* adj_out) {
   launch_bin(c, S, sub, 0);
   launch_p2g(c, S, t, sub);
+  launch_grid(c, t);
   PROF_BEGIN(c, 3);
-  if (maxc_of(c->P.K) == 1)
-    k_g2p_adj<1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, adj_in, c->Ntot, c->perm, c->tile_start,
-                                                               c->tile_count, c->active, step_cvo(c, t), c->blocks,
-                                                               c->ablocks, c->part, c->tile_acc, c->flags);
-  else
-    k_g2p_adj<4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, adj_in, c->Ntot, c->perm, c->tile_start,
-                                                               c->tile_count, c->active, step_cvo(c, t), c->blocks,
-                                                               c->ablocks, c->part, c->tile_acc, c->flags);
+  k_g2p_adj<<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, adj_in, c->Ntot, c->perm, c->tile_start,
+                                                          c->tile_count, c->active, c->gv, c->ablocks, c->part,
+                                                          c->tile_acc, c->flags);
   PROF_END(c, 3);
   ++c->launches;
-  const int m = maxc_of(c->P.K);
+  PROF_BEGIN(c, 10);
+  if (maxc_of(c->P.K) == 1)
+    k_grid_adj<1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, c->tile_count, c->active, step_cvo(c, t),
+                                                                c->ablocks, c->gmp, c->gmb, c->tile_acc, c->flags);
+  else
+    k_grid_adj<4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, c->tile_count, c->active, step_cvo(c, t),
+                                                                c->ablocks, c->gmp, c->gmb, c->tile_acc, c->flags);
+  PROF_END(c, 10);
+  ++c->launches;
   const int G = c->P.G;
   PROF_BEGIN(c, 4);
-  if (m == 1) {
-    if (G <= 1)
-      launch_p2g_adj<1, 1>(c, S, t, adj_out);
-    else if (G <= 8)
-      launch_p2g_adj<1, 8>(c, S, t, adj_out);
-    else
-      launch_p2g_adj<1, 16>(c, S, t, adj_out);
-  } else {
-    if (G <= 1)
-      launch_p2g_adj<4, 1>(c, S, t, adj_out);
-    else
-      launch_p2g_adj<4, 16>(c, S, t, adj_out);
-  }
+  if (G <= 1)
+    launch_p2g_adj<1>(c, S, t, adj_out);
+  else if (G <= 8)
+    launch_p2g_adj<8>(c, S, t, adj_out);
+  else
+    launch_p2g_adj<16>(c, S, t, adj_out);
   PROF_END(c, 4);
   ++c->launches;
   const int Kc = c->P.K > 0 ? c->P.K : 1;
@@ -521,7 +532,13 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
     P.grav[a] = (float)cfg->gravity[a];
   }
   P.Tn = P.td[0] * P.td[1] * P.td[2];
-  if (2 * (size_t)P.Tn * sizeof(int) > 200 * 1024) return fail("dm_create: grid too large for the bin kernel");
+  {
+    int nw = (int)((160 * 1024) / ((size_t)P.Tn * sizeof(int)));
+    nw = nw > 16 ? 16 : nw;
+    if (nw < 1) return fail("dm_create: grid too large for the bin kernel");
+    ctx->bin_warps = nw;
+    cudaFuncSetAttribute(k_bin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(nw * P.Tn * sizeof(int)));
+  }
   P.dx = (float)cfg->dx;
   P.inv_dx = (float)(1.0 / cfg->dx);
   P.dt = (float)cfg->dt;
@@ -579,9 +596,12 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
     for (int i = 0; i < 2; ++i)
       ok = ok && dalloc(ctx, &ctx->scratch[i], 24 * N) && dalloc(ctx, &ctx->scratch_attr[i], N);
   ok = ok && dalloc(ctx, &ctx->adj[0], 24 * N) && dalloc(ctx, &ctx->adj[1], 24 * N) && dalloc(ctx, &ctx->part, 12 * N);
-  ok = ok && dalloc(ctx, &ctx->keys, N) && dalloc(ctx, &ctx->perm, N) && dalloc(ctx, &ctx->tile_start, TT) &&
+  ok = ok && dalloc(ctx, &ctx->keys, N) && dalloc(ctx, &ctx->perm, N) && dalloc(ctx, &ctx->ptile, N) &&
+       dalloc(ctx, &ctx->tile_start, TT) &&
        dalloc(ctx, &ctx->tile_count, TT) && dalloc(ctx, &ctx->env_abase, P.E) && dalloc(ctx, &ctx->env_acount, P.E) &&
        dalloc(ctx, &ctx->active, TT);
+  const size_t NN = (size_t)P.E * P.dims[0] * P.dims[1] * P.dims[2];
+  ok = ok && dalloc(ctx, &ctx->gmp, NN) && dalloc(ctx, &ctx->gv, NN) && dalloc(ctx, &ctx->gmb, NN);
   ok = ok && dalloc(ctx, &ctx->blocks, TT * kExt3) && dalloc(ctx, &ctx->ablocks, TT * kExt3) &&
        dalloc(ctx, &ctx->tile_acc, TT * kNacc) && dalloc(ctx, &ctx->flags, 1);
   ok = ok && dalloc(ctx, &ctx->cvo_tape, (size_t)cfg->max_steps * P.E * Kc * 9) &&
@@ -602,7 +622,7 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<4, 16>, kWarps * 32, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<16>, kWarps * 32, 0);
   if (occ < 1) occ = 1;
   ctx->grid_tiles = dev_sms * (occ < 8 ? 8 : occ);
   if (reset_flags(ctx) != DM_OK) return ctx;
@@ -613,8 +633,8 @@ void dm_destroy(DmContext* ctx) {
   if (!ctx) return;
   void* ptrs[] = {ctx->store,     ctx->store_attr, ctx->seg,       ctx->seg_attr,   ctx->scratch[0], ctx->scratch[1],
                   ctx->scratch_attr[0], ctx->scratch_attr[1], ctx->adj[0], ctx->adj[1], ctx->part, ctx->keys,
-                  ctx->perm,      ctx->tile_start, ctx->tile_count, ctx->env_abase, ctx->env_acount, ctx->active,
-                  ctx->blocks,    ctx->ablocks,    ctx->tile_acc,   ctx->flags,      ctx->cvo_tape,  ctx->act_tape,
+                  ctx->perm,      ctx->ptile, ctx->tile_start, ctx->tile_count, ctx->env_abase, ctx->env_acount, ctx->active,
+                  ctx->blocks,    ctx->ablocks,    ctx->tile_acc,   ctx->gmp, ctx->gv, ctx->gmb,   ctx->flags,      ctx->cvo_tape,  ctx->act_tape,
                   ctx->obs_tape,  ctx->gcvo,       ctx->gact,       ctx->gmu,        ctx->glam};
   for (void* p : ptrs)
     if (p) cudaFree(p);

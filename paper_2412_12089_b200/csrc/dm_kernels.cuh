@@ -158,53 +158,65 @@ __device__ __forceinline__ void store_state(const StateView& S, size_t i, v3<flo
 }
 
 // ============================ binning ============================
-// One CTA per env: keys, interior check (p2g's stencil_base, mpm.hpp:149-161),
-// tile histogram, dense tile table, active-tile list, stable permutation.
+// One CTA per env (nw warps): keys + interior check (p2g's stencil_base,
+// mpm.hpp:149-161), per-warp tile histograms over contiguous particle chunks,
+// dense tile table, active-tile list, and a stable counting sort: every warp
+// scatters its chunk in index order from its own per-tile cursor, so the
+// permutation equals std::stable_sort by key.
 __global__ void __launch_bounds__(512) k_bin(DevParams P, StateView S, int* keys, int* perm, int* tile_start,
                                              int* tile_count, int2* active, int* env_abase, int* env_acount,
                                              DevFlags* flags, int substep, int check_vmax) {
-  extern __shared__ int sh[];
-  int* hist = sh;           // [Tn]
-  int* cursor = sh + P.Tn;  // [Tn]
+  extern __shared__ int cnt[];  // [nw][Tn]
   __shared__ int s_part[512 / 32 + 1][2];
   __shared__ int s_base;
   const int e = blockIdx.x;
+  const int nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const size_t base = (size_t)e * P.N;
-  for (int t = threadIdx.x; t < P.Tn; t += blockDim.x) hist[t] = 0;
+  for (int t = threadIdx.x; t < nw * P.Tn; t += blockDim.x) cnt[t] = 0;
   __syncthreads();
+  const int chunk = (P.N + nw - 1) / nw;
+  const int p0 = wid * chunk, p1 = min(P.N, p0 + chunk);
+  int* my = cnt + wid * P.Tn;
   float vmax = 0.f;
-  for (int p = threadIdx.x; p < P.N; p += blockDim.x) {
-    const size_t i = base + p;
-    float x[3] = {S.c(0, i), S.c(1, i), S.c(2, i)};
-    int b[3];
-    float fx[3];
-    const int bad = stencil_base(x, P.inv_dx, (double)P.dx, P.dims, b, fx);
-    if (bad >= 0) {
-      report(flags, e, substep, 0, attr_index(S.attr[i]), bad, kErrP2GInterior);
+  for (int c0 = p0; c0 < p1; c0 += 32) {
+    const int p = c0 + lane;
+    int key = -1 - lane;
+    if (p < p1) {
+      const size_t i = base + p;
+      float x[3] = {S.c(0, i), S.c(1, i), S.c(2, i)};
+      int b[3];
+      float fx[3];
+      const int bad = stencil_base(x, P.inv_dx, (double)P.dx, P.dims, b, fx);
+      if (bad >= 0) {
+        report(flags, e, substep, 0, attr_index(S.attr[i]), bad, kErrP2GInterior);
 #pragma unroll
-      for (int a = 0; a < 3; ++a) b[a] = b[a] < 1 ? 1 : (b[a] > P.dims[a] - 4 ? P.dims[a] - 4 : b[a]);
+        for (int a = 0; a < 3; ++a) b[a] = b[a] < 1 ? 1 : (b[a] > P.dims[a] - 4 ? P.dims[a] - 4 : b[a]);
+      }
+      key = ((b[0] >> 2) * P.td[1] + (b[1] >> 2)) * P.td[2] + (b[2] >> 2);
+      keys[i] = key;
+      if (check_vmax) vmax = fmaxf(vmax, fmaxf(fabsf(S.c(3, i)), fmaxf(fabsf(S.c(4, i)), fabsf(S.c(5, i)))));
     }
-    const int key = ((b[0] >> 2) * P.td[1] + (b[1] >> 2)) * P.td[2] + (b[2] >> 2);
-    keys[i] = key;
-    atomicAdd(&hist[key], 1);
-    if (check_vmax) vmax = fmaxf(vmax, fmaxf(fabsf(S.c(3, i)), fmaxf(fabsf(S.c(4, i)), fabsf(S.c(5, i)))));
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    if (p < p1 && lane == __ffs(peers) - 1) my[key] += __popc(peers);
+    __syncwarp();
   }
   if (check_vmax) {
     for (int o = 16; o > 0; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(&flags->vmax_bits, __float_as_uint(vmax));
+    if (lane == 0) atomicMax(&flags->vmax_bits, __float_as_uint(vmax));
   }
   __syncthreads();
-  // exclusive scan of (count, active) over Tn bins: each thread a contiguous chunk
+  // per bin: total count; exclusive scan over bins of (count, active)
   const int nt = blockDim.x;
   const int per = (P.Tn + nt - 1) / nt;
   const int t0 = threadIdx.x * per, t1 = min(P.Tn, t0 + per);
   int sc = 0, sa = 0;
   for (int t = t0; t < t1; ++t) {
-    sc += hist[t];
-    sa += hist[t] > 0;
+    int h = 0;
+    for (int w = 0; w < nw; ++w) h += cnt[w * P.Tn + t];
+    sc += h;
+    sa += h > 0;
   }
-  // block scan of per-thread sums (warp shuffles + one level)
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int ic = sc, ia = sa;
   for (int o = 1; o < 32; o <<= 1) {
     const int yc = __shfl_up_sync(0xffffffffu, ic, o);
@@ -221,7 +233,6 @@ __global__ void __launch_bounds__(512) k_bin(DevParams P, StateView S, int* keys
   __syncthreads();
   if (threadIdx.x == 0) {
     int rc = 0, ra = 0;
-    const int nw = nt / 32;
     for (int w = 0; w < nw; ++w) {
       const int c = s_part[w][0], a = s_part[w][1];
       s_part[w][0] = rc;
@@ -229,8 +240,6 @@ __global__ void __launch_bounds__(512) k_bin(DevParams P, StateView S, int* keys
       rc += c;
       ra += a;
     }
-    s_part[nw][0] = rc;
-    s_part[nw][1] = ra;
     s_base = atomicAdd(&flags->active_count, ra);
     env_abase[e] = s_base;
     env_acount[e] = ra;
@@ -239,40 +248,187 @@ __global__ void __launch_bounds__(512) k_bin(DevParams P, StateView S, int* keys
   int oc = s_part[wid][0] + ic - sc, oa = s_part[wid][1] + ia - sa;
   const size_t tb = (size_t)e * P.Tn;
   for (int t = t0; t < t1; ++t) {
-    const int c = hist[t];
-    tile_start[tb + t] = oc;
+    const int st = oc;
+    for (int w = 0; w < nw; ++w) {  // per-warp cursors in warp (= index) order
+      const int c = cnt[w * P.Tn + t];
+      cnt[w * P.Tn + t] = oc;
+      oc += c;
+    }
+    const int c = oc - st;
+    tile_start[tb + t] = st;
     tile_count[tb + t] = c;
-    cursor[t] = oc;
     if (c > 0) {
       active[s_base + oa] = make_int2(e, t);
       ++oa;
     }
-    oc += c;
   }
   __syncthreads();
-  // stable scatter (one warp, particles in index order)
-  if (wid == 0) {
-    for (int c0 = 0; c0 < P.N; c0 += 32) {
-      const int p = c0 + lane;
-      const int key = p < P.N ? keys[base + p] : -1 - lane;
-      const unsigned peers = __match_any_sync(0xffffffffu, key);
+  for (int c0 = p0; c0 < p1; c0 += 32) {
+    const int p = c0 + lane;
+    const int key = p < p1 ? keys[base + p] : -1 - lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const int leader = __ffs(peers) - 1;
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    int pos = 0;
+    if (lane == leader && p < p1) {
+      pos = my[key];
+      my[key] = pos + __popc(peers);
+    }
+    pos = __shfl_sync(0xffffffffu, pos, leader);
+    if (p < p1) perm[base + pos + rank] = (int)(base + p);
+    __syncwarp();
+  }
+}
+
+// Second sort level: within every active tile, a stable counting sort by the
+// cell inside the tile (64 buckets).  Final key = tile * 64 + cell; particles
+// of one cell become contiguous so the stencil scatters can accumulate runs in
+// registers.  Equals std::stable_sort by the full key (the tile pass is stable).
+__global__ void __launch_bounds__(kWarps * 32) k_cellsort(DevParams P, StateView S, const int* __restrict__ ptile,
+                                                          int* __restrict__ perm, int* __restrict__ keys,
+                                                          const int* __restrict__ tile_start,
+                                                          const int* __restrict__ tile_count,
+                                                          const int2* __restrict__ active, const DevFlags* flags) {
+  __shared__ int c64[kWarps][64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int* cnt = c64[warp];
+  const int n_active = *(const volatile int*)&flags->active_count;
+  for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
+    const int2 et = active[a];
+    const int e = et.x, t = et.y;
+    const size_t tix = (size_t)e * P.Tn + t;
+    const int start = tile_start[tix], n = tile_count[tix];
+    const size_t base = (size_t)e * P.N + start;
+    cnt[lane] = 0;
+    cnt[lane + 32] = 0;
+    __syncwarp();
+    auto cell_of = [&](int src) {
+      float x[3] = {S.c(0, src), S.c(1, src), S.c(2, src)};
+      int b[3];
+      float fx[3];
+      if (stencil_base(x, P.inv_dx, (double)P.dx, P.dims, b, fx) >= 0) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) b[d] = b[d] < 1 ? 1 : (b[d] > P.dims[d] - 4 ? P.dims[d] - 4 : b[d]);
+      }
+      return ((b[0] & 3) * 4 + (b[1] & 3)) * 4 + (b[2] & 3);
+    };
+    for (int c0 = 0; c0 < n; c0 += 32) {
+      const bool ok = c0 + lane < n;
+      const int cell = ok ? cell_of(ptile[base + c0 + lane]) : 64 + lane;
+      const unsigned peers = __match_any_sync(0xffffffffu, cell);
+      if (ok && lane == __ffs(peers) - 1) cnt[cell] += __popc(peers);
+      __syncwarp();
+    }
+    // exclusive scan over the 64 buckets (2 per lane)
+    const int a0 = cnt[2 * lane], a1 = cnt[2 * lane + 1];
+    int incl = a0 + a1;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int ex = incl - a0 - a1;
+    __syncwarp();
+    cnt[2 * lane] = ex;
+    cnt[2 * lane + 1] = ex + a0;
+    __syncwarp();
+    for (int c0 = 0; c0 < n; c0 += 32) {
+      const bool ok = c0 + lane < n;
+      const int src = ok ? ptile[base + c0 + lane] : 0;
+      const int cell = ok ? cell_of(src) : 64 + lane;
+      const unsigned peers = __match_any_sync(0xffffffffu, cell);
       const int leader = __ffs(peers) - 1;
       const int rank = __popc(peers & ((1u << lane) - 1u));
       int pos = 0;
-      if (lane == leader && p < P.N) {
-        pos = cursor[key];
-        cursor[key] = pos + __popc(peers);
+      if (ok && lane == leader) {
+        pos = cnt[cell];
+        cnt[cell] = pos + __popc(peers);
       }
       pos = __shfl_sync(0xffffffffu, pos, leader);
-      if (p < P.N) perm[base + pos + rank] = (int)(base + p);
+      if (ok) {
+        perm[base + pos + rank] = src;
+        keys[src] = t * 64 + cell;
+      }
       __syncwarp();
     }
   }
 }
 
+// ---- run-accumulated deterministic scatter ----
+// Phase 1 (lanes = particles) stages a payload per particle: the local base
+// node (linear in the 6^3 block), the 3x3 separable weights, and the affine
+// contribution (m, q, Ad) with node value w_o (m, q + Ad o).  Phase 2 (lanes =
+// the 27 stencil nodes) walks the chunk's particles in order; particles are
+// cell-sorted, so a lane accumulates the run of particles sharing a base cell
+// in registers and touches shared memory once per run.  Fixed order: no
+// atomics, bit-reproducible.
+struct RunAcc {
+  int cur;
+  float4 acc;
+};
+
+__device__ __forceinline__ void stage_payload(float* __restrict__ pp, int lbl, const Stencil<float>& sc, float m,
+                                              v3<float> q, const m3<float>& Ad) {
+  pp[0] = __int_as_float(lbl);
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    pp[1 + r] = sc.w[0][r];
+    pp[4 + r] = sc.w[1][r];
+    pp[7 + r] = sc.w[2][r];
+  }
+  pp[10] = m;
+  pp[11] = q.x;
+  pp[12] = q.y;
+  pp[13] = q.z;
+#pragma unroll
+  for (int r = 0; r < 9; ++r) pp[14 + r] = Ad.a[r];
+}
+
+__device__ __forceinline__ void run_flush(float4* __restrict__ blk, RunAcc& ra, int off) {
+  if (ra.cur >= 0) {
+    float4 b = blk[ra.cur + off];
+    b.x += ra.acc.x;
+    b.y += ra.acc.y;
+    b.z += ra.acc.z;
+    b.w += ra.acc.w;
+    blk[ra.cur + off] = b;
+  }
+  ra.acc = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+__device__ __forceinline__ void scatter_runs(float4* __restrict__ blk, const float* __restrict__ pay, int nv, int lane,
+                                             RunAcc& ra) {
+  if (lane < 27) {
+    const int oi = lane / 9, oj = (lane / 3) % 3, ok = lane % 3;
+    const int off = (oi * kExt + oj) * kExt + ok;
+    const float fo_i = (float)oi, fo_j = (float)oj, fo_k = (float)ok;
+    for (int k = 0; k < nv; ++k) {
+      const float* pk = pay + k * kPay;
+      const int lb = __float_as_int(pk[0]);
+      if (lb != ra.cur) {
+        run_flush(blk, ra, off);
+        ra.cur = lb;
+      }
+      const float w = pk[1 + oi] * pk[4 + oj] * pk[7 + ok];
+      const float cx = pk[11] + pk[14] * fo_i + pk[15] * fo_j + pk[16] * fo_k;
+      const float cy = pk[12] + pk[17] * fo_i + pk[18] * fo_j + pk[19] * fo_k;
+      const float cz = pk[13] + pk[20] * fo_i + pk[21] * fo_j + pk[22] * fo_k;
+      ra.acc.x += w * pk[10];
+      ra.acc.y += w * cx;
+      ra.acc.z += w * cy;
+      ra.acc.w += w * cz;
+    }
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void scatter_finish(float4* __restrict__ blk, int lane, RunAcc& ra) {
+  if (lane < 27) run_flush(blk, ra, ((lane / 9) * kExt + (lane / 3) % 3) * kExt + lane % 3);
+  __syncwarp();
+}
+
 // ============================ P2G ============================
-// Per active tile: stage particle payloads (lanes = particles), scatter into
-// the warp's 6^3 shared block (lanes = stencil nodes), write the block.
+// Per active tile: stage particle payloads (lanes = particles), scatter runs
+// into the warp's 6^3 shared block (lanes = stencil nodes), write the block.
 template <int MAXC>
 __global__ void __launch_bounds__(kWarps * 32) k_p2g(DevParams P, StateView S, const int* __restrict__ perm,
                                                      const int* __restrict__ tile_start,
@@ -284,9 +440,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_p2g(DevParams P, StateView S, c
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_active = *(volatile int*)&flags->active_count;
   const TransferCtx<float> T = tctx(P);
-  const int oi = lane / 9, oj = (lane / 3) % 3, ok = lane % 3;
-  float* pw = pay[warp];
   float4* bw = blk[warp];
+  float* pw = pay[warp];
   for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
     const int2 et = active[a];
     const int e = et.x, t = et.y;
@@ -295,7 +450,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_p2g(DevParams P, StateView S, c
     const size_t tix = (size_t)e * P.Tn + t;
     const int start = tile_start[tix], cnt = tile_count[tix];
     for (int i = lane; i < kExt3; i += 32) bw[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    __syncwarp();
+    RunAcc ra;
+    ra.cur = -1;
+    ra.acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int c0 = 0; c0 < cnt; c0 += 32) {
       if (c0 + lane < cnt) {
         const int src = perm[(size_t)e * P.N + start + c0 + lane];
@@ -314,113 +471,161 @@ __global__ void __launch_bounds__(kWarps * 32) k_p2g(DevParams P, StateView S, c
         v3<float> q;
         m3<float> Ad;
         p2g_payload(A, L.mass, v, sc, P.dx, q, Ad);
-        float* pp = pw + lane * kPay;
-        const int lb = tile_local(sc.base[0], o[0]) | (tile_local(sc.base[1], o[1]) << 8) | (tile_local(sc.base[2], o[2]) << 16);
-        pp[0] = __int_as_float(lb);
-#pragma unroll
-        for (int r = 0; r < 3; ++r) {
-          pp[1 + r] = sc.w[0][r];
-          pp[4 + r] = sc.w[1][r];
-          pp[7 + r] = sc.w[2][r];
-        }
-        pp[10] = L.mass;
-        pp[11] = q.x;
-        pp[12] = q.y;
-        pp[13] = q.z;
-#pragma unroll
-        for (int r = 0; r < 9; ++r) pp[14 + r] = Ad.a[r];
+        const int lbl = (tile_local(sc.base[0], o[0]) * kExt + tile_local(sc.base[1], o[1])) * kExt +
+                        tile_local(sc.base[2], o[2]);
+        stage_payload(pw + lane * kPay, lbl, sc, L.mass, q, Ad);
       }
       __syncwarp();
-      const int nv = min(32, cnt - c0);
-      if (lane < 27) {
-        const float fo_i = (float)oi, fo_j = (float)oj, fo_k = (float)ok;
-        for (int k = 0; k < nv; ++k) {
-          const float* pk = pw + k * kPay;
-          const int lb = __float_as_int(pk[0]);
-          const int nx = (lb & 0xff) + oi, ny = ((lb >> 8) & 0xff) + oj, nz = ((lb >> 16) & 0xff) + ok;
-          const float w = pk[1 + oi] * pk[4 + oj] * pk[7 + ok];
-          const float cx = pk[11] + pk[14] * fo_i + pk[15] * fo_j + pk[16] * fo_k;
-          const float cy = pk[12] + pk[17] * fo_i + pk[18] * fo_j + pk[19] * fo_k;
-          const float cz = pk[13] + pk[20] * fo_i + pk[21] * fo_j + pk[22] * fo_k;
-          const int nd = (nx * kExt + ny) * kExt + nz;
-          float4 b = bw[nd];
-          b.x += w * pk[10];
-          b.y += w * cx;
-          b.z += w * cy;
-          b.w += w * cz;
-          bw[nd] = b;
-          __syncwarp(0x07ffffffu);
-        }
-      }
-      __syncwarp();
+      scatter_runs(bw, pw, min(32, cnt - c0), lane, ra);
     }
+    scatter_finish(bw, lane, ra);
     float4* dst = blocks + tix * kExt3;
     for (int i = lane; i < kExt3; i += 32) dst[i] = bw[i];
     __syncwarp();
   }
 }
 
-// Sum the blocks covering global node g (ascending tile order); returns
-// whether any active tile covers it, and the first such tile (owner).
-__device__ __forceinline__ float4 gather_node(const DevParams& P, const int* __restrict__ tile_count,
-                                              const float4* __restrict__ blocks, int e, const int tc[3], const int g[3],
-                                              int* owner) {
+// ---- node ownership ----
+// A node is covered by the extended blocks of up to 2 tiles per axis; its
+// value is the sum of the covering active tiles' blocks in ascending tile
+// order and it is computed (owned) by the first active covering tile.
+// nbr: 27-bit activity mask of the 3x3x3 tile neighbourhood (bit = (rx+1)*9 +
+// (ry+1)*3 + (rz+1)).
+__device__ __forceinline__ unsigned neighbour_mask(const DevParams& P, const int* __restrict__ tile_count, int e,
+                                                   const int tc[3], int lane) {
+  bool act = false;
+  if (lane < 27) {
+    const int sx = tc[0] + lane / 9 - 1, sy = tc[1] + (lane / 3) % 3 - 1, sz = tc[2] + lane % 3 - 1;
+    if (sx >= 0 && sx < P.td[0] && sy >= 0 && sy < P.td[1] && sz >= 0 && sz < P.td[2])
+      act = tile_count[(size_t)e * P.Tn + (sx * P.td[1] + sy) * P.td[2] + sz] > 0;
+  }
+  return __ballot_sync(0xffffffffu, act);
+}
+
+// candidate range per axis for local coordinate a in [0, 6): rel in [lo, hi]
+__device__ __forceinline__ void cand_range(int a, int& lo, int& hi) {
+  lo = a < 2 ? -1 : 0;
+  hi = a >= 4 ? 1 : 0;
+}
+
+__device__ __forceinline__ bool owns_node(unsigned nbr, const int l[3]) {
+  int lo[3], hi[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) cand_range(l[d], lo[d], hi[d]);
+  for (int rx = lo[0]; rx <= hi[0]; ++rx)
+    for (int ry = lo[1]; ry <= hi[1]; ++ry)
+      for (int rz = lo[2]; rz <= hi[2]; ++rz) {
+        if (rx == 0 && ry == 0 && rz == 0) return true;  // reached self first
+        if (nbr & (1u << ((rx + 1) * 9 + (ry + 1) * 3 + (rz + 1)))) return false;
+      }
+  return true;
+}
+
+// Compacted list (ascending) of the tile's owned, in-grid nodes; returns count.
+__device__ __forceinline__ int owned_nodes(const DevParams& P, unsigned nbr, const int tc[3], short* list, int lane) {
+  __syncwarp();  // previous tile's readers are done with the list
+  int n = 0;
+  for (int i0 = 0; i0 < kExt3; i0 += 32) {
+    const int i = i0 + lane;
+    bool ok = false;
+    if (i < kExt3) {
+      const int l[3] = {i / 36, (i / 6) % 6, i % 6};
+      const int g[3] = {tc[0] * kTile + l[0], tc[1] * kTile + l[1], tc[2] * kTile + l[2]};
+      ok = g[0] < P.dims[0] && g[1] < P.dims[1] && g[2] < P.dims[2] && owns_node(nbr, l);
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, ok);
+    if (ok) list[n + __popc(b & ((1u << lane) - 1u))] = (short)i;
+    n += __popc(b);
+  }
+  __syncwarp();
+  return n;
+}
+
+__device__ __forceinline__ float4 sum_blocks(const DevParams& P, const float4* __restrict__ blocks, unsigned nbr, int e,
+                                             const int tc[3], const int l[3]) {
+  int lo[3], hi[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) cand_range(l[d], lo[d], hi[d]);
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  *owner = -1;
-  for (int sx = tc[0] - 1; sx <= tc[0] + 1; ++sx) {
-    const int lx = g[0] - sx * kTile;
-    if (sx < 0 || sx >= P.td[0] || lx < 0 || lx >= kExt) continue;
-    for (int sy = tc[1] - 1; sy <= tc[1] + 1; ++sy) {
-      const int ly = g[1] - sy * kTile;
-      if (sy < 0 || sy >= P.td[1] || ly < 0 || ly >= kExt) continue;
-      for (int sz = tc[2] - 1; sz <= tc[2] + 1; ++sz) {
-        const int lz = g[2] - sz * kTile;
-        if (sz < 0 || sz >= P.td[2] || lz < 0 || lz >= kExt) continue;
-        const int st = (sx * P.td[1] + sy) * P.td[2] + sz;
-        const size_t six = (size_t)e * P.Tn + st;
-        if (tile_count[six] == 0) continue;
-        if (*owner < 0) *owner = st;
-        const float4 b = blocks[six * kExt3 + (lx * kExt + ly) * kExt + lz];
+  for (int rx = lo[0]; rx <= hi[0]; ++rx)
+    for (int ry = lo[1]; ry <= hi[1]; ++ry)
+      for (int rz = lo[2]; rz <= hi[2]; ++rz) {
+        if (!(nbr & (1u << ((rx + 1) * 9 + (ry + 1) * 3 + (rz + 1))))) continue;
+        const int st = ((tc[0] + rx) * P.td[1] + (tc[1] + ry)) * P.td[2] + (tc[2] + rz);
+        const int lx = l[0] - 4 * rx, ly = l[1] - 4 * ry, lz = l[2] - 4 * rz;
+        const float4 b = blocks[((size_t)e * P.Tn + st) * kExt3 + (lx * kExt + ly) * kExt + lz];
         acc.x += b.x;
         acc.y += b.y;
         acc.z += b.z;
         acc.w += b.w;
       }
-    }
-  }
   return acc;
 }
 
-// ============================ G2P ============================
+__device__ __forceinline__ size_t node_lin(const DevParams& P, int e, const int g[3]) {
+  return (size_t)e * P.dims[0] * P.dims[1] * P.dims[2] + ((size_t)g[0] * P.dims[1] + g[1]) * P.dims[2] + g[2];
+}
+
+// ============================ grid update ============================
+// Owned nodes of every active tile: sum the covering blocks, update
+// (mpm.hpp:256-305 + extensions), write (mass, momentum) and velocity to the
+// dense per-env grid.
 template <int MAXC>
+__global__ void __launch_bounds__(kWarps * 32) k_grid(DevParams P, const int* __restrict__ tile_count,
+                                                      const int2* __restrict__ active, const float* __restrict__ cvo,
+                                                      const float4* __restrict__ blocks, float4* __restrict__ gmp,
+                                                      float4* __restrict__ gv, const DevFlags* flags) {
+  __shared__ short own[kWarps][kExt3];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_active = *(const volatile int*)&flags->active_count;
+  const NodeCtx<float> G = nctx(P);
+  for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
+    const int2 et = active[a];
+    const int e = et.x, t = et.y;
+    const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
+    const unsigned nbr = neighbour_mask(P, tile_count, e, tc, lane);
+    Col<float> cols[MAXC];
+    load_cols<MAXC>(P, cvo + (size_t)e * P.K * 9, cols);
+    const int n_own = owned_nodes(P, nbr, tc, own[warp], lane);
+    for (int q = lane; q < n_own; q += 32) {
+      const int i = own[warp][q];
+      const int l[3] = {i / 36, (i / 6) % 6, i % 6};
+      const int g[3] = {tc[0] * kTile + l[0], tc[1] * kTile + l[1], tc[2] * kTile + l[2]};
+      const float4 mm = sum_blocks(P, blocks, nbr, e, tc, l);
+      const v3<float> v = node_update<float, MAXC>(G, cols, P.K, g, mm.x, mk3(mm.y, mm.z, mm.w));
+      const size_t n = node_lin(P, e, g);
+      gmp[n] = mm;
+      gv[n] = make_float4(v.x, v.y, v.z, 0.f);
+    }
+  }
+}
+
+// Loads the tile's 6^3 block of a dense grid into shared memory.
+__device__ __forceinline__ void load_tile_grid(const DevParams& P, const float4* __restrict__ grid, int e,
+                                               const int o[3], float4* dst, int lane) {
+  for (int i = lane; i < kExt3; i += 32) {
+    const int g[3] = {o[0] + i / 36, o[1] + (i / 6) % 6, o[2] + i % 6};
+    dst[i] = (g[0] < P.dims[0] && g[1] < P.dims[1] && g[2] < P.dims[2]) ? grid[node_lin(P, e, g)]
+                                                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// ============================ G2P ============================
 __global__ void __launch_bounds__(kWarps * 32) k_g2p(DevParams P, StateView S, StateView Sout,
                                                      const int* __restrict__ perm, const int* __restrict__ tile_start,
                                                      const int* __restrict__ tile_count, const int2* __restrict__ active,
-                                                     const float* __restrict__ cvo, const float4* __restrict__ blocks,
-                                                     DevFlags* flags, int substep) {
+                                                     const float4* __restrict__ gv, DevFlags* flags, int substep) {
   __shared__ float4 vg[kWarps][kExt3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_active = *(volatile int*)&flags->active_count;
   const TransferCtx<float> T = tctx(P);
-  const NodeCtx<float> G = nctx(P);
   float4* vw = vg[warp];
   for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
     const int2 et = active[a];
     const int e = et.x, t = et.y;
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
-    Col<float> cols[MAXC];
-    load_cols<MAXC>(P, cvo + (size_t)e * P.K * 9, cols);
-    for (int i = lane; i < kExt3; i += 32) {
-      const int g[3] = {o[0] + i / 36, o[1] + (i / 6) % 6, o[2] + i % 6};
-      v3<float> v = zero3<float>();
-      if (g[0] < P.dims[0] && g[1] < P.dims[1] && g[2] < P.dims[2]) {
-        int own;
-        const float4 mm = gather_node(P, tile_count, blocks, e, tc, g, &own);
-        v = node_update<float, MAXC>(G, cols, P.K, g, mm.x, mk3(mm.y, mm.z, mm.w));
-      }
-      vw[i] = make_float4(v.x, v.y, v.z, 0.f);
-    }
+    load_tile_grid(P, gv, e, o, vw, lane);
     __syncwarp();
     const size_t tix = (size_t)e * P.Tn + t;
     const int start = tile_start[tix], cnt = tile_count[tix];
@@ -441,7 +646,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_g2p(DevParams P, StateView S, S
       };
       v3<float> xn = mk3(x[0], x[1], x[2]);
       bool bad_adv = false, bad_det = false;
-      g2p_particle(P.law[attr_mat(at)], T, sc, getv, xn, v, C, F, &bad_adv, &bad_det);
+      g2p_particle_sep(P.law[attr_mat(at)], T, sc, getv, xn, v, C, F, &bad_adv, &bad_det);
       if (bad_adv) report(flags, e, substep, 1, attr_index(at), 0, kErrG2PInterior);
       if (bad_det) report(flags, e, substep, 1, attr_index(at), attr_mat(at), kErrDetF);
       store_state(Sout, dst, xn, v, F, C);
@@ -455,48 +660,36 @@ __global__ void __launch_bounds__(kWarps * 32) k_g2p(DevParams P, StateView S, S
 // Reads the start-of-substep state (via perm) and the cotangent of the
 // end-of-substep state (sorted position); writes particle-side partial
 // cotangents (sorted position) and a 6^3 block of node-velocity cotangents.
-template <int MAXC>
-__global__ void __launch_bounds__(kWarps * 32) k_g2p_adj(DevParams P, StateView S, const float* __restrict__ adj_in,
+__global__ void __launch_bounds__(kWarps * 32, 4) k_g2p_adj(DevParams P, StateView S, const float* __restrict__ adj_in,
                                                          size_t astride, const int* __restrict__ perm,
                                                          const int* __restrict__ tile_start,
                                                          const int* __restrict__ tile_count,
-                                                         const int2* __restrict__ active, const float* __restrict__ cvo,
-                                                         const float4* __restrict__ blocks, float4* __restrict__ ablocks,
-                                                         float* __restrict__ part, float* __restrict__ tile_acc,
-                                                         const DevFlags* flags) {
+                                                         const int2* __restrict__ active, const float4* __restrict__ gv,
+                                                         float4* __restrict__ ablocks, float* __restrict__ part,
+                                                         float* __restrict__ tile_acc, const DevFlags* flags) {
   __shared__ float4 vg[kWarps][kExt3];
   __shared__ float4 ab[kWarps][kExt3];
   __shared__ float pay[kWarps][32 * kPay];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TransferCtx<float> T = tctx(P);
-  const NodeCtx<float> G = nctx(P);
   float4* vw = vg[warp];
   float4* aw = ab[warp];
   float* pw = pay[warp];
-  const int oi = lane / 9, oj = (lane / 3) % 3, ok = lane % 3;
   const int n_active = *(const volatile int*)&flags->active_count;
   for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
     const int2 et = active[a];
     const int e = et.x, t = et.y;
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
-    Col<float> cols[MAXC];
-    load_cols<MAXC>(P, cvo + (size_t)e * P.K * 9, cols);
-    for (int i = lane; i < kExt3; i += 32) {
-      const int g[3] = {o[0] + i / 36, o[1] + (i / 6) % 6, o[2] + i % 6};
-      v3<float> v = zero3<float>();
-      if (g[0] < P.dims[0] && g[1] < P.dims[1] && g[2] < P.dims[2]) {
-        int own;
-        const float4 mm = gather_node(P, tile_count, blocks, e, tc, g, &own);
-        v = node_update<float, MAXC>(G, cols, P.K, g, mm.x, mk3(mm.y, mm.z, mm.w));
-      }
-      vw[i] = make_float4(v.x, v.y, v.z, 0.f);
-      aw[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    load_tile_grid(P, gv, e, o, vw, lane);
+    for (int i = lane; i < kExt3; i += 32) aw[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncwarp();
     const size_t tix = (size_t)e * P.Tn + t;
     const int start = tile_start[tix], cnt = tile_count[tix];
-    float mub[4] = {0.f, 0.f, 0.f, 0.f};
+    double mub[4] = {0.0, 0.0, 0.0, 0.0};  // fp64: cancelling per-particle sums
+    RunAcc ra;
+    ra.cur = -1;
+    ra.acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int c0 = 0; c0 < cnt; c0 += 32) {
       if (c0 + lane < cnt) {
         const size_t dst = (size_t)e * P.N + start + c0 + lane;
@@ -525,7 +718,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_g2p_adj(DevParams P, StateView 
         m3<float> Fp, Bd;
         const int mi = attr_mat(at);
         float mu_l = 0.f;
-        g2p_vjp(P.law[mi], T, sc, getv, F, xb, vb, Cb, Fb, xp, Fp, gq, Bd, mu_l);
+        g2p_vjp_sep(P.law[mi], T, sc, getv, F, xb, vb, Cb, Fb, xp, Fp, gq, Bd, mu_l);
 #pragma unroll
         for (int m = 0; m < 4; ++m)
           if (m == mi) mub[m] += mu_l;
@@ -534,40 +727,12 @@ __global__ void __launch_bounds__(kWarps * 32) k_g2p_adj(DevParams P, StateView 
         part[2 * astride + dst] = xp.z;
 #pragma unroll
         for (int q = 0; q < 9; ++q) part[(3 + q) * astride + dst] = Fp.a[q];
-        float* pp = pw + lane * kPay;
-        pp[0] = __int_as_float(lb[0] | (lb[1] << 8) | (lb[2] << 16));
-#pragma unroll
-        for (int r = 0; r < 3; ++r) {
-          pp[1 + r] = sc.w[0][r];
-          pp[4 + r] = sc.w[1][r];
-          pp[7 + r] = sc.w[2][r];
-        }
-        pp[11] = gq.x;
-        pp[12] = gq.y;
-        pp[13] = gq.z;
-#pragma unroll
-        for (int r = 0; r < 9; ++r) pp[14 + r] = Bd.a[r];
+        stage_payload(pw + lane * kPay, (lb[0] * kExt + lb[1]) * kExt + lb[2], sc, 0.f, gq, Bd);
       }
       __syncwarp();
-      const int nv = min(32, cnt - c0);
-      if (lane < 27) {
-        const float fo_i = (float)oi, fo_j = (float)oj, fo_k = (float)ok;
-        for (int k = 0; k < nv; ++k) {
-          const float* pk = pw + k * kPay;
-          const int lb = __float_as_int(pk[0]);
-          const int nx = (lb & 0xff) + oi, ny = ((lb >> 8) & 0xff) + oj, nz = ((lb >> 16) & 0xff) + ok;
-          const float w = pk[1 + oi] * pk[4 + oj] * pk[7 + ok];
-          const int nd = (nx * kExt + ny) * kExt + nz;
-          float4 b = aw[nd];
-          b.x += w * (pk[11] + pk[14] * fo_i + pk[15] * fo_j + pk[16] * fo_k);
-          b.y += w * (pk[12] + pk[17] * fo_i + pk[18] * fo_j + pk[19] * fo_k);
-          b.z += w * (pk[13] + pk[20] * fo_i + pk[21] * fo_j + pk[22] * fo_k);
-          aw[nd] = b;
-          __syncwarp(0x07ffffffu);
-        }
-      }
-      __syncwarp();
+      scatter_runs(aw, pw, min(32, cnt - c0), lane, ra);
     }
+    scatter_finish(aw, lane, ra);
     float4* dst = ablocks + tix * kExt3;
     for (int i = lane; i < kExt3; i += 32) dst[i] = aw[i];
 #pragma unroll
@@ -575,27 +740,74 @@ __global__ void __launch_bounds__(kWarps * 32) k_g2p_adj(DevParams P, StateView 
       for (int off = 16; off > 0; off >>= 1) mub[m] += __shfl_xor_sync(0xffffffffu, mub[m], off);
     if (lane == 0)
 #pragma unroll
-      for (int m = 0; m < 4; ++m) tile_acc[tix * kNacc + kAccMuG + m] = mub[m];
+      for (int m = 0; m < 4; ++m) tile_acc[tix * kNacc + kAccMuG + m] = (float)mub[m];
+    __syncwarp();
+  }
+}
+
+// ============================ grid adjoint ============================
+// Owned nodes: node-velocity cotangent (sum of the covering adjoint blocks)
+// -> (mass, momentum) cotangents in the dense grid; collider cotangents
+// reduced per tile (each node counted once, by its owner).
+template <int MAXC>
+__global__ void __launch_bounds__(kWarps * 32) k_grid_adj(DevParams P, const int* __restrict__ tile_count,
+                                                          const int2* __restrict__ active, const float* __restrict__ cvo,
+                                                          const float4* __restrict__ ablocks,
+                                                          const float4* __restrict__ gmp, float4* __restrict__ gmb,
+                                                          float* __restrict__ tile_acc, const DevFlags* flags) {
+  __shared__ short own[kWarps][kExt3];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_active = *(const volatile int*)&flags->active_count;
+  const NodeCtx<float> G = nctx(P);
+  for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
+    const int2 et = active[a];
+    const int e = et.x, t = et.y;
+    const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
+    const unsigned nbr = neighbour_mask(P, tile_count, e, tc, lane);
+    Col<float> cols[MAXC];
+    load_cols<MAXC>(P, cvo + (size_t)e * P.K * 9, cols);
+    float cg[MAXC * 9];
+#pragma unroll
+    for (int q = 0; q < MAXC * 9; ++q) cg[q] = 0.f;
+    const int n_own = owned_nodes(P, nbr, tc, own[warp], lane);
+    for (int q = lane; q < n_own; q += 32) {
+      const int i = own[warp][q];
+      const int l[3] = {i / 36, (i / 6) % 6, i % 6};
+      const int g[3] = {tc[0] * kTile + l[0], tc[1] * kTile + l[1], tc[2] * kTile + l[2]};
+      const float4 vb = sum_blocks(P, ablocks, nbr, e, tc, l);
+      const size_t n = node_lin(P, e, g);
+      const float4 mm = gmp[n];
+      float mbar;
+      v3<float> pbar;
+      // adjoint blocks carry (unused, vbar.x, vbar.y, vbar.z) -- emit_contrib layout
+      node_update_vjp<float, MAXC>(G, cols, P.K, g, mm.x, mk3(mm.y, mm.z, mm.w), mk3(vb.y, vb.z, vb.w), mbar, pbar,
+                                   cg);
+      gmb[n] = make_float4(mbar, pbar.x, pbar.y, pbar.z);
+    }
+#pragma unroll
+    for (int q = 0; q < MAXC * 9; ++q)
+      for (int off = 16; off > 0; off >>= 1) cg[q] += __shfl_xor_sync(0xffffffffu, cg[q], off);
+    if (lane == 0) {
+      float* ta = tile_acc + ((size_t)e * P.Tn + t) * kNacc;
+#pragma unroll
+      for (int q = 0; q < MAXC * 9; ++q) ta[kAccCol + q] = cg[q];
+    }
     __syncwarp();
   }
 }
 
 // ============================ P2G adjoint ============================
-template <int MAXC, int NG>
-__global__ void __launch_bounds__(kWarps * 32) k_p2g_adj(DevParams P, StateView S, const int* __restrict__ perm,
+template <int NG>
+__global__ void __launch_bounds__(kWarps * 32, 4) k_p2g_adj(DevParams P, StateView S, const int* __restrict__ perm,
                                                          const int* __restrict__ tile_start,
                                                          const int* __restrict__ tile_count,
-                                                         const int2* __restrict__ active, const float* __restrict__ cvo,
-                                                         const float* __restrict__ act,
-                                                         const float4* __restrict__ blocks,
-                                                         const float4* __restrict__ ablocks,
-                                                         const float* __restrict__ part, float* __restrict__ adj_out,
-                                                         size_t astride, float* __restrict__ tile_acc,
-                                                         const DevFlags* flags) {
+                                                         const int2* __restrict__ active, const float* __restrict__ act,
+                                                         const float4* __restrict__ gmb, const float* __restrict__ part,
+                                                         float* __restrict__ adj_out, size_t astride,
+                                                         float* __restrict__ tile_acc, const DevFlags* flags) {
   __shared__ float4 mb[kWarps][kExt3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TransferCtx<float> T = tctx(P);
-  const NodeCtx<float> G = nctx(P);
   float4* bw = mb[warp];
   const int n_active = *(const volatile int*)&flags->active_count;
   for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
@@ -603,36 +815,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_p2g_adj(DevParams P, StateView 
     const int e = et.x, t = et.y;
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
-    Col<float> cols[MAXC];
-    load_cols<MAXC>(P, cvo + (size_t)e * P.K * 9, cols);
-    float cg[MAXC * 9];
-#pragma unroll
-    for (int q = 0; q < MAXC * 9; ++q) cg[q] = 0.f;
-    for (int i = lane; i < kExt3; i += 32) {
-      const int g[3] = {o[0] + i / 36, o[1] + (i / 6) % 6, o[2] + i % 6};
-      float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (g[0] < P.dims[0] && g[1] < P.dims[1] && g[2] < P.dims[2]) {
-        int own, own2;
-        const float4 mm = gather_node(P, tile_count, blocks, e, tc, g, &own);
-        const float4 vb = gather_node(P, tile_count, ablocks, e, tc, g, &own2);
-        float mbar;
-        v3<float> pbar;
-        float cgl[MAXC * 9];
-#pragma unroll
-        for (int q = 0; q < MAXC * 9; ++q) cgl[q] = 0.f;
-        node_update_vjp<float, MAXC>(G, cols, P.K, g, mm.x, mk3(mm.y, mm.z, mm.w), mk3(vb.x, vb.y, vb.z), mbar,
-                                     pbar, cgl);
-        if (own == t)
-#pragma unroll
-          for (int q = 0; q < MAXC * 9; ++q) cg[q] += cgl[q];
-        out = make_float4(mbar, pbar.x, pbar.y, pbar.z);
-      }
-      bw[i] = out;
-    }
+    load_tile_grid(P, gmb, e, o, bw, lane);
     __syncwarp();
     const size_t tix = (size_t)e * P.Tn + t;
     const int start = tile_start[tix], cnt = tile_count[tix];
-    float mub[4] = {0.f, 0.f, 0.f, 0.f}, lab[4] = {0.f, 0.f, 0.f, 0.f};
+    double mub[4] = {0.0, 0.0, 0.0, 0.0}, lab[4] = {0.0, 0.0, 0.0, 0.0};  // fp64: cancelling sums
     float actb[NG];
 #pragma unroll
     for (int q = 0; q < NG; ++q) actb[q] = 0.f;
@@ -660,7 +847,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_p2g_adj(DevParams P, StateView 
       const int mi = attr_mat(at), gi = min(attr_group(at), P.G > 0 ? P.G - 1 : 0);
       const float av = act ? act[e * P.G + gi] : 0.f;
       float mu_l = 0.f, la_l = 0.f, ac_l = 0.f;
-      p2g_vjp(P.law[mi], T, sc, getmb, v, F, C, av, xb, vb, Fb, Cb, mu_l, la_l, ac_l);
+      p2g_vjp_sep(P.law[mi], T, sc, getmb, v, F, C, av, xb, vb, Fb, Cb, mu_l, la_l, ac_l);
 #pragma unroll
       for (int m = 0; m < 4; ++m)
         if (m == mi) {
@@ -682,7 +869,6 @@ __global__ void __launch_bounds__(kWarps * 32) k_p2g_adj(DevParams P, StateView 
         adj_out[(15 + q) * astride + src] = Cb.a[q];
       }
     }
-    // warp reductions (fixed butterfly order -> deterministic)
 #pragma unroll
     for (int m = 0; m < 4; ++m)
       for (int off = 16; off > 0; off >>= 1) {
@@ -692,18 +878,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_p2g_adj(DevParams P, StateView 
 #pragma unroll
     for (int q = 0; q < NG; ++q)
       for (int off = 16; off > 0; off >>= 1) actb[q] += __shfl_xor_sync(0xffffffffu, actb[q], off);
-#pragma unroll
-    for (int q = 0; q < MAXC * 9; ++q)
-      for (int off = 16; off > 0; off >>= 1) cg[q] += __shfl_xor_sync(0xffffffffu, cg[q], off);
     if (lane == 0) {
       float* ta = tile_acc + tix * kNacc;
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
-        ta[kAccMu + m] = mub[m];
-        ta[kAccLam + m] = lab[m];
+        ta[kAccMu + m] = (float)mub[m];
+        ta[kAccLam + m] = (float)lab[m];
       }
-#pragma unroll
-      for (int q = 0; q < MAXC * 9; ++q) ta[kAccCol + q] = cg[q];
 #pragma unroll
       for (int q = 0; q < NG; ++q) ta[kAccAct + q] = actb[q];
     }
@@ -720,7 +901,7 @@ __global__ void k_env_reduce(DevParams P, const int2* __restrict__ active, const
   const int e = blockIdx.x, f = threadIdx.x;
   if (f >= kNacc) return;
   const int b = env_abase[e], n = env_acount[e];
-  float s = 0.f;
+  double s = 0.0;
   for (int i = 0; i < n; ++i) {
     const int2 et = active[b + i];
     s += tile_acc[((size_t)et.x * P.Tn + et.y) * kNacc + f];

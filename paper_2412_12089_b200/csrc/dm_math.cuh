@@ -10,8 +10,12 @@
 
 #ifdef __CUDACC__
 #define DM_HD __host__ __device__ __forceinline__
+// large, rarely-hot helpers kept out of line: one copy of the collider code
+// instead of one per call site keeps the grid kernels inside the I-cache
+#define DM_HD_NOINLINE __host__ __device__ __noinline__
 #else
 #define DM_HD inline
+#define DM_HD_NOINLINE inline
 #endif
 
 namespace dm {

@@ -417,7 +417,7 @@ DM_HD v3<R> cyl_query_vjp(const CylQ<R>& c, R dbar, v3<R> nbar) {
 
 // Query: d, n at point p; relb(dbar, nbar) computed by collider_query_vjp.
 template <class R>
-DM_HD void collider_query(const Col<R>& col, v3<R> p, R& d, v3<R>& n) {
+DM_HD_NOINLINE void collider_query(const Col<R>& col, v3<R> p, R& d, v3<R>& n) {
   const v3<R> rel = p - col.c;
   switch (col.kind) {
     case kPlane:
@@ -464,7 +464,7 @@ DM_HD void collider_query(const Col<R>& col, v3<R> p, R& d, v3<R>& n) {
 
 // Returns pbar (gradient w.r.t. the query point; center gets -pbar).
 template <class R>
-DM_HD v3<R> collider_query_vjp(const Col<R>& col, v3<R> p, R dbar, v3<R> nbar) {
+DM_HD_NOINLINE v3<R> collider_query_vjp(const Col<R>& col, v3<R> p, R dbar, v3<R> nbar) {
   const v3<R> rel = p - col.c;
   switch (col.kind) {
     case kPlane:
@@ -523,7 +523,7 @@ DM_HD v3<R> collide(const Col<R>& col, R alpha_c, R mu_b, v3<R> node, v3<R> v) {
 // Adjoint of collide: given vout_bar, returns v_bar and accumulates the
 // collider's center / velocity / omega cotangents.
 template <class R>
-DM_HD v3<R> collide_vjp(const Col<R>& col, R alpha_c, R mu_b, v3<R> node, v3<R> v, v3<R> vb_out, v3<R>& cbar,
+DM_HD_NOINLINE v3<R> collide_vjp(const Col<R>& col, R alpha_c, R mu_b, v3<R> node, v3<R> v, v3<R> vb_out, v3<R>& cbar,
                         v3<R>& velbar, v3<R>& ombar) {
   R d;
   v3<R> n;

@@ -5,7 +5,7 @@ Run here (the reference is not on the GPU box): python tests/golden/make_golden.
 Contents:
   in_x/v/F/C, ref_x/v/F/C : 8 substeps of the reference mpm_step<double>
                             (elastoplastic, moving sphere, slip boundary)
-  bin_x, bin_keys, bin_perm: fp32 positions, 4^3-tile keys and stable
+  bin_x, bin_keys, bin_perm: fp32 positions, (4^3 tile, cell) keys and stable
                             permutation computed independently in numpy
 """
 import os
@@ -28,7 +28,8 @@ ref, _ = O.ref_rollout(sim, mats, cols, st, 8)
 
 bx = (0.1 + 0.8 * rng.random((2000, 3))).astype(np.float32)
 g = np.floor((bx * np.float32(48.0)).astype(np.float32) - np.float32(0.5)).astype(np.int64)
-keys = (((g[:, 0] >> 2) * 12 + (g[:, 1] >> 2)) * 12 + (g[:, 2] >> 2)).astype(np.int32)
+keys = ((((g[:, 0] >> 2) * 12 + (g[:, 1] >> 2)) * 12 + (g[:, 2] >> 2)) * 64 +
+        ((g[:, 0] & 3) * 4 + (g[:, 1] & 3)) * 4 + (g[:, 2] & 3)).astype(np.int32)
 perm = np.argsort(keys, kind="stable").astype(np.int32)
 np.savez_compressed(os.path.join(HERE, "oracle_golden.npz"),
                     **{"in_" + k: st[k] for k in "xvFC"}, **{"ref_" + k: ref[k] for k in "xvFC"},

@@ -159,7 +159,7 @@ void substep(const Setup& s, St& st, int n, const int* mat, const int* grp, cons
     m3<R> F, C;
     for (int i = 0; i < 9; ++i) F.a[i] = st.F[9 * p + i];
     bool ba = false, bd = false;
-    g2p_particle(s.laws[mat[p]], s.t, sc, getv, x, v, C, F, &ba, &bd);
+    g2p_particle_sep(s.laws[mat[p]], s.t, sc, getv, x, v, C, F, &ba, &bd);
     if (ba) throw std::runtime_error("g2p: particle " + std::to_string(p) + " advected outside grid interior");
     for (int a = 0; a < 3; ++a) {
       st.x[3 * p + a] = x[a];
@@ -286,7 +286,7 @@ extern "C" int hc_rollout(const OrSim* sim, const OrMat* mats, int nmat, const O
           }
           v3<R> xp, gq;
           m3<R> Fp, Bd;
-          g2p_vjp(s.laws[material[p]], s.t, sc, getv, Fm, mk3(bar.x[3 * p], bar.x[3 * p + 1], bar.x[3 * p + 2]),
+          g2p_vjp_sep(s.laws[material[p]], s.t, sc, getv, Fm, mk3(bar.x[3 * p], bar.x[3 * p + 1], bar.x[3 * p + 2]),
                   mk3(bar.v[3 * p], bar.v[3 * p + 1], bar.v[3 * p + 2]), Cb, Fb, xp, Fp, gq, Bd, mub[material[p]]);
           for (int a2 = 0; a2 < 3; ++a2) xpart[3 * p + a2] = xp[a2];
           for (int i = 0; i < 9; ++i) Fpart[9 * p + i] = Fp.a[i];
@@ -341,7 +341,7 @@ extern "C" int hc_rollout(const OrSim* sim, const OrMat* mats, int nmat, const O
           v3<R> xb = mk3(xpart[3 * p], xpart[3 * p + 1], xpart[3 * p + 2]), vb = zero3<R>();
           R actb = 0.0;
           const R av = a ? a[group[p]] : 0.0;
-          p2g_vjp(s.laws[material[p]], s.t, sc, getmb, mk3(s0.v[3 * p], s0.v[3 * p + 1], s0.v[3 * p + 2]), Fm, Cm, av,
+          p2g_vjp_sep(s.laws[material[p]], s.t, sc, getmb, mk3(s0.v[3 * p], s0.v[3 * p + 1], s0.v[3 * p + 2]), Fm, Cm, av,
                   xb, vb, Fb, Cb, mub[material[p]], lamb[material[p]], actb);
           if (nact) gact[t * nact + group[p]] += actb;
           for (int a2 = 0; a2 < 3; ++a2) {

@@ -410,6 +410,7 @@ def test_sort_keys_and_stability():
     x = (0.1 + 0.8 * rng.random((5000, 3))).astype(np.float32)
     keys = O.bin_keys(sim, x)
     b = np.floor((x * np.float32(48.0)).astype(np.float32) - np.float32(0.5)).astype(int)
-    assert np.array_equal(keys, ((b[:, 0] >> 2) * 12 + (b[:, 1] >> 2)) * 12 + (b[:, 2] >> 2))
+    assert np.array_equal(keys, (((b[:, 0] >> 2) * 12 + (b[:, 1] >> 2)) * 12 + (b[:, 2] >> 2)) * 64 +
+                          ((b[:, 0] & 3) * 4 + (b[:, 1] & 3)) * 4 + (b[:, 2] & 3))
     perm = O.stable_sort(keys)
     assert np.array_equal(perm, np.argsort(keys, kind="stable"))
