@@ -49,3 +49,16 @@ def rollout(O, sim, mats, cols, state, n_ctrl, n_sub, act=None, loss=None, dobs_
         raise RuntimeError(err.value.decode())
     return {"obs": obs, "x": g[0], "v": g[1], "F": g[2], "C": g[3], "cvo": gcvo[:, :len(cols)], "act": gact[:, :nact],
             "E": gE[:len(mats)]}
+
+
+def build_cpp_smoke():
+    """Builds tests/native/cpp_adapter_smoke against the in-tree libdiffmpm.so."""
+    root = os.path.dirname(os.path.dirname(HERE))
+    exe = os.path.join(HERE, "cpp_adapter_smoke")
+    src = os.path.join(HERE, "cpp_adapter_smoke.cpp")
+    libdir = os.path.join(root, "paper_2412_12089_b200")
+    deps = [src, os.path.join(root, "include", "diffmpm", "mpm_batch.hpp"), os.path.join(root, "include", "diffmpm.h")]
+    if not os.path.exists(exe) or os.path.getmtime(exe) < max(os.path.getmtime(d) for d in deps):
+        subprocess.check_call(["g++", "-std=c++17", "-O2", "-I", os.path.join(root, "include"), "-o", exe, src,
+                               "-L", libdir, "-ldiffmpm", f"-Wl,-rpath,{libdir}", "-Wl,-rpath,$ORIGIN/../../paper_2412_12089_b200"])
+    return exe
