@@ -44,9 +44,20 @@ struct DmContext {
   uint32_t* scratch_attr[2] = {nullptr, nullptr};
   float* adj[2] = {nullptr, nullptr};  // [24][Ntot]
   float* part = nullptr;               // [12][Ntot]
-  int *keys = nullptr, *perm = nullptr, *ptile = nullptr, *tile_start = nullptr, *tile_count = nullptr;
-  int *env_abase = nullptr, *env_acount = nullptr;
-  int2* active = nullptr;
+  int *keys = nullptr, *ptile = nullptr;  // sort scratch
+  // sort artifacts per substep slot of a recompute segment ([ck][...]); the
+  // forward pass uses slot 0, a segment replay fills slot q for substep s0+q
+  int *perm_all = nullptr, *tstart_all = nullptr, *tcount_all = nullptr;
+  int *abase_all = nullptr, *acount_all = nullptr, *nact_all = nullptr;
+  int2* active_all = nullptr;
+  // per active tile (by slot) 6^3 grid blocks of the replayed substeps:
+  // velocity and (mass, momentum), read by the adjoint substep instead of
+  // re-running bin / p2g / grid
+  float4 *gvb_pool = nullptr, *gmpb_pool = nullptr;
+  size_t blk_cap = 0;
+  int max_active_seen = 0;
+  float* tail = nullptr;  // replay output of a segment's last substep
+  uint32_t* tail_attr = nullptr;
   float4 *blocks = nullptr, *ablocks = nullptr;
   float4 *gmp = nullptr, *gv = nullptr, *gmb = nullptr;  // dense per-env grids
   int bin_warps = 16;
@@ -142,14 +153,42 @@ void prof_flush(DmContext* c) {
 #define PROF_BEGIN(c, cls) prof_mark(c, cls)
 #define PROF_END(c, cls) prof_mark(c, cls)
 
-void launch_bin(DmContext* c, const StateView& S, int sub, int check_vmax) {
-  cudaMemsetAsync(&c->flags->active_count, 0, sizeof(int), c->stream);
+struct Slot {
+  int* perm;
+  int* tile_start;
+  int* tile_count;
+  int2* active;
+  int* env_abase;
+  int* env_acount;
+  int* nact;
+  float4* gvb;   // per-slot grid blocks (replay only)
+  float4* gmpb;
+};
+
+Slot slot(DmContext* c, int q) {
+  const size_t TT = (size_t)c->P.E * c->P.Tn;
+  Slot s;
+  s.perm = c->perm_all + (size_t)q * c->Ntot;
+  s.tile_start = c->tstart_all + (size_t)q * TT;
+  s.tile_count = c->tcount_all + (size_t)q * TT;
+  s.active = c->active_all + (size_t)q * TT;
+  s.env_abase = c->abase_all + (size_t)q * c->P.E;
+  s.env_acount = c->acount_all + (size_t)q * c->P.E;
+  s.nact = c->nact_all + q;
+  s.gvb = c->gvb_pool ? c->gvb_pool + (size_t)q * c->blk_cap * kExt3 : nullptr;
+  s.gmpb = c->gmpb_pool ? c->gmpb_pool + (size_t)q * c->blk_cap * kExt3 : nullptr;
+  return s;
+}
+
+void launch_bin(DmContext* c, const StateView& S, const Slot& q, int sub, int check_vmax) {
+  cudaMemsetAsync(q.nact, 0, sizeof(int), c->stream);
   const size_t shm = (size_t)c->bin_warps * c->P.Tn * sizeof(int);
   PROF_BEGIN(c, 0);
-  k_bin<<<c->P.E, 32 * c->bin_warps, shm, c->stream>>>(c->P, S, c->keys, c->ptile, c->tile_start, c->tile_count,
-                                                       c->active, c->env_abase, c->env_acount, c->flags, sub, check_vmax);
-  k_cellsort<<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, c->ptile, c->perm, c->keys, c->tile_start,
-                                                           c->tile_count, c->active, c->flags);
+  k_bin<<<c->P.E, 32 * c->bin_warps, shm, c->stream>>>(c->P, S, c->keys, c->ptile, q.tile_start, q.tile_count,
+                                                       q.active, q.env_abase, q.env_acount, c->flags, q.nact, sub,
+                                                       check_vmax);
+  k_cellsort<<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, c->ptile, q.perm, c->keys, q.tile_start,
+                                                           q.tile_count, q.active, q.nact, c->flags);
   ++c->launches;
   PROF_END(c, 0);
   ++c->launches;
@@ -160,84 +199,86 @@ const float* step_act(DmContext* c, int t) {
   return c->P.G > 0 ? c->act_tape + (size_t)t * c->P.E * c->P.G : nullptr;
 }
 
-void launch_p2g(DmContext* c, const StateView& S, int t, int sub) {
+void launch_p2g(DmContext* c, const StateView& S, const Slot& q, int t, int sub) {
   PROF_BEGIN(c, 1);
   if (maxc_of(c->P.K) == 1)
-    k_p2g<1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, c->perm, c->tile_start, c->tile_count, c->active,
-                                                           step_act(c, t), c->blocks, c->flags, sub);
+    k_p2g<1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.active,
+                                                           step_act(c, t), c->blocks, c->flags, q.nact, sub);
   else
-    k_p2g<4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, c->perm, c->tile_start, c->tile_count, c->active,
-                                                           step_act(c, t), c->blocks, c->flags, sub);
+    k_p2g<4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.active,
+                                                           step_act(c, t), c->blocks, c->flags, q.nact, sub);
   PROF_END(c, 1);
   ++c->launches;
 }
 
-void launch_grid(DmContext* c, int t) {
+void launch_grid(DmContext* c, const Slot& q, int t) {
   PROF_BEGIN(c, 9);
   if (maxc_of(c->P.K) == 1)
-    k_grid<1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, c->tile_count, c->active, step_cvo(c, t), c->blocks,
-                                                            c->gmp, c->gv, c->flags);
+    k_grid<1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.active, step_cvo(c, t), c->blocks,
+                                                            c->gmp, c->gv, q.nact);
   else
-    k_grid<4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, c->tile_count, c->active, step_cvo(c, t), c->blocks,
-                                                            c->gmp, c->gv, c->flags);
+    k_grid<4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.active, step_cvo(c, t), c->blocks,
+                                                            c->gmp, c->gv, q.nact);
   PROF_END(c, 9);
   ++c->launches;
 }
 
-void launch_g2p(DmContext* c, const StateView& S, const StateView& So, int t, int sub) {
+void launch_g2p(DmContext* c, const StateView& S, const StateView& So, const Slot& q, int t, int sub, bool dump) {
   PROF_BEGIN(c, 2);
-  k_g2p<<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, c->perm, c->tile_start, c->tile_count, c->active,
-                                                      c->gv, c->flags, sub);
+  k_g2p<<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, q.perm, q.tile_start, q.tile_count, q.active,
+                                                      c->gv, c->flags, q.nact, sub, c->gmp, dump ? q.gvb : nullptr,
+                                                      dump ? q.gmpb : nullptr);
   PROF_END(c, 2);
   ++c->launches;
 }
 
-void forward_substep(DmContext* c, const StateView& S, const StateView& So, int t, int sub, int check_vmax) {
-  launch_bin(c, S, sub, check_vmax);
-  launch_p2g(c, S, t, sub);
-  launch_grid(c, t);
-  launch_g2p(c, S, So, t, sub);
+void forward_substep(DmContext* c, const StateView& S, const StateView& So, int t, int sub, int check_vmax, int qi,
+                     bool dump) {
+  const Slot q = slot(c, qi);
+  launch_bin(c, S, q, sub, check_vmax);
+  launch_p2g(c, S, q, t, sub);
+  launch_grid(c, q, t);
+  launch_g2p(c, S, So, q, t, sub, dump);
 }
 
 template <int NG>
-void launch_p2g_adj(DmContext* c, const StateView& S, int t, float* adj_out) {
-  k_p2g_adj<NG><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, c->perm, c->tile_start, c->tile_count,
-                                                              c->active, step_act(c, t), c->gmb, c->part, adj_out,
-                                                              c->Ntot, c->tile_acc, c->flags);
+void launch_p2g_adj(DmContext* c, const StateView& S, const Slot& q, int t, float* adj_out) {
+  k_p2g_adj<NG><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.active,
+                                                              step_act(c, t), c->gmb, c->part, adj_out, c->Ntot,
+                                                              c->tile_acc, q.nact);
 }
 
-void backward_substep(DmContext* c, const StateView& S, int t, int sub, const float* adj_in, float* adj_out) {
-  launch_bin(c, S, sub, 0);
-  launch_p2g(c, S, t, sub);
-  launch_grid(c, t);
+// Adjoint of one substep from the replay's stored artifacts (slot qi).
+void backward_substep(DmContext* c, const StateView& S, int t, int qi, const float* adj_in, float* adj_out) {
+  const Slot q = slot(c, qi);
   PROF_BEGIN(c, 3);
-  k_g2p_adj<<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, adj_in, c->Ntot, c->perm, c->tile_start,
-                                                          c->tile_count, c->active, c->gv, c->ablocks, c->part,
-                                                          c->tile_acc, c->flags);
+  k_g2p_adj<<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, adj_in, c->Ntot, q.perm, q.tile_start,
+                                                          q.tile_count, q.active, q.gvb, c->ablocks, c->part,
+                                                          c->tile_acc, q.nact);
   PROF_END(c, 3);
   ++c->launches;
   PROF_BEGIN(c, 10);
   if (maxc_of(c->P.K) == 1)
-    k_grid_adj<1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, c->tile_count, c->active, step_cvo(c, t),
-                                                                c->ablocks, c->gmp, c->gmb, c->tile_acc, c->flags);
+    k_grid_adj<1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.active, step_cvo(c, t),
+                                                                c->ablocks, q.gmpb, c->gmb, c->tile_acc, q.nact);
   else
-    k_grid_adj<4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, c->tile_count, c->active, step_cvo(c, t),
-                                                                c->ablocks, c->gmp, c->gmb, c->tile_acc, c->flags);
+    k_grid_adj<4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.active, step_cvo(c, t),
+                                                                c->ablocks, q.gmpb, c->gmb, c->tile_acc, q.nact);
   PROF_END(c, 10);
   ++c->launches;
   const int G = c->P.G;
   PROF_BEGIN(c, 4);
   if (G <= 1)
-    launch_p2g_adj<1>(c, S, t, adj_out);
+    launch_p2g_adj<1>(c, S, q, t, adj_out);
   else if (G <= 8)
-    launch_p2g_adj<8>(c, S, t, adj_out);
+    launch_p2g_adj<8>(c, S, q, t, adj_out);
   else
-    launch_p2g_adj<16>(c, S, t, adj_out);
+    launch_p2g_adj<16>(c, S, q, t, adj_out);
   PROF_END(c, 4);
   ++c->launches;
   const int Kc = c->P.K > 0 ? c->P.K : 1;
   PROF_BEGIN(c, 5);
-  k_env_reduce<<<c->P.E, kNacc, 0, c->stream>>>(c->P, c->active, c->env_abase, c->env_acount, c->tile_acc,
+  k_env_reduce<<<c->P.E, kNacc, 0, c->stream>>>(c->P, q.active, q.env_abase, q.env_acount, c->tile_acc,
                                                 c->gcvo + (size_t)t * c->P.E * Kc * 9,
                                                 c->gact + (size_t)t * c->P.E * (G > 0 ? G : 1), c->gmu, c->glam);
   PROF_END(c, 5);
@@ -273,6 +314,7 @@ int check_flags(DmContext* ctx, bool cfl) {
   DM_CUDA(cudaMemcpyAsync(ctx->h_flags, ctx->flags, sizeof(DevFlags), cudaMemcpyDeviceToHost, ctx->stream));
   DM_CUDA(cudaStreamSynchronize(ctx->stream));
   DM_CUDA(cudaGetLastError());
+  if (ctx->h_flags->max_active > ctx->max_active_seen) ctx->max_active_seen = ctx->h_flags->max_active;
   if (ctx->h_flags->err_key != ~0ull) {
     ctx->err = fmt_error(ctx, ctx->h_flags->err_key);
     ctx->poisoned = true;
@@ -292,7 +334,7 @@ int reset_flags(DmContext* ctx) {
   DevFlags f;
   f.err_key = ~0ull;
   f.vmax_bits = 0;
-  f.active_count = 0;
+  f.max_active = 0;
   DM_CUDA(cudaMemcpyAsync(ctx->flags, &f, sizeof(DevFlags), cudaMemcpyHostToDevice, ctx->stream));
   DM_CUDA(cudaStreamSynchronize(ctx->stream));
   return DM_OK;
@@ -369,7 +411,7 @@ int step_impl(DmContext* ctx, const float* cvo, const float* act, float* obs, cu
   const int S = ctx->cfg.substeps;
   for (int q = 0; q < S; ++q) {
     const int s = t * S + q;
-    forward_substep(ctx, fwd_state(ctx, s), fwd_state(ctx, s + 1), t, q, q == 0);
+    forward_substep(ctx, fwd_state(ctx, s), fwd_state(ctx, s + 1), t, q, q == 0, 0, false);
   }
   float* o = ctx->obs_tape + (size_t)t * E * DM_OBS_DIM;
   PROF_BEGIN(ctx, 6);
@@ -394,6 +436,23 @@ int backward_impl(DmContext* ctx, const float* dobs, const float* dfx, const flo
   if (T == 0) {
     ctx->err = "backward: no recorded steps";
     return DM_ERR_ARG;
+  }
+  {
+    // grid-block pool for one replayed segment: exactly the forward pass's
+    // largest active-tile count (the replay is bit-identical to it)
+    const size_t need = (size_t)(ctx->max_active_seen > 0 ? ctx->max_active_seen : 1);
+    if (ctx->blk_cap < need) {
+      if (ctx->gvb_pool) cudaFree(ctx->gvb_pool);
+      if (ctx->gmpb_pool) cudaFree(ctx->gmpb_pool);
+      ctx->bytes -= 2 * ctx->blk_cap * ctx->ck * kExt3 * sizeof(float4);
+      ctx->gvb_pool = ctx->gmpb_pool = nullptr;
+      ctx->blk_cap = 0;
+      if (!dalloc(ctx, &ctx->gvb_pool, need * ctx->ck * kExt3) || !dalloc(ctx, &ctx->gmpb_pool, need * ctx->ck * kExt3)) {
+        ctx->err = "backward: out of device memory for the replay grid blocks";
+        return DM_ERR_CUDA;
+      }
+      ctx->blk_cap = need;
+    }
   }
   DM_CUDA(cudaMemsetAsync(ctx->gcvo, 0, (size_t)T * E * Kc * 9 * sizeof(double), ctx->stream));
   DM_CUDA(cudaMemsetAsync(ctx->gact, 0, (size_t)T * E * Gc * sizeof(double), ctx->stream));
@@ -441,9 +500,16 @@ int backward_impl(DmContext* ctx, const float* dobs, const float* dfx, const flo
     }
     for (int s0 = s_end - ck; s0 >= t * S; s0 -= ck) {
       // replay the segment's forward (tape.hpp:229-233)
-      for (int s = s0; s < s0 + ck - 1; ++s) forward_substep(ctx, seg_state(ctx, s0, s), seg_state(ctx, s0, s + 1), t, s - t * S, 0);
-      for (int s = s0 + ck - 1; s >= s0; --s) {
-        backward_substep(ctx, seg_state(ctx, s0, s), t, s - t * S, ctx->adj[cur], ctx->adj[cur ^ 1]);
+      // replay the segment's forward (tape.hpp:229-233), keeping every
+      // substep's sort and grid blocks for its adjoint
+      for (int q = 0; q < ck; ++q) {
+        const int s = s0 + q;
+        const StateView So = q + 1 < ck ? seg_state(ctx, s0, s + 1) : view(ctx->tail, ctx->tail_attr, ctx->Ntot);
+        forward_substep(ctx, seg_state(ctx, s0, s), So, t, s - t * S, 0, q, true);
+      }
+      for (int q = ck - 1; q >= 0; --q) {
+        const int s = s0 + q;
+        backward_substep(ctx, seg_state(ctx, s0, s), t, q, ctx->adj[cur], ctx->adj[cur ^ 1]);
         cur ^= 1;
       }
     }
@@ -596,10 +662,11 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
     for (int i = 0; i < 2; ++i)
       ok = ok && dalloc(ctx, &ctx->scratch[i], 24 * N) && dalloc(ctx, &ctx->scratch_attr[i], N);
   ok = ok && dalloc(ctx, &ctx->adj[0], 24 * N) && dalloc(ctx, &ctx->adj[1], 24 * N) && dalloc(ctx, &ctx->part, 12 * N);
-  ok = ok && dalloc(ctx, &ctx->keys, N) && dalloc(ctx, &ctx->perm, N) && dalloc(ctx, &ctx->ptile, N) &&
-       dalloc(ctx, &ctx->tile_start, TT) &&
-       dalloc(ctx, &ctx->tile_count, TT) && dalloc(ctx, &ctx->env_abase, P.E) && dalloc(ctx, &ctx->env_acount, P.E) &&
-       dalloc(ctx, &ctx->active, TT);
+  ok = ok && dalloc(ctx, &ctx->keys, N) && dalloc(ctx, &ctx->ptile, N) &&
+       dalloc(ctx, &ctx->perm_all, (size_t)ck * N) && dalloc(ctx, &ctx->tstart_all, (size_t)ck * TT) &&
+       dalloc(ctx, &ctx->tcount_all, (size_t)ck * TT) && dalloc(ctx, &ctx->active_all, (size_t)ck * TT) &&
+       dalloc(ctx, &ctx->abase_all, (size_t)ck * P.E) && dalloc(ctx, &ctx->acount_all, (size_t)ck * P.E) &&
+       dalloc(ctx, &ctx->nact_all, (size_t)ck) && dalloc(ctx, &ctx->tail, 24 * N) && dalloc(ctx, &ctx->tail_attr, N);
   const size_t NN = (size_t)P.E * P.dims[0] * P.dims[1] * P.dims[2];
   ok = ok && dalloc(ctx, &ctx->gmp, NN) && dalloc(ctx, &ctx->gv, NN) && dalloc(ctx, &ctx->gmb, NN);
   ok = ok && dalloc(ctx, &ctx->blocks, TT * kExt3) && dalloc(ctx, &ctx->ablocks, TT * kExt3) &&
@@ -633,7 +700,8 @@ void dm_destroy(DmContext* ctx) {
   if (!ctx) return;
   void* ptrs[] = {ctx->store,     ctx->store_attr, ctx->seg,       ctx->seg_attr,   ctx->scratch[0], ctx->scratch[1],
                   ctx->scratch_attr[0], ctx->scratch_attr[1], ctx->adj[0], ctx->adj[1], ctx->part, ctx->keys,
-                  ctx->perm,      ctx->ptile, ctx->tile_start, ctx->tile_count, ctx->env_abase, ctx->env_acount, ctx->active,
+                  ctx->perm_all,  ctx->ptile, ctx->tstart_all, ctx->tcount_all, ctx->abase_all, ctx->acount_all,
+                  ctx->active_all, ctx->nact_all, ctx->tail, ctx->tail_attr, ctx->gvb_pool, ctx->gmpb_pool,
                   ctx->blocks,    ctx->ablocks,    ctx->tile_acc,   ctx->gmp, ctx->gv, ctx->gmb,   ctx->flags,      ctx->cvo_tape,  ctx->act_tape,
                   ctx->obs_tape,  ctx->gcvo,       ctx->gact,       ctx->gmu,        ctx->glam};
   for (void* p : ptrs)
@@ -711,11 +779,11 @@ int dm_profile(DmContext* ctx, int enable, double* ms, long long* counts) {
 int dm_debug_sort(DmContext* ctx, int* keys, int* perm) {
   if (!ctx || !ctx->store) return DM_ERR_ARG;
   const int s = ctx->steps * ctx->cfg.substeps;
-  launch_bin(ctx, fwd_state(ctx, s), 0, 0);
+  launch_bin(ctx, fwd_state(ctx, s), slot(ctx, 0), 0, 0);
   const size_t N = ctx->Ntot;
   std::vector<int> p(N);
   DM_CUDA(cudaMemcpyAsync(keys, ctx->keys, N * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  DM_CUDA(cudaMemcpyAsync(p.data(), ctx->perm, N * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  DM_CUDA(cudaMemcpyAsync(p.data(), slot(ctx, 0).perm, N * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   DM_CUDA(cudaStreamSynchronize(ctx->stream));
   for (size_t i = 0; i < N; ++i) perm[i] = p[i] - (int)((i / ctx->P.N) * ctx->P.N);
   return check_flags(ctx, false);

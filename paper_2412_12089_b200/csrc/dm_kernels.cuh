@@ -60,7 +60,7 @@ struct StateView {
 struct DevFlags {
   unsigned long long err_key;  // min over (env, substep, stage, particle, axis, code)
   unsigned int vmax_bits;      // max |v| component (CFL warning, mpm.hpp:355-361)
-  int active_count;
+  int max_active;              // largest active-tile count seen (sizes the replay block pool)
 };
 
 __device__ __forceinline__ uint32_t attr_index(uint32_t a) { return a & 0xFFFFFu; }
@@ -165,7 +165,7 @@ __device__ __forceinline__ void store_state(const StateView& S, size_t i, v3<flo
 // permutation equals std::stable_sort by key.
 __global__ void __launch_bounds__(512) k_bin(DevParams P, StateView S, int* keys, int* perm, int* tile_start,
                                              int* tile_count, int2* active, int* env_abase, int* env_acount,
-                                             DevFlags* flags, int substep, int check_vmax) {
+                                             DevFlags* flags, int* nact, int substep, int check_vmax) {
   extern __shared__ int cnt[];  // [nw][Tn]
   __shared__ int s_part[512 / 32 + 1][2];
   __shared__ int s_base;
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(512) k_bin(DevParams P, StateView S, int* keys
       rc += c;
       ra += a;
     }
-    s_base = atomicAdd(&flags->active_count, ra);
+    s_base = atomicAdd(nact, ra);
     env_abase[e] = s_base;
     env_acount[e] = ra;
   }
@@ -288,11 +288,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_cellsort(DevParams P, StateView
                                                           int* __restrict__ perm, int* __restrict__ keys,
                                                           const int* __restrict__ tile_start,
                                                           const int* __restrict__ tile_count,
-                                                          const int2* __restrict__ active, const DevFlags* flags) {
+                                                          const int2* __restrict__ active, const int* nact,
+                                                          DevFlags* flags) {
   __shared__ int c64[kWarps][64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int* cnt = c64[warp];
-  const int n_active = *(const volatile int*)&flags->active_count;
+  const int n_active = *(const volatile int*)nact;
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicMax(&flags->max_active, n_active);
   for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
     const int2 et = active[a];
     const int e = et.x, t = et.y;
@@ -434,11 +436,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_p2g(DevParams P, StateView S, c
                                                      const int* __restrict__ tile_start,
                                                      const int* __restrict__ tile_count, const int2* __restrict__ active,
                                                      const float* __restrict__ act, float4* __restrict__ blocks,
-                                                     DevFlags* flags, int substep) {
+                                                     DevFlags* flags, const int* nact, int substep) {
   __shared__ float4 blk[kWarps][kExt3];
   __shared__ float pay[kWarps][32 * kPay];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_active = *(volatile int*)&flags->active_count;
+  const int n_active = *(const volatile int*)nact;
   const TransferCtx<float> T = tctx(P);
   float4* bw = blk[warp];
   float* pw = pay[warp];
@@ -574,10 +576,10 @@ template <int MAXC>
 __global__ void __launch_bounds__(kWarps * 32) k_grid(DevParams P, const int* __restrict__ tile_count,
                                                       const int2* __restrict__ active, const float* __restrict__ cvo,
                                                       const float4* __restrict__ blocks, float4* __restrict__ gmp,
-                                                      float4* __restrict__ gv, const DevFlags* flags) {
+                                                      float4* __restrict__ gv, const int* nact) {
   __shared__ short own[kWarps][kExt3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_active = *(const volatile int*)&flags->active_count;
+  const int n_active = *(const volatile int*)nact;
   const NodeCtx<float> G = nctx(P);
   for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
     const int2 et = active[a];
@@ -614,10 +616,12 @@ __device__ __forceinline__ void load_tile_grid(const DevParams& P, const float4*
 __global__ void __launch_bounds__(kWarps * 32) k_g2p(DevParams P, StateView S, StateView Sout,
                                                      const int* __restrict__ perm, const int* __restrict__ tile_start,
                                                      const int* __restrict__ tile_count, const int2* __restrict__ active,
-                                                     const float4* __restrict__ gv, DevFlags* flags, int substep) {
+                                                     const float4* __restrict__ gv, DevFlags* flags, const int* nact,
+                                                     int substep, const float4* __restrict__ gmp,
+                                                     float4* __restrict__ out_gv, float4* __restrict__ out_gmp) {
   __shared__ float4 vg[kWarps][kExt3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_active = *(volatile int*)&flags->active_count;
+  const int n_active = *(const volatile int*)nact;
   const TransferCtx<float> T = tctx(P);
   float4* vw = vg[warp];
   for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
@@ -627,6 +631,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_g2p(DevParams P, StateView S, S
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
     load_tile_grid(P, gv, e, o, vw, lane);
     __syncwarp();
+    if (out_gv) {  // segment replay: keep the tile's grid for the adjoint substep
+      for (int i = lane; i < kExt3; i += 32) out_gv[(size_t)a * kExt3 + i] = vw[i];
+      load_tile_grid(P, gmp, e, o, out_gmp + (size_t)a * kExt3, lane);
+    }
     const size_t tix = (size_t)e * P.Tn + t;
     const int start = tile_start[tix], cnt = tile_count[tix];
     for (int c0 = lane; c0 < cnt; c0 += 32) {
@@ -664,9 +672,9 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_g2p_adj(DevParams P, StateVi
                                                          size_t astride, const int* __restrict__ perm,
                                                          const int* __restrict__ tile_start,
                                                          const int* __restrict__ tile_count,
-                                                         const int2* __restrict__ active, const float4* __restrict__ gv,
+                                                         const int2* __restrict__ active, const float4* __restrict__ gvb,
                                                          float4* __restrict__ ablocks, float* __restrict__ part,
-                                                         float* __restrict__ tile_acc, const DevFlags* flags) {
+                                                         float* __restrict__ tile_acc, const int* nact) {
   __shared__ float4 vg[kWarps][kExt3];
   __shared__ float4 ab[kWarps][kExt3];
   __shared__ float pay[kWarps][32 * kPay];
@@ -675,14 +683,16 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_g2p_adj(DevParams P, StateVi
   float4* vw = vg[warp];
   float4* aw = ab[warp];
   float* pw = pay[warp];
-  const int n_active = *(const volatile int*)&flags->active_count;
+  const int n_active = *(const volatile int*)nact;
   for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
     const int2 et = active[a];
     const int e = et.x, t = et.y;
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
-    load_tile_grid(P, gv, e, o, vw, lane);
-    for (int i = lane; i < kExt3; i += 32) aw[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = lane; i < kExt3; i += 32) {
+      vw[i] = gvb[(size_t)a * kExt3 + i];  // the replayed substep's grid, stored per tile slot
+      aw[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     __syncwarp();
     const size_t tix = (size_t)e * P.Tn + t;
     const int start = tile_start[tix], cnt = tile_count[tix];
@@ -753,11 +763,11 @@ template <int MAXC>
 __global__ void __launch_bounds__(kWarps * 32) k_grid_adj(DevParams P, const int* __restrict__ tile_count,
                                                           const int2* __restrict__ active, const float* __restrict__ cvo,
                                                           const float4* __restrict__ ablocks,
-                                                          const float4* __restrict__ gmp, float4* __restrict__ gmb,
-                                                          float* __restrict__ tile_acc, const DevFlags* flags) {
+                                                          const float4* __restrict__ gmpb, float4* __restrict__ gmb,
+                                                          float* __restrict__ tile_acc, const int* nact) {
   __shared__ short own[kWarps][kExt3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_active = *(const volatile int*)&flags->active_count;
+  const int n_active = *(const volatile int*)nact;
   const NodeCtx<float> G = nctx(P);
   for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
     const int2 et = active[a];
@@ -776,7 +786,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_grid_adj(DevParams P, const int
       const int g[3] = {tc[0] * kTile + l[0], tc[1] * kTile + l[1], tc[2] * kTile + l[2]};
       const float4 vb = sum_blocks(P, ablocks, nbr, e, tc, l);
       const size_t n = node_lin(P, e, g);
-      const float4 mm = gmp[n];
+      const float4 mm = gmpb[(size_t)a * kExt3 + i];  // this tile's stored (mass, momentum) block
       float mbar;
       v3<float> pbar;
       // adjoint blocks carry (unused, vbar.x, vbar.y, vbar.z) -- emit_contrib layout
@@ -804,12 +814,12 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_p2g_adj(DevParams P, StateVi
                                                          const int2* __restrict__ active, const float* __restrict__ act,
                                                          const float4* __restrict__ gmb, const float* __restrict__ part,
                                                          float* __restrict__ adj_out, size_t astride,
-                                                         float* __restrict__ tile_acc, const DevFlags* flags) {
+                                                         float* __restrict__ tile_acc, const int* nact) {
   __shared__ float4 mb[kWarps][kExt3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TransferCtx<float> T = tctx(P);
   float4* bw = mb[warp];
-  const int n_active = *(const volatile int*)&flags->active_count;
+  const int n_active = *(const volatile int*)nact;
   for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
     const int2 et = active[a];
     const int e = et.x, t = et.y;
