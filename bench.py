@@ -74,7 +74,9 @@ def init_dist(world, local):
     import torch
     import torch.distributed as dist
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    backend = "nccl" if torch.cuda.is_available() else "gloo"
+    # BENCH_DIST_BACKEND=gloo lets the multi-rank path run with several ranks
+    # on one device (tests only; the timing reduction is a scalar all-reduce)
+    backend = os.environ.get("BENCH_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
     if backend == "nccl":
         torch.cuda.set_device(local)
     dist.init_process_group(backend)
@@ -85,7 +87,8 @@ def max_over_ranks(dist, value: float) -> float:
     if dist is None:
         return value
     import torch
-    t = torch.tensor([value], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    on_gpu = torch.cuda.is_available() and dist.get_backend() == "nccl"
+    t = torch.tensor([value], dtype=torch.float64, device="cuda" if on_gpu else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -225,6 +228,8 @@ ALG_BYTES = {  # algorithmic HBM bytes per particle per launch (DESIGN.md "Roofl
 
 def run_ours(args, scene, rank, world, local, dist):
     import torch
+    if torch.cuda.device_count() < world:  # several ranks sharing a device (multi-rank test only)
+        local = local % max(1, torch.cuda.device_count())
     from paper_2412_12089_b200 import api
     from paper_2412_12089_b200.losses import loss_and_dobs, loss_and_dobs_torch
 

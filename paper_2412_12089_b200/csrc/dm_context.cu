@@ -61,6 +61,7 @@ struct DmContext {
   float4 *blocks = nullptr, *ablocks = nullptr;
   float4 *gmp = nullptr, *gv = nullptr, *gmb = nullptr;  // dense per-env grids
   int bin_warps = 16;
+  int law = -1;  // the batch's single law kind (compile-time specialised kernels), -1: mixed
   float* tile_acc = nullptr;
   DevFlags* flags = nullptr;
   DevFlags* h_flags = nullptr;
@@ -153,6 +154,16 @@ void prof_flush(DmContext* c) {
 #define PROF_BEGIN(c, cls) prof_mark(c, cls)
 #define PROF_END(c, cls) prof_mark(c, cls)
 
+// Runs `launch` with the kernel template specialised for the batch's law.
+#define DM_LAW_DISPATCH(c, LAUNCH)      \
+  switch ((c)->law) {                   \
+    case kFixedCorotated: LAUNCH(0); break; \
+    case kNeoHookean: LAUNCH(1); break;     \
+    case kElastoplastic: LAUNCH(2); break;  \
+    case kFluid: LAUNCH(3); break;          \
+    default: LAUNCH(-1); break;             \
+  }
+
 struct Slot {
   int* perm;
   int* tile_start;
@@ -201,12 +212,11 @@ const float* step_act(DmContext* c, int t) {
 
 void launch_p2g(DmContext* c, const StateView& S, const Slot& q, int t, int sub) {
   PROF_BEGIN(c, 1);
-  if (maxc_of(c->P.K) == 1)
-    k_p2g<1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.active,
-                                                           step_act(c, t), c->blocks, c->flags, q.nact, sub);
-  else
-    k_p2g<4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.active,
-                                                           step_act(c, t), c->blocks, c->flags, q.nact, sub);
+#define L_P2G(LW)                                                                                               \
+  k_p2g<LW><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.active, \
+                                                          step_act(c, t), c->blocks, c->flags, q.nact, sub)
+  DM_LAW_DISPATCH(c, L_P2G);
+#undef L_P2G
   PROF_END(c, 1);
   ++c->launches;
 }
@@ -225,9 +235,12 @@ void launch_grid(DmContext* c, const Slot& q, int t) {
 
 void launch_g2p(DmContext* c, const StateView& S, const StateView& So, const Slot& q, int t, int sub, bool dump) {
   PROF_BEGIN(c, 2);
-  k_g2p<<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, q.perm, q.tile_start, q.tile_count, q.active,
-                                                      c->gv, c->flags, q.nact, sub, c->gmp, dump ? q.gvb : nullptr,
-                                                      dump ? q.gmpb : nullptr);
+#define L_G2P(LW)                                                                                                \
+  k_g2p<LW><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, q.perm, q.tile_start, q.tile_count,        \
+                                                          q.active, c->gv, c->flags, q.nact, sub, c->gmp,         \
+                                                          dump ? q.gvb : nullptr, dump ? q.gmpb : nullptr)
+  DM_LAW_DISPATCH(c, L_G2P);
+#undef L_G2P
   PROF_END(c, 2);
   ++c->launches;
 }
@@ -241,9 +254,9 @@ void forward_substep(DmContext* c, const StateView& S, const StateView& So, int 
   launch_g2p(c, S, So, q, t, sub, dump);
 }
 
-template <int NG>
+template <int LAW, int NG>
 void launch_p2g_adj(DmContext* c, const StateView& S, const Slot& q, int t, float* adj_out) {
-  k_p2g_adj<NG><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.active,
+  k_p2g_adj<LAW, NG><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.active,
                                                               step_act(c, t), c->gmb, c->part, adj_out, c->Ntot,
                                                               c->tile_acc, q.nact);
 }
@@ -252,9 +265,12 @@ void launch_p2g_adj(DmContext* c, const StateView& S, const Slot& q, int t, floa
 void backward_substep(DmContext* c, const StateView& S, int t, int qi, const float* adj_in, float* adj_out) {
   const Slot q = slot(c, qi);
   PROF_BEGIN(c, 3);
-  k_g2p_adj<<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, adj_in, c->Ntot, q.perm, q.tile_start,
-                                                          q.tile_count, q.active, q.gvb, c->ablocks, c->part,
-                                                          c->tile_acc, q.nact);
+#define L_G2PA(LW)                                                                                            \
+  k_g2p_adj<LW><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, adj_in, c->Ntot, q.perm, q.tile_start, \
+                                                              q.tile_count, q.active, q.gvb, c->ablocks,    \
+                                                              c->part, c->tile_acc, q.nact)
+  DM_LAW_DISPATCH(c, L_G2PA);
+#undef L_G2PA
   PROF_END(c, 3);
   ++c->launches;
   PROF_BEGIN(c, 10);
@@ -268,12 +284,15 @@ void backward_substep(DmContext* c, const StateView& S, int t, int qi, const flo
   ++c->launches;
   const int G = c->P.G;
   PROF_BEGIN(c, 4);
-  if (G <= 1)
-    launch_p2g_adj<1>(c, S, q, t, adj_out);
-  else if (G <= 8)
-    launch_p2g_adj<8>(c, S, q, t, adj_out);
-  else
-    launch_p2g_adj<16>(c, S, q, t, adj_out);
+#define L_P2GA(LW)                              \
+  if (G <= 1)                                   \
+    launch_p2g_adj<LW, 1>(c, S, q, t, adj_out); \
+  else if (G <= 8)                              \
+    launch_p2g_adj<LW, 8>(c, S, q, t, adj_out); \
+  else                                          \
+    launch_p2g_adj<LW, 16>(c, S, q, t, adj_out)
+  DM_LAW_DISPATCH(c, L_P2GA);
+#undef L_P2GA
   PROF_END(c, 4);
   ++c->launches;
   const int Kc = c->P.K > 0 ? c->P.K : 1;
@@ -638,6 +657,9 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
     L.dlam_dE = (float)ctx->dlam_dE[m];
     ctx->law_kind[m] = M.kind;
   }
+  ctx->law = mats[0].kind;
+  for (int m = 1; m < num_materials; ++m)
+    if (mats[m].kind != ctx->law) ctx->law = -1;
   for (int c = 0; c < P.K; ++c) {
     ColShape& s = P.shape[c];
     s.kind = shapes[c].kind;
@@ -689,7 +711,7 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<16>, kWarps * 32, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<-1, 16>, kWarps * 32, 0);
   if (occ < 1) occ = 1;
   ctx->grid_tiles = dev_sms * (occ < 8 ? 8 : occ);
   if (reset_flags(ctx) != DM_OK) return ctx;

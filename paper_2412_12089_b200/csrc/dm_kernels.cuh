@@ -85,6 +85,18 @@ __device__ __forceinline__ int tile_local(int base, int origin) {
   return l < 0 ? 0 : (l > kTile - 1 ? kTile - 1 : l);
 }
 
+// Constitutive law with its kind fixed at compile time (LAW >= 0): the
+// law switch folds away, so a kernel instantiated for the fluid or
+// neo-Hookean law carries no SVD code and needs far fewer registers.
+// LAW < 0 keeps the runtime dispatch (mixed-law batches).
+template <int LAW>
+__device__ __forceinline__ Law<float> law_of(const DevParams& P, int mi) {
+  Law<float> L = P.law[mi];
+  if (LAW >= 0) L.kind = LAW;
+  return L;
+}
+constexpr int kLawBlocks(int law) { return (law == kFluid || law == kNeoHookean) ? 6 : 4; }
+
 __device__ __forceinline__ TransferCtx<float> tctx(const DevParams& P) {
   TransferCtx<float> t;
   t.dims[0] = P.dims[0];
@@ -431,8 +443,8 @@ __device__ __forceinline__ void scatter_finish(float4* __restrict__ blk, int lan
 // ============================ P2G ============================
 // Per active tile: stage particle payloads (lanes = particles), scatter runs
 // into the warp's 6^3 shared block (lanes = stencil nodes), write the block.
-template <int MAXC>
-__global__ void __launch_bounds__(kWarps * 32) k_p2g(DevParams P, StateView S, const int* __restrict__ perm,
+template <int LAW>
+__global__ void __launch_bounds__(kWarps * 32, kLawBlocks(LAW)) k_p2g(DevParams P, StateView S, const int* __restrict__ perm,
                                                      const int* __restrict__ tile_start,
                                                      const int* __restrict__ tile_count, const int2* __restrict__ active,
                                                      const float* __restrict__ act, float4* __restrict__ blocks,
@@ -465,7 +477,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_p2g(DevParams P, StateView S, c
         const uint32_t at = S.attr[src];
         Stencil<float> sc;
         make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
-        const Law<float>& L = P.law[attr_mat(at)];
+        const Law<float> L = law_of<LAW>(P, attr_mat(at));
         const float av = act ? act[e * P.G + min(attr_group(at), P.G - 1)] : 0.f;
         bool bad = false;
         const m3<float> A = p2g_affine(L, T, F, C, av, &bad);
@@ -613,7 +625,8 @@ __device__ __forceinline__ void load_tile_grid(const DevParams& P, const float4*
 }
 
 // ============================ G2P ============================
-__global__ void __launch_bounds__(kWarps * 32) k_g2p(DevParams P, StateView S, StateView Sout,
+template <int LAW>
+__global__ void __launch_bounds__(kWarps * 32, kLawBlocks(LAW)) k_g2p(DevParams P, StateView S, StateView Sout,
                                                      const int* __restrict__ perm, const int* __restrict__ tile_start,
                                                      const int* __restrict__ tile_count, const int2* __restrict__ active,
                                                      const float4* __restrict__ gv, DevFlags* flags, const int* nact,
@@ -654,7 +667,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_g2p(DevParams P, StateView S, S
       };
       v3<float> xn = mk3(x[0], x[1], x[2]);
       bool bad_adv = false, bad_det = false;
-      g2p_particle_sep(P.law[attr_mat(at)], T, sc, getv, xn, v, C, F, &bad_adv, &bad_det);
+      g2p_particle_sep(law_of<LAW>(P, attr_mat(at)), T, sc, getv, xn, v, C, F, &bad_adv, &bad_det);
       if (bad_adv) report(flags, e, substep, 1, attr_index(at), 0, kErrG2PInterior);
       if (bad_det) report(flags, e, substep, 1, attr_index(at), attr_mat(at), kErrDetF);
       store_state(Sout, dst, xn, v, F, C);
@@ -668,6 +681,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_g2p(DevParams P, StateView S, S
 // Reads the start-of-substep state (via perm) and the cotangent of the
 // end-of-substep state (sorted position); writes particle-side partial
 // cotangents (sorted position) and a 6^3 block of node-velocity cotangents.
+template <int LAW>
 __global__ void __launch_bounds__(kWarps * 32, 4) k_g2p_adj(DevParams P, StateView S, const float* __restrict__ adj_in,
                                                          size_t astride, const int* __restrict__ perm,
                                                          const int* __restrict__ tile_start,
@@ -728,7 +742,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_g2p_adj(DevParams P, StateVi
         m3<float> Fp, Bd;
         const int mi = attr_mat(at);
         float mu_l = 0.f;
-        g2p_vjp_sep(P.law[mi], T, sc, getv, F, xb, vb, Cb, Fb, xp, Fp, gq, Bd, mu_l);
+        g2p_vjp_sep(law_of<LAW>(P, mi), T, sc, getv, F, xb, vb, Cb, Fb, xp, Fp, gq, Bd, mu_l);
 #pragma unroll
         for (int m = 0; m < 4; ++m)
           if (m == mi) mub[m] += mu_l;
@@ -807,7 +821,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_grid_adj(DevParams P, const int
 }
 
 // ============================ P2G adjoint ============================
-template <int NG>
+template <int LAW, int NG>
 __global__ void __launch_bounds__(kWarps * 32, 4) k_p2g_adj(DevParams P, StateView S, const int* __restrict__ perm,
                                                          const int* __restrict__ tile_start,
                                                          const int* __restrict__ tile_count,
@@ -857,7 +871,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_p2g_adj(DevParams P, StateVi
       const int mi = attr_mat(at), gi = min(attr_group(at), P.G > 0 ? P.G - 1 : 0);
       const float av = act ? act[e * P.G + gi] : 0.f;
       float mu_l = 0.f, la_l = 0.f, ac_l = 0.f;
-      p2g_vjp_sep(P.law[mi], T, sc, getmb, v, F, C, av, xb, vb, Fb, Cb, mu_l, la_l, ac_l);
+      p2g_vjp_sep(law_of<LAW>(P, mi), T, sc, getmb, v, F, C, av, xb, vb, Fb, Cb, mu_l, la_l, ac_l);
 #pragma unroll
       for (int m = 0; m < 4; ++m)
         if (m == mi) {
