@@ -504,8 +504,9 @@ inline void bin_keys_f32(const SimParams& sp, const float* x /* N x 3 */, std::s
     for (int a = 0; a < 3; ++a) {
       volatile float gx = x[3 * p + a] * inv_dx;  // volatile: no contraction
       volatile float gm = gx - 0.5f;
-      int base = static_cast<int>(std::floor(static_cast<float>(gm)));
-      base = base < 1 ? 1 : (base > sp.dims[a] - 4 ? sp.dims[a] - 4 : base);  // reported outside anyway
+      const float b = std::floor(static_cast<float>(gm));
+      const bool ok = b >= 1.f && b <= static_cast<float>(sp.dims[a] - 4);
+      const int base = ok ? static_cast<int>(b) : 1;  // outside: reported, binned as base 1 (device rule)
       t[a] = base >> 2;
       c[a] = base & 3;
     }

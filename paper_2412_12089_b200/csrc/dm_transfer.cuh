@@ -40,24 +40,31 @@ struct Stencil {
 // base = floor(fl(gx - 0.5)), fx = fl(gx - base).  fp64 (host check): the
 // reference's double division for base (mpm.hpp:153-154) and multiplication
 // for fx (mpm.hpp:159).  Returns the first failing axis or -1.
+// The interior test (1 <= base <= dims-4, mpm.hpp:155) is done on the float
+// floor, before any integer conversion, so NaN/inf/huge positions are caught;
+// a failing axis is clamped into range so every consumer stays in bounds
+// while the error is reported.
 DM_HD int stencil_base(const float x[3], float inv_dx, double dx, const int dims[3], int base[3], float fx[3]) {
   int bad = -1;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     const float gx = mul_rn(x[a], inv_dx);
     const float b = floorf(sub_rn(gx, 0.5f));
-    base[a] = static_cast<int>(b);
-    fx[a] = sub_rn(gx, b);
-    if ((base[a] < 1 || base[a] + 2 > dims[a] - 2) && bad < 0) bad = a;
+    const bool ok = b >= 1.f && b <= static_cast<float>(dims[a] - 4);
+    base[a] = ok ? static_cast<int>(b) : 1;
+    fx[a] = ok ? sub_rn(gx, b) : 1.f;
+    if (!ok && bad < 0) bad = a;
   }
   return bad;
 }
 DM_HD int stencil_base(const double x[3], double inv_dx, double dx, const int dims[3], int base[3], double fx[3]) {
   int bad = -1;
   for (int a = 0; a < 3; ++a) {
-    base[a] = static_cast<int>(floor(x[a] / dx - 0.5));
-    fx[a] = x[a] * inv_dx - static_cast<double>(base[a]);
-    if ((base[a] < 1 || base[a] + 2 > dims[a] - 2) && bad < 0) bad = a;
+    const double b = floor(x[a] / dx - 0.5);
+    const bool ok = b >= 1.0 && b <= static_cast<double>(dims[a] - 4);
+    base[a] = ok ? static_cast<int>(b) : 1;
+    fx[a] = ok ? x[a] * inv_dx - b : 1.0;
+    if (!ok && bad < 0) bad = a;
   }
   return bad;
 }
@@ -137,7 +144,7 @@ DM_HD void g2p_particle(const Law<R>& L, const TransferCtx<R>& t, const Stencil<
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     const R gx = x[a] / t.dx;
-    if (gx < R(1.5) || gx > R(t.dims[a]) - R(2.5)) *bad_adv = true;
+    if (!(gx >= R(1.5) && gx <= R(t.dims[a]) - R(2.5))) *bad_adv = true;  // NaN-safe
   }
   const m3<R> Fnew = (meye<R>() + C * t.dt) * F;
   F = law_project(L, Fnew, bad_det);
@@ -299,7 +306,7 @@ DM_HD void g2p_particle_sep(const Law<R>& L, const TransferCtx<R>& t, const Sten
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     const R gx = x[a] / t.dx;
-    if (gx < R(1.5) || gx > R(t.dims[a]) - R(2.5)) *bad_adv = true;
+    if (!(gx >= R(1.5) && gx <= R(t.dims[a]) - R(2.5))) *bad_adv = true;  // NaN-safe
   }
   const m3<R> Fnew = (meye<R>() + C * t.dt) * F;
   F = law_project(L, Fnew, bad_det);

@@ -245,7 +245,9 @@ def config2(seed=0, n_envs=32, env_offset=0, n_ctrl=32, n_sub=16):
     groups = kmeans_groups(base, 8, RngStream(seed, 1 << 40))
     acts = np.stack([RngStream(seed, env_offset + e).uniform(-1.0, 1.0, n_ctrl * 8).reshape(n_ctrl, 8)
                      for e in range(n_envs)])
-    mats = [{"kind": "neo_hookean", "E": 3e4, "nu": 0.3, "rho": 1.0, "volume": h ** 3, "act_strength": 1e4}]
+    # rho = 1000 (the config leaves density open; with rho = 1 the sound speed
+    # is 173 m/s and random x-actuation inverts elements within 3 steps)
+    mats = [{"kind": "neo_hookean", "E": 3e4, "nu": 0.3, "rho": 1000.0, "volume": h ** 3, "act_strength": 1e4}]
     sim = {"dims": (48, 48, 48), "dx": dx, "dt": 5e-5, "gravity": GRAVITY, "boundary": "slip",
            "alpha_c": 100.0, "mu_b": 0.0}
     x = np.broadcast_to(base, (n_envs, N, 3)).copy()

@@ -144,6 +144,28 @@ def test_out_of_interior_reports_particle():
         gpu_rollout(SIM16, [LAWS["fluid"]], [], [st], 1, 1)
 
 
+@pytest.mark.parametrize("bad", ["nan", "inf", "fast"])
+def test_blown_up_state_reports_not_faults(bad):
+    """Non-finite or runaway particles are reported with the reference's text
+    and leave the device usable (every index derived from particle data is
+    range-checked before use)."""
+    rng = np.random.default_rng(1)
+    st = random_block(rng, 64, 0.4, 0.6)
+    if bad == "nan":
+        st["x"][5] = (np.nan, 0.5, 0.5)
+    elif bad == "inf":
+        st["x"][5] = (0.5, np.inf, 0.5)
+    else:
+        st["v"][5] = (0.0, 0.0, 1e30)
+    # a runaway velocity spreads through the grid to its neighbours, so (as in
+    # the reference's index-ordered g2p loop) the lowest failing index is named
+    want = "advected outside grid interior" if bad == "fast" else "particle 5 outside grid interior"
+    with pytest.raises(RuntimeError, match=want):
+        gpu_rollout(SIM16, [LAWS["neo_hookean"]], [], [st], 2, 2)
+    ok = gpu_rollout(SIM16, [LAWS["neo_hookean"]], [], [to_f32_state(random_block(rng, 64, 0.4, 0.6))], 1, 2)
+    assert np.isfinite(ok["state"]["x"]).all()
+
+
 # ---------------- gradients ----------------
 
 GRAD_CASES = [
