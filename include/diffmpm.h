@@ -31,7 +31,7 @@ extern "C" {
 #define DM_MAX_COLLIDERS 4
 #define DM_MAX_GROUPS 16
 #define DM_MAX_MATERIALS 4
-#define DM_OBS_DIM 7 /* com(3), var(3), spill(1) */
+#define DM_OBS_DIM 7 /* com(3), var(3), spill(1); + 8 per pooled group, see dm_obs_dim */
 
 /* MpmMaterial (mpm.hpp:23-41) extended: kind 0 fixed-corotated,
  * 1 neo-Hookean (fem.hpp:124-142) + x-axis actuation, 2 elastoplastic
@@ -71,6 +71,8 @@ typedef struct {
   int max_steps;         /* tape capacity in control steps */
   int checkpoint_every;  /* substeps per recompute segment; 0 = one per control step (algo.hpp:79-104) */
   double spill_half, spill_temp; /* spill observable footprint (tasks.hpp:606-614) */
+  int obs_groups;        /* pooled per-group statistics appended to the observables (config 5):
+                            per group mean x (3), mean v (3), var z (1), mean |v| (1) */
 } DmConfig;
 
 typedef struct DmContext DmContext;
@@ -123,6 +125,29 @@ int dm_backward_device(DmContext* ctx, const float* dobs, const float* dfinal_x,
                        const float* dfinal_F, const float* dfinal_C, float* dx0, float* dv0, float* dF0,
                        float* dC0, float* dcvo, float* dact, double* dE);
 
+/* Incremental backward, one control step at a time in reverse order, for
+ * callers whose per-step cotangents depend on the previous step's results
+ * (a policy in the loop: action_t = pi(obs_t)).  begin: final-state
+ * cotangent (any pointer may be NULL); step: cotangent of the observables of
+ * the latest unprocessed step t (dobs_t [E][obs_dim], may be NULL), returns
+ * that step's actuation / collider cotangents (dact_t [E][G], dcvo_t
+ * [E][K][9], may be NULL); end: initial-state and Young's modulus cotangents.
+ * dm_backward is begin + steps T-1..0 + end. */
+int dm_backward_begin(DmContext* ctx, const float* dfinal_x, const float* dfinal_v, const float* dfinal_F,
+                      const float* dfinal_C);
+int dm_backward_begin_device(DmContext* ctx, const float* dfinal_x, const float* dfinal_v, const float* dfinal_F,
+                             const float* dfinal_C);
+int dm_backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dact_t);
+int dm_backward_step_device(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dact_t);
+int dm_backward_end(DmContext* ctx, float* dx0, float* dv0, float* dF0, float* dC0, double* dE);
+int dm_backward_end_device(DmContext* ctx, float* dx0, float* dv0, float* dF0, float* dC0, double* dE);
+
+/* Observables of the current state without stepping (the reset observation,
+ * Task::observe, tasks.hpp:286-304).  cvo [E][K][9] may be NULL (no spill). */
+int dm_observe(DmContext* ctx, const float* cvo, float* obs);
+int dm_observe_device(DmContext* ctx, const float* cvo, float* obs);
+/* Observable dimension per env: DM_OBS_DIM + 8 * obs_groups. */
+int dm_obs_dim(const DmContext* ctx);
 /* Number of control steps currently on the tape. */
 int dm_tape_steps(const DmContext* ctx);
 

@@ -57,6 +57,7 @@ struct Config {
   int max_steps = 1;                     // tape capacity (control steps)
   int checkpoint_every = 0;              // 0: one recompute segment per control step
   double spill_half = 0.0, spill_temp = 0.0;
+  int obs_groups = 0;  // pooled per-group statistics appended to the observables
 };
 
 // Cotangents returned by backward (Tape::grad of every leaf, tape.hpp:166-170).
@@ -92,6 +93,7 @@ class MpmBatch {
     c.checkpoint_every = cfg.checkpoint_every;
     c.spill_half = cfg.spill_half;
     c.spill_temp = cfg.spill_temp;
+    c.obs_groups = cfg.obs_groups;
     std::vector<DmMaterial> dm(mats.size());
     for (std::size_t i = 0; i < mats.size(); ++i) {
       dm[i] = DmMaterial{static_cast<int>(mats[i].kind), mats[i].youngs,       mats[i].poisson,
@@ -158,7 +160,7 @@ class MpmBatch {
   // One recorded control step (Task::step + step_checkpointed).  cvo [E][K][9],
   // act [E][G]; returns the observables [E][7] (com, var, spill).
   std::vector<float> step(const std::vector<float>& cvo, const std::vector<float>& act = {}) {
-    std::vector<float> obs(static_cast<std::size_t>(E_) * DM_OBS_DIM);
+    std::vector<float> obs(static_cast<std::size_t>(E_) * dm_obs_dim(ctx_));
     check(dm_step(ctx_, cvo.empty() ? nullptr : cvo.data(), act.empty() ? nullptr : act.data(), obs.data()));
     return obs;
   }

@@ -43,7 +43,7 @@ class DmConfig(C.Structure):
                 ("dx", C.c_double), ("dt", C.c_double), ("gravity", C.c_double * 3), ("boundary", C.c_int),
                 ("alpha_c", C.c_double), ("mu_b", C.c_double), ("num_colliders", C.c_int), ("num_groups", C.c_int),
                 ("substeps", C.c_int), ("max_steps", C.c_int), ("checkpoint_every", C.c_int),
-                ("spill_half", C.c_double), ("spill_temp", C.c_double)]
+                ("spill_half", C.c_double), ("spill_temp", C.c_double), ("obs_groups", C.c_int)]
 
 
 _LIB = None
@@ -67,6 +67,15 @@ _SIGS = {
     "dm_debug_sort": (C.c_int, [_P, _P, _P]),
     "dm_launch_count": (C.c_ulonglong, [_P]),
     "dm_profile": (C.c_int, [_P, C.c_int, _P, _P]),
+    "dm_backward_begin": (C.c_int, [_P] * 5),
+    "dm_backward_begin_device": (C.c_int, [_P] * 5),
+    "dm_backward_step": (C.c_int, [_P] * 4),
+    "dm_backward_step_device": (C.c_int, [_P] * 4),
+    "dm_backward_end": (C.c_int, [_P] * 6),
+    "dm_backward_end_device": (C.c_int, [_P] * 6),
+    "dm_obs_dim": (C.c_int, [_P]),
+    "dm_observe": (C.c_int, [_P] * 3),
+    "dm_observe_device": (C.c_int, [_P] * 3),
 }
 
 PROF_CLASSES = ("bin", "p2g", "g2p", "g2p_adj", "p2g_adj", "env_reduce", "obs", "obs_adj", "layout", "grid",
@@ -119,7 +128,7 @@ class MpmBatch:
 
     def __init__(self, sim: dict, materials: list, colliders: list, num_envs: int, particles_per_env: int,
                  substeps: int, max_steps: int, num_groups: int = 0, checkpoint_every: int = 0,
-                 spill_half: float = 0.0, spill_temp: float = 0.0, device: int = 0):
+                 spill_half: float = 0.0, spill_temp: float = 0.0, device: int = 0, obs_groups: int = 0):
         L = lib()
         cfg = DmConfig()
         cfg.device = device
@@ -139,6 +148,7 @@ class MpmBatch:
         cfg.checkpoint_every = checkpoint_every
         cfg.spill_half = spill_half
         cfg.spill_temp = spill_temp
+        cfg.obs_groups = obs_groups
         mats = (DmMaterial * len(materials))()
         for i, m in enumerate(materials):
             mats[i].kind = KIND_LAW[m["kind"]]
@@ -172,6 +182,7 @@ class MpmBatch:
             L.dm_destroy(self._h)
             self._h = None
             raise (ValueError if "substeps" in text else RuntimeError)(text)
+        self.obs_dim = int(L.dm_obs_dim(self._h))
 
     # ---- plumbing ----
     def close(self):
@@ -243,7 +254,7 @@ class MpmBatch:
             return obs
         c = _f32(cvo) if cvo is not None else None
         a = _f32(act) if act is not None else None
-        o = np.empty((self.E, OBS_DIM), np.float32) if obs is None else obs
+        o = np.empty((self.E, self.obs_dim), np.float32) if obs is None else obs
         self._check(self._L.dm_step(self._h, _ptr(c), _ptr(a), _ptr(o)))
         return o
 
@@ -278,6 +289,47 @@ class MpmBatch:
                                         *(_ptr(res.get(k)) for k in ("x", "v", "F", "C", "cvo", "act", "E"))))
         return res
 
+    def observe(self, cvo=None, obs=None):
+        """Observables of the current state (reset observation) [E, obs_dim]."""
+        if _is_dev(obs) or _is_dev(cvo):
+            self._check(self._L.dm_observe_device(self._h, _ptr(cvo), _ptr(obs)))
+            return obs
+        o = np.empty((self.E, self.obs_dim), np.float32) if obs is None else obs
+        self._check(self._L.dm_observe(self._h, _ptr(_f32(cvo) if cvo is not None else None), _ptr(o)))
+        return o
+
+    # ---- incremental backward (policy in the loop) ----
+    def backward_begin(self, dfinal=None):
+        dfinal = dfinal or {}
+        vals = [dfinal.get(k) for k in ("x", "v", "F", "C")]
+        if any(_is_dev(a) for a in vals):
+            self._check(self._L.dm_backward_begin_device(self._h, *(_ptr(a) for a in vals)))
+        else:
+            vals = [_f32(a) for a in vals]
+            self._check(self._L.dm_backward_begin(self._h, *(_ptr(a) for a in vals)))
+
+    def backward_step(self, dobs_t=None, out_cvo=None, out_act=None):
+        """Processes the latest unprocessed control step.  dobs_t [E, obs_dim]
+        (torch CUDA tensors use the device path).  Returns (dcvo_t, dact_t)."""
+        if _is_dev(dobs_t) or _is_dev(out_act) or _is_dev(out_cvo):
+            self._check(self._L.dm_backward_step_device(self._h, _ptr(dobs_t), _ptr(out_cvo), _ptr(out_act)))
+            return out_cvo, out_act
+        d = _f32(dobs_t) if dobs_t is not None else None
+        c = np.zeros((self.E, self.K, 9), np.float32) if self.K else None
+        a = np.zeros((self.E, self.G), np.float32) if self.G else None
+        self._check(self._L.dm_backward_step(self._h, _ptr(d), _ptr(c), _ptr(a)))
+        return c, a
+
+    def backward_end(self, out=None):
+        if out is not None:
+            self._check(self._L.dm_backward_end_device(self._h, *(_ptr(out.get(k)) for k in ("x", "v", "F", "C", "E"))))
+            return out
+        res = {"x": np.zeros((self.E, self.N, 3), np.float32), "v": np.zeros((self.E, self.N, 3), np.float32),
+               "F": np.zeros((self.E, self.N, 9), np.float32), "C": np.zeros((self.E, self.N, 9), np.float32),
+               "E": np.zeros((self.E, self.n_materials), np.float64)}
+        self._check(self._L.dm_backward_end(self._h, *(_ptr(res[k]) for k in ("x", "v", "F", "C", "E"))))
+        return res
+
     def profile(self, enable: bool = True):
         """Returns {class: (ms, launches)} accumulated since the last call and
         switches per-kernel CUDA-event timing on/off."""
@@ -302,7 +354,8 @@ def from_scene(scene, max_steps=None, checkpoint_every=None, device=0) -> MpmBat
     return MpmBatch(scene.sim, scene.materials, scene.colliders, scene.n_envs, scene.n_per_env, scene.n_sub,
                     max_steps or scene.n_ctrl, num_groups=getattr(scene.task, "n_act", 0),
                     checkpoint_every=scene.checkpoint_every if checkpoint_every is None else checkpoint_every,
-                    spill_half=ls.get("spill_half", 0.0), spill_temp=ls.get("spill_temp", 0.0), device=device)
+                    spill_half=ls.get("spill_half", 0.0), spill_temp=ls.get("spill_temp", 0.0), device=device,
+                    obs_groups=scene.extra.get("obs_groups", 0))
 
 
 def run_scene(sim_batch: MpmBatch, scene, want_grad=True):
@@ -311,11 +364,13 @@ def run_scene(sim_batch: MpmBatch, scene, want_grad=True):
     from .losses import loss_and_dobs
     cvo, act = scene.cvo_act()
     sim_batch.set_state(scene.x, scene.v, scene.F, scene.C, scene.material, scene.group)
-    obs = np.zeros((scene.n_ctrl, scene.n_envs, OBS_DIM), np.float32)
+    obs = np.zeros((scene.n_ctrl, scene.n_envs, sim_batch.obs_dim), np.float32)
     for t in range(scene.n_ctrl):
         obs[t] = sim_batch.step(cvo[:, t] if scene.colliders else None,
                                 act[:, t] if getattr(scene.task, "n_act", 0) else None)
-    loss, dobs = loss_and_dobs(scene.loss, np.transpose(obs, (1, 0, 2)))
+    loss, dobs = loss_and_dobs(scene.loss, np.transpose(obs[:, :, :OBS_DIM], (1, 0, 2)))
+    if sim_batch.obs_dim > OBS_DIM:
+        dobs = np.concatenate([dobs, np.zeros(dobs.shape[:2] + (sim_batch.obs_dim - OBS_DIM,))], axis=-1)
     out = {"loss": loss, "obs": obs}
     if want_grad:
         g = sim_batch.backward(dobs=np.ascontiguousarray(np.transpose(dobs, (1, 0, 2)), dtype=np.float32))

@@ -62,6 +62,10 @@ struct DmContext {
   float4 *gmp = nullptr, *gv = nullptr, *gmb = nullptr;  // dense per-env grids
   int bin_warps = 16;
   int law = -1;  // the batch's single law kind (compile-time specialised kernels), -1: mixed
+  int od = DM_OBS_DIM;  // observable dimension per env
+  float* dobs_buf = nullptr;  // [E][od] staging for one step's observable cotangent
+  int bwd_t = -1;   // next control step the incremental backward processes (-1: not running)
+  int bwd_cur = 0;  // which adj buffer holds the running state cotangent
   float* tile_acc = nullptr;
   DevFlags* flags = nullptr;
   DevFlags* h_flags = nullptr;
@@ -377,6 +381,7 @@ int set_state_impl(DmContext* ctx, const float* x, const float* v, const float* 
                                                                      ctx->P.N, S0);
   ++ctx->launches;
   ctx->steps = 0;
+  ctx->bwd_t = -1;
   ctx->poisoned = false;
   const int rc = reset_flags(ctx);
   if (rc != DM_OK) return rc;
@@ -432,24 +437,23 @@ int step_impl(DmContext* ctx, const float* cvo, const float* act, float* obs, cu
     const int s = t * S + q;
     forward_substep(ctx, fwd_state(ctx, s), fwd_state(ctx, s + 1), t, q, q == 0, 0, false);
   }
-  float* o = ctx->obs_tape + (size_t)t * E * DM_OBS_DIM;
+  float* o = ctx->obs_tape + (size_t)t * E * ctx->od;
   PROF_BEGIN(ctx, 6);
   k_obs<<<E, 256, 0, ctx->stream>>>(ctx->P, fwd_state(ctx, (t + 1) * S), step_cvo(ctx, t), (float)ctx->cfg.spill_half,
-                                    (float)ctx->cfg.spill_temp, o);
+                                    (float)ctx->cfg.spill_temp, ctx->cfg.obs_groups, o, ctx->od);
   PROF_END(ctx, 6);
   ++ctx->launches;
-  if (obs) DM_CUDA(cudaMemcpyAsync(obs, o, (size_t)E * DM_OBS_DIM * sizeof(float), kout, ctx->stream));
+  if (obs) DM_CUDA(cudaMemcpyAsync(obs, o, (size_t)E * ctx->od * sizeof(float), kout, ctx->stream));
   const int rc = check_flags(ctx, true);
   if (rc != DM_OK) return rc;
   ctx->steps = t + 1;
   return DM_OK;
 }
 
-int backward_impl(DmContext* ctx, const float* dobs, const float* dfx, const float* dfv, const float* dfF,
-                  const float* dfC, float* dx0, float* dv0, float* dF0, float* dC0, float* dcvo, float* dact,
-                  double* dE, cudaMemcpyKind kin, cudaMemcpyKind kout) {
+int backward_begin(DmContext* ctx, const float* dfx, const float* dfv, const float* dfF, const float* dfC,
+                   cudaMemcpyKind kin) {
   if (ctx->poisoned) return DM_ERR_RUNTIME;
-  const int T = ctx->steps, S = ctx->cfg.substeps, E = ctx->P.E;
+  const int T = ctx->steps, E = ctx->P.E;
   const int Kc = ctx->P.K > 0 ? ctx->P.K : 1, Gc = ctx->P.G > 0 ? ctx->P.G : 1;
   const size_t N = ctx->Ntot;
   if (T == 0) {
@@ -477,93 +481,101 @@ int backward_impl(DmContext* ctx, const float* dobs, const float* dfx, const flo
   DM_CUDA(cudaMemsetAsync(ctx->gact, 0, (size_t)T * E * Gc * sizeof(double), ctx->stream));
   DM_CUDA(cudaMemsetAsync(ctx->gmu, 0, (size_t)E * 4 * sizeof(double), ctx->stream));
   DM_CUDA(cudaMemsetAsync(ctx->glam, 0, (size_t)E * 4 * sizeof(double), ctx->stream));
-  // dobs staged in part (T*E*7 floats) -- copied per step below
-  float* dobs_dev = nullptr;
-  if (dobs) {
-    if (!dalloc(ctx, &dobs_dev, (size_t)T * E * DM_OBS_DIM)) {
-      ctx->err = "backward: out of device memory";
-      return DM_ERR_CUDA;
-    }
-    DM_CUDA(cudaMemcpyAsync(dobs_dev, dobs, (size_t)T * E * DM_OBS_DIM * sizeof(float), kin, ctx->stream));
-  }
   // final-state cotangent in the physical order of the final state
-  int cur = 0;
-  float* A = ctx->adj[cur];
-  {
-    const StateView Sf = fwd_state(ctx, T * S);
-    if (dfx || dfv || dfF || dfC) {
-      float* stg = ctx->adj[1];
-      if (dfx) DM_CUDA(cudaMemcpyAsync(stg, dfx, 3 * N * sizeof(float), kin, ctx->stream));
-      if (dfv) DM_CUDA(cudaMemcpyAsync(stg + 3 * N, dfv, 3 * N * sizeof(float), kin, ctx->stream));
-      if (dfF) DM_CUDA(cudaMemcpyAsync(stg + 6 * N, dfF, 9 * N * sizeof(float), kin, ctx->stream));
-      if (dfC) DM_CUDA(cudaMemcpyAsync(stg + 15 * N, dfC, 9 * N * sizeof(float), kin, ctx->stream));
-      k_aos_to_soa_perm<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>(
-          (int)N, ctx->P.N, dfx ? stg : nullptr, dfv ? stg + 3 * N : nullptr, dfF ? stg + 6 * N : nullptr,
-          dfC ? stg + 15 * N : nullptr, Sf.attr, A, N);
-      ++ctx->launches;
-    } else {
-      DM_CUDA(cudaMemsetAsync(A, 0, 24 * N * sizeof(float), ctx->stream));
-    }
-  }
-  const int ck = ctx->ck;
-  for (int t = T - 1; t >= 0; --t) {
-    const int s_end = (t + 1) * S;
-    if (dobs_dev) {
-      PROF_BEGIN(ctx, 7);
-      k_obs_adj<<<E, 256, 0, ctx->stream>>>(ctx->P, store_view(ctx, s_end / ck), step_cvo(ctx, t),
-                                            (float)ctx->cfg.spill_half, (float)ctx->cfg.spill_temp,
-                                            dobs_dev + (size_t)t * E * DM_OBS_DIM, ctx->adj[cur], N,
-                                            ctx->gcvo + (size_t)t * E * Kc * 9);
-      PROF_END(ctx, 7);
-      ++ctx->launches;
-    }
-    for (int s0 = s_end - ck; s0 >= t * S; s0 -= ck) {
-      // replay the segment's forward (tape.hpp:229-233)
-      // replay the segment's forward (tape.hpp:229-233), keeping every
-      // substep's sort and grid blocks for its adjoint
-      for (int q = 0; q < ck; ++q) {
-        const int s = s0 + q;
-        const StateView So = q + 1 < ck ? seg_state(ctx, s0, s + 1) : view(ctx->tail, ctx->tail_attr, ctx->Ntot);
-        forward_substep(ctx, seg_state(ctx, s0, s), So, t, s - t * S, 0, q, true);
-      }
-      for (int q = ck - 1; q >= 0; --q) {
-        const int s = s0 + q;
-        backward_substep(ctx, seg_state(ctx, s0, s), t, q, ctx->adj[cur], ctx->adj[cur ^ 1]);
-        cur ^= 1;
-      }
-    }
-  }
-  // outputs
-  {
-    float* out = ctx->adj[cur ^ 1];
-    const StateView S0 = store_view(ctx, 0);
-    k_soa_to_aos<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>((int)N, ctx->P.N, ctx->adj[cur], S0.attr, N,
-                                                                       out, out + 3 * N, out + 6 * N, out + 15 * N);
+  ctx->bwd_cur = 0;
+  float* A = ctx->adj[0];
+  const StateView Sf = fwd_state(ctx, T * ctx->cfg.substeps);
+  if (dfx || dfv || dfF || dfC) {
+    float* stg = ctx->adj[1];
+    if (dfx) DM_CUDA(cudaMemcpyAsync(stg, dfx, 3 * N * sizeof(float), kin, ctx->stream));
+    if (dfv) DM_CUDA(cudaMemcpyAsync(stg + 3 * N, dfv, 3 * N * sizeof(float), kin, ctx->stream));
+    if (dfF) DM_CUDA(cudaMemcpyAsync(stg + 6 * N, dfF, 9 * N * sizeof(float), kin, ctx->stream));
+    if (dfC) DM_CUDA(cudaMemcpyAsync(stg + 15 * N, dfC, 9 * N * sizeof(float), kin, ctx->stream));
+    k_aos_to_soa_perm<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>(
+        (int)N, ctx->P.N, dfx ? stg : nullptr, dfv ? stg + 3 * N : nullptr, dfF ? stg + 6 * N : nullptr,
+        dfC ? stg + 15 * N : nullptr, Sf.attr, A, N);
     ++ctx->launches;
-    if (dx0) DM_CUDA(cudaMemcpyAsync(dx0, out, 3 * N * sizeof(float), kout, ctx->stream));
-    if (dv0) DM_CUDA(cudaMemcpyAsync(dv0, out + 3 * N, 3 * N * sizeof(float), kout, ctx->stream));
-    if (dF0) DM_CUDA(cudaMemcpyAsync(dF0, out + 6 * N, 9 * N * sizeof(float), kout, ctx->stream));
-    if (dC0) DM_CUDA(cudaMemcpyAsync(dC0, out + 15 * N, 9 * N * sizeof(float), kout, ctx->stream));
+  } else {
+    DM_CUDA(cudaMemsetAsync(A, 0, 24 * N * sizeof(float), ctx->stream));
   }
-  std::vector<double> h;
-  if (dcvo && ctx->P.K > 0) {
-    h.resize((size_t)T * E * Kc * 9);
-    DM_CUDA(cudaMemcpyAsync(h.data(), ctx->gcvo, h.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    DM_CUDA(cudaStreamSynchronize(ctx->stream));
-    std::vector<float> f(h.begin(), h.end());
-    DM_CUDA(cudaMemcpy(dcvo, f.data(), f.size() * sizeof(float), kout == cudaMemcpyDeviceToDevice
-                                                                          ? cudaMemcpyHostToDevice
-                                                                          : cudaMemcpyHostToHost));
+  ctx->bwd_t = T - 1;
+  return DM_OK;
+}
+
+// Converts an fp64 device array to fp32 into dst (host or device).
+int copy_out_f32(DmContext* ctx, float* dst, const double* src, size_t n, cudaMemcpyKind kout) {
+  std::vector<double> h(n);
+  DM_CUDA(cudaMemcpyAsync(h.data(), src, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  DM_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::vector<float> f(h.begin(), h.end());
+  DM_CUDA(cudaMemcpy(dst, f.data(), n * sizeof(float),
+                     kout == cudaMemcpyDeviceToDevice ? cudaMemcpyHostToDevice : cudaMemcpyHostToHost));
+  return DM_OK;
+}
+
+int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dact_t, cudaMemcpyKind kin,
+                  cudaMemcpyKind kout) {
+  if (ctx->poisoned) return DM_ERR_RUNTIME;
+  if (ctx->bwd_t < 0) {
+    ctx->err = "backward_step: no backward in progress (call dm_backward_begin)";
+    return DM_ERR_ARG;
   }
-  if (dact && ctx->P.G > 0) {
-    h.resize((size_t)T * E * Gc);
-    DM_CUDA(cudaMemcpyAsync(h.data(), ctx->gact, h.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    DM_CUDA(cudaStreamSynchronize(ctx->stream));
-    std::vector<float> f(h.begin(), h.end());
-    DM_CUDA(cudaMemcpy(dact, f.data(), f.size() * sizeof(float), kout == cudaMemcpyDeviceToDevice
-                                                                         ? cudaMemcpyHostToDevice
-                                                                         : cudaMemcpyHostToHost));
+  const int t = ctx->bwd_t, S = ctx->cfg.substeps, E = ctx->P.E, ck = ctx->ck;
+  const int Kc = ctx->P.K > 0 ? ctx->P.K : 1, Gc = ctx->P.G > 0 ? ctx->P.G : 1;
+  const size_t N = ctx->Ntot;
+  int cur = ctx->bwd_cur;
+  const int s_end = (t + 1) * S;
+  if (dobs_t) {
+    DM_CUDA(cudaMemcpyAsync(ctx->dobs_buf, dobs_t, (size_t)E * ctx->od * sizeof(float), kin, ctx->stream));
+    PROF_BEGIN(ctx, 7);
+    k_obs_adj<<<E, 256, 0, ctx->stream>>>(ctx->P, store_view(ctx, s_end / ck), step_cvo(ctx, t),
+                                          (float)ctx->cfg.spill_half, (float)ctx->cfg.spill_temp,
+                                          ctx->cfg.obs_groups, ctx->dobs_buf, ctx->od, ctx->adj[cur], N,
+                                          ctx->gcvo + (size_t)t * E * Kc * 9);
+    PROF_END(ctx, 7);
+    ++ctx->launches;
   }
+  for (int s0 = s_end - ck; s0 >= t * S; s0 -= ck) {
+    // replay the segment's forward (tape.hpp:229-233), keeping every
+    // substep's sort and grid blocks for its adjoint
+    for (int q = 0; q < ck; ++q) {
+      const int s = s0 + q;
+      const StateView So = q + 1 < ck ? seg_state(ctx, s0, s + 1) : view(ctx->tail, ctx->tail_attr, ctx->Ntot);
+      forward_substep(ctx, seg_state(ctx, s0, s), So, t, s - t * S, 0, q, true);
+    }
+    for (int q = ck - 1; q >= 0; --q) {
+      const int s = s0 + q;
+      backward_substep(ctx, seg_state(ctx, s0, s), t, q, ctx->adj[cur], ctx->adj[cur ^ 1]);
+      cur ^= 1;
+    }
+  }
+  ctx->bwd_cur = cur;
+  ctx->bwd_t = t - 1;
+  int rc = DM_OK;
+  if (dcvo_t && ctx->P.K > 0)
+    rc = copy_out_f32(ctx, dcvo_t, ctx->gcvo + (size_t)t * E * Kc * 9, (size_t)E * Kc * 9, kout);
+  if (rc == DM_OK && dact_t && ctx->P.G > 0)
+    rc = copy_out_f32(ctx, dact_t, ctx->gact + (size_t)t * E * Gc, (size_t)E * Gc, kout);
+  return rc;
+}
+
+int backward_end(DmContext* ctx, float* dx0, float* dv0, float* dF0, float* dC0, double* dE, cudaMemcpyKind kout) {
+  if (ctx->poisoned) return DM_ERR_RUNTIME;
+  if (ctx->bwd_t != -1) {
+    ctx->err = "backward_end: steps remain (call dm_backward_step for every recorded step)";
+    return DM_ERR_ARG;
+  }
+  const int E = ctx->P.E, cur = ctx->bwd_cur;
+  const size_t N = ctx->Ntot;
+  float* out = ctx->adj[cur ^ 1];
+  const StateView S0 = store_view(ctx, 0);
+  k_soa_to_aos<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>((int)N, ctx->P.N, ctx->adj[cur], S0.attr, N, out,
+                                                                     out + 3 * N, out + 6 * N, out + 15 * N);
+  ++ctx->launches;
+  if (dx0) DM_CUDA(cudaMemcpyAsync(dx0, out, 3 * N * sizeof(float), kout, ctx->stream));
+  if (dv0) DM_CUDA(cudaMemcpyAsync(dv0, out + 3 * N, 3 * N * sizeof(float), kout, ctx->stream));
+  if (dF0) DM_CUDA(cudaMemcpyAsync(dF0, out + 6 * N, 9 * N * sizeof(float), kout, ctx->stream));
+  if (dC0) DM_CUDA(cudaMemcpyAsync(dC0, out + 15 * N, 9 * N * sizeof(float), kout, ctx->stream));
   if (dE) {
     std::vector<double> mu((size_t)E * 4), la((size_t)E * 4);
     DM_CUDA(cudaMemcpyAsync(mu.data(), ctx->gmu, mu.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -573,16 +585,28 @@ int backward_impl(DmContext* ctx, const float* dobs, const float* dfx, const flo
     for (int e = 0; e < E; ++e)
       for (int m = 0; m < ctx->nmat; ++m)
         g[(size_t)e * ctx->nmat + m] = mu[e * 4 + m] * ctx->dmu_dE[m] + la[e * 4 + m] * ctx->dlam_dE[m];
-    DM_CUDA(cudaMemcpy(dE, g.data(), g.size() * sizeof(double), kout == cudaMemcpyDeviceToDevice
-                                                                       ? cudaMemcpyHostToDevice
-                                                                       : cudaMemcpyHostToHost));
+    DM_CUDA(cudaMemcpy(dE, g.data(), g.size() * sizeof(double),
+                       kout == cudaMemcpyDeviceToDevice ? cudaMemcpyHostToDevice : cudaMemcpyHostToHost));
   }
   DM_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (dobs_dev) {
-    cudaFree(dobs_dev);
-    ctx->bytes -= (size_t)T * E * DM_OBS_DIM * sizeof(float);
-  }
+  ctx->bwd_t = -1;
   return check_flags(ctx, false);
+}
+
+int backward_impl(DmContext* ctx, const float* dobs, const float* dfx, const float* dfv, const float* dfF,
+                  const float* dfC, float* dx0, float* dv0, float* dF0, float* dC0, float* dcvo, float* dact,
+                  double* dE, cudaMemcpyKind kin, cudaMemcpyKind kout) {
+  int rc = backward_begin(ctx, dfx, dfv, dfF, dfC, kin);
+  if (rc != DM_OK) return rc;
+  const int T = ctx->steps, E = ctx->P.E;
+  const int Kc = ctx->P.K > 0 ? ctx->P.K : 1, Gc = ctx->P.G > 0 ? ctx->P.G : 1;
+  for (int t = T - 1; t >= 0; --t) {
+    rc = backward_step(ctx, dobs ? dobs + (size_t)t * E * ctx->od : nullptr,
+                       dcvo ? dcvo + (size_t)t * E * Kc * 9 : nullptr, dact ? dact + (size_t)t * E * Gc : nullptr,
+                       kin, kout);
+    if (rc != DM_OK) return rc;
+  }
+  return backward_end(ctx, dx0, dv0, dF0, dC0, dE, kout);
 }
 
 }  // namespace
@@ -608,6 +632,8 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   if (cudaSetDevice(cfg->device) != cudaSuccess) return fail("dm_create: cudaSetDevice failed");
   ctx->ck = ck;
   ctx->nmat = num_materials;
+  if (cfg->obs_groups < 0 || cfg->obs_groups > DM_MAX_GROUPS) return fail("dm_create: obs_groups must be 0..16");
+  ctx->od = DM_OBS_DIM + 8 * cfg->obs_groups;
   DevParams& P = ctx->P;
   P.E = cfg->num_envs;
   P.N = cfg->particles_per_env;
@@ -695,7 +721,8 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
        dalloc(ctx, &ctx->tile_acc, TT * kNacc) && dalloc(ctx, &ctx->flags, 1);
   ok = ok && dalloc(ctx, &ctx->cvo_tape, (size_t)cfg->max_steps * P.E * Kc * 9) &&
        dalloc(ctx, &ctx->act_tape, (size_t)cfg->max_steps * P.E * Gc) &&
-       dalloc(ctx, &ctx->obs_tape, (size_t)cfg->max_steps * P.E * DM_OBS_DIM) &&
+       dalloc(ctx, &ctx->obs_tape, (size_t)cfg->max_steps * P.E * ctx->od) &&
+       dalloc(ctx, &ctx->dobs_buf, (size_t)P.E * ctx->od) &&
        dalloc(ctx, &ctx->gcvo, (size_t)cfg->max_steps * P.E * Kc * 9) &&
        dalloc(ctx, &ctx->gact, (size_t)cfg->max_steps * P.E * Gc) && dalloc(ctx, &ctx->gmu, (size_t)P.E * 4) &&
        dalloc(ctx, &ctx->glam, (size_t)P.E * 4);
@@ -725,7 +752,7 @@ void dm_destroy(DmContext* ctx) {
                   ctx->perm_all,  ctx->ptile, ctx->tstart_all, ctx->tcount_all, ctx->abase_all, ctx->acount_all,
                   ctx->active_all, ctx->nact_all, ctx->tail, ctx->tail_attr, ctx->gvb_pool, ctx->gmpb_pool,
                   ctx->blocks,    ctx->ablocks,    ctx->tile_acc,   ctx->gmp, ctx->gv, ctx->gmb,   ctx->flags,      ctx->cvo_tape,  ctx->act_tape,
-                  ctx->obs_tape,  ctx->gcvo,       ctx->gact,       ctx->gmu,        ctx->glam};
+                  ctx->obs_tape,  ctx->dobs_buf, ctx->gcvo,       ctx->gact,       ctx->gmu,        ctx->glam};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
@@ -796,6 +823,60 @@ int dm_profile(DmContext* ctx, int enable, double* ms, long long* counts) {
   }
   ctx->prof = enable != 0;
   return DM_OK;
+}
+
+int dm_backward_begin(DmContext* ctx, const float* dfx, const float* dfv, const float* dfF, const float* dfC) {
+  if (!ctx || !ctx->store) return DM_ERR_ARG;
+  return backward_begin(ctx, dfx, dfv, dfF, dfC, cudaMemcpyHostToDevice);
+}
+int dm_backward_begin_device(DmContext* ctx, const float* dfx, const float* dfv, const float* dfF, const float* dfC) {
+  if (!ctx || !ctx->store) return DM_ERR_ARG;
+  return backward_begin(ctx, dfx, dfv, dfF, dfC, cudaMemcpyDeviceToDevice);
+}
+int dm_backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dact_t) {
+  if (!ctx || !ctx->store) return DM_ERR_ARG;
+  return backward_step(ctx, dobs_t, dcvo_t, dact_t, cudaMemcpyHostToDevice, cudaMemcpyDeviceToHost);
+}
+int dm_backward_step_device(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dact_t) {
+  if (!ctx || !ctx->store) return DM_ERR_ARG;
+  return backward_step(ctx, dobs_t, dcvo_t, dact_t, cudaMemcpyDeviceToDevice, cudaMemcpyDeviceToDevice);
+}
+int dm_backward_end(DmContext* ctx, float* dx0, float* dv0, float* dF0, float* dC0, double* dE) {
+  if (!ctx || !ctx->store) return DM_ERR_ARG;
+  return backward_end(ctx, dx0, dv0, dF0, dC0, dE, cudaMemcpyDeviceToHost);
+}
+int dm_backward_end_device(DmContext* ctx, float* dx0, float* dv0, float* dF0, float* dC0, double* dE) {
+  if (!ctx || !ctx->store) return DM_ERR_ARG;
+  return backward_end(ctx, dx0, dv0, dF0, dC0, dE, cudaMemcpyDeviceToDevice);
+}
+int dm_obs_dim(const DmContext* ctx) { return ctx ? ctx->od : DM_OBS_DIM; }
+
+static int observe_impl(DmContext* ctx, const float* cvo, float* obs, cudaMemcpyKind kin, cudaMemcpyKind kout) {
+  if (!ctx || !ctx->store) return DM_ERR_ARG;
+  if (ctx->poisoned) return DM_ERR_RUNTIME;
+  const int E = ctx->P.E, K = ctx->P.K;
+  // stage the pose in the slot after the last recorded step (unused until the next dm_step)
+  const int t = ctx->steps < ctx->cfg.max_steps ? ctx->steps : ctx->cfg.max_steps - 1;
+  DevParams P = ctx->P;
+  if (K > 0 && cvo)
+    DM_CUDA(cudaMemcpyAsync(const_cast<float*>(step_cvo(ctx, t)), cvo, (size_t)E * K * 9 * sizeof(float), kin,
+                            ctx->stream));
+  else
+    P.K = 0;  // no pose: no spill statistic
+  float* o = ctx->obs_tape + (size_t)t * E * ctx->od;
+  k_obs<<<E, 256, 0, ctx->stream>>>(P, fwd_state(ctx, ctx->steps * ctx->cfg.substeps), step_cvo(ctx, t),
+                                    (float)ctx->cfg.spill_half, (float)ctx->cfg.spill_temp, ctx->cfg.obs_groups, o,
+                                    ctx->od);
+  ++ctx->launches;
+  DM_CUDA(cudaMemcpyAsync(obs, o, (size_t)E * ctx->od * sizeof(float), kout, ctx->stream));
+  DM_CUDA(cudaStreamSynchronize(ctx->stream));
+  return DM_OK;
+}
+int dm_observe(DmContext* ctx, const float* cvo, float* obs) {
+  return observe_impl(ctx, cvo, obs, cudaMemcpyHostToDevice, cudaMemcpyDeviceToHost);
+}
+int dm_observe_device(DmContext* ctx, const float* cvo, float* obs) {
+  return observe_impl(ctx, cvo, obs, cudaMemcpyDeviceToDevice, cudaMemcpyDeviceToDevice);
 }
 
 int dm_debug_sort(DmContext* ctx, int* keys, int* perm) {

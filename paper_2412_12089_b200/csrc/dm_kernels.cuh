@@ -958,10 +958,12 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   return r;
 }
 
-// com(3), var(3), spill(1) per env (tasks.hpp:286-304, 604-615); fp64 sums
-// in a fixed order (deterministic).
+// Per env observables after a control step: com(3), var(3), spill(1)
+// (tasks.hpp:286-304, 604-615) followed, when ngr > 0, by pooled statistics of
+// each actuation group g (config 5's 64-d observation): mean x (3), mean v (3),
+// var z (1), mean |v| (1).  fp64 sums in a fixed order (deterministic).
 __global__ void __launch_bounds__(256) k_obs(DevParams P, StateView S, const float* __restrict__ cvo, float spill_half,
-                                             float spill_temp, float* __restrict__ obs) {
+                                             float spill_temp, int ngr, float* __restrict__ obs, int od) {
   __shared__ double sh[8];
   const int e = blockIdx.x;
   const size_t base = (size_t)e * P.N;
@@ -990,8 +992,8 @@ __global__ void __launch_bounds__(256) k_obs(DevParams P, StateView S, const flo
 #pragma unroll
   for (int a = 0; a < 3; ++a) v[a] = block_sum(q[a], sh) / P.N;
   const double spt = block_sum(sp, sh) / P.N;
+  float* o = obs + (size_t)e * od;
   if (threadIdx.x == 0) {
-    float* o = obs + (size_t)e * 7;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       o[a] = (float)m[a];
@@ -999,17 +1001,61 @@ __global__ void __launch_bounds__(256) k_obs(DevParams P, StateView S, const flo
     }
     o[6] = (float)spt;
   }
+  for (int g = 0; g < ngr; ++g) {
+    double c = 0.0, sx[3] = {0.0, 0.0, 0.0}, sv[3] = {0.0, 0.0, 0.0}, sa = 0.0;
+    for (int p = threadIdx.x; p < P.N; p += blockDim.x) {
+      const size_t i = base + p;
+      if (attr_group(S.attr[i]) != g) continue;
+      c += 1.0;
+      double v2 = 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        sx[a] += (double)S.c(a, i);
+        const double va = (double)S.c(3 + a, i);
+        sv[a] += va;
+        v2 += va * va;
+      }
+      sa += sqrt(v2);
+    }
+    const double n = fmax(block_sum(c, sh), 1.0);
+    double mx[3], mv[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      mx[a] = block_sum(sx[a], sh) / n;
+      mv[a] = block_sum(sv[a], sh) / n;
+    }
+    const double ma = block_sum(sa, sh) / n;
+    double sz = 0.0;
+    for (int p = threadIdx.x; p < P.N; p += blockDim.x) {
+      const size_t i = base + p;
+      if (attr_group(S.attr[i]) != g) continue;
+      const double d = (double)S.c(2, i) - mx[2];
+      sz += d * d;
+    }
+    const double vz = block_sum(sz, sh) / n;
+    if (threadIdx.x == 0) {
+      float* og = o + 7 + 8 * g;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        og[a] = (float)mx[a];
+        og[3 + a] = (float)mv[a];
+      }
+      og[6] = (float)vz;
+      og[7] = (float)ma;
+    }
+  }
 }
 
 // Adds the observable cotangent into the state cotangent (physical order of
 // that state) and the spill's collider-center cotangent into gcvo_t.
 __global__ void __launch_bounds__(256) k_obs_adj(DevParams P, StateView S, const float* __restrict__ cvo,
-                                                 float spill_half, float spill_temp, const float* __restrict__ dobs,
-                                                 float* __restrict__ adj, size_t astride, double* __restrict__ gcvo_t) {
+                                                 float spill_half, float spill_temp, int ngr,
+                                                 const float* __restrict__ dobs, int od, float* __restrict__ adj,
+                                                 size_t astride, double* __restrict__ gcvo_t) {
   __shared__ double sh[8];
   const int e = blockIdx.x;
   const size_t base = (size_t)e * P.N;
-  const float* ob = dobs + (size_t)e * 7;
+  const float* ob = dobs + (size_t)e * od;
   double s[3] = {0.0, 0.0, 0.0};
   for (int p = threadIdx.x; p < P.N; p += blockDim.x)
 #pragma unroll
@@ -1050,6 +1096,43 @@ __global__ void __launch_bounds__(256) k_obs_adj(DevParams P, StateView S, const
     if (threadIdx.x == 0) {
       gcvo_t[(size_t)e * P.K * 9 + 0] += gcx;
       gcvo_t[(size_t)e * P.K * 9 + 1] += gcy;
+    }
+  }
+  // pooled group statistics
+  for (int gi = 0; gi < ngr; ++gi) {
+    const float* og = ob + 7 + 8 * gi;
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) any = any || og[k] != 0.f;
+    if (!any) continue;
+    double c = 0.0, sz = 0.0;
+    for (int p = threadIdx.x; p < P.N; p += blockDim.x) {
+      const size_t i = base + p;
+      if (attr_group(S.attr[i]) != gi) continue;
+      c += 1.0;
+      sz += (double)S.c(2, i);
+    }
+    const double n = fmax(block_sum(c, sh), 1.0);
+    const double mz = block_sum(sz, sh) / n;
+    for (int p = threadIdx.x; p < P.N; p += blockDim.x) {
+      const size_t i = base + p;
+      if (attr_group(S.attr[i]) != gi) continue;
+      double vv[3], v2 = 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        vv[a] = (double)S.c(3 + a, i);
+        v2 += vv[a] * vv[a];
+      }
+      const double vn = sqrt(v2);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        double gx = og[a] / n;
+        if (a == 2) gx += og[6] * 2.0 * ((double)S.c(2, i) - mz) / n;
+        adj[a * astride + i] += (float)gx;
+        double gv = og[3 + a] / n;
+        if (vn > 0.0) gv += og[7] * vv[a] / (vn * n);
+        adj[(3 + a) * astride + i] += (float)gv;
+      }
     }
   }
 }

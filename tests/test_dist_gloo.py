@@ -73,3 +73,58 @@ def test_env_sharding_world2_matches_single():
                        for e in range(4)])
     assert np.array_equal(sharded, single)
     assert mx == 2.0
+
+
+def _grad_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+    os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    from paper_2412_12089_b200.sapo import SapoTrainer, MLP
+    net = MLP([4, 8, 1])
+    torch.manual_seed(rank)
+    for p in net.parameters():
+        dist.broadcast(p.data, 0)
+    x = torch.full((3, 4), float(rank + 1))
+    net(x).sum().backward()
+    fake = SapoTrainer.__new__(SapoTrainer)
+    fake.dist = dist
+    fake.dev = torch.device("cpu")
+    SapoTrainer._allreduce_grads(fake, list(net.parameters()))
+    tot = SapoTrainer._allreduce_scalar(fake, float(rank + 1))
+    if rank == 0:
+        out.put(([p.grad.clone() for p in net.parameters()], tot, [p.detach().clone() for p in net.parameters()]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sapo_gradient_allreduce_world2():
+    """Actor/critic gradients are summed over ranks (each rank's loss carries
+    1/N_global), as the NCCL path does on GPUs."""
+    import torch
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_grad_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    grads, tot, params = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    from paper_2412_12089_b200.sapo import MLP
+    net = MLP([4, 8, 1])
+    with torch.no_grad():
+        for p, q_ in zip(net.parameters(), params):
+            p.copy_(q_)
+    for r in range(2):
+        net(torch.full((3, 4), float(r + 1))).sum().backward()
+    for p, g in zip(net.parameters(), grads):
+        assert torch.allclose(p.grad, g, atol=1e-6)
+    assert tot == 3.0
