@@ -10,8 +10,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_cpp_adapter_smoke():
-    exe = os.path.join(ROOT, "tests", "native", "cpp_adapter_smoke")
-    assert os.path.exists(exe), "built by __graft_entry__.build()"
+    import hostcheck
+    exe = hostcheck.build_cpp_smoke()  # rebuilt when the ABI headers changed
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     print(out.stdout, out.stderr)
     assert out.returncode == 0, out.stdout + out.stderr
