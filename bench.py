@@ -370,14 +370,59 @@ def run_ours(args, scene, rank, world, local, dist):
             json.dump(line, f, indent=1)
 
 
+def run_sapo(args, rank, world, local, dist):
+    """Config 5: full SAPO iterations (rollout with the policy in the loop,
+    analytic gradient through the simulator, twin-critic TD(lambda), NCCL
+    all-reduce of actor/critic gradients).  512 envs per GPU (weak scaling)."""
+    import torch
+    from paper_2412_12089_b200.sapo import SapoTrainer
+    torch.cuda.set_device(local)
+    per = (args.envs // world) if args.envs else 512
+    H = args.ctrl or 32
+    tr = SapoTrainer(seed=0, n_envs=per, env_offset=rank * per, n_global=per * world, horizon=H, n_sub=16,
+                     dist=dist, device=local)
+    for _ in range(args.warmup):
+        tr.iteration()
+    launches0 = tr.sim.launches
+    barrier(dist)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            stats = tr.iteration()
+        torch.cuda.synchronize()
+        ms_rank = (time.perf_counter() - t0) * 1e3 / args.steps
+    ms = max_over_ranks(dist, ms_rank)
+    if rank != 0:
+        return
+    units = per * world * tr.N * H * 16
+    line = {"metric": METRIC, "value": units / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "cfg5_sapo_iteration", "envs": per * world, "envs_per_gpu": per,
+                       "particles_per_env": tr.N, "horizon": H, "substeps_per_step": 16,
+                       "critic_passes": tr.critic_passes, "nets": "actor 64-256x3-16, twin critics 64-256x3-1, ELU+LN"},
+            "env_steps_per_s": per * world * H / (ms / 1e3), "gpu_launches": int((tr.sim.launches - launches0) // args.steps),
+            "clocks": clk.summary(), "last_iteration": stats,
+            "timing": "host wall clock around whole iterations (sim + torch nets + NCCL), max over ranks"}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
     if args.impl == "reference" and rank != 0:
         return
     dist = init_dist(world, local) if args.impl == "ours" else None
+    if args.config == 5 and args.impl == "ours":
+        run_sapo(args, rank, world, local, dist)
+        if dist is not None:
+            dist.destroy_process_group()
+        return
     from paper_2412_12089_b200 import scenes
-    total = args.envs or {1: 1, 2: 32, 3: 256, 4: 1024}[args.config]
+    total = args.envs or {1: 1, 2: 32, 3: 256, 4: 1024, 5: 512}[args.config]
+    if args.config == 5:
+        args.config = 2  # the reference arm times config 5's simulator (config 2 physics)
     per = total // world if args.impl == "ours" else min(total, cpu_threads())
     kw = {"n_envs": per, "env_offset": rank * per if args.impl == "ours" else 0}
     if args.ctrl:
