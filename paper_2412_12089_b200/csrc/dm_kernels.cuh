@@ -154,6 +154,15 @@ __device__ __forceinline__ void load_state(const StateView& S, size_t i, float x
   }
 }
 
+// G2P and its adjoint only read x and F of the start-of-substep state
+// (v and C are outputs): 48 B instead of 96 B per particle.
+__device__ __forceinline__ void load_xF(const StateView& S, size_t i, float x[3], m3<float>& F) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) x[a] = S.c(a, i);
+#pragma unroll
+  for (int q = 0; q < 9; ++q) F.a[q] = S.c(6 + q, i);
+}
+
 __device__ __forceinline__ void store_state(const StateView& S, size_t i, v3<float> x, v3<float> v, const m3<float>& F,
                                             const m3<float>& C) {
   S.c(0, i) = x.x;
@@ -650,13 +659,16 @@ __global__ void __launch_bounds__(kWarps * 32, kLawBlocks(LAW)) k_g2p(DevParams 
     }
     const size_t tix = (size_t)e * P.Tn + t;
     const int start = tile_start[tix], cnt = tile_count[tix];
+    const size_t row = (size_t)e * P.N + start;
+    int src_next = lane < cnt ? perm[row + lane] : 0;  // index prefetch: one chunk ahead
     for (int c0 = lane; c0 < cnt; c0 += 32) {
-      const size_t dst = (size_t)e * P.N + start + c0;
-      const int src = perm[dst];
+      const size_t dst = row + c0;
+      const int src = src_next;
+      if (c0 + 32 < cnt) src_next = perm[dst + 32];
       float x[3];
       v3<float> v;
       m3<float> F, C;
-      load_state(S, src, x, v, F, C);
+      load_xF(S, src, x, F);
       const uint32_t at = S.attr[src];
       Stencil<float> sc;
       make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
@@ -682,7 +694,7 @@ __global__ void __launch_bounds__(kWarps * 32, kLawBlocks(LAW)) k_g2p(DevParams 
 // end-of-substep state (sorted position); writes particle-side partial
 // cotangents (sorted position) and a 6^3 block of node-velocity cotangents.
 template <int LAW>
-__global__ void __launch_bounds__(kWarps * 32, 4) k_g2p_adj(DevParams P, StateView S, const float* __restrict__ adj_in,
+__global__ void __launch_bounds__(kWarps * 32, 3) k_g2p_adj(DevParams P, StateView S, const float* __restrict__ adj_in,
                                                          size_t astride, const int* __restrict__ perm,
                                                          const int* __restrict__ tile_start,
                                                          const int* __restrict__ tile_count,
@@ -719,9 +731,8 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_g2p_adj(DevParams P, StateVi
         const size_t dst = (size_t)e * P.N + start + c0 + lane;
         const int src = perm[dst];
         float x[3];
-        v3<float> v;
-        m3<float> F, C;
-        load_state(S, src, x, v, F, C);
+        m3<float> F;
+        load_xF(S, src, x, F);
         const uint32_t at = S.attr[src];
         Stencil<float> sc;
         make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
@@ -847,9 +858,12 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_p2g_adj(DevParams P, StateVi
     float actb[NG];
 #pragma unroll
     for (int q = 0; q < NG; ++q) actb[q] = 0.f;
+    const size_t row = (size_t)e * P.N + start;
+    int src_next = lane < cnt ? perm[row + lane] : 0;  // index prefetch: one chunk ahead
     for (int c0 = lane; c0 < cnt; c0 += 32) {
-      const size_t j = (size_t)e * P.N + start + c0;
-      const int src = perm[j];
+      const size_t j = row + c0;
+      const int src = src_next;
+      if (c0 + 32 < cnt) src_next = perm[j + 32];
       float x[3];
       v3<float> v;
       m3<float> F, C;
