@@ -217,7 +217,7 @@ const float* step_act(DmContext* c, int t) {
 void launch_p2g(DmContext* c, const StateView& S, const Slot& q, int t, int sub) {
   PROF_BEGIN(c, 1);
 #define L_P2G(LW)                                                                                               \
-  k_p2g<LW><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.active, \
+  k_p2g<LW><<<c->grid_tiles, kWarps * 32, kP2gSmem, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.active, \
                                                           step_act(c, t), c->blocks, c->flags, q.nact, sub)
   DM_LAW_DISPATCH(c, L_P2G);
 #undef L_P2G
@@ -270,7 +270,7 @@ void backward_substep(DmContext* c, const StateView& S, int t, int qi, const flo
   const Slot q = slot(c, qi);
   PROF_BEGIN(c, 3);
 #define L_G2PA(LW)                                                                                            \
-  k_g2p_adj<LW><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, adj_in, c->Ntot, q.perm, q.tile_start, \
+  k_g2p_adj<LW><<<c->grid_tiles, kWarps * 32, kG2pAdjSmem, c->stream>>>(c->P, S, adj_in, c->Ntot, q.perm, q.tile_start, \
                                                               q.tile_count, q.active, q.gvb, c->ablocks,    \
                                                               c->part, c->tile_acc, q.nact)
   DM_LAW_DISPATCH(c, L_G2PA);
@@ -696,6 +696,17 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
     s.radius = (float)shapes[c].radius;
     s.length = (float)shapes[c].length;
     s.thickness = (float)shapes[c].thickness;
+  }
+  {
+#define DM_SMEM_ATTR(LW)                                                                                   \
+  cudaFuncSetAttribute(k_p2g<LW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kP2gSmem);            \
+  cudaFuncSetAttribute(k_g2p_adj<LW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kG2pAdjSmem)
+    DM_SMEM_ATTR(0);
+    DM_SMEM_ATTR(1);
+    DM_SMEM_ATTR(2);
+    DM_SMEM_ATTR(3);
+    DM_SMEM_ATTR(-1);
+#undef DM_SMEM_ATTR
   }
   ctx->Ntot = (size_t)P.E * P.N;
   const size_t N = ctx->Ntot;

@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_cellsort(DevParams P, StateView
 // atomics, bit-reproducible.
 struct RunAcc {
   int cur;
-  float4 acc;
+  float4 acc[3];
 };
 
 __device__ __forceinline__ void stage_payload(float* __restrict__ pp, int lbl, const Stencil<float>& sc, float m,
@@ -406,65 +406,104 @@ __device__ __forceinline__ void stage_payload(float* __restrict__ pp, int lbl, c
   for (int r = 0; r < 9; ++r) pp[14 + r] = Ad.a[r];
 }
 
-__device__ __forceinline__ void run_flush(float4* __restrict__ blk, RunAcc& ra, int off) {
-  if (ra.cur >= 0) {
-    float4 b = blk[ra.cur + off];
-    b.x += ra.acc.x;
-    b.y += ra.acc.y;
-    b.z += ra.acc.z;
-    b.w += ra.acc.w;
-    blk[ra.cur + off] = b;
-  }
-  ra.acc = make_float4(0.f, 0.f, 0.f, 0.f);
+__device__ __forceinline__ void run_reset(RunAcc& ra) {
+  ra.cur = -1;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) ra.acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
-__device__ __forceinline__ void scatter_runs(float4* __restrict__ blk, const float* __restrict__ pay, int nv, int lane,
+// Adds the lane's three run sums (nodes (i, j, 0..2) of the run's base) into
+// its group's block copy.
+__device__ __forceinline__ void run_flush(float4* __restrict__ blk, RunAcc& ra, int off) {
+  if (ra.cur >= 0) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      float4 b = blk[ra.cur + off + k];
+      b.x += ra.acc[k].x;
+      b.y += ra.acc[k].y;
+      b.z += ra.acc[k].z;
+      b.w += ra.acc[k].w;
+      blk[ra.cur + off + k] = b;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) ra.acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// Lanes 0..26 = 3 groups x 9 stencil columns (i, j); group g takes the
+// chunk's particles k = g, g+3, ... (a sorted subsequence, so same-cell runs
+// stay contiguous) and each lane accumulates the 3 nodes (i, j, 0..2) of its
+// column.  Each group flushes into its own block copy (no write races); the
+// copies are summed in fixed order by scatter_store.
+template <bool HASM>
+__device__ __forceinline__ void scatter_runs(float4* __restrict__ blk3, const float* __restrict__ pay, int nv, int lane,
                                              RunAcc& ra) {
   if (lane < 27) {
-    const int oi = lane / 9, oj = (lane / 3) % 3, ok = lane % 3;
-    const int off = (oi * kExt + oj) * kExt + ok;
-    const float fo_i = (float)oi, fo_j = (float)oj, fo_k = (float)ok;
-    for (int k = 0; k < nv; ++k) {
+    const int g = lane / 9, i = (lane % 9) / 3, j = lane % 3;
+    float4* blk = blk3 + g * kExt3;
+    const int off = (i * kExt + j) * kExt;
+    const float fi = (float)i, fj = (float)j;
+    for (int k = g; k < nv; k += 3) {
       const float* pk = pay + k * kPay;
       const int lb = __float_as_int(pk[0]);
       if (lb != ra.cur) {
         run_flush(blk, ra, off);
         ra.cur = lb;
       }
-      const float w = pk[1 + oi] * pk[4 + oj] * pk[7 + ok];
-      const float cx = pk[11] + pk[14] * fo_i + pk[15] * fo_j + pk[16] * fo_k;
-      const float cy = pk[12] + pk[17] * fo_i + pk[18] * fo_j + pk[19] * fo_k;
-      const float cz = pk[13] + pk[20] * fo_i + pk[21] * fo_j + pk[22] * fo_k;
-      ra.acc.x += w * pk[10];
-      ra.acc.y += w * cx;
-      ra.acc.z += w * cy;
-      ra.acc.w += w * cz;
+      const float wij = pk[1 + i] * pk[4 + j];
+      const float bx = pk[11] + pk[14] * fi + pk[15] * fj;
+      const float by = pk[12] + pk[17] * fi + pk[18] * fj;
+      const float bz = pk[13] + pk[20] * fi + pk[21] * fj;
+      const float ax = pk[16], ay = pk[19], az = pk[22];
+      const float m = HASM ? pk[10] : 0.f;
+#pragma unroll
+      for (int kk = 0; kk < 3; ++kk) {
+        const float w = wij * pk[7 + kk];
+        const float fk = (float)kk;
+        if (HASM) ra.acc[kk].x += w * m;
+        ra.acc[kk].y += w * (bx + ax * fk);
+        ra.acc[kk].z += w * (by + ay * fk);
+        ra.acc[kk].w += w * (bz + az * fk);
+      }
     }
   }
   __syncwarp();
 }
 
-__device__ __forceinline__ void scatter_finish(float4* __restrict__ blk, int lane, RunAcc& ra) {
-  if (lane < 27) run_flush(blk, ra, ((lane / 9) * kExt + (lane / 3) % 3) * kExt + lane % 3);
+__device__ __forceinline__ void scatter_zero(float4* __restrict__ blk3, int lane) {
+  for (int i = lane; i < 3 * kExt3; i += 32) blk3[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// Final flush, then block = copy0 + copy1 + copy2 (fixed order) -> dst.
+__device__ __forceinline__ void scatter_store(float4* __restrict__ blk3, int lane, RunAcc& ra, float4* __restrict__ dst) {
+  if (lane < 27) run_flush(blk3 + (lane / 9) * kExt3, ra, (((lane % 9) / 3) * kExt + lane % 3) * kExt);
+  __syncwarp();
+  for (int i = lane; i < kExt3; i += 32) {
+    const float4 a = blk3[i], b = blk3[kExt3 + i], c = blk3[2 * kExt3 + i];
+    dst[i] = make_float4((a.x + b.x) + c.x, (a.y + b.y) + c.y, (a.z + b.z) + c.z, (a.w + b.w) + c.w);
+  }
   __syncwarp();
 }
+
+// dynamic shared memory of the scatter kernels (bytes per CTA)
+constexpr size_t kP2gSmem = (size_t)kWarps * (3 * kExt3 * sizeof(float4) + 32 * kPay * sizeof(float));
+constexpr size_t kG2pAdjSmem = (size_t)kWarps * (4 * kExt3 * sizeof(float4) + 32 * kPay * sizeof(float));
 
 // ============================ P2G ============================
 // Per active tile: stage particle payloads (lanes = particles), scatter runs
 // into the warp's 6^3 shared block (lanes = stencil nodes), write the block.
 template <int LAW>
-__global__ void __launch_bounds__(kWarps * 32, kLawBlocks(LAW)) k_p2g(DevParams P, StateView S, const int* __restrict__ perm,
+__global__ void __launch_bounds__(kWarps * 32, 4) k_p2g(DevParams P, StateView S, const int* __restrict__ perm,
                                                      const int* __restrict__ tile_start,
                                                      const int* __restrict__ tile_count, const int2* __restrict__ active,
                                                      const float* __restrict__ act, float4* __restrict__ blocks,
                                                      DevFlags* flags, const int* nact, int substep) {
-  __shared__ float4 blk[kWarps][kExt3];
-  __shared__ float pay[kWarps][32 * kPay];
+  extern __shared__ float4 dsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_active = *(const volatile int*)nact;
   const TransferCtx<float> T = tctx(P);
-  float4* bw = blk[warp];
-  float* pw = pay[warp];
+  float4* bw = dsm + warp * 3 * kExt3;  // 3 group copies of the 6^3 block
+  float* pw = reinterpret_cast<float*>(dsm + kWarps * 3 * kExt3) + warp * 32 * kPay;
   for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
     const int2 et = active[a];
     const int e = et.x, t = et.y;
@@ -472,10 +511,9 @@ __global__ void __launch_bounds__(kWarps * 32, kLawBlocks(LAW)) k_p2g(DevParams 
     const int o[3] = {tx * kTile, ty * kTile, tz * kTile};
     const size_t tix = (size_t)e * P.Tn + t;
     const int start = tile_start[tix], cnt = tile_count[tix];
-    for (int i = lane; i < kExt3; i += 32) bw[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    scatter_zero(bw, lane);
     RunAcc ra;
-    ra.cur = -1;
-    ra.acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    run_reset(ra);
     for (int c0 = 0; c0 < cnt; c0 += 32) {
       if (c0 + lane < cnt) {
         const int src = perm[(size_t)e * P.N + start + c0 + lane];
@@ -499,12 +537,9 @@ __global__ void __launch_bounds__(kWarps * 32, kLawBlocks(LAW)) k_p2g(DevParams 
         stage_payload(pw + lane * kPay, lbl, sc, L.mass, q, Ad);
       }
       __syncwarp();
-      scatter_runs(bw, pw, min(32, cnt - c0), lane, ra);
+      scatter_runs<true>(bw, pw, min(32, cnt - c0), lane, ra);
     }
-    scatter_finish(bw, lane, ra);
-    float4* dst = blocks + tix * kExt3;
-    for (int i = lane; i < kExt3; i += 32) dst[i] = bw[i];
-    __syncwarp();
+    scatter_store(bw, lane, ra, blocks + tix * kExt3);
   }
 }
 
@@ -701,31 +736,26 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_g2p_adj(DevParams P, StateVi
                                                          const int2* __restrict__ active, const float4* __restrict__ gvb,
                                                          float4* __restrict__ ablocks, float* __restrict__ part,
                                                          float* __restrict__ tile_acc, const int* nact) {
-  __shared__ float4 vg[kWarps][kExt3];
-  __shared__ float4 ab[kWarps][kExt3];
-  __shared__ float pay[kWarps][32 * kPay];
+  extern __shared__ float4 dsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TransferCtx<float> T = tctx(P);
-  float4* vw = vg[warp];
-  float4* aw = ab[warp];
-  float* pw = pay[warp];
+  float4* vw = dsm + warp * 4 * kExt3;  // the tile's node velocities
+  float4* aw = vw + kExt3;              // 3 group copies of the cotangent block
+  float* pw = reinterpret_cast<float*>(dsm + kWarps * 4 * kExt3) + warp * 32 * kPay;
   const int n_active = *(const volatile int*)nact;
   for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
     const int2 et = active[a];
     const int e = et.x, t = et.y;
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
-    for (int i = lane; i < kExt3; i += 32) {
-      vw[i] = gvb[(size_t)a * kExt3 + i];  // the replayed substep's grid, stored per tile slot
-      aw[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    for (int i = lane; i < kExt3; i += 32) vw[i] = gvb[(size_t)a * kExt3 + i];  // the replayed substep's grid, by slot
+    scatter_zero(aw, lane);
     __syncwarp();
     const size_t tix = (size_t)e * P.Tn + t;
     const int start = tile_start[tix], cnt = tile_count[tix];
     double mub[4] = {0.0, 0.0, 0.0, 0.0};  // fp64: cancelling per-particle sums
     RunAcc ra;
-    ra.cur = -1;
-    ra.acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    run_reset(ra);
     for (int c0 = 0; c0 < cnt; c0 += 32) {
       if (c0 + lane < cnt) {
         const size_t dst = (size_t)e * P.N + start + c0 + lane;
@@ -765,11 +795,9 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_g2p_adj(DevParams P, StateVi
         stage_payload(pw + lane * kPay, (lb[0] * kExt + lb[1]) * kExt + lb[2], sc, 0.f, gq, Bd);
       }
       __syncwarp();
-      scatter_runs(aw, pw, min(32, cnt - c0), lane, ra);
+      scatter_runs<false>(aw, pw, min(32, cnt - c0), lane, ra);
     }
-    scatter_finish(aw, lane, ra);
-    float4* dst = ablocks + tix * kExt3;
-    for (int i = lane; i < kExt3; i += 32) dst[i] = aw[i];
+    scatter_store(aw, lane, ra, ablocks + tix * kExt3);
 #pragma unroll
     for (int m = 0; m < 4; ++m)
       for (int off = 16; off > 0; off >>= 1) mub[m] += __shfl_xor_sync(0xffffffffu, mub[m], off);
