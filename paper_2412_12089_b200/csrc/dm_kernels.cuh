@@ -29,7 +29,7 @@ constexpr int kTile = 4;
 constexpr int kExt = 6;  // tile + quadratic stencil reach
 constexpr int kExt3 = kExt * kExt * kExt;
 constexpr int kWarps = 4;  // warps per CTA in tile kernels
-constexpr int kPay = 25;   // payload stride (floats, odd: conflict-free writes)
+constexpr int kPay = 28;   // payload stride (floats; 7 float4, conflict-free STS.128 / 3-way LDS.128)
 constexpr int kNacc = 64;  // per-tile cotangent accumulators
 constexpr int kAccMu = 0, kAccLam = 4, kAccMuG = 8, kAccCol = 12, kAccAct = 48;
 
@@ -389,21 +389,19 @@ struct RunAcc {
   float4 acc[3];
 };
 
+// Payload (7 float4 per particle; stride 28 floats keeps both the per-lane
+// STS.128 writes and the 3-group LDS.128 reads conflict-free):
+//   0: (lbl, m, w0_0, w0_1)  1: (w0_2, w1_0, w1_1, w1_2)  2: (w2_0..2, 0)
+//   3..5: row r of (q | Ad) = (q_r, Ad_r0, Ad_r1, Ad_r2)
 __device__ __forceinline__ void stage_payload(float* __restrict__ pp, int lbl, const Stencil<float>& sc, float m,
                                               v3<float> q, const m3<float>& Ad) {
-  pp[0] = __int_as_float(lbl);
-#pragma unroll
-  for (int r = 0; r < 3; ++r) {
-    pp[1 + r] = sc.w[0][r];
-    pp[4 + r] = sc.w[1][r];
-    pp[7 + r] = sc.w[2][r];
-  }
-  pp[10] = m;
-  pp[11] = q.x;
-  pp[12] = q.y;
-  pp[13] = q.z;
-#pragma unroll
-  for (int r = 0; r < 9; ++r) pp[14 + r] = Ad.a[r];
+  float4* p4 = reinterpret_cast<float4*>(pp);
+  p4[0] = make_float4(__int_as_float(lbl), m, sc.w[0][0], sc.w[0][1]);
+  p4[1] = make_float4(sc.w[0][2], sc.w[1][0], sc.w[1][1], sc.w[1][2]);
+  p4[2] = make_float4(sc.w[2][0], sc.w[2][1], sc.w[2][2], 0.f);
+  p4[3] = make_float4(q.x, Ad.a[0], Ad.a[1], Ad.a[2]);
+  p4[4] = make_float4(q.y, Ad.a[3], Ad.a[4], Ad.a[5]);
+  p4[5] = make_float4(q.z, Ad.a[6], Ad.a[7], Ad.a[8]);
 }
 
 __device__ __forceinline__ void run_reset(RunAcc& ra) {
@@ -445,20 +443,24 @@ __device__ __forceinline__ void scatter_runs(float4* __restrict__ blk3, const fl
     const float fi = (float)i, fj = (float)j;
     for (int k = g; k < nv; k += 3) {
       const float* pk = pay + k * kPay;
-      const int lb = __float_as_int(pk[0]);
+      const float4* p4 = reinterpret_cast<const float4*>(pk);
+      const float2 lm = *reinterpret_cast<const float2*>(pk);
+      const int lb = __float_as_int(lm.x);
       if (lb != ra.cur) {
         run_flush(blk, ra, off);
         ra.cur = lb;
       }
-      const float wij = pk[1 + i] * pk[4 + j];
-      const float bx = pk[11] + pk[14] * fi + pk[15] * fj;
-      const float by = pk[12] + pk[17] * fi + pk[18] * fj;
-      const float bz = pk[13] + pk[20] * fi + pk[21] * fj;
-      const float ax = pk[16], ay = pk[19], az = pk[22];
-      const float m = HASM ? pk[10] : 0.f;
+      const float wij = pk[2 + i] * pk[5 + j];
+      const float4 w2 = p4[2], rx = p4[3], ry = p4[4], rz = p4[5];
+      const float bx = rx.x + rx.y * fi + rx.z * fj;
+      const float by = ry.x + ry.y * fi + ry.z * fj;
+      const float bz = rz.x + rz.y * fi + rz.z * fj;
+      const float ax = rx.w, ay = ry.w, az = rz.w;
+      const float m = HASM ? lm.y : 0.f;
+      const float w2k[3] = {w2.x, w2.y, w2.z};
 #pragma unroll
       for (int kk = 0; kk < 3; ++kk) {
-        const float w = wij * pk[7 + kk];
+        const float w = wij * w2k[kk];
         const float fk = (float)kk;
         if (HASM) ra.acc[kk].x += w * m;
         ra.acc[kk].y += w * (bx + ax * fk);
