@@ -266,11 +266,12 @@ void launch_p2g_adj(DmContext* c, const StateView& S, const Slot& q, int t, floa
 }
 
 // Adjoint of one substep from the replay's stored artifacts (slot qi).
-void backward_substep(DmContext* c, const StateView& S, int t, int qi, const float* adj_in, float* adj_out) {
+void backward_substep(DmContext* c, const StateView& S, const StateView& Sn, int t, int qi, const float* adj_in,
+                      float* adj_out) {
   const Slot q = slot(c, qi);
   PROF_BEGIN(c, 3);
 #define L_G2PA(LW)                                                                                            \
-  k_g2p_adj<LW><<<c->grid_tiles, kWarps * 32, kG2pAdjSmem, c->stream>>>(c->P, S, adj_in, c->Ntot, q.perm, q.tile_start, \
+  k_g2p_adj<LW><<<c->grid_tiles, kWarps * 32, kG2pAdjSmem, c->stream>>>(c->P, S, Sn, adj_in, c->Ntot, q.perm, q.tile_start, \
                                                               q.tile_count, q.active, q.gvb, c->ablocks,    \
                                                               c->part, c->tile_acc, q.nact)
   DM_LAW_DISPATCH(c, L_G2PA);
@@ -545,7 +546,8 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
     }
     for (int q = ck - 1; q >= 0; --q) {
       const int s = s0 + q;
-      backward_substep(ctx, seg_state(ctx, s0, s), t, q, ctx->adj[cur], ctx->adj[cur ^ 1]);
+      const StateView Sn = q + 1 < ck ? seg_state(ctx, s0, s + 1) : view(ctx->tail, ctx->tail_attr, ctx->Ntot);
+      backward_substep(ctx, seg_state(ctx, s0, s), Sn, t, q, ctx->adj[cur], ctx->adj[cur ^ 1]);
       cur ^= 1;
     }
   }

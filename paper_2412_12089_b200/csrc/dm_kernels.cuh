@@ -458,14 +458,17 @@ __device__ __forceinline__ void scatter_runs(float4* __restrict__ blk3, const fl
       const float ax = rx.w, ay = ry.w, az = rz.w;
       const float m = HASM ? lm.y : 0.f;
       const float w2k[3] = {w2.x, w2.y, w2.z};
+      // node (i, j, kk) value: b + kk a  (b = q + Ad_0 i + Ad_1 j, a = Ad_2)
+      const float cx[3] = {bx, bx + ax, fmaf(ax, 2.f, bx)};
+      const float cy[3] = {by, by + ay, fmaf(ay, 2.f, by)};
+      const float cz[3] = {bz, bz + az, fmaf(az, 2.f, bz)};
 #pragma unroll
       for (int kk = 0; kk < 3; ++kk) {
         const float w = wij * w2k[kk];
-        const float fk = (float)kk;
         if (HASM) ra.acc[kk].x += w * m;
-        ra.acc[kk].y += w * (bx + ax * fk);
-        ra.acc[kk].z += w * (by + ay * fk);
-        ra.acc[kk].w += w * (bz + az * fk);
+        ra.acc[kk].y += w * cx[kk];
+        ra.acc[kk].z += w * cy[kk];
+        ra.acc[kk].w += w * cz[kk];
       }
     }
   }
@@ -731,7 +734,7 @@ __global__ void __launch_bounds__(kWarps * 32, kLawBlocks(LAW)) k_g2p(DevParams 
 // end-of-substep state (sorted position); writes particle-side partial
 // cotangents (sorted position) and a 6^3 block of node-velocity cotangents.
 template <int LAW>
-__global__ void __launch_bounds__(kWarps * 32, 3) k_g2p_adj(DevParams P, StateView S, const float* __restrict__ adj_in,
+__global__ void __launch_bounds__(kWarps * 32, 3) k_g2p_adj(DevParams P, StateView S, StateView Sn, const float* __restrict__ adj_in,
                                                          size_t astride, const int* __restrict__ perm,
                                                          const int* __restrict__ tile_start,
                                                          const int* __restrict__ tile_count,
@@ -785,7 +788,12 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_g2p_adj(DevParams P, StateVi
         m3<float> Fp, Bd;
         const int mi = attr_mat(at);
         float mu_l = 0.f;
-        g2p_vjp_sep(law_of<LAW>(P, mi), T, sc, getv, F, xb, vb, Cb, Fb, xp, Fp, gq, Bd, mu_l);
+        // the replay's G2P outputs for this particle: the next state at the same sorted slot
+        const v3<float> vn = mk3(Sn.c(3, dst), Sn.c(4, dst), Sn.c(5, dst));
+        m3<float> Cn;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) Cn.a[q] = Sn.c(15 + q, dst);
+        g2p_vjp_given(law_of<LAW>(P, mi), T, sc, getv, F, vn, Cn, xb, vb, Cb, Fb, xp, Fp, gq, Bd, mu_l);
 #pragma unroll
         for (int m = 0; m < 4; ++m)
           if (m == mi) mub[m] += mu_l;

@@ -334,14 +334,27 @@ struct FxBar {
 
 // Adjoint of g2p_particle_sep (same contract as g2p_vjp).
 template <class R, class GetV>
+DM_HD void g2p_vjp_given(const Law<R>& L, const TransferCtx<R>& t, const Stencil<R>& s, GetV getv, const m3<R>& F,
+                         v3<R> vnew, const m3<R>& Cn, v3<R> xb_o, v3<R> vb_o, const m3<R>& Cb_o, const m3<R>& Fb_o,
+                         v3<R>& xb_part, m3<R>& Fb_part, v3<R>& gq, m3<R>& Bd, R& mubar);
+template <class R, class GetV>
 DM_HD void g2p_vjp_sep(const Law<R>& L, const TransferCtx<R>& t, const Stencil<R>& s, GetV getv, const m3<R>& F,
                        v3<R> xb_o, v3<R> vb_o, const m3<R>& Cb_o, const m3<R>& Fb_o, v3<R>& xb_part, m3<R>& Fb_part,
                        v3<R>& gq, m3<R>& Bd, R& mubar) {
   v3<R> vnew;
   m3<R> B;
   g2p_gather_sep(s, t.dx, getv, vnew, B);
+  const m3<R> Cn = B * (R(4) * t.inv_dx * t.inv_dx);
+  g2p_vjp_given(L, t, s, getv, F, vnew, Cn, xb_o, vb_o, Cb_o, Fb_o, xb_part, Fb_part, gq, Bd, mubar);
+}
+
+// g2p_vjp_sep with the forward's G2P outputs (v', C' = the next state's v, C,
+// bit-identical to a re-gather) supplied instead of recomputed.
+template <class R, class GetV>
+DM_HD void g2p_vjp_given(const Law<R>& L, const TransferCtx<R>& t, const Stencil<R>& s, GetV getv, const m3<R>& F,
+                         v3<R> vnew, const m3<R>& Cn, v3<R> xb_o, v3<R> vb_o, const m3<R>& Cb_o, const m3<R>& Fb_o,
+                         v3<R>& xb_part, m3<R>& Fb_part, v3<R>& gq, m3<R>& Bd, R& mubar) {
   const R c4 = R(4) * t.inv_dx * t.inv_dx;
-  const m3<R> Cn = B * c4;
   const m3<R> Ad = meye<R>() + Cn * t.dt;
   const m3<R> Fnew = Ad * F;
   const m3<R> Fnb = law_project_vjp(L, Fnew, Fb_o, mubar);
