@@ -49,7 +49,7 @@ struct DmContext {
   // forward pass uses slot 0, a segment replay fills slot q for substep s0+q
   int *perm_all = nullptr, *tstart_all = nullptr, *tcount_all = nullptr;
   int *abase_all = nullptr, *acount_all = nullptr, *nact_all = nullptr;
-  int2* active_all = nullptr;
+  int4* active_all = nullptr;
   // per active tile (by slot) 6^3 grid blocks of the replayed substeps:
   // velocity and (mass, momentum), read by the adjoint substep instead of
   // re-running bin / p2g / grid
@@ -172,7 +172,7 @@ struct Slot {
   int* perm;
   int* tile_start;
   int* tile_count;
-  int2* active;
+  int4* active;
   int* env_abase;
   int* env_acount;
   int* nact;
@@ -260,7 +260,12 @@ void forward_substep(DmContext* c, const StateView& S, const StateView& So, int 
 
 template <int LAW, int NG>
 void launch_p2g_adj(DmContext* c, const StateView& S, const Slot& q, int t, float* adj_out) {
-  k_p2g_adj<LAW, NG><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.active,
+  if (c->P.nmat == 1)
+    k_p2g_adj<LAW, NG, 1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.active,
+                                                              step_act(c, t), c->gmb, c->part, adj_out, c->Ntot,
+                                                              c->tile_acc, q.nact);
+  else
+  k_p2g_adj<LAW, NG, 4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.active,
                                                               step_act(c, t), c->gmb, c->part, adj_out, c->Ntot,
                                                               c->tile_acc, q.nact);
 }
@@ -271,9 +276,14 @@ void backward_substep(DmContext* c, const StateView& S, const StateView& Sn, int
   const Slot q = slot(c, qi);
   PROF_BEGIN(c, 3);
 #define L_G2PA(LW)                                                                                            \
-  k_g2p_adj<LW><<<c->grid_tiles, kWarps * 32, kG2pAdjSmem, c->stream>>>(c->P, S, Sn, adj_in, c->Ntot, q.perm, q.tile_start, \
-                                                              q.tile_count, q.active, q.gvb, c->ablocks,    \
-                                                              c->part, c->tile_acc, q.nact)
+  if (c->P.nmat == 1)                                                                                          \
+    k_g2p_adj<LW, 1><<<c->grid_tiles, kWarps * 32, kG2pAdjSmem, c->stream>>>(c->P, S, Sn, adj_in, c->Ntot, q.perm, \
+                                                              q.tile_start, q.tile_count, q.active, q.gvb,  \
+                                                              c->ablocks, c->part, c->tile_acc, q.nact);    \
+  else                                                                                                         \
+    k_g2p_adj<LW, 4><<<c->grid_tiles, kWarps * 32, kG2pAdjSmem, c->stream>>>(c->P, S, Sn, adj_in, c->Ntot, q.perm, \
+                                                              q.tile_start, q.tile_count, q.active, q.gvb,  \
+                                                              c->ablocks, c->part, c->tile_acc, q.nact)
   DM_LAW_DISPATCH(c, L_G2PA);
 #undef L_G2PA
   PROF_END(c, 3);
@@ -702,7 +712,8 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   {
 #define DM_SMEM_ATTR(LW)                                                                                   \
   cudaFuncSetAttribute(k_p2g<LW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kP2gSmem);            \
-  cudaFuncSetAttribute(k_g2p_adj<LW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kG2pAdjSmem)
+  cudaFuncSetAttribute(k_g2p_adj<LW, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kG2pAdjSmem); \
+  cudaFuncSetAttribute(k_g2p_adj<LW, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kG2pAdjSmem)
     DM_SMEM_ATTR(0);
     DM_SMEM_ATTR(1);
     DM_SMEM_ATTR(2);
@@ -751,7 +762,7 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<-1, 16>, kWarps * 32, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<-1, 16, 4>, kWarps * 32, 0);
   if (occ < 1) occ = 1;
   ctx->grid_tiles = dev_sms * (occ < 8 ? 8 : occ);
   if (reset_flags(ctx) != DM_OK) return ctx;

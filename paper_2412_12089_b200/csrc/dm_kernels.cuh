@@ -96,6 +96,7 @@ __device__ __forceinline__ Law<float> law_of(const DevParams& P, int mi) {
   return L;
 }
 constexpr int kLawBlocks(int law) { return (law == kFluid || law == kNeoHookean) ? 6 : 4; }
+constexpr int kG2pBlocks(int law) { return (law == kFluid || law == kNeoHookean) ? 5 : 4; }
 
 __device__ __forceinline__ TransferCtx<float> tctx(const DevParams& P) {
   TransferCtx<float> t;
@@ -185,7 +186,7 @@ __device__ __forceinline__ void store_state(const StateView& S, size_t i, v3<flo
 // scatters its chunk in index order from its own per-tile cursor, so the
 // permutation equals std::stable_sort by key.
 __global__ void __launch_bounds__(512) k_bin(DevParams P, StateView S, int* keys, int* perm, int* tile_start,
-                                             int* tile_count, int2* active, int* env_abase, int* env_acount,
+                                             int* tile_count, int4* active, int* env_abase, int* env_acount,
                                              DevFlags* flags, int* nact, int substep, int check_vmax) {
   extern __shared__ int cnt[];  // [nw][Tn]
   __shared__ int s_part[512 / 32 + 1][2];
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(512) k_bin(DevParams P, StateView S, int* keys
     tile_start[tb + t] = st;
     tile_count[tb + t] = c;
     if (c > 0) {
-      active[s_base + oa] = make_int2(e, t);
+      active[s_base + oa] = make_int4(e, t, st, c);
       ++oa;
     }
   }
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_cellsort(DevParams P, StateView
                                                           int* __restrict__ perm, int* __restrict__ keys,
                                                           const int* __restrict__ tile_start,
                                                           const int* __restrict__ tile_count,
-                                                          const int2* __restrict__ active, const int* nact,
+                                                          const int4* __restrict__ active, const int* nact,
                                                           DevFlags* flags) {
   __shared__ int c64[kWarps][64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -317,10 +318,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_cellsort(DevParams P, StateView
   const int n_active = *(const volatile int*)nact;
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicMax(&flags->max_active, n_active);
   for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
-    const int2 et = active[a];
+    const int4 et = active[a];
     const int e = et.x, t = et.y;
-    const size_t tix = (size_t)e * P.Tn + t;
-    const int start = tile_start[tix], n = tile_count[tix];
+    const int start = et.z, n = et.w;
     const size_t base = (size_t)e * P.N + start;
     cnt[lane] = 0;
     cnt[lane + 32] = 0;
@@ -389,23 +389,31 @@ struct RunAcc {
   float4 acc[3];
 };
 
-// Payload (7 float4 per particle; stride 28 floats keeps both the per-lane
-// STS.128 writes and the 3-group LDS.128 reads conflict-free):
-//   0: (lbl, m, w0_0, w0_1)  1: (w0_2, w1_0, w1_1, w1_2)  2: (w2_0..2, 0)
-//   3..5: row r of (q | Ad) = (q_r, Ad_r0, Ad_r1, Ad_r2)
+// Payload (7 float4 per particle, stride 28 floats):
+//   0: (lbl, m, wz0, wz1)  1: (wz2, w00, w01, w02)  2: (w10, w11, w12, w20)
+//   3: (w21, w22, -, -)    4..6: row r of (q | Ad) = (q_r, Ad_r0, Ad_r1, Ad_r2)
+// with w_ij = wx_i * wy_j precomputed (float index 5 + 3 i + j).
 __device__ __forceinline__ void stage_payload(float* __restrict__ pp, int lbl, const Stencil<float>& sc, float m,
                                               v3<float> q, const m3<float>& Ad) {
   float4* p4 = reinterpret_cast<float4*>(pp);
-  p4[0] = make_float4(__int_as_float(lbl), m, sc.w[0][0], sc.w[0][1]);
-  p4[1] = make_float4(sc.w[0][2], sc.w[1][0], sc.w[1][1], sc.w[1][2]);
-  p4[2] = make_float4(sc.w[2][0], sc.w[2][1], sc.w[2][2], 0.f);
-  p4[3] = make_float4(q.x, Ad.a[0], Ad.a[1], Ad.a[2]);
-  p4[4] = make_float4(q.y, Ad.a[3], Ad.a[4], Ad.a[5]);
-  p4[5] = make_float4(q.z, Ad.a[6], Ad.a[7], Ad.a[8]);
+  float w[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) w[3 * i + j] = sc.w[0][i] * sc.w[1][j];
+  p4[0] = make_float4(__int_as_float(lbl), m, sc.w[2][0], sc.w[2][1]);
+  p4[1] = make_float4(sc.w[2][2], w[0], w[1], w[2]);
+  p4[2] = make_float4(w[3], w[4], w[5], w[6]);
+  p4[3] = make_float4(w[7], w[8], 0.f, 0.f);
+  p4[4] = make_float4(q.x, Ad.a[0], Ad.a[1], Ad.a[2]);
+  p4[5] = make_float4(q.y, Ad.a[3], Ad.a[4], Ad.a[5]);
+  p4[6] = make_float4(q.z, Ad.a[6], Ad.a[7], Ad.a[8]);
 }
 
+// cur starts at node 0 of the block: the first flush then adds zeros there
+// (x + 0 == x), so the flush needs no branch.
 __device__ __forceinline__ void run_reset(RunAcc& ra) {
-  ra.cur = -1;
+  ra.cur = 0;
 #pragma unroll
   for (int k = 0; k < 3; ++k) ra.acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
@@ -413,26 +421,49 @@ __device__ __forceinline__ void run_reset(RunAcc& ra) {
 // Adds the lane's three run sums (nodes (i, j, 0..2) of the run's base) into
 // its group's block copy.
 __device__ __forceinline__ void run_flush(float4* __restrict__ blk, RunAcc& ra, int off) {
-  if (ra.cur >= 0) {
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      float4 b = blk[ra.cur + off + k];
-      b.x += ra.acc[k].x;
-      b.y += ra.acc[k].y;
-      b.z += ra.acc[k].z;
-      b.w += ra.acc[k].w;
-      blk[ra.cur + off + k] = b;
-    }
+  for (int k = 0; k < 3; ++k) {
+    float4 b = blk[ra.cur + off + k];
+    b.x += ra.acc[k].x;
+    b.y += ra.acc[k].y;
+    b.z += ra.acc[k].z;
+    b.w += ra.acc[k].w;
+    blk[ra.cur + off + k] = b;
   }
 #pragma unroll
   for (int k = 0; k < 3; ++k) ra.acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
-// Lanes 0..26 = 3 groups x 9 stencil columns (i, j); group g takes the
-// chunk's particles k = g, g+3, ... (a sorted subsequence, so same-cell runs
-// stay contiguous) and each lane accumulates the 3 nodes (i, j, 0..2) of its
-// column.  Each group flushes into its own block copy (no write races); the
-// copies are summed in fixed order by scatter_store.
+// Lanes 0..26 = 3 groups x 9 stencil columns (i, j).  A staged chunk of 32
+// cell-sorted particles is cut into three contiguous segments (kSeg each) and
+// group g walks segment g in order, so a run is a cell's particles within the
+// segment and a lane flushes about once per cell; each lane accumulates the 3
+// nodes (i, j, 0..2) of its column.  Each group flushes into its own block
+// copy (no write races); the copies are summed in fixed order by
+// scatter_store.  The next particle's payload is loaded while the current one
+// accumulates (shared-memory latency off the critical path).
+constexpr int kSeg = 11;
+
+struct PayLane {
+  int lb;
+  float m, wij, wz[3];
+  float4 r[3];
+};
+
+__device__ __forceinline__ void load_pay(const float* __restrict__ pk, int wi, PayLane& p) {
+  const float4* p4 = reinterpret_cast<const float4*>(pk);
+  const float4 h = p4[0];
+  p.lb = __float_as_int(h.x);
+  p.m = h.y;
+  p.wz[0] = h.z;
+  p.wz[1] = h.w;
+  p.wz[2] = pk[4];
+  p.wij = pk[wi];
+  p.r[0] = p4[4];
+  p.r[1] = p4[5];
+  p.r[2] = p4[6];
+}
+
 template <bool HASM>
 __device__ __forceinline__ void scatter_runs(float4* __restrict__ blk3, const float* __restrict__ pay, int nv, int lane,
                                              RunAcc& ra) {
@@ -440,35 +471,36 @@ __device__ __forceinline__ void scatter_runs(float4* __restrict__ blk3, const fl
     const int g = lane / 9, i = (lane % 9) / 3, j = lane % 3;
     float4* blk = blk3 + g * kExt3;
     const int off = (i * kExt + j) * kExt;
+    const int wi = 5 + 3 * i + j;
     const float fi = (float)i, fj = (float)j;
-    for (int k = g; k < nv; k += 3) {
-      const float* pk = pay + k * kPay;
-      const float4* p4 = reinterpret_cast<const float4*>(pk);
-      const float2 lm = *reinterpret_cast<const float2*>(pk);
-      const int lb = __float_as_int(lm.x);
-      if (lb != ra.cur) {
-        run_flush(blk, ra, off);
-        ra.cur = lb;
-      }
-      const float wij = pk[2 + i] * pk[5 + j];
-      const float4 w2 = p4[2], rx = p4[3], ry = p4[4], rz = p4[5];
-      const float bx = rx.x + rx.y * fi + rx.z * fj;
-      const float by = ry.x + ry.y * fi + ry.z * fj;
-      const float bz = rz.x + rz.y * fi + rz.z * fj;
-      const float ax = rx.w, ay = ry.w, az = rz.w;
-      const float m = HASM ? lm.y : 0.f;
-      const float w2k[3] = {w2.x, w2.y, w2.z};
-      // node (i, j, kk) value: b + kk a  (b = q + Ad_0 i + Ad_1 j, a = Ad_2)
-      const float cx[3] = {bx, bx + ax, fmaf(ax, 2.f, bx)};
-      const float cy[3] = {by, by + ay, fmaf(ay, 2.f, by)};
-      const float cz[3] = {bz, bz + az, fmaf(az, 2.f, bz)};
+    const int k0 = g * kSeg, k1 = min(nv, k0 + kSeg);
+    if (k0 < k1) {
+      PayLane cur;
+      load_pay(pay + k0 * kPay, wi, cur);
+      for (int k = k0; k < k1; ++k) {
+        PayLane nxt;
+        if (k + 1 < k1) load_pay(pay + (k + 1) * kPay, wi, nxt);
+        if (cur.lb != ra.cur) {
+          run_flush(blk, ra, off);
+          ra.cur = cur.lb;
+        }
+        // node (i, j, kk) value: b + kk a  (b = q + Ad_0 i + Ad_1 j, a = Ad_2)
+        const float bx = fmaf(cur.r[0].z, fj, fmaf(cur.r[0].y, fi, cur.r[0].x));
+        const float by = fmaf(cur.r[1].z, fj, fmaf(cur.r[1].y, fi, cur.r[1].x));
+        const float bz = fmaf(cur.r[2].z, fj, fmaf(cur.r[2].y, fi, cur.r[2].x));
+        const float ax = cur.r[0].w, ay = cur.r[1].w, az = cur.r[2].w;
+        const float cx[3] = {bx, bx + ax, fmaf(ax, 2.f, bx)};
+        const float cy[3] = {by, by + ay, fmaf(ay, 2.f, by)};
+        const float cz[3] = {bz, bz + az, fmaf(az, 2.f, bz)};
 #pragma unroll
-      for (int kk = 0; kk < 3; ++kk) {
-        const float w = wij * w2k[kk];
-        if (HASM) ra.acc[kk].x += w * m;
-        ra.acc[kk].y += w * cx[kk];
-        ra.acc[kk].z += w * cy[kk];
-        ra.acc[kk].w += w * cz[kk];
+        for (int kk = 0; kk < 3; ++kk) {
+          const float w = cur.wij * cur.wz[kk];
+          if (HASM) ra.acc[kk].x += w * cur.m;
+          ra.acc[kk].y += w * cx[kk];
+          ra.acc[kk].z += w * cy[kk];
+          ra.acc[kk].w += w * cz[kk];
+        }
+        cur = nxt;
       }
     }
   }
@@ -494,13 +526,78 @@ __device__ __forceinline__ void scatter_store(float4* __restrict__ blk3, int lan
 constexpr size_t kP2gSmem = (size_t)kWarps * (3 * kExt3 * sizeof(float4) + 32 * kPay * sizeof(float));
 constexpr size_t kG2pAdjSmem = (size_t)kWarps * (4 * kExt3 * sizeof(float4) + 32 * kPay * sizeof(float));
 
+// Persistent tile loop with the next two tiles' descriptors (env, tile,
+// start, count) loaded ahead: `nxt` is known when the current tile starts
+// (so its grid block can be prefetched), `prefetch` fetches the one after.
+struct TileIter {
+  int a, stride, n;
+  int4 cur, nxt, nxt2;
+  __device__ __forceinline__ TileIter(const int4* __restrict__ active, int a0, int stride_, int n_) {
+    a = a0;
+    stride = stride_;
+    n = n_;
+    cur = a < n ? active[a] : make_int4(0, 0, 0, 0);
+    nxt = a + stride < n ? active[a + stride] : make_int4(0, 0, 0, 0);
+    nxt2 = make_int4(0, 0, 0, 0);
+  }
+  __device__ __forceinline__ bool valid() const { return a < n; }
+  __device__ __forceinline__ bool has_next() const { return a + stride < n; }
+  __device__ __forceinline__ void prefetch(const int4* __restrict__ active) {
+    if (a + 2 * stride < n) nxt2 = active[a + 2 * stride];
+  }
+  __device__ __forceinline__ void advance() {
+    a += stride;
+    cur = nxt;
+    nxt = nxt2;
+  }
+};
+
+// cp.async (LDGSTS) 16-byte copies; src_size 0 zero-fills (out-of-grid nodes)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Starts the asynchronous load of tile d's 6^3 block of a dense grid.
+__device__ __forceinline__ void prefetch_tile_grid(const DevParams& P, const float4* __restrict__ grid, int4 d,
+                                                   float4* dst, int lane) {
+  const int t = d.y;
+  const int o[3] = {(t / (P.td[2] * P.td[1])) * kTile, ((t / P.td[2]) % P.td[1]) * kTile, (t % P.td[2]) * kTile};
+  const size_t eb = (size_t)d.x * P.dims[0] * P.dims[1] * P.dims[2];
+  for (int i = lane; i < kExt3; i += 32) {
+    const int g0 = o[0] + i / 36, g1 = o[1] + (i / 6) % 6, g2 = o[2] + i % 6;
+    const bool in = g0 < P.dims[0] && g1 < P.dims[1] && g2 < P.dims[2];
+    cp_async16(dst + i, in ? grid + eb + ((size_t)g0 * P.dims[1] + g1) * P.dims[2] + g2 : grid, in);
+  }
+}
+
+// Particle state of one chunk slot held in registers (software pipeline:
+// the next chunk's loads are issued before the current chunk's scatter).
+struct PState {
+  float x[3];
+  v3<float> v;
+  m3<float> F, C;
+  uint32_t at;
+};
+
+__device__ __forceinline__ void load_pstate(const StateView& S, int src, PState& p) {
+  load_state(S, src, p.x, p.v, p.F, p.C);
+  p.at = S.attr[src];
+}
+
 // ============================ P2G ============================
 // Per active tile: stage particle payloads (lanes = particles), scatter runs
 // into the warp's 6^3 shared block (lanes = stencil nodes), write the block.
+// The next chunk's state loads are in flight during the current scatter.
 template <int LAW>
 __global__ void __launch_bounds__(kWarps * 32, 4) k_p2g(DevParams P, StateView S, const int* __restrict__ perm,
                                                      const int* __restrict__ tile_start,
-                                                     const int* __restrict__ tile_count, const int2* __restrict__ active,
+                                                     const int* __restrict__ tile_count, const int4* __restrict__ active,
                                                      const float* __restrict__ act, float4* __restrict__ blocks,
                                                      DevFlags* flags, const int* nact, int substep) {
   extern __shared__ float4 dsm[];
@@ -509,39 +606,41 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_p2g(DevParams P, StateView S
   const TransferCtx<float> T = tctx(P);
   float4* bw = dsm + warp * 3 * kExt3;  // 3 group copies of the 6^3 block
   float* pw = reinterpret_cast<float*>(dsm + kWarps * 3 * kExt3) + warp * 32 * kPay;
-  for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
-    const int2 et = active[a];
-    const int e = et.x, t = et.y;
+  for (TileIter ti(active, blockIdx.x * kWarps + warp, gridDim.x * kWarps, n_active); ti.valid(); ti.advance()) {
+    ti.prefetch(active);
+    const int e = ti.cur.x, t = ti.cur.y, start = ti.cur.z, cnt = ti.cur.w;
     const int tz = t % P.td[2], ty = (t / P.td[2]) % P.td[1], tx = t / (P.td[2] * P.td[1]);
     const int o[3] = {tx * kTile, ty * kTile, tz * kTile};
     const size_t tix = (size_t)e * P.Tn + t;
-    const int start = tile_start[tix], cnt = tile_count[tix];
+    const int* prow = perm + (size_t)e * P.N + start;
+    bool ok = lane < cnt;
+    PState ps;
+    if (ok) load_pstate(S, prow[lane], ps);
+    int src_n = 32 + lane < cnt ? prow[32 + lane] : 0;
     scatter_zero(bw, lane);
     RunAcc ra;
     run_reset(ra);
     for (int c0 = 0; c0 < cnt; c0 += 32) {
-      if (c0 + lane < cnt) {
-        const int src = perm[(size_t)e * P.N + start + c0 + lane];
-        float x[3];
-        v3<float> v;
-        m3<float> F, C;
-        load_state(S, src, x, v, F, C);
-        const uint32_t at = S.attr[src];
+      if (ok) {
         Stencil<float> sc;
-        make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
-        const Law<float> L = law_of<LAW>(P, attr_mat(at));
-        const float av = act ? act[e * P.G + min(attr_group(at), P.G - 1)] : 0.f;
+        make_stencil(ps.x, P.inv_dx, (double)P.dx, P.dims, sc);
+        const Law<float> L = law_of<LAW>(P, attr_mat(ps.at));
+        const float av = act ? act[e * P.G + min(attr_group(ps.at), P.G - 1)] : 0.f;
         bool bad = false;
-        const m3<float> A = p2g_affine(L, T, F, C, av, &bad);
-        if (bad) report(flags, e, substep, 0, attr_index(at), attr_mat(at), kErrDetF);
+        const m3<float> A = p2g_affine(L, T, ps.F, ps.C, av, &bad);
+        if (bad) report(flags, e, substep, 0, attr_index(ps.at), attr_mat(ps.at), kErrDetF);
         v3<float> q;
         m3<float> Ad;
-        p2g_payload(A, L.mass, v, sc, P.dx, q, Ad);
+        p2g_payload(A, L.mass, ps.v, sc, P.dx, q, Ad);
         const int lbl = (tile_local(sc.base[0], o[0]) * kExt + tile_local(sc.base[1], o[1])) * kExt +
                         tile_local(sc.base[2], o[2]);
         stage_payload(pw + lane * kPay, lbl, sc, L.mass, q, Ad);
       }
       __syncwarp();
+      // software pipeline: issue the next chunk's loads before this chunk's scatter
+      ok = c0 + 32 + lane < cnt;
+      if (ok) load_pstate(S, src_n, ps);
+      src_n = c0 + 64 + lane < cnt ? prow[c0 + 64 + lane] : 0;
       scatter_runs<true>(bw, pw, min(32, cnt - c0), lane, ra);
     }
     scatter_store(bw, lane, ra, blocks + tix * kExt3);
@@ -635,7 +734,7 @@ __device__ __forceinline__ size_t node_lin(const DevParams& P, int e, const int 
 // dense per-env grid.
 template <int MAXC>
 __global__ void __launch_bounds__(kWarps * 32) k_grid(DevParams P, const int* __restrict__ tile_count,
-                                                      const int2* __restrict__ active, const float* __restrict__ cvo,
+                                                      const int4* __restrict__ active, const float* __restrict__ cvo,
                                                       const float4* __restrict__ blocks, float4* __restrict__ gmp,
                                                       float4* __restrict__ gv, const int* nact) {
   __shared__ short own[kWarps][kExt3];
@@ -643,7 +742,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_grid(DevParams P, const int* __
   const int n_active = *(const volatile int*)nact;
   const NodeCtx<float> G = nctx(P);
   for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
-    const int2 et = active[a];
+    const int4 et = active[a];
     const int e = et.x, t = et.y;
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const unsigned nbr = neighbour_mask(P, tile_count, e, tc, lane);
@@ -674,71 +773,101 @@ __device__ __forceinline__ void load_tile_grid(const DevParams& P, const float4*
 }
 
 // ============================ G2P ============================
+// Tile grids are double-buffered in shared memory with cp.async (the next
+// tile's 6^3 velocity block streams in while the current tile computes) and
+// the next chunk's particle loads are issued before the current chunk's math.
 template <int LAW>
-__global__ void __launch_bounds__(kWarps * 32, kLawBlocks(LAW)) k_g2p(DevParams P, StateView S, StateView Sout,
+__global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams P, StateView S, StateView Sout,
                                                      const int* __restrict__ perm, const int* __restrict__ tile_start,
-                                                     const int* __restrict__ tile_count, const int2* __restrict__ active,
+                                                     const int* __restrict__ tile_count, const int4* __restrict__ active,
                                                      const float4* __restrict__ gv, DevFlags* flags, const int* nact,
                                                      int substep, const float4* __restrict__ gmp,
                                                      float4* __restrict__ out_gv, float4* __restrict__ out_gmp) {
-  __shared__ float4 vg[kWarps][kExt3];
+  __shared__ __align__(16) float4 vg[kWarps][2][kExt3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_active = *(const volatile int*)nact;
   const TransferCtx<float> T = tctx(P);
-  float4* vw = vg[warp];
-  for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
-    const int2 et = active[a];
-    const int e = et.x, t = et.y;
+  TileIter ti(active, blockIdx.x * kWarps + warp, gridDim.x * kWarps, n_active);
+  if (ti.valid()) prefetch_tile_grid(P, gv, ti.cur, vg[warp][0], lane);
+  cp_async_commit();
+  for (int buf = 0; ti.valid(); ti.advance(), buf ^= 1) {
+    if (ti.has_next()) prefetch_tile_grid(P, gv, ti.nxt, vg[warp][buf ^ 1], lane);
+    cp_async_commit();
+    ti.prefetch(active);
+    const int a = ti.a;
+    const int e = ti.cur.x, t = ti.cur.y, start = ti.cur.z, cnt = ti.cur.w;
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
-    load_tile_grid(P, gv, e, o, vw, lane);
+    const size_t row = (size_t)e * P.N + start;
+    bool ok = lane < cnt;
+    float x[3];
+    m3<float> F;
+    uint32_t at = 0;
+    if (ok) {
+      const int src = perm[row + lane];
+      load_xF(S, src, x, F);
+      at = S.attr[src];
+    }
+    int src_n = lane + 32 < cnt ? perm[row + lane + 32] : 0;
+    cp_async_wait<1>();  // this tile's grid has landed
     __syncwarp();
+    float4* vw = vg[warp][buf];
     if (out_gv) {  // segment replay: keep the tile's grid for the adjoint substep
       for (int i = lane; i < kExt3; i += 32) out_gv[(size_t)a * kExt3 + i] = vw[i];
       load_tile_grid(P, gmp, e, o, out_gmp + (size_t)a * kExt3, lane);
     }
-    const size_t tix = (size_t)e * P.Tn + t;
-    const int start = tile_start[tix], cnt = tile_count[tix];
-    const size_t row = (size_t)e * P.N + start;
-    int src_next = lane < cnt ? perm[row + lane] : 0;  // index prefetch: one chunk ahead
-    for (int c0 = lane; c0 < cnt; c0 += 32) {
-      const size_t dst = row + c0;
-      const int src = src_next;
-      if (c0 + 32 < cnt) src_next = perm[dst + 32];
-      float x[3];
-      v3<float> v;
-      m3<float> F, C;
-      load_xF(S, src, x, F);
-      const uint32_t at = S.attr[src];
-      Stencil<float> sc;
-      make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
-      const int lb[3] = {tile_local(sc.base[0], o[0]), tile_local(sc.base[1], o[1]), tile_local(sc.base[2], o[2])};
-      auto getv = [&](int i, int j, int k) {
-        const float4 q = vw[((lb[0] + i) * kExt + (lb[1] + j)) * kExt + lb[2] + k];
-        return mk3(q.x, q.y, q.z);
-      };
-      v3<float> xn = mk3(x[0], x[1], x[2]);
-      bool bad_adv = false, bad_det = false;
-      g2p_particle_sep(law_of<LAW>(P, attr_mat(at)), T, sc, getv, xn, v, C, F, &bad_adv, &bad_det);
-      if (bad_adv) report(flags, e, substep, 1, attr_index(at), 0, kErrG2PInterior);
-      if (bad_det) report(flags, e, substep, 1, attr_index(at), attr_mat(at), kErrDetF);
-      store_state(Sout, dst, xn, v, F, C);
-      Sout.attr[dst] = at;
+    for (int c0 = 0; c0 < cnt; c0 += 32) {
+      // next chunk's loads in flight during this chunk's math
+      const bool ok_n = c0 + 32 + lane < cnt;
+      float xn_[3];
+      m3<float> Fn_;
+      uint32_t at_n = 0;
+      if (ok_n) {
+        load_xF(S, src_n, xn_, Fn_);
+        at_n = S.attr[src_n];
+      }
+      src_n = c0 + 64 + lane < cnt ? perm[row + c0 + 64 + lane] : 0;
+      if (ok) {
+        const size_t dst = row + c0 + lane;
+        Stencil<float> sc;
+        make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
+        const int lb[3] = {tile_local(sc.base[0], o[0]), tile_local(sc.base[1], o[1]), tile_local(sc.base[2], o[2])};
+        auto getv = [&](int i, int j, int k) {
+          const float4 q = vw[((lb[0] + i) * kExt + (lb[1] + j)) * kExt + lb[2] + k];
+          return mk3(q.x, q.y, q.z);
+        };
+        v3<float> xn = mk3(x[0], x[1], x[2]), v;
+        m3<float> C;
+        bool bad_adv = false, bad_det = false;
+        g2p_particle_sep(law_of<LAW>(P, attr_mat(at)), T, sc, getv, xn, v, C, F, &bad_adv, &bad_det);
+        if (bad_adv) report(flags, e, substep, 1, attr_index(at), 0, kErrG2PInterior);
+        if (bad_det) report(flags, e, substep, 1, attr_index(at), attr_mat(at), kErrDetF);
+        store_state(Sout, dst, xn, v, F, C);
+        Sout.attr[dst] = at;
+      }
+      ok = ok_n;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) x[q] = xn_[q];
+      F = Fn_;
+      at = at_n;
     }
-    __syncwarp();
+    __syncwarp();  // every lane is done with vw before it is refilled
   }
+  cp_async_wait<0>();
 }
 
 // ============================ G2P adjoint ============================
 // Reads the start-of-substep state (via perm) and the cotangent of the
 // end-of-substep state (sorted position); writes particle-side partial
 // cotangents (sorted position) and a 6^3 block of node-velocity cotangents.
-template <int LAW>
+// The next chunk's gathered (x, F) loads are in flight during the current
+// chunk's scatter.
+template <int LAW, int NM>
 __global__ void __launch_bounds__(kWarps * 32, 3) k_g2p_adj(DevParams P, StateView S, StateView Sn, const float* __restrict__ adj_in,
                                                          size_t astride, const int* __restrict__ perm,
                                                          const int* __restrict__ tile_start,
                                                          const int* __restrict__ tile_count,
-                                                         const int2* __restrict__ active, const float4* __restrict__ gvb,
+                                                         const int4* __restrict__ active, const float4* __restrict__ gvb,
                                                          float4* __restrict__ ablocks, float* __restrict__ part,
                                                          float* __restrict__ tile_acc, const int* nact) {
   extern __shared__ float4 dsm[];
@@ -748,27 +877,38 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_g2p_adj(DevParams P, StateVi
   float4* aw = vw + kExt3;              // 3 group copies of the cotangent block
   float* pw = reinterpret_cast<float*>(dsm + kWarps * 4 * kExt3) + warp * 32 * kPay;
   const int n_active = *(const volatile int*)nact;
-  for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
-    const int2 et = active[a];
-    const int e = et.x, t = et.y;
+  for (TileIter ti(active, blockIdx.x * kWarps + warp, gridDim.x * kWarps, n_active); ti.valid(); ti.advance()) {
+    ti.prefetch(active);
+    const int a = ti.a;
+    const int e = ti.cur.x, t = ti.cur.y, start = ti.cur.z, cnt = ti.cur.w;
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
-    for (int i = lane; i < kExt3; i += 32) vw[i] = gvb[(size_t)a * kExt3 + i];  // the replayed substep's grid, by slot
-    scatter_zero(aw, lane);
-    __syncwarp();
+    // the replayed substep's grid, by slot (asynchronous; overlaps the first loads)
+    for (int i = lane; i < kExt3; i += 32) cp_async16(vw + i, gvb + (size_t)a * kExt3 + i, true);
+    cp_async_commit();
     const size_t tix = (size_t)e * P.Tn + t;
-    const int start = tile_start[tix], cnt = tile_count[tix];
-    double mub[4] = {0.0, 0.0, 0.0, 0.0};  // fp64: cancelling per-particle sums
+    const size_t row = (size_t)e * P.N + start;
+    bool ok = lane < cnt;
+    float x[3];
+    m3<float> F;
+    uint32_t at = 0;
+    if (ok) {
+      const int src = perm[row + lane];
+      load_xF(S, src, x, F);
+      at = S.attr[src];
+    }
+    int src_n = 32 + lane < cnt ? perm[row + 32 + lane] : 0;
+    scatter_zero(aw, lane);
+    double mub[NM];  // fp64: cancelling per-particle sums (NM = materials)
+#pragma unroll
+    for (int m = 0; m < NM; ++m) mub[m] = 0.0;
     RunAcc ra;
     run_reset(ra);
+    cp_async_wait<0>();
+    __syncwarp();
     for (int c0 = 0; c0 < cnt; c0 += 32) {
-      if (c0 + lane < cnt) {
-        const size_t dst = (size_t)e * P.N + start + c0 + lane;
-        const int src = perm[dst];
-        float x[3];
-        m3<float> F;
-        load_xF(S, src, x, F);
-        const uint32_t at = S.attr[src];
+      if (ok) {
+        const size_t dst = row + c0 + lane;
         Stencil<float> sc;
         make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
         const int lb[3] = {tile_local(sc.base[0], o[0]), tile_local(sc.base[1], o[1]), tile_local(sc.base[2], o[2])};
@@ -795,7 +935,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_g2p_adj(DevParams P, StateVi
         for (int q = 0; q < 9; ++q) Cn.a[q] = Sn.c(15 + q, dst);
         g2p_vjp_given(law_of<LAW>(P, mi), T, sc, getv, F, vn, Cn, xb, vb, Cb, Fb, xp, Fp, gq, Bd, mu_l);
 #pragma unroll
-        for (int m = 0; m < 4; ++m)
+        for (int m = 0; m < NM; ++m)
           if (m == mi) mub[m] += mu_l;
         part[0 * astride + dst] = xp.x;
         part[1 * astride + dst] = xp.y;
@@ -805,15 +945,21 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_g2p_adj(DevParams P, StateVi
         stage_payload(pw + lane * kPay, (lb[0] * kExt + lb[1]) * kExt + lb[2], sc, 0.f, gq, Bd);
       }
       __syncwarp();
+      ok = c0 + 32 + lane < cnt;
+      if (ok) {
+        load_xF(S, src_n, x, F);
+        at = S.attr[src_n];
+      }
+      src_n = c0 + 64 + lane < cnt ? perm[row + c0 + 64 + lane] : 0;
       scatter_runs<false>(aw, pw, min(32, cnt - c0), lane, ra);
     }
     scatter_store(aw, lane, ra, ablocks + tix * kExt3);
 #pragma unroll
-    for (int m = 0; m < 4; ++m)
+    for (int m = 0; m < NM; ++m)
       for (int off = 16; off > 0; off >>= 1) mub[m] += __shfl_xor_sync(0xffffffffu, mub[m], off);
     if (lane == 0)
 #pragma unroll
-      for (int m = 0; m < 4; ++m) tile_acc[tix * kNacc + kAccMuG + m] = (float)mub[m];
+      for (int m = 0; m < NM; ++m) tile_acc[tix * kNacc + kAccMuG + m] = (float)mub[m];
     __syncwarp();
   }
 }
@@ -824,7 +970,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_g2p_adj(DevParams P, StateVi
 // reduced per tile (each node counted once, by its owner).
 template <int MAXC>
 __global__ void __launch_bounds__(kWarps * 32) k_grid_adj(DevParams P, const int* __restrict__ tile_count,
-                                                          const int2* __restrict__ active, const float* __restrict__ cvo,
+                                                          const int4* __restrict__ active, const float* __restrict__ cvo,
                                                           const float4* __restrict__ ablocks,
                                                           const float4* __restrict__ gmpb, float4* __restrict__ gmb,
                                                           float* __restrict__ tile_acc, const int* nact) {
@@ -833,7 +979,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_grid_adj(DevParams P, const int
   const int n_active = *(const volatile int*)nact;
   const NodeCtx<float> G = nctx(P);
   for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
-    const int2 et = active[a];
+    const int4 et = active[a];
     const int e = et.x, t = et.y;
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const unsigned nbr = neighbour_mask(P, tile_count, e, tc, lane);
@@ -870,34 +1016,44 @@ __global__ void __launch_bounds__(kWarps * 32) k_grid_adj(DevParams P, const int
 }
 
 // ============================ P2G adjoint ============================
-template <int LAW, int NG>
-__global__ void __launch_bounds__(kWarps * 32, 4) k_p2g_adj(DevParams P, StateView S, const int* __restrict__ perm,
+#ifndef DM_P2GADJ_MINB
+#define DM_P2GADJ_MINB 4
+#endif
+template <int LAW, int NG, int NM>
+__global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevParams P, StateView S, const int* __restrict__ perm,
                                                          const int* __restrict__ tile_start,
                                                          const int* __restrict__ tile_count,
-                                                         const int2* __restrict__ active, const float* __restrict__ act,
+                                                         const int4* __restrict__ active, const float* __restrict__ act,
                                                          const float4* __restrict__ gmb, const float* __restrict__ part,
                                                          float* __restrict__ adj_out, size_t astride,
                                                          float* __restrict__ tile_acc, const int* nact) {
-  __shared__ float4 mb[kWarps][kExt3];
+  __shared__ __align__(16) float4 mb[kWarps][2][kExt3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TransferCtx<float> T = tctx(P);
-  float4* bw = mb[warp];
   const int n_active = *(const volatile int*)nact;
-  for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
-    const int2 et = active[a];
-    const int e = et.x, t = et.y;
+  TileIter ti(active, blockIdx.x * kWarps + warp, gridDim.x * kWarps, n_active);
+  if (ti.valid()) prefetch_tile_grid(P, gmb, ti.cur, mb[warp][0], lane);
+  cp_async_commit();
+  for (int buf = 0; ti.valid(); ti.advance(), buf ^= 1) {
+    __syncwarp();  // every lane is done with the buffer about to be refilled
+    if (ti.has_next()) prefetch_tile_grid(P, gmb, ti.nxt, mb[warp][buf ^ 1], lane);
+    cp_async_commit();
+    ti.prefetch(active);
+    const int e = ti.cur.x, t = ti.cur.y, start = ti.cur.z, cnt = ti.cur.w;
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
-    load_tile_grid(P, gmb, e, o, bw, lane);
-    __syncwarp();
+    float4* bw = mb[warp][buf];
     const size_t tix = (size_t)e * P.Tn + t;
-    const int start = tile_start[tix], cnt = tile_count[tix];
-    double mub[4] = {0.0, 0.0, 0.0, 0.0}, lab[4] = {0.0, 0.0, 0.0, 0.0};  // fp64: cancelling sums
+    double mub[NM], lab[NM];  // fp64: cancelling sums (NM = materials)
+#pragma unroll
+    for (int m = 0; m < NM; ++m) mub[m] = lab[m] = 0.0;
     float actb[NG];
 #pragma unroll
     for (int q = 0; q < NG; ++q) actb[q] = 0.f;
     const size_t row = (size_t)e * P.N + start;
     int src_next = lane < cnt ? perm[row + lane] : 0;  // index prefetch: one chunk ahead
+    cp_async_wait<1>();  // this tile's grid has landed
+    __syncwarp();
     for (int c0 = lane; c0 < cnt; c0 += 32) {
       const size_t j = row + c0;
       const int src = src_next;
@@ -925,7 +1081,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_p2g_adj(DevParams P, StateVi
       float mu_l = 0.f, la_l = 0.f, ac_l = 0.f;
       p2g_vjp_sep(law_of<LAW>(P, mi), T, sc, getmb, v, F, C, av, xb, vb, Fb, Cb, mu_l, la_l, ac_l);
 #pragma unroll
-      for (int m = 0; m < 4; ++m)
+      for (int m = 0; m < NM; ++m)
         if (m == mi) {
           mub[m] += mu_l;
           lab[m] += la_l;
@@ -946,7 +1102,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_p2g_adj(DevParams P, StateVi
       }
     }
 #pragma unroll
-    for (int m = 0; m < 4; ++m)
+    for (int m = 0; m < NM; ++m)
       for (int off = 16; off > 0; off >>= 1) {
         mub[m] += __shfl_xor_sync(0xffffffffu, mub[m], off);
         lab[m] += __shfl_xor_sync(0xffffffffu, lab[m], off);
@@ -957,7 +1113,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_p2g_adj(DevParams P, StateVi
     if (lane == 0) {
       float* ta = tile_acc + tix * kNacc;
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
+      for (int m = 0; m < NM; ++m) {
         ta[kAccMu + m] = (float)mub[m];
         ta[kAccLam + m] = (float)lab[m];
       }
@@ -966,11 +1122,12 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_p2g_adj(DevParams P, StateVi
     }
     __syncwarp();
   }
+  cp_async_wait<0>();
 }
 
 // Per env: sum the env's tile accumulators in tile order into the step's
 // (double) parameter cotangents.
-__global__ void k_env_reduce(DevParams P, const int2* __restrict__ active, const int* __restrict__ env_abase,
+__global__ void k_env_reduce(DevParams P, const int4* __restrict__ active, const int* __restrict__ env_abase,
                              const int* __restrict__ env_acount, const float* __restrict__ tile_acc,
                              double* __restrict__ gcvo_t, double* __restrict__ gact_t, double* __restrict__ gmu,
                              double* __restrict__ glam) {
@@ -979,7 +1136,7 @@ __global__ void k_env_reduce(DevParams P, const int2* __restrict__ active, const
   const int b = env_abase[e], n = env_acount[e];
   double s = 0.0;
   for (int i = 0; i < n; ++i) {
-    const int2 et = active[b + i];
+    const int4 et = active[b + i];
     s += tile_acc[((size_t)et.x * P.Tn + et.y) * kNacc + f];
   }
   if (f < 4) {
