@@ -225,14 +225,29 @@ void launch_p2g(DmContext* c, const StateView& S, const Slot& q, int t, int sub)
   ++c->launches;
 }
 
+// Grid kernels: one collider -> its kind fixed at compile time (CK), else the
+// runtime switch over up to 4 colliders.
+#define DM_GRID_DISPATCH(c, LAUNCH)                       \
+  if (maxc_of((c)->P.K) == 1) {                           \
+    switch ((c)->P.K == 1 ? (c)->P.shape[0].kind : -1) {  \
+      case kPlane: LAUNCH(1, kPlane); break;              \
+      case kSphere: LAUNCH(1, kSphere); break;            \
+      case kBox: LAUNCH(1, kBox); break;                  \
+      case kCylinder: LAUNCH(1, kCylinder); break;        \
+      case kHollowBox: LAUNCH(1, kHollowBox); break;      \
+      default: LAUNCH(1, -1); break;                      \
+    }                                                     \
+  } else {                                                \
+    LAUNCH(4, -1);                                        \
+  }
+
 void launch_grid(DmContext* c, const Slot& q, int t) {
   PROF_BEGIN(c, 9);
-  if (maxc_of(c->P.K) == 1)
-    k_grid<1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.active, step_cvo(c, t), c->blocks,
-                                                            c->gmp, c->gv, q.nact);
-  else
-    k_grid<4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.active, step_cvo(c, t), c->blocks,
-                                                            c->gmp, c->gv, q.nact);
+#define L_GRID(MC, CK)                                                                                        \
+  k_grid<MC, CK><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.active, step_cvo(c, t), \
+                                                               c->blocks, c->gmp, c->gv, q.nact)
+  DM_GRID_DISPATCH(c, L_GRID);
+#undef L_GRID
   PROF_END(c, 9);
   ++c->launches;
 }
@@ -289,12 +304,12 @@ void backward_substep(DmContext* c, const StateView& S, const StateView& Sn, int
   PROF_END(c, 3);
   ++c->launches;
   PROF_BEGIN(c, 10);
-  if (maxc_of(c->P.K) == 1)
-    k_grid_adj<1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.active, step_cvo(c, t),
-                                                                c->ablocks, q.gmpb, c->gmb, c->tile_acc, q.nact);
-  else
-    k_grid_adj<4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.active, step_cvo(c, t),
-                                                                c->ablocks, q.gmpb, c->gmb, c->tile_acc, q.nact);
+#define L_GRIDA(MC, CK)                                                                                   \
+  k_grid_adj<MC, CK><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.active,        \
+                                                                   step_cvo(c, t), c->ablocks, q.gmpb,   \
+                                                                   c->gmb, c->tile_acc, q.nact)
+  DM_GRID_DISPATCH(c, L_GRIDA);
+#undef L_GRIDA
   PROF_END(c, 10);
   ++c->launches;
   const int G = c->P.G;

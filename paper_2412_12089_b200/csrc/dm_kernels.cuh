@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(512) k_bin(DevParams P, StateView S, int* keys
         for (int a = 0; a < 3; ++a) b[a] = b[a] < 1 ? 1 : (b[a] > P.dims[a] - 4 ? P.dims[a] - 4 : b[a]);
       }
       key = ((b[0] >> 2) * P.td[1] + (b[1] >> 2)) * P.td[2] + (b[2] >> 2);
-      keys[i] = key;
+      keys[i] = key * 64 + ((b[0] & 3) * 4 + (b[1] & 3)) * 4 + (b[2] & 3);  // full key: tile * 64 + cell
       if (check_vmax) vmax = fmaxf(vmax, fmaxf(fabsf(S.c(3, i)), fmaxf(fabsf(S.c(4, i)), fabsf(S.c(5, i)))));
     }
     const unsigned peers = __match_any_sync(0xffffffffu, key);
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(512) k_bin(DevParams P, StateView S, int* keys
   __syncthreads();
   for (int c0 = p0; c0 < p1; c0 += 32) {
     const int p = c0 + lane;
-    const int key = p < p1 ? keys[base + p] : -1 - lane;
+    const int key = p < p1 ? keys[base + p] >> 6 : -1 - lane;
     const unsigned peers = __match_any_sync(0xffffffffu, key);
     const int leader = __ffs(peers) - 1;
     const int rank = __popc(peers & ((1u << lane) - 1u));
@@ -319,22 +319,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_cellsort(DevParams P, StateView
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicMax(&flags->max_active, n_active);
   for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
     const int4 et = active[a];
-    const int e = et.x, t = et.y;
+    const int e = et.x;
     const int start = et.z, n = et.w;
     const size_t base = (size_t)e * P.N + start;
     cnt[lane] = 0;
     cnt[lane + 32] = 0;
     __syncwarp();
-    auto cell_of = [&](int src) {
-      float x[3] = {S.c(0, src), S.c(1, src), S.c(2, src)};
-      int b[3];
-      float fx[3];
-      if (stencil_base(x, P.inv_dx, (double)P.dx, P.dims, b, fx) >= 0) {
-#pragma unroll
-        for (int d = 0; d < 3; ++d) b[d] = b[d] < 1 ? 1 : (b[d] > P.dims[d] - 4 ? P.dims[d] - 4 : b[d]);
-      }
-      return ((b[0] & 3) * 4 + (b[1] & 3)) * 4 + (b[2] & 3);
-    };
+    auto cell_of = [&](int src) { return keys[src] & 63; };  // k_bin stored the full key
     for (int c0 = 0; c0 < n; c0 += 32) {
       const bool ok = c0 + lane < n;
       const int cell = ok ? cell_of(ptile[base + c0 + lane]) : 64 + lane;
@@ -367,10 +358,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_cellsort(DevParams P, StateView
         cnt[cell] = pos + __popc(peers);
       }
       pos = __shfl_sync(0xffffffffu, pos, leader);
-      if (ok) {
-        perm[base + pos + rank] = src;
-        keys[src] = t * 64 + cell;
-      }
+      if (ok) perm[base + pos + rank] = src;
       __syncwarp();
     }
   }
@@ -464,6 +452,33 @@ __device__ __forceinline__ void load_pay(const float* __restrict__ pk, int wi, P
   p.r[2] = p4[6];
 }
 
+// One particle's contribution to the lane's column run.
+template <bool HASM>
+__device__ __forceinline__ void run_add(float4* __restrict__ blk, RunAcc& ra, int off, float fi, float fj,
+                                        const PayLane& p) {
+  if (p.lb != ra.cur) {
+    run_flush(blk, ra, off);
+    ra.cur = p.lb;
+  }
+  // node (i, j, kk) value: b + kk a  (b = q + Ad_0 i + Ad_1 j, a = Ad_2)
+  const float bx = fmaf(p.r[0].z, fj, fmaf(p.r[0].y, fi, p.r[0].x));
+  const float by = fmaf(p.r[1].z, fj, fmaf(p.r[1].y, fi, p.r[1].x));
+  const float bz = fmaf(p.r[2].z, fj, fmaf(p.r[2].y, fi, p.r[2].x));
+  const float ax = p.r[0].w, ay = p.r[1].w, az = p.r[2].w;
+  const float cx[3] = {bx, bx + ax, fmaf(ax, 2.f, bx)};
+  const float cy[3] = {by, by + ay, fmaf(ay, 2.f, by)};
+  const float cz[3] = {bz, bz + az, fmaf(az, 2.f, bz)};
+#pragma unroll
+  for (int kk = 0; kk < 3; ++kk) {
+    const float w = p.wij * p.wz[kk];
+    if (HASM) ra.acc[kk].x += w * p.m;
+    ra.acc[kk].y += w * cx[kk];
+    ra.acc[kk].z += w * cy[kk];
+    ra.acc[kk].w += w * cz[kk];
+  }
+}
+
+// Two payload register sets alternate (no register moves between particles).
 template <bool HASM>
 __device__ __forceinline__ void scatter_runs(float4* __restrict__ blk3, const float* __restrict__ pay, int nv, int lane,
                                              RunAcc& ra) {
@@ -475,33 +490,16 @@ __device__ __forceinline__ void scatter_runs(float4* __restrict__ blk3, const fl
     const float fi = (float)i, fj = (float)j;
     const int k0 = g * kSeg, k1 = min(nv, k0 + kSeg);
     if (k0 < k1) {
-      PayLane cur;
-      load_pay(pay + k0 * kPay, wi, cur);
-      for (int k = k0; k < k1; ++k) {
-        PayLane nxt;
-        if (k + 1 < k1) load_pay(pay + (k + 1) * kPay, wi, nxt);
-        if (cur.lb != ra.cur) {
-          run_flush(blk, ra, off);
-          ra.cur = cur.lb;
-        }
-        // node (i, j, kk) value: b + kk a  (b = q + Ad_0 i + Ad_1 j, a = Ad_2)
-        const float bx = fmaf(cur.r[0].z, fj, fmaf(cur.r[0].y, fi, cur.r[0].x));
-        const float by = fmaf(cur.r[1].z, fj, fmaf(cur.r[1].y, fi, cur.r[1].x));
-        const float bz = fmaf(cur.r[2].z, fj, fmaf(cur.r[2].y, fi, cur.r[2].x));
-        const float ax = cur.r[0].w, ay = cur.r[1].w, az = cur.r[2].w;
-        const float cx[3] = {bx, bx + ax, fmaf(ax, 2.f, bx)};
-        const float cy[3] = {by, by + ay, fmaf(ay, 2.f, by)};
-        const float cz[3] = {bz, bz + az, fmaf(az, 2.f, bz)};
-#pragma unroll
-        for (int kk = 0; kk < 3; ++kk) {
-          const float w = cur.wij * cur.wz[kk];
-          if (HASM) ra.acc[kk].x += w * cur.m;
-          ra.acc[kk].y += w * cx[kk];
-          ra.acc[kk].z += w * cy[kk];
-          ra.acc[kk].w += w * cz[kk];
-        }
-        cur = nxt;
+      PayLane pa, pb;
+      load_pay(pay + k0 * kPay, wi, pa);
+      int k = k0;
+      for (; k + 1 < k1; k += 2) {
+        load_pay(pay + (k + 1) * kPay, wi, pb);
+        run_add<HASM>(blk, ra, off, fi, fj, pa);
+        if (k + 2 < k1) load_pay(pay + (k + 2) * kPay, wi, pa);
+        run_add<HASM>(blk, ra, off, fi, fj, pb);
       }
+      if (k < k1) run_add<HASM>(blk, ra, off, fi, fj, pa);
     }
   }
   __syncwarp();
@@ -670,30 +668,48 @@ __device__ __forceinline__ void cand_range(int a, int& lo, int& hi) {
   hi = a >= 4 ? 1 : 0;
 }
 
-__device__ __forceinline__ bool owns_node(unsigned nbr, const int l[3]) {
-  int lo[3], hi[3];
+// Per local node i of the 6^3 block: `cand` = neighbourhood bits of the tiles
+// whose extended block covers it (<= 8, self included), `prior` = the subset
+// ordered before self.  Ascending bit order = ascending tile order, so
+// iterating the set bits of nbr & cand sums the covering blocks in the fixed
+// order, and a tile owns node i iff nbr & prior == 0.  Built once per CTA.
+struct NodeMasks {
+  unsigned cand[kExt3], prior[kExt3];
+};
+
+__device__ __forceinline__ void build_node_masks(NodeMasks& m) {
+  for (int i = threadIdx.x; i < kExt3; i += blockDim.x) {
+    const int l[3] = {i / 36, (i / 6) % 6, i % 6};
+    int lo[3], hi[3];
 #pragma unroll
-  for (int d = 0; d < 3; ++d) cand_range(l[d], lo[d], hi[d]);
-  for (int rx = lo[0]; rx <= hi[0]; ++rx)
-    for (int ry = lo[1]; ry <= hi[1]; ++ry)
-      for (int rz = lo[2]; rz <= hi[2]; ++rz) {
-        if (rx == 0 && ry == 0 && rz == 0) return true;  // reached self first
-        if (nbr & (1u << ((rx + 1) * 9 + (ry + 1) * 3 + (rz + 1)))) return false;
-      }
-  return true;
+    for (int d = 0; d < 3; ++d) cand_range(l[d], lo[d], hi[d]);
+    unsigned c = 0u, pr = 0u;
+    bool before = true;
+    for (int rx = lo[0]; rx <= hi[0]; ++rx)
+      for (int ry = lo[1]; ry <= hi[1]; ++ry)
+        for (int rz = lo[2]; rz <= hi[2]; ++rz) {
+          const unsigned bit = 1u << ((rx + 1) * 9 + (ry + 1) * 3 + (rz + 1));
+          if (rx == 0 && ry == 0 && rz == 0) before = false;
+          c |= bit;
+          if (before) pr |= bit;
+        }
+    m.cand[i] = c;
+    m.prior[i] = pr & ~(1u << 13);
+  }
+  __syncthreads();
 }
 
 // Compacted list (ascending) of the tile's owned, in-grid nodes; returns count.
-__device__ __forceinline__ int owned_nodes(const DevParams& P, unsigned nbr, const int tc[3], short* list, int lane) {
+__device__ __forceinline__ int owned_nodes(const DevParams& P, const NodeMasks& nm, unsigned nbr, const int tc[3],
+                                           short* list, int lane) {
   __syncwarp();  // previous tile's readers are done with the list
   int n = 0;
   for (int i0 = 0; i0 < kExt3; i0 += 32) {
     const int i = i0 + lane;
     bool ok = false;
     if (i < kExt3) {
-      const int l[3] = {i / 36, (i / 6) % 6, i % 6};
-      const int g[3] = {tc[0] * kTile + l[0], tc[1] * kTile + l[1], tc[2] * kTile + l[2]};
-      ok = g[0] < P.dims[0] && g[1] < P.dims[1] && g[2] < P.dims[2] && owns_node(nbr, l);
+      const int g[3] = {tc[0] * kTile + i / 36, tc[1] * kTile + (i / 6) % 6, tc[2] * kTile + i % 6};
+      ok = g[0] < P.dims[0] && g[1] < P.dims[1] && g[2] < P.dims[2] && (nbr & nm.prior[i]) == 0u;
     }
     const unsigned b = __ballot_sync(0xffffffffu, ok);
     if (ok) list[n + __popc(b & ((1u << lane) - 1u))] = (short)i;
@@ -703,24 +719,21 @@ __device__ __forceinline__ int owned_nodes(const DevParams& P, unsigned nbr, con
   return n;
 }
 
-__device__ __forceinline__ float4 sum_blocks(const DevParams& P, const float4* __restrict__ blocks, unsigned nbr, int e,
-                                             const int tc[3], const int l[3]) {
-  int lo[3], hi[3];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) cand_range(l[d], lo[d], hi[d]);
+__device__ __forceinline__ float4 sum_blocks(const DevParams& P, const NodeMasks& nm, const float4* __restrict__ blocks,
+                                             unsigned nbr, int e, const int tc[3], int i) {
+  const int l[3] = {i / 36, (i / 6) % 6, i % 6};
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int rx = lo[0]; rx <= hi[0]; ++rx)
-    for (int ry = lo[1]; ry <= hi[1]; ++ry)
-      for (int rz = lo[2]; rz <= hi[2]; ++rz) {
-        if (!(nbr & (1u << ((rx + 1) * 9 + (ry + 1) * 3 + (rz + 1))))) continue;
-        const int st = ((tc[0] + rx) * P.td[1] + (tc[1] + ry)) * P.td[2] + (tc[2] + rz);
-        const int lx = l[0] - 4 * rx, ly = l[1] - 4 * ry, lz = l[2] - 4 * rz;
-        const float4 b = blocks[((size_t)e * P.Tn + st) * kExt3 + (lx * kExt + ly) * kExt + lz];
-        acc.x += b.x;
-        acc.y += b.y;
-        acc.z += b.z;
-        acc.w += b.w;
-      }
+  for (unsigned m = nbr & nm.cand[i]; m; m &= m - 1u) {
+    const int bit = __ffs(m) - 1;
+    const int rx = bit / 9 - 1, ry = (bit / 3) % 3 - 1, rz = bit % 3 - 1;
+    const int st = ((tc[0] + rx) * P.td[1] + (tc[1] + ry)) * P.td[2] + (tc[2] + rz);
+    const int lx = l[0] - 4 * rx, ly = l[1] - 4 * ry, lz = l[2] - 4 * rz;
+    const float4 b = blocks[((size_t)e * P.Tn + st) * kExt3 + (lx * kExt + ly) * kExt + lz];
+    acc.x += b.x;
+    acc.y += b.y;
+    acc.z += b.z;
+    acc.w += b.w;
+  }
   return acc;
 }
 
@@ -732,12 +745,15 @@ __device__ __forceinline__ size_t node_lin(const DevParams& P, int e, const int 
 // Owned nodes of every active tile: sum the covering blocks, update
 // (mpm.hpp:256-305 + extensions), write (mass, momentum) and velocity to the
 // dense per-env grid.
-template <int MAXC>
-__global__ void __launch_bounds__(kWarps * 32) k_grid(DevParams P, const int* __restrict__ tile_count,
+template <int MAXC, int CK>
+__global__ void __launch_bounds__(kWarps * 32, 6) k_grid(DevParams P, const int* __restrict__ tile_count,
                                                       const int4* __restrict__ active, const float* __restrict__ cvo,
                                                       const float4* __restrict__ blocks, float4* __restrict__ gmp,
                                                       float4* __restrict__ gv, const int* nact) {
   __shared__ short own[kWarps][kExt3];
+  __shared__ NodeMasks nm;
+  __shared__ Col<float> scol[kWarps][MAXC];
+  build_node_masks(nm);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_active = *(const volatile int*)nact;
   const NodeCtx<float> G = nctx(P);
@@ -746,15 +762,17 @@ __global__ void __launch_bounds__(kWarps * 32) k_grid(DevParams P, const int* __
     const int e = et.x, t = et.y;
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const unsigned nbr = neighbour_mask(P, tile_count, e, tc, lane);
-    Col<float> cols[MAXC];
-    load_cols<MAXC>(P, cvo + (size_t)e * P.K * 9, cols);
-    const int n_own = owned_nodes(P, nbr, tc, own[warp], lane);
+    Col<float>* cols = scol[warp];  // the env's colliders, in shared memory (frees registers)
+    __syncwarp();
+    if (lane == 0) load_cols<MAXC>(P, cvo + (size_t)e * P.K * 9, cols);
+    __syncwarp();
+    const int n_own = owned_nodes(P, nm, nbr, tc, own[warp], lane);
     for (int q = lane; q < n_own; q += 32) {
       const int i = own[warp][q];
       const int l[3] = {i / 36, (i / 6) % 6, i % 6};
       const int g[3] = {tc[0] * kTile + l[0], tc[1] * kTile + l[1], tc[2] * kTile + l[2]};
-      const float4 mm = sum_blocks(P, blocks, nbr, e, tc, l);
-      const v3<float> v = node_update<float, MAXC>(G, cols, P.K, g, mm.x, mk3(mm.y, mm.z, mm.w));
+      const float4 mm = sum_blocks(P, nm, blocks, nbr, e, tc, i);
+      const v3<float> v = node_update<float, MAXC, CK>(G, cols, P.K, g, mm.x, mk3(mm.y, mm.z, mm.w));
       const size_t n = node_lin(P, e, g);
       gmp[n] = mm;
       gv[n] = make_float4(v.x, v.y, v.z, 0.f);
@@ -968,13 +986,19 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_g2p_adj(DevParams P, StateVi
 // Owned nodes: node-velocity cotangent (sum of the covering adjoint blocks)
 // -> (mass, momentum) cotangents in the dense grid; collider cotangents
 // reduced per tile (each node counted once, by its owner).
-template <int MAXC>
-__global__ void __launch_bounds__(kWarps * 32) k_grid_adj(DevParams P, const int* __restrict__ tile_count,
+template <int MAXC, int CK>
+#ifndef DM_GRIDADJ_MINB
+#define DM_GRIDADJ_MINB 4
+#endif
+__global__ void __launch_bounds__(kWarps * 32, DM_GRIDADJ_MINB) k_grid_adj(DevParams P, const int* __restrict__ tile_count,
                                                           const int4* __restrict__ active, const float* __restrict__ cvo,
                                                           const float4* __restrict__ ablocks,
                                                           const float4* __restrict__ gmpb, float4* __restrict__ gmb,
                                                           float* __restrict__ tile_acc, const int* nact) {
   __shared__ short own[kWarps][kExt3];
+  __shared__ NodeMasks nm;
+  __shared__ Col<float> scol[kWarps][MAXC];
+  build_node_masks(nm);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_active = *(const volatile int*)nact;
   const NodeCtx<float> G = nctx(P);
@@ -983,23 +1007,25 @@ __global__ void __launch_bounds__(kWarps * 32) k_grid_adj(DevParams P, const int
     const int e = et.x, t = et.y;
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const unsigned nbr = neighbour_mask(P, tile_count, e, tc, lane);
-    Col<float> cols[MAXC];
-    load_cols<MAXC>(P, cvo + (size_t)e * P.K * 9, cols);
+    Col<float>* cols = scol[warp];  // the env's colliders, in shared memory (frees registers)
+    __syncwarp();
+    if (lane == 0) load_cols<MAXC>(P, cvo + (size_t)e * P.K * 9, cols);
+    __syncwarp();
     float cg[MAXC * 9];
 #pragma unroll
     for (int q = 0; q < MAXC * 9; ++q) cg[q] = 0.f;
-    const int n_own = owned_nodes(P, nbr, tc, own[warp], lane);
+    const int n_own = owned_nodes(P, nm, nbr, tc, own[warp], lane);
     for (int q = lane; q < n_own; q += 32) {
       const int i = own[warp][q];
       const int l[3] = {i / 36, (i / 6) % 6, i % 6};
       const int g[3] = {tc[0] * kTile + l[0], tc[1] * kTile + l[1], tc[2] * kTile + l[2]};
-      const float4 vb = sum_blocks(P, ablocks, nbr, e, tc, l);
+      const float4 vb = sum_blocks(P, nm, ablocks, nbr, e, tc, i);
       const size_t n = node_lin(P, e, g);
       const float4 mm = gmpb[(size_t)a * kExt3 + i];  // this tile's stored (mass, momentum) block
       float mbar;
       v3<float> pbar;
       // adjoint blocks carry (unused, vbar.x, vbar.y, vbar.z) -- emit_contrib layout
-      node_update_vjp<float, MAXC>(G, cols, P.K, g, mm.x, mk3(mm.y, mm.z, mm.w), mk3(vb.y, vb.z, vb.w), mbar, pbar,
+      node_update_vjp<float, MAXC, CK>(G, cols, P.K, g, mm.x, mk3(mm.y, mm.z, mm.w), mk3(vb.y, vb.z, vb.w), mbar, pbar,
                                    cg);
       gmb[n] = make_float4(mbar, pbar.x, pbar.y, pbar.z);
     }

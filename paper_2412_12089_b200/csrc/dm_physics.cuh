@@ -416,10 +416,12 @@ DM_HD v3<R> cyl_query_vjp(const CylQ<R>& c, R dbar, v3<R> nbar) {
 }
 
 // Query: d, n at point p; relb(dbar, nbar) computed by collider_query_vjp.
-template <class R>
+// CK >= 0 fixes the collider kind at compile time (the switch folds: small
+// code for single-kind batches); CK = -1 dispatches on col.kind.
+template <class R, int CK = -1>
 DM_HD_NOINLINE void collider_query(const Col<R>& col, v3<R> p, R& d, v3<R>& n) {
   const v3<R> rel = p - col.c;
-  switch (col.kind) {
+  switch (CK >= 0 ? CK : col.kind) {
     case kPlane:
       d = dot(rel, col.nrm);
       n = col.nrm;
@@ -463,10 +465,10 @@ DM_HD_NOINLINE void collider_query(const Col<R>& col, v3<R> p, R& d, v3<R>& n) {
 }
 
 // Returns pbar (gradient w.r.t. the query point; center gets -pbar).
-template <class R>
+template <class R, int CK = -1>
 DM_HD_NOINLINE v3<R> collider_query_vjp(const Col<R>& col, v3<R> p, R dbar, v3<R> nbar) {
   const v3<R> rel = p - col.c;
-  switch (col.kind) {
+  switch (CK >= 0 ? CK : col.kind) {
     case kPlane:
       return col.nrm * dbar;
     case kSphere: {
@@ -503,11 +505,11 @@ struct Coupling {
 };
 
 // One collider applied to node velocity v (mpm.hpp:275-294 + rotation).
-template <class R>
+template <class R, int CK = -1>
 DM_HD v3<R> collide(const Col<R>& col, R alpha_c, R mu_b, v3<R> node, v3<R> v) {
   R d;
   v3<R> n;
-  collider_query(col, node, d, n);
+  collider_query<R, CK>(col, node, d, n);
   const R s = d < R(0) ? R(1) : r_exp(-alpha_c * r_max(d, R(0)));
   const v3<R> vcol = col.vel + cross(col.om, node - col.c);
   const v3<R> rel = v - vcol;
@@ -522,12 +524,12 @@ DM_HD v3<R> collide(const Col<R>& col, R alpha_c, R mu_b, v3<R> node, v3<R> v) {
 
 // Adjoint of collide: given vout_bar, returns v_bar and accumulates the
 // collider's center / velocity / omega cotangents.
-template <class R>
+template <class R, int CK = -1>
 DM_HD_NOINLINE v3<R> collide_vjp(const Col<R>& col, R alpha_c, R mu_b, v3<R> node, v3<R> v, v3<R> vb_out, v3<R>& cbar,
                         v3<R>& velbar, v3<R>& ombar) {
   R d;
   v3<R> n;
-  collider_query(col, node, d, n);
+  collider_query<R, CK>(col, node, d, n);
   const v3<R> r = node - col.c;
   const v3<R> vcol = col.vel + cross(col.om, r);
   const v3<R> rel = v - vcol;
@@ -574,7 +576,7 @@ DM_HD_NOINLINE v3<R> collide_vjp(const Col<R>& col, R alpha_c, R mu_b, v3<R> nod
   const v3<R> rb = cross(vcolb, col.om);
   cbar -= rb;
   // query
-  cbar -= collider_query_vjp(col, node, db, nb);
+  cbar -= collider_query_vjp<R, CK>(col, node, db, nb);
   return vb;
 }
 
@@ -614,7 +616,7 @@ DM_HD int boundary_apply(const NodeCtx<R>& g, const int idx[3], v3<R>& v) {
 }
 
 // Forward node update; returns velocity.  mass <= 0 -> zero (mpm.hpp:265-268).
-template <class R, int MAXC>
+template <class R, int MAXC, int CK = -1>
 DM_HD v3<R> node_update(const NodeCtx<R>& g, const Col<R>* cols, int ncol, const int idx[3], R mass, v3<R> mom) {
   if (!(mass > R(0))) return zero3<R>();
   const R inv = R(1) / mass;
@@ -623,14 +625,14 @@ DM_HD v3<R> node_update(const NodeCtx<R>& g, const Col<R>* cols, int ncol, const
   v.y += g.dt * g.gravity.y;
   v.z += g.dt * g.gravity.z;
   const v3<R> node = mk3(R(idx[0]) * g.dx, R(idx[1]) * g.dx, R(idx[2]) * g.dx);
-  for (int c = 0; c < ncol && c < MAXC; ++c) v = collide(cols[c], g.alpha_c, g.mu_b, node, v);
+  for (int c = 0; c < ncol && c < MAXC; ++c) v = collide<R, CK>(cols[c], g.alpha_c, g.mu_b, node, v);
   boundary_apply(g, idx, v);
   return v;
 }
 
 // Node adjoint: from vbar_out to (mass_bar, mom_bar); collider cotangents
 // accumulated into cgrad[c*9 + {0..8}] (center, velocity, omega).
-template <class R, int MAXC>
+template <class R, int MAXC, int CK = -1>
 DM_HD void node_update_vjp(const NodeCtx<R>& g, const Col<R>* cols, int ncol, const int idx[3], R mass, v3<R> mom,
                            v3<R> vb, R& massb, v3<R>& momb, R* cgrad) {
   massb = R(0);
@@ -645,7 +647,7 @@ DM_HD void node_update_vjp(const NodeCtx<R>& g, const Col<R>* cols, int ncol, co
   v3<R> vs[MAXC + 1];
   vs[0] = v0;
   const int nc = ncol < MAXC ? ncol : MAXC;
-  for (int c = 0; c < nc; ++c) vs[c + 1] = collide(cols[c], g.alpha_c, g.mu_b, node, vs[c]);
+  for (int c = 0; c < nc; ++c) vs[c + 1] = collide<R, CK>(cols[c], g.alpha_c, g.mu_b, node, vs[c]);
   v3<R> vfin = vs[nc];
   const int mask = boundary_apply(g, idx, vfin);
 #pragma unroll
@@ -653,7 +655,7 @@ DM_HD void node_update_vjp(const NodeCtx<R>& g, const Col<R>* cols, int ncol, co
     if (mask & (1 << a)) vb[a] = R(0);
   for (int c = nc - 1; c >= 0; --c) {
     v3<R> cb = zero3<R>(), velb = zero3<R>(), omb = zero3<R>();
-    vb = collide_vjp(cols[c], g.alpha_c, g.mu_b, node, vs[c], vb, cb, velb, omb);
+    vb = collide_vjp<R, CK>(cols[c], g.alpha_c, g.mu_b, node, vs[c], vb, cb, velb, omb);
     R* o = cgrad + 9 * c;
     o[0] += cb.x;
     o[1] += cb.y;
