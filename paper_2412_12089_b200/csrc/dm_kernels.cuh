@@ -611,15 +611,17 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_p2g(DevParams P, StateView S
     const int o[3] = {tx * kTile, ty * kTile, tz * kTile};
     const size_t tix = (size_t)e * P.Tn + t;
     const int* prow = perm + (size_t)e * P.N + start;
-    bool ok = lane < cnt;
+    // perm indices two chunks ahead in two parity slots (no register moves
+    // between chunks, so a refill never waits on the load it replaces)
     PState ps;
-    if (ok) load_pstate(S, prow[lane], ps);
-    int src_n = 32 + lane < cnt ? prow[32 + lane] : 0;
+    if (lane < cnt) load_pstate(S, prow[lane], ps);
+    int s1 = 32 + lane < cnt ? prow[32 + lane] : 0;
+    int s0 = 64 + lane < cnt ? prow[64 + lane] : 0;
     scatter_zero(bw, lane);
     RunAcc ra;
     run_reset(ra);
-    for (int c0 = 0; c0 < cnt; c0 += 32) {
-      if (ok) {
+    auto chunk = [&](int c0, int& s_next) {
+      if (c0 + lane < cnt) {
         Stencil<float> sc;
         make_stencil(ps.x, P.inv_dx, (double)P.dx, P.dims, sc);
         const Law<float> L = law_of<LAW>(P, attr_mat(ps.at));
@@ -636,10 +638,14 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_p2g(DevParams P, StateView S
       }
       __syncwarp();
       // software pipeline: issue the next chunk's loads before this chunk's scatter
-      ok = c0 + 32 + lane < cnt;
-      if (ok) load_pstate(S, src_n, ps);
-      src_n = c0 + 64 + lane < cnt ? prow[c0 + 64 + lane] : 0;
+      if (c0 + 32 + lane < cnt) load_pstate(S, s_next, ps);
+      s_next = c0 + 96 + lane < cnt ? prow[c0 + 96 + lane] : 0;
       scatter_runs<true>(bw, pw, min(32, cnt - c0), lane, ra);
+    };
+    for (int c0 = 0; c0 < cnt; c0 += 64) {
+      chunk(c0, s1);
+      if (c0 + 32 >= cnt) break;
+      chunk(c0 + 32, s0);
     }
     scatter_store(bw, lane, ra, blocks + tix * kExt3);
   }
@@ -817,16 +823,18 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
     const size_t row = (size_t)e * P.N + start;
-    bool ok = lane < cnt;
-    float x[3];
-    m3<float> F;
-    uint32_t at = 0;
-    if (ok) {
+    // two particle-state buffers (chunks alternate) and perm indices two
+    // chunks ahead in parity slots: no register moves between chunks
+    float xa[3], xb[3];
+    m3<float> Fa, Fb;
+    uint32_t ata = 0, atb = 0;
+    if (lane < cnt) {
       const int src = perm[row + lane];
-      load_xF(S, src, x, F);
-      at = S.attr[src];
+      load_xF(S, src, xa, Fa);
+      ata = S.attr[src];
     }
-    int src_n = lane + 32 < cnt ? perm[row + lane + 32] : 0;
+    int s1 = lane + 32 < cnt ? perm[row + lane + 32] : 0;
+    int s0 = lane + 64 < cnt ? perm[row + lane + 64] : 0;
     cp_async_wait<1>();  // this tile's grid has landed
     __syncwarp();
     float4* vw = vg[warp][buf];
@@ -834,40 +842,39 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
       for (int i = lane; i < kExt3; i += 32) out_gv[(size_t)a * kExt3 + i] = vw[i];
       load_tile_grid(P, gmp, e, o, out_gmp + (size_t)a * kExt3, lane);
     }
-    for (int c0 = 0; c0 < cnt; c0 += 32) {
-      // next chunk's loads in flight during this chunk's math
-      const bool ok_n = c0 + 32 + lane < cnt;
-      float xn_[3];
-      m3<float> Fn_;
-      uint32_t at_n = 0;
-      if (ok_n) {
-        load_xF(S, src_n, xn_, Fn_);
-        at_n = S.attr[src_n];
+    auto body = [&](int c0, const float x[3], m3<float> F, uint32_t at) {
+      if (c0 + lane >= cnt) return;
+      const size_t dst = row + c0 + lane;
+      Stencil<float> sc;
+      make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
+      const int lb[3] = {tile_local(sc.base[0], o[0]), tile_local(sc.base[1], o[1]), tile_local(sc.base[2], o[2])};
+      auto getv = [&](int i, int j, int k) {
+        const float4 q = vw[((lb[0] + i) * kExt + (lb[1] + j)) * kExt + lb[2] + k];
+        return mk3(q.x, q.y, q.z);
+      };
+      v3<float> xn = mk3(x[0], x[1], x[2]), v;
+      m3<float> C;
+      bool bad_adv = false, bad_det = false;
+      g2p_particle_sep(law_of<LAW>(P, attr_mat(at)), T, sc, getv, xn, v, C, F, &bad_adv, &bad_det);
+      if (bad_adv) report(flags, e, substep, 1, attr_index(at), 0, kErrG2PInterior);
+      if (bad_det) report(flags, e, substep, 1, attr_index(at), attr_mat(at), kErrDetF);
+      store_state(Sout, dst, xn, v, F, C);
+      Sout.attr[dst] = at;
+    };
+    for (int c0 = 0; c0 < cnt; c0 += 64) {
+      if (c0 + 32 + lane < cnt) {  // chunk c0 + 32 -> buffer b
+        load_xF(S, s1, xb, Fb);
+        atb = S.attr[s1];
       }
-      src_n = c0 + 64 + lane < cnt ? perm[row + c0 + 64 + lane] : 0;
-      if (ok) {
-        const size_t dst = row + c0 + lane;
-        Stencil<float> sc;
-        make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
-        const int lb[3] = {tile_local(sc.base[0], o[0]), tile_local(sc.base[1], o[1]), tile_local(sc.base[2], o[2])};
-        auto getv = [&](int i, int j, int k) {
-          const float4 q = vw[((lb[0] + i) * kExt + (lb[1] + j)) * kExt + lb[2] + k];
-          return mk3(q.x, q.y, q.z);
-        };
-        v3<float> xn = mk3(x[0], x[1], x[2]), v;
-        m3<float> C;
-        bool bad_adv = false, bad_det = false;
-        g2p_particle_sep(law_of<LAW>(P, attr_mat(at)), T, sc, getv, xn, v, C, F, &bad_adv, &bad_det);
-        if (bad_adv) report(flags, e, substep, 1, attr_index(at), 0, kErrG2PInterior);
-        if (bad_det) report(flags, e, substep, 1, attr_index(at), attr_mat(at), kErrDetF);
-        store_state(Sout, dst, xn, v, F, C);
-        Sout.attr[dst] = at;
+      s1 = c0 + 96 + lane < cnt ? perm[row + c0 + 96 + lane] : 0;
+      body(c0, xa, Fa, ata);
+      if (c0 + 32 >= cnt) break;
+      if (c0 + 64 + lane < cnt) {  // chunk c0 + 64 -> buffer a
+        load_xF(S, s0, xa, Fa);
+        ata = S.attr[s0];
       }
-      ok = ok_n;
-#pragma unroll
-      for (int q = 0; q < 3; ++q) x[q] = xn_[q];
-      F = Fn_;
-      at = at_n;
+      s0 = c0 + 128 + lane < cnt ? perm[row + c0 + 128 + lane] : 0;
+      body(c0 + 32, xb, Fb, atb);
     }
     __syncwarp();  // every lane is done with vw before it is refilled
   }
@@ -906,16 +913,16 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_g2p_adj(DevParams P, StateVi
     cp_async_commit();
     const size_t tix = (size_t)e * P.Tn + t;
     const size_t row = (size_t)e * P.N + start;
-    bool ok = lane < cnt;
     float x[3];
     m3<float> F;
     uint32_t at = 0;
-    if (ok) {
+    if (lane < cnt) {
       const int src = perm[row + lane];
       load_xF(S, src, x, F);
       at = S.attr[src];
     }
-    int src_n = 32 + lane < cnt ? perm[row + 32 + lane] : 0;
+    int s1 = 32 + lane < cnt ? perm[row + 32 + lane] : 0;  // perm two chunks ahead, parity slots
+    int s0 = 64 + lane < cnt ? perm[row + 64 + lane] : 0;
     scatter_zero(aw, lane);
     double mub[NM];  // fp64: cancelling per-particle sums (NM = materials)
 #pragma unroll
@@ -924,8 +931,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_g2p_adj(DevParams P, StateVi
     run_reset(ra);
     cp_async_wait<0>();
     __syncwarp();
-    for (int c0 = 0; c0 < cnt; c0 += 32) {
-      if (ok) {
+    auto chunk = [&](int c0, int& s_next) {
+      if (c0 + lane < cnt) {
         const size_t dst = row + c0 + lane;
         Stencil<float> sc;
         make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
@@ -963,13 +970,17 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_g2p_adj(DevParams P, StateVi
         stage_payload(pw + lane * kPay, (lb[0] * kExt + lb[1]) * kExt + lb[2], sc, 0.f, gq, Bd);
       }
       __syncwarp();
-      ok = c0 + 32 + lane < cnt;
-      if (ok) {
-        load_xF(S, src_n, x, F);
-        at = S.attr[src_n];
+      if (c0 + 32 + lane < cnt) {
+        load_xF(S, s_next, x, F);
+        at = S.attr[s_next];
       }
-      src_n = c0 + 64 + lane < cnt ? perm[row + c0 + 64 + lane] : 0;
+      s_next = c0 + 96 + lane < cnt ? perm[row + c0 + 96 + lane] : 0;
       scatter_runs<false>(aw, pw, min(32, cnt - c0), lane, ra);
+    };
+    for (int c0 = 0; c0 < cnt; c0 += 64) {
+      chunk(c0, s1);
+      if (c0 + 32 >= cnt) break;
+      chunk(c0 + 32, s0);
     }
     scatter_store(aw, lane, ra, ablocks + tix * kExt3);
 #pragma unroll
