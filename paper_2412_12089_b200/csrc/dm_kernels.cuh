@@ -555,6 +555,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool va
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 16 : 0) : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -1053,8 +1057,12 @@ __global__ void __launch_bounds__(kWarps * 32, DM_GRIDADJ_MINB) k_grid_adj(DevPa
 }
 
 // ============================ P2G adjoint ============================
+// Per tile: the (mass, momentum) cotangent block and chunk 0 stream in with
+// cp.async; each chunk's particle data is staged in shared memory by cp.async
+// while the previous chunk computes (no registers held for the prefetch).
+constexpr int kP2gAdjStage = 38;  // staged words per particle: state 24, attr, part 12, perm index
 #ifndef DM_P2GADJ_MINB
-#define DM_P2GADJ_MINB 4
+#define DM_P2GADJ_MINB 3
 #endif
 template <int LAW, int NG, int NM>
 __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevParams P, StateView S, const int* __restrict__ perm,
@@ -1064,42 +1072,75 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
                                                          const float4* __restrict__ gmb, const float* __restrict__ part,
                                                          float* __restrict__ adj_out, size_t astride,
                                                          float* __restrict__ tile_acc, const int* nact) {
-  __shared__ __align__(16) float4 mb[kWarps][2][kExt3];
+  __shared__ __align__(16) float4 mb[kWarps][kExt3];
+  __shared__ float stg[kWarps][kP2gAdjStage * 32];  // next chunk: [field][lane]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TransferCtx<float> T = tctx(P);
   const int n_active = *(const volatile int*)nact;
-  TileIter ti(active, blockIdx.x * kWarps + warp, gridDim.x * kWarps, n_active);
-  if (ti.valid()) prefetch_tile_grid(P, gmb, ti.cur, mb[warp][0], lane);
-  cp_async_commit();
-  for (int buf = 0; ti.valid(); ti.advance(), buf ^= 1) {
-    __syncwarp();  // every lane is done with the buffer about to be refilled
-    if (ti.has_next()) prefetch_tile_grid(P, gmb, ti.nxt, mb[warp][buf ^ 1], lane);
-    cp_async_commit();
+  float4* bw = mb[warp];
+  float* sg = stg[warp];
+  for (TileIter ti(active, blockIdx.x * kWarps + warp, gridDim.x * kWarps, n_active); ti.valid(); ti.advance()) {
     ti.prefetch(active);
     const int e = ti.cur.x, t = ti.cur.y, start = ti.cur.z, cnt = ti.cur.w;
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
-    float4* bw = mb[warp][buf];
     const size_t tix = (size_t)e * P.Tn + t;
+    const size_t row = (size_t)e * P.N + start;
     double mub[NM], lab[NM];  // fp64: cancelling sums (NM = materials)
 #pragma unroll
     for (int m = 0; m < NM; ++m) mub[m] = lab[m] = 0.0;
     float actb[NG];
 #pragma unroll
     for (int q = 0; q < NG; ++q) actb[q] = 0.f;
-    const size_t row = (size_t)e * P.N + start;
-    int src_next = lane < cnt ? perm[row + lane] : 0;  // index prefetch: one chunk ahead
-    cp_async_wait<1>();  // this tile's grid has landed
-    __syncwarp();
-    for (int c0 = lane; c0 < cnt; c0 += 32) {
-      const size_t j = row + c0;
-      const int src = src_next;
-      if (c0 + 32 < cnt) src_next = perm[j + 32];
+    // cp.async staging of one chunk's particle data (state + attr via perm,
+    // particle-side cotangents at the sorted slot, and the perm index itself)
+    auto stage = [&](int c0, int src) {
+#pragma unroll
+      for (int f = 0; f < 24; ++f) cp_async4(sg + f * 32 + lane, S.f + f * S.stride + src);
+      cp_async4(sg + 24 * 32 + lane, S.attr + src);
+#pragma unroll
+      for (int f = 0; f < 12; ++f) cp_async4(sg + (25 + f) * 32 + lane, part + f * astride + row + c0 + lane);
+      sg[37 * 32 + lane] = __int_as_float(src);
+    };
+    int s1 = 32 + lane < cnt ? perm[row + 32 + lane] : 0;  // perm two chunks ahead, parity slots
+    int s0 = lane < cnt ? perm[row + lane] : 0;
+    __syncwarp();  // previous tile's readers are done with bw and sg
+    prefetch_tile_grid(P, gmb, ti.cur, bw, lane);
+    if (lane < cnt) stage(0, s0);
+    cp_async_commit();
+    s0 = 64 + lane < cnt ? perm[row + 64 + lane] : 0;
+    for (int c0 = 0, k = 0; c0 < cnt; c0 += 32, ++k) {
+      cp_async_wait<0>();
+      __syncwarp();
+      const bool ok = c0 + lane < cnt;
       float x[3];
-      v3<float> v;
-      m3<float> F, C;
-      load_state(S, src, x, v, F, C);
-      const uint32_t at = S.attr[src];
+      v3<float> v, xb;
+      m3<float> F, C, Fb;
+      uint32_t at = 0;
+      int src = 0;
+      if (ok) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) x[a] = sg[a * 32 + lane];
+        v = mk3(sg[3 * 32 + lane], sg[4 * 32 + lane], sg[5 * 32 + lane]);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+          F.a[q] = sg[(6 + q) * 32 + lane];
+          C.a[q] = sg[(15 + q) * 32 + lane];
+          Fb.a[q] = sg[(28 + q) * 32 + lane];
+        }
+        at = __float_as_uint(sg[24 * 32 + lane]);
+        xb = mk3(sg[25 * 32 + lane], sg[26 * 32 + lane], sg[27 * 32 + lane]);
+        src = __float_as_int(sg[37 * 32 + lane]);
+      }
+      __syncwarp();  // every lane has its chunk in registers: refill the staging buffer
+      // chunk k + 1's index sits in parity slot (k + 1) & 1; refill it with chunk k + 3's
+      const bool odd = k & 1;
+      if (c0 + 32 + lane < cnt) stage(c0 + 32, odd ? s0 : s1);
+      cp_async_commit();
+      const int s_new = c0 + 96 + lane < cnt ? perm[row + c0 + 96 + lane] : 0;
+      s0 = odd ? s_new : s0;
+      s1 = odd ? s1 : s_new;
+      if (!ok) continue;
       Stencil<float> sc;
       make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
       const int lb[3] = {tile_local(sc.base[0], o[0]), tile_local(sc.base[1], o[1]), tile_local(sc.base[2], o[2])};
@@ -1108,10 +1149,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
         m_ = q.x;
         p_ = mk3(q.y, q.z, q.w);
       };
-      v3<float> xb = mk3(part[0 * astride + j], part[1 * astride + j], part[2 * astride + j]);
-      m3<float> Fb, Cb = mzero<float>();
-#pragma unroll
-      for (int q = 0; q < 9; ++q) Fb.a[q] = part[(3 + q) * astride + j];
+      m3<float> Cb = mzero<float>();
       v3<float> vb = zero3<float>();
       const int mi = attr_mat(at), gi = min(attr_group(at), P.G > 0 ? P.G - 1 : 0);
       const float av = act ? act[e * P.G + gi] : 0.f;
@@ -1157,7 +1195,6 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
 #pragma unroll
       for (int q = 0; q < NG; ++q) ta[kAccAct + q] = actb[q];
     }
-    __syncwarp();
   }
   cp_async_wait<0>();
 }
