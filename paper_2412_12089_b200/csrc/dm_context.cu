@@ -61,6 +61,7 @@ struct DmContext {
   float4 *blocks = nullptr, *ablocks = nullptr;
   float4 *gmp = nullptr, *gv = nullptr, *gmb = nullptr;  // dense per-env grids
   int bin_warps = 16;
+  bool bin_u16 = true;
   int law = -1;  // the batch's single law kind (compile-time specialised kernels), -1: mixed
   int od = DM_OBS_DIM;  // observable dimension per env
   float* dobs_buf = nullptr;  // [E][od] staging for one step's observable cotangent
@@ -197,11 +198,15 @@ Slot slot(DmContext* c, int q) {
 
 void launch_bin(DmContext* c, const StateView& S, const Slot& q, int sub, int check_vmax) {
   cudaMemsetAsync(q.nact, 0, sizeof(int), c->stream);
-  const size_t shm = (size_t)c->bin_warps * c->P.Tn * sizeof(int);
   PROF_BEGIN(c, 0);
-  k_bin<<<c->P.E, 32 * c->bin_warps, shm, c->stream>>>(c->P, S, c->keys, c->ptile, q.tile_start, q.tile_count,
-                                                       q.active, q.env_abase, q.env_acount, c->flags, q.nact, sub,
-                                                       check_vmax);
+  if (c->bin_u16)
+    k_bin<unsigned short><<<c->P.E, 32 * c->bin_warps, (size_t)c->bin_warps * c->P.Tn * 2, c->stream>>>(
+        c->P, S, c->keys, c->ptile, q.tile_start, q.tile_count, q.active, q.env_abase, q.env_acount, c->flags, q.nact,
+        sub, check_vmax);
+  else
+    k_bin<int><<<c->P.E, 32 * c->bin_warps, (size_t)c->bin_warps * c->P.Tn * 4, c->stream>>>(
+        c->P, S, c->keys, c->ptile, q.tile_start, q.tile_count, q.active, q.env_abase, q.env_acount, c->flags, q.nact,
+        sub, check_vmax);
   k_cellsort<<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, c->ptile, q.perm, c->keys, q.tile_start,
                                                            q.tile_count, q.active, q.nact, c->flags);
   ++c->launches;
@@ -671,11 +676,15 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   }
   P.Tn = P.td[0] * P.td[1] * P.td[2];
   {
-    int nw = (int)((160 * 1024) / ((size_t)P.Tn * sizeof(int)));
+    // 16-bit histogram words when a warp's count and an env's cursor fit
+    ctx->bin_u16 = P.N <= 65535;
+    const size_t wb = ctx->bin_u16 ? 2 : 4;
+    int nw = (int)((160 * 1024) / ((size_t)P.Tn * wb));
     nw = nw > 16 ? 16 : nw;
     if (nw < 1) return fail("dm_create: grid too large for the bin kernel");
     ctx->bin_warps = nw;
-    cudaFuncSetAttribute(k_bin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(nw * P.Tn * sizeof(int)));
+    cudaFuncSetAttribute(k_bin<unsigned short>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(nw * P.Tn * 2));
+    cudaFuncSetAttribute(k_bin<int>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(nw * P.Tn * 4));
   }
   P.dx = (float)cfg->dx;
   P.inv_dx = (float)(1.0 / cfg->dx);

@@ -185,10 +185,14 @@ __device__ __forceinline__ void store_state(const StateView& S, size_t i, v3<flo
 // dense tile table, active-tile list, and a stable counting sort: every warp
 // scatters its chunk in index order from its own per-tile cursor, so the
 // permutation equals std::stable_sort by key.
+// CT: histogram / cursor word (unsigned short when particles per env fit in
+// 16 bits: half the shared memory, twice the resident CTAs).
+template <class CT>
 __global__ void __launch_bounds__(512) k_bin(DevParams P, StateView S, int* keys, int* perm, int* tile_start,
                                              int* tile_count, int4* active, int* env_abase, int* env_acount,
                                              DevFlags* flags, int* nact, int substep, int check_vmax) {
-  extern __shared__ int cnt[];  // [nw][Tn]
+  extern __shared__ __align__(16) unsigned char bin_smem[];
+  CT* cnt = reinterpret_cast<CT*>(bin_smem);  // [nw][Tn]
   __shared__ int s_part[512 / 32 + 1][2];
   __shared__ int s_base;
   const int e = blockIdx.x;
@@ -199,7 +203,7 @@ __global__ void __launch_bounds__(512) k_bin(DevParams P, StateView S, int* keys
   __syncthreads();
   const int chunk = (P.N + nw - 1) / nw;
   const int p0 = wid * chunk, p1 = min(P.N, p0 + chunk);
-  int* my = cnt + wid * P.Tn;
+  CT* my = cnt + wid * P.Tn;
   float vmax = 0.f;
   for (int c0 = p0; c0 < p1; c0 += 32) {
     const int p = c0 + lane;
@@ -220,7 +224,7 @@ __global__ void __launch_bounds__(512) k_bin(DevParams P, StateView S, int* keys
       if (check_vmax) vmax = fmaxf(vmax, fmaxf(fabsf(S.c(3, i)), fmaxf(fabsf(S.c(4, i)), fabsf(S.c(5, i)))));
     }
     const unsigned peers = __match_any_sync(0xffffffffu, key);
-    if (p < p1 && lane == __ffs(peers) - 1) my[key] += __popc(peers);
+    if (p < p1 && lane == __ffs(peers) - 1) my[key] = (CT)(my[key] + __popc(peers));
     __syncwarp();
   }
   if (check_vmax) {
@@ -273,7 +277,7 @@ __global__ void __launch_bounds__(512) k_bin(DevParams P, StateView S, int* keys
     const int st = oc;
     for (int w = 0; w < nw; ++w) {  // per-warp cursors in warp (= index) order
       const int c = cnt[w * P.Tn + t];
-      cnt[w * P.Tn + t] = oc;
+      cnt[w * P.Tn + t] = (CT)oc;
       oc += c;
     }
     const int c = oc - st;
@@ -294,7 +298,7 @@ __global__ void __launch_bounds__(512) k_bin(DevParams P, StateView S, int* keys
     int pos = 0;
     if (lane == leader && p < p1) {
       pos = my[key];
-      my[key] = pos + __popc(peers);
+      my[key] = (CT)(pos + __popc(peers));
     }
     pos = __shfl_sync(0xffffffffu, pos, leader);
     if (p < p1) perm[base + pos + rank] = (int)(base + p);
