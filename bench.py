@@ -338,6 +338,17 @@ def run_ours(args, scene, rank, world, local, dist):
     per_launch_units = E * N  # every launch of these kernels sweeps all particles once
     achieved = ALG_BYTES[dom] * per_launch_units / (dom_ms / dom_n / 1e3) / 1e9
     total_prof = sum(v[0] for v in prof.values())
+    # DRAM traffic of the dominant kernel from the committed ncu --set full
+    # capture (profiles/ncu_summary.json, bytes per particle), per launch here
+    traffic, traffic_src = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            ks = json.load(f)
+        kinfo = ks["kernels"][dom]
+        traffic = kinfo["dram_bytes_per_particle"] * per_launch_units
+        traffic_src = "%s (%s, cfg4 steady state)" % (ks.get("source", "profiles/ncu_summary.json"), kinfo["kernel"])
+    except Exception:
+        pass
     path_gbs = 480.0 * units_rank / (ms_rank / 1e3) / 1e9
 
     cpu = None
@@ -355,7 +366,8 @@ def run_ours(args, scene, rank, world, local, dist):
                    "particle_substeps_per_step": units_rank * world,
                    "l2": "inputs larger than L2 (state %.2f GB per rank)" % (E * N * 96 / 1e9)},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
+                     "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_source": peak_src,
                      "alg_bytes_per_particle": ALG_BYTES[dom], "kernel_share": dom_ms / total_prof,
                      "path_alg_gbs": path_gbs, "path_frac": path_gbs / hbm},
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
