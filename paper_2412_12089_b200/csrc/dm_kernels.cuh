@@ -96,7 +96,10 @@ __device__ __forceinline__ Law<float> law_of(const DevParams& P, int mi) {
   return L;
 }
 constexpr int kLawBlocks(int law) { return (law == kFluid || law == kNeoHookean) ? 6 : 4; }
-constexpr int kG2pBlocks(int law) { return (law == kFluid || law == kNeoHookean) ? 5 : 4; }
+#ifndef DM_G2P_MINB
+#define DM_G2P_MINB 4
+#endif
+constexpr int kG2pBlocks(int law) { return (law == kFluid || law == kNeoHookean) ? DM_G2P_MINB : 4; }
 
 __device__ __forceinline__ TransferCtx<float> tctx(const DevParams& P) {
   TransferCtx<float> t;
