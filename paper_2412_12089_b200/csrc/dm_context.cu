@@ -69,6 +69,7 @@ struct DmContext {
   int bwd_cur = 0;  // which adj buffer holds the running state cotangent
   float* tile_acc = nullptr;
   DevFlags* flags = nullptr;
+  int* wq = nullptr;  // dynamic tile-scheduling counter
   DevFlags* h_flags = nullptr;
   float *cvo_tape = nullptr, *act_tape = nullptr, *obs_tape = nullptr;
   double *gcvo = nullptr, *gact = nullptr, *gmu = nullptr, *glam = nullptr;
@@ -181,6 +182,9 @@ struct Slot {
   float4* gmpb;
 };
 
+// zeroes the dynamic tile-scheduling counter before a tile kernel
+void wq_reset(DmContext* c) { cudaMemsetAsync(c->wq, 0, sizeof(int), c->stream); }
+
 Slot slot(DmContext* c, int q) {
   const size_t TT = (size_t)c->P.E * c->P.Tn;
   Slot s;
@@ -207,8 +211,9 @@ void launch_bin(DmContext* c, const StateView& S, const Slot& q, int sub, int ch
     k_bin<int><<<c->P.E, 32 * c->bin_warps, (size_t)c->bin_warps * c->P.Tn * 4, c->stream>>>(
         c->P, S, c->keys, c->ptile, q.tile_start, q.tile_count, q.active, q.env_abase, q.env_acount, c->flags, q.nact,
         sub, check_vmax);
+  wq_reset(c);
   k_cellsort<<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, c->ptile, q.perm, c->keys, q.tile_start,
-                                                           q.tile_count, q.active, q.nact, c->flags);
+                                                           q.tile_count, q.active, q.nact, c->flags, c->wq);
   ++c->launches;
   PROF_END(c, 0);
   ++c->launches;
@@ -220,10 +225,11 @@ const float* step_act(DmContext* c, int t) {
 }
 
 void launch_p2g(DmContext* c, const StateView& S, const Slot& q, int t, int sub) {
+  wq_reset(c);
   PROF_BEGIN(c, 1);
 #define L_P2G(LW)                                                                                               \
   k_p2g<LW><<<c->grid_tiles, kWarps * 32, kP2gSmem, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.active, \
-                                                          step_act(c, t), c->blocks, c->flags, q.nact, sub)
+                                                          step_act(c, t), c->blocks, c->flags, q.nact, sub, c->wq)
   DM_LAW_DISPATCH(c, L_P2G);
 #undef L_P2G
   PROF_END(c, 1);
@@ -247,10 +253,11 @@ void launch_p2g(DmContext* c, const StateView& S, const Slot& q, int t, int sub)
   }
 
 void launch_grid(DmContext* c, const Slot& q, int t) {
+  wq_reset(c);
   PROF_BEGIN(c, 9);
 #define L_GRID(MC, CK)                                                                                        \
   k_grid<MC, CK><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.active, step_cvo(c, t), \
-                                                               c->blocks, c->gmp, c->gv, q.nact)
+                                                               c->blocks, c->gmp, c->gv, q.nact, c->wq)
   DM_GRID_DISPATCH(c, L_GRID);
 #undef L_GRID
   PROF_END(c, 9);
@@ -258,11 +265,12 @@ void launch_grid(DmContext* c, const Slot& q, int t) {
 }
 
 void launch_g2p(DmContext* c, const StateView& S, const StateView& So, const Slot& q, int t, int sub, bool dump) {
+  wq_reset(c);
   PROF_BEGIN(c, 2);
 #define L_G2P(LW)                                                                                                \
   k_g2p<LW><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, q.perm, q.tile_start, q.tile_count,        \
                                                           q.active, c->gv, c->flags, q.nact, sub, c->gmp,         \
-                                                          dump ? q.gvb : nullptr, dump ? q.gmpb : nullptr)
+                                                          dump ? q.gvb : nullptr, dump ? q.gmpb : nullptr, c->wq)
   DM_LAW_DISPATCH(c, L_G2P);
 #undef L_G2P
   PROF_END(c, 2);
@@ -280,39 +288,42 @@ void forward_substep(DmContext* c, const StateView& S, const StateView& So, int 
 
 template <int LAW, int NG>
 void launch_p2g_adj(DmContext* c, const StateView& S, const Slot& q, int t, float* adj_out) {
+  wq_reset(c);
   if (c->P.nmat == 1)
     k_p2g_adj<LAW, NG, 1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.active,
                                                               step_act(c, t), c->gmb, c->part, adj_out, c->Ntot,
-                                                              c->tile_acc, q.nact);
+                                                              c->tile_acc, q.nact, c->wq);
   else
   k_p2g_adj<LAW, NG, 4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.active,
                                                               step_act(c, t), c->gmb, c->part, adj_out, c->Ntot,
-                                                              c->tile_acc, q.nact);
+                                                              c->tile_acc, q.nact, c->wq);
 }
 
 // Adjoint of one substep from the replay's stored artifacts (slot qi).
 void backward_substep(DmContext* c, const StateView& S, const StateView& Sn, int t, int qi, const float* adj_in,
                       float* adj_out) {
   const Slot q = slot(c, qi);
+  wq_reset(c);
   PROF_BEGIN(c, 3);
 #define L_G2PA(LW)                                                                                            \
   if (c->P.nmat == 1)                                                                                          \
     k_g2p_adj<LW, 1><<<c->grid_tiles, kWarps * 32, kG2pAdjSmem, c->stream>>>(c->P, S, Sn, adj_in, c->Ntot, q.perm, \
                                                               q.tile_start, q.tile_count, q.active, q.gvb,  \
-                                                              c->ablocks, c->part, c->tile_acc, q.nact);    \
+                                                              c->ablocks, c->part, c->tile_acc, q.nact, c->wq); \
   else                                                                                                         \
     k_g2p_adj<LW, 4><<<c->grid_tiles, kWarps * 32, kG2pAdjSmem, c->stream>>>(c->P, S, Sn, adj_in, c->Ntot, q.perm, \
                                                               q.tile_start, q.tile_count, q.active, q.gvb,  \
-                                                              c->ablocks, c->part, c->tile_acc, q.nact)
+                                                              c->ablocks, c->part, c->tile_acc, q.nact, c->wq)
   DM_LAW_DISPATCH(c, L_G2PA);
 #undef L_G2PA
   PROF_END(c, 3);
   ++c->launches;
+  wq_reset(c);
   PROF_BEGIN(c, 10);
 #define L_GRIDA(MC, CK)                                                                                   \
   k_grid_adj<MC, CK><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.active,        \
                                                                    step_cvo(c, t), c->ablocks, q.gmpb,   \
-                                                                   c->gmb, c->tile_acc, q.nact)
+                                                                   c->gmb, c->tile_acc, q.nact, c->wq)
   DM_GRID_DISPATCH(c, L_GRIDA);
 #undef L_GRIDA
   PROF_END(c, 10);
@@ -766,7 +777,7 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   const size_t NN = (size_t)P.E * P.dims[0] * P.dims[1] * P.dims[2];
   ok = ok && dalloc(ctx, &ctx->gmp, NN) && dalloc(ctx, &ctx->gv, NN) && dalloc(ctx, &ctx->gmb, NN);
   ok = ok && dalloc(ctx, &ctx->blocks, TT * kExt3) && dalloc(ctx, &ctx->ablocks, TT * kExt3) &&
-       dalloc(ctx, &ctx->tile_acc, TT * kNacc) && dalloc(ctx, &ctx->flags, 1);
+       dalloc(ctx, &ctx->tile_acc, TT * kNacc) && dalloc(ctx, &ctx->flags, 1) && dalloc(ctx, &ctx->wq, 4);
   ok = ok && dalloc(ctx, &ctx->cvo_tape, (size_t)cfg->max_steps * P.E * Kc * 9) &&
        dalloc(ctx, &ctx->act_tape, (size_t)cfg->max_steps * P.E * Gc) &&
        dalloc(ctx, &ctx->obs_tape, (size_t)cfg->max_steps * P.E * ctx->od) &&
@@ -799,7 +810,7 @@ void dm_destroy(DmContext* ctx) {
                   ctx->scratch_attr[0], ctx->scratch_attr[1], ctx->adj[0], ctx->adj[1], ctx->part, ctx->keys,
                   ctx->perm_all,  ctx->ptile, ctx->tstart_all, ctx->tcount_all, ctx->abase_all, ctx->acount_all,
                   ctx->active_all, ctx->nact_all, ctx->tail, ctx->tail_attr, ctx->gvb_pool, ctx->gmpb_pool,
-                  ctx->blocks,    ctx->ablocks,    ctx->tile_acc,   ctx->gmp, ctx->gv, ctx->gmb,   ctx->flags,      ctx->cvo_tape,  ctx->act_tape,
+                  ctx->blocks,    ctx->ablocks,    ctx->tile_acc,   ctx->gmp, ctx->gv, ctx->gmb,   ctx->flags, ctx->wq, ctx->cvo_tape,  ctx->act_tape,
                   ctx->obs_tape,  ctx->dobs_buf, ctx->gcvo,       ctx->gact,       ctx->gmu,        ctx->glam};
   for (void* p : ptrs)
     if (p) cudaFree(p);

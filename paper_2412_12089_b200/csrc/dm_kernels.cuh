@@ -77,6 +77,15 @@ __device__ __forceinline__ void report(DevFlags* fl, int env, int sub, int stage
   atomicMin(&fl->err_key, k);
 }
 
+// Dynamic tile scheduling: warps take active-tile indices from a per-launch
+// counter (zeroed before the launch), so the load balances to within one
+// tile; lane 0 grabs and broadcasts.
+__device__ __forceinline__ int grab_tile(int* ctr, int lane, int n = 1) {
+  int a = 0;
+  if (lane == 0) a = atomicAdd(ctr, n);
+  return __shfl_sync(0xffffffffu, a, 0);
+}
+
 // Local base inside the tile, in [0, 4).  Always in range for valid particles
 // (the bin key comes from the same fp32 base); clamped for particles already
 // reported outside the interior so shared-memory indices stay in bounds.
@@ -318,13 +327,14 @@ __global__ void __launch_bounds__(kWarps * 32) k_cellsort(DevParams P, StateView
                                                           const int* __restrict__ tile_start,
                                                           const int* __restrict__ tile_count,
                                                           const int4* __restrict__ active, const int* nact,
-                                                          DevFlags* flags) {
+                                                          DevFlags* flags, int* __restrict__ wq) {
   __shared__ int c64[kWarps][64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int* cnt = c64[warp];
   const int n_active = *(const volatile int*)nact;
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicMax(&flags->max_active, n_active);
-  for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
+  for (int a = grab_tile(wq, lane), an = a < n_active ? grab_tile(wq, lane) : n_active; a < n_active;
+       a = an, an = a < n_active ? grab_tile(wq, lane) : n_active) {
     const int4 et = active[a];
     const int e = et.x;
     const int start = et.z, n = et.w;
@@ -531,27 +541,36 @@ __device__ __forceinline__ void scatter_store(float4* __restrict__ blk3, int lan
 constexpr size_t kP2gSmem = (size_t)kWarps * (3 * kExt3 * sizeof(float4) + 32 * kPay * sizeof(float));
 constexpr size_t kG2pAdjSmem = (size_t)kWarps * (4 * kExt3 * sizeof(float4) + 32 * kPay * sizeof(float));
 
-// Persistent tile loop with the next two tiles' descriptors (env, tile,
-// start, count) loaded ahead: `nxt` is known when the current tile starts
-// (so its grid block can be prefetched), `prefetch` fetches the one after.
+// Persistent tile loop: the next two tiles' descriptors (env, tile, start,
+// count) are loaded ahead (`nxt` is known when the current tile starts, so
+// its grid block can be prefetched) and the index after them is grabbed
+// ahead, so neither the atomic nor the descriptor load is on the critical path.
 struct TileIter {
-  int a, stride, n;
+  int a, a1, a2, a3, n, lane;
+  int* ctr;
   int4 cur, nxt, nxt2;
-  __device__ __forceinline__ TileIter(const int4* __restrict__ active, int a0, int stride_, int n_) {
-    a = a0;
-    stride = stride_;
+  __device__ __forceinline__ TileIter(const int4* __restrict__ active, int* ctr_, int n_, int lane_) {
     n = n_;
+    lane = lane_;
+    ctr = ctr_;
+    a = grab_tile(ctr, lane, 2);
+    a1 = a + 1;
+    a2 = grab_tile(ctr, lane);
+    a3 = n;
     cur = a < n ? active[a] : make_int4(0, 0, 0, 0);
-    nxt = a + stride < n ? active[a + stride] : make_int4(0, 0, 0, 0);
+    nxt = a1 < n ? active[a1] : make_int4(0, 0, 0, 0);
     nxt2 = make_int4(0, 0, 0, 0);
   }
   __device__ __forceinline__ bool valid() const { return a < n; }
-  __device__ __forceinline__ bool has_next() const { return a + stride < n; }
+  __device__ __forceinline__ bool has_next() const { return a1 < n; }
   __device__ __forceinline__ void prefetch(const int4* __restrict__ active) {
-    if (a + 2 * stride < n) nxt2 = active[a + 2 * stride];
+    if (a2 < n) nxt2 = active[a2];
+    a3 = a2 < n ? grab_tile(ctr, lane) : n;
   }
   __device__ __forceinline__ void advance() {
-    a += stride;
+    a = a1;
+    a1 = a2;
+    a2 = a3;
     cur = nxt;
     nxt = nxt2;
   }
@@ -608,14 +627,14 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_p2g(DevParams P, StateView S
                                                      const int* __restrict__ tile_start,
                                                      const int* __restrict__ tile_count, const int4* __restrict__ active,
                                                      const float* __restrict__ act, float4* __restrict__ blocks,
-                                                     DevFlags* flags, const int* nact, int substep) {
+                                                     DevFlags* flags, const int* nact, int substep, int* __restrict__ wq) {
   extern __shared__ float4 dsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_active = *(const volatile int*)nact;
   const TransferCtx<float> T = tctx(P);
   float4* bw = dsm + warp * 3 * kExt3;  // 3 group copies of the 6^3 block
   float* pw = reinterpret_cast<float*>(dsm + kWarps * 3 * kExt3) + warp * 32 * kPay;
-  for (TileIter ti(active, blockIdx.x * kWarps + warp, gridDim.x * kWarps, n_active); ti.valid(); ti.advance()) {
+  for (TileIter ti(active, wq, n_active, lane); ti.valid(); ti.advance()) {
     ti.prefetch(active);
     const int e = ti.cur.x, t = ti.cur.y, start = ti.cur.z, cnt = ti.cur.w;
     const int tz = t % P.td[2], ty = (t / P.td[2]) % P.td[1], tx = t / (P.td[2] * P.td[1]);
@@ -766,7 +785,7 @@ template <int MAXC, int CK>
 __global__ void __launch_bounds__(kWarps * 32, 6) k_grid(DevParams P, const int* __restrict__ tile_count,
                                                       const int4* __restrict__ active, const float* __restrict__ cvo,
                                                       const float4* __restrict__ blocks, float4* __restrict__ gmp,
-                                                      float4* __restrict__ gv, const int* nact) {
+                                                      float4* __restrict__ gv, const int* nact, int* __restrict__ wq) {
   __shared__ short own[kWarps][kExt3];
   __shared__ NodeMasks nm;
   __shared__ Col<float> scol[kWarps][MAXC];
@@ -774,7 +793,8 @@ __global__ void __launch_bounds__(kWarps * 32, 6) k_grid(DevParams P, const int*
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_active = *(const volatile int*)nact;
   const NodeCtx<float> G = nctx(P);
-  for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
+  for (int a = grab_tile(wq, lane), an = a < n_active ? grab_tile(wq, lane) : n_active; a < n_active;
+       a = an, an = a < n_active ? grab_tile(wq, lane) : n_active) {
     const int4 et = active[a];
     const int e = et.x, t = et.y;
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
@@ -817,12 +837,12 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
                                                      const int* __restrict__ tile_count, const int4* __restrict__ active,
                                                      const float4* __restrict__ gv, DevFlags* flags, const int* nact,
                                                      int substep, const float4* __restrict__ gmp,
-                                                     float4* __restrict__ out_gv, float4* __restrict__ out_gmp) {
+                                                     float4* __restrict__ out_gv, float4* __restrict__ out_gmp, int* __restrict__ wq) {
   __shared__ __align__(16) float4 vg[kWarps][2][kExt3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_active = *(const volatile int*)nact;
   const TransferCtx<float> T = tctx(P);
-  TileIter ti(active, blockIdx.x * kWarps + warp, gridDim.x * kWarps, n_active);
+  TileIter ti(active, wq, n_active, lane);
   if (ti.valid()) prefetch_tile_grid(P, gv, ti.cur, vg[warp][0], lane);
   cp_async_commit();
   for (int buf = 0; ti.valid(); ti.advance(), buf ^= 1) {
@@ -905,7 +925,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_g2p_adj(DevParams P, StateVi
                                                          const int* __restrict__ tile_count,
                                                          const int4* __restrict__ active, const float4* __restrict__ gvb,
                                                          float4* __restrict__ ablocks, float* __restrict__ part,
-                                                         float* __restrict__ tile_acc, const int* nact) {
+                                                         float* __restrict__ tile_acc, const int* nact, int* __restrict__ wq) {
   extern __shared__ float4 dsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TransferCtx<float> T = tctx(P);
@@ -913,7 +933,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_g2p_adj(DevParams P, StateVi
   float4* aw = vw + kExt3;              // 3 group copies of the cotangent block
   float* pw = reinterpret_cast<float*>(dsm + kWarps * 4 * kExt3) + warp * 32 * kPay;
   const int n_active = *(const volatile int*)nact;
-  for (TileIter ti(active, blockIdx.x * kWarps + warp, gridDim.x * kWarps, n_active); ti.valid(); ti.advance()) {
+  for (TileIter ti(active, wq, n_active, lane); ti.valid(); ti.advance()) {
     ti.prefetch(active);
     const int a = ti.a;
     const int e = ti.cur.x, t = ti.cur.y, start = ti.cur.z, cnt = ti.cur.w;
@@ -1016,7 +1036,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_GRIDADJ_MINB) k_grid_adj(DevPa
                                                           const int4* __restrict__ active, const float* __restrict__ cvo,
                                                           const float4* __restrict__ ablocks,
                                                           const float4* __restrict__ gmpb, float4* __restrict__ gmb,
-                                                          float* __restrict__ tile_acc, const int* nact) {
+                                                          float* __restrict__ tile_acc, const int* nact, int* __restrict__ wq) {
   __shared__ short own[kWarps][kExt3];
   __shared__ NodeMasks nm;
   __shared__ Col<float> scol[kWarps][MAXC];
@@ -1024,7 +1044,8 @@ __global__ void __launch_bounds__(kWarps * 32, DM_GRIDADJ_MINB) k_grid_adj(DevPa
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_active = *(const volatile int*)nact;
   const NodeCtx<float> G = nctx(P);
-  for (int a = blockIdx.x * kWarps + warp; a < n_active; a += gridDim.x * kWarps) {
+  for (int a = grab_tile(wq, lane), an = a < n_active ? grab_tile(wq, lane) : n_active; a < n_active;
+       a = an, an = a < n_active ? grab_tile(wq, lane) : n_active) {
     const int4 et = active[a];
     const int e = et.x, t = et.y;
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
@@ -1078,7 +1099,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
                                                          const int4* __restrict__ active, const float* __restrict__ act,
                                                          const float4* __restrict__ gmb, const float* __restrict__ part,
                                                          float* __restrict__ adj_out, size_t astride,
-                                                         float* __restrict__ tile_acc, const int* nact) {
+                                                         float* __restrict__ tile_acc, const int* nact, int* __restrict__ wq) {
   __shared__ __align__(16) float4 mb[kWarps][kExt3];
   __shared__ float stg[kWarps][kP2gAdjStage * 32];  // next chunk: [field][lane]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1086,7 +1107,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
   const int n_active = *(const volatile int*)nact;
   float4* bw = mb[warp];
   float* sg = stg[warp];
-  for (TileIter ti(active, blockIdx.x * kWarps + warp, gridDim.x * kWarps, n_active); ti.valid(); ti.advance()) {
+  for (TileIter ti(active, wq, n_active, lane); ti.valid(); ti.advance()) {
     ti.prefetch(active);
     const int e = ti.cur.x, t = ti.cur.y, start = ti.cur.z, cnt = ti.cur.w;
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
