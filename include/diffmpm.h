@@ -151,6 +151,37 @@ int dm_obs_dim(const DmContext* ctx);
 /* Number of control steps currently on the tape. */
 int dm_tape_steps(const DmContext* ctx);
 
+/* Device-side env reset: EnvBatch::reset / reset_env (env.hpp:66-96) with a
+ * sample_box lattice (mpm.hpp:371-395) and per-env RngStream(seed, env)
+ * draws (rng.hpp:11-55, env.hpp:71), generated on the GPU bit-identically to
+ * the host generator (paper_2412_12089_b200/scenes.py lattice_reset_host) --
+ * no host upload at reset.  Per env e (global index env_offset + e), in
+ * double precision without contraction, then rounded to fp32:
+ *   d_a   = origin_lo + (origin_hi - origin_lo) * u_{a+1}      a < origin_draws (else 0)
+ *   x_p,a = (origin_a + d_a) + ((ijk_p,a + 0.5) * spacing_a)  lattice (i, j, k)-major
+ *   x_p,a += jitter_lo + (jitter_hi - jitter_lo) * u_{D + 3p + a + 1}      if jitter_hi > jitter_lo
+ *   v_p,a  = velocity_sigma * normal (Box-Muller cosine, rng.hpp:35-43, draws after the jitter)
+ *   F = I, C = 0
+ * u_k = k-th double of the env's stream.  Envs whose mask byte is 0 keep
+ * their current state; the tape restarts at step 0 (the state is a new
+ * initial state, as dm_set_state).  origin_delta [E][3] receives d (may be
+ * NULL); particle_group [N] gives every env's per-particle actuation group
+ * (may be NULL: spec.group). */
+typedef struct {
+  double origin[3];
+  double spacing[3];
+  int counts[3]; /* nx * ny * nz == particles_per_env */
+  int origin_draws;
+  double origin_lo, origin_hi;
+  double jitter_lo, jitter_hi;
+  double velocity_sigma;
+  int material, group;
+} DmLatticeReset;
+int dm_reset_lattice(DmContext* ctx, const DmLatticeReset* spec, unsigned long long seed, int env_offset,
+                     const unsigned char* env_mask, const int* particle_group, double* origin_delta);
+int dm_reset_lattice_device(DmContext* ctx, const DmLatticeReset* spec, unsigned long long seed, int env_offset,
+                            const unsigned char* env_mask, const int* particle_group, double* origin_delta);
+
 /* Parity hooks: bin keys / stable permutation of the
  * current state (per env, local indices) and the current physical order's
  * original particle ids. */

@@ -18,6 +18,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <cstdint>
 #include <vector>
 
 #include "../diffmpm.h"
@@ -145,6 +146,20 @@ class MpmBatch {
       throw std::invalid_argument("set_state: array sizes do not match num_envs x particles_per_env");
     check(dm_set_state(ctx_, x.data(), v.data(), F.data(), C.data(), material.data(),
                        group.empty() ? nullptr : group.data()));
+  }
+
+  // EnvBatch::reset(seed) / reset_env(i) (env.hpp:66-96) on the device:
+  // envs with a nonzero mask byte (all when `mask` is empty) get a fresh
+  // seeded lattice state; returns the per-env origin offsets [E][3].
+  std::vector<double> reset_lattice(const DmLatticeReset& spec, std::uint64_t seed, int env_offset = 0,
+                                    const std::vector<unsigned char>& mask = {},
+                                    const std::vector<int>& particle_group = {}) {
+    if (!mask.empty() && mask.size() != static_cast<std::size_t>(E_))
+      throw std::invalid_argument("reset_lattice: mask size must equal num_envs");
+    std::vector<double> delta(static_cast<std::size_t>(E_) * 3);
+    check(dm_reset_lattice(ctx_, &spec, seed, env_offset, mask.empty() ? nullptr : mask.data(),
+                           particle_group.empty() ? nullptr : particle_group.data(), delta.data()));
+    return delta;
   }
 
   // lower_state (env.hpp:49-53)

@@ -46,6 +46,13 @@ class DmConfig(C.Structure):
                 ("spill_half", C.c_double), ("spill_temp", C.c_double), ("obs_groups", C.c_int)]
 
 
+class DmLatticeReset(C.Structure):
+    _fields_ = [("origin", C.c_double * 3), ("spacing", C.c_double * 3), ("counts", C.c_int * 3),
+                ("origin_draws", C.c_int), ("origin_lo", C.c_double), ("origin_hi", C.c_double),
+                ("jitter_lo", C.c_double), ("jitter_hi", C.c_double), ("velocity_sigma", C.c_double),
+                ("material", C.c_int), ("group", C.c_int)]
+
+
 _LIB = None
 
 _P = C.c_void_p
@@ -76,6 +83,8 @@ _SIGS = {
     "dm_obs_dim": (C.c_int, [_P]),
     "dm_observe": (C.c_int, [_P] * 3),
     "dm_observe_device": (C.c_int, [_P] * 3),
+    "dm_reset_lattice": (C.c_int, [_P, C.POINTER(DmLatticeReset), C.c_ulonglong, C.c_int, _P, _P, _P]),
+    "dm_reset_lattice_device": (C.c_int, [_P, C.POINTER(DmLatticeReset), C.c_ulonglong, C.c_int, _P, _P, _P]),
 }
 
 PROF_CLASSES = ("bin", "p2g", "g2p", "g2p_adj", "p2g_adj", "env_reduce", "obs", "obs_adj", "layout", "grid",
@@ -232,6 +241,34 @@ class MpmBatch:
             raise ValueError("set_state: actuation group out of range")
         self._keep = arrs
         self._check(self._L.dm_set_state(self._h, *(_ptr(a) for a in arrs)))
+
+    def reset_lattice(self, spec: dict, seed: int, env_offset: int = 0, env_mask=None, particle_group=None,
+                      origin_delta=None):
+        """Device-side reset (EnvBatch::reset / reset_env, env.hpp:66-96) of the
+        envs whose mask byte is nonzero (all when env_mask is None) from a
+        lattice spec (scenes.lattice_reset_spec): no host upload of the state;
+        bit-identical to scenes.lattice_reset_host.  Restarts the tape.
+        Returns the per-env origin offsets [E,3] (numpy) unless torch
+        CUDA `env_mask` / `origin_delta` are given (device path)."""
+        r = DmLatticeReset()
+        r.origin[:] = list(spec["origin"])
+        r.spacing[:] = list(spec["spacing"])
+        r.counts[:] = list(spec["counts"])
+        r.origin_draws = spec.get("origin_draws", 0)
+        r.origin_lo, r.origin_hi = spec.get("origin_range", (0.0, 0.0))
+        r.jitter_lo, r.jitter_hi = spec.get("jitter", (0.0, 0.0))
+        r.velocity_sigma = spec.get("velocity_sigma", 0.0)
+        r.material = spec.get("material", 0)
+        r.group = spec.get("group", 0)
+        if _is_dev(env_mask) or _is_dev(origin_delta) or _is_dev(particle_group):
+            self._check(self._L.dm_reset_lattice_device(self._h, C.byref(r), seed, env_offset, _ptr(env_mask),
+                                                        _ptr(particle_group), _ptr(origin_delta)))
+            return origin_delta
+        m = None if env_mask is None else np.ascontiguousarray(env_mask, dtype=np.uint8)
+        g = None if particle_group is None else np.ascontiguousarray(particle_group, dtype=np.int32)
+        d = np.zeros((self.E, 3), np.float64)
+        self._check(self._L.dm_reset_lattice(self._h, C.byref(r), seed, env_offset, _ptr(m), _ptr(g), _ptr(d)))
+        return d
 
     def get_state(self, out=None):
         """Current state in the original particle order (numpy, or into torch tensors `out`)."""

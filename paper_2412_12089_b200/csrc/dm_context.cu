@@ -841,6 +841,86 @@ int dm_set_state_device(DmContext* ctx, const float* x, const float* v, const fl
   if (!ctx || !ctx->store) return DM_ERR_ARG;
   return set_state_impl(ctx, x, v, F, C, material, group, cudaMemcpyDeviceToDevice);
 }
+namespace {
+// Device-side reset (dm_reset_lattice): masked envs regenerated on the GPU,
+// the others keep their current state; the tape restarts at step 0.
+int reset_lattice_impl(DmContext* ctx, const DmLatticeReset* spec, unsigned long long seed, int env_offset,
+                       const unsigned char* mask, const int* pgroup, double* odelta, bool dev) {
+  if (!ctx || !ctx->store || !spec) return DM_ERR_ARG;
+  const int E = ctx->P.E, N = ctx->P.N;
+  if ((long long)spec->counts[0] * spec->counts[1] * spec->counts[2] != N || spec->counts[0] < 1 ||
+      spec->counts[1] < 1 || spec->counts[2] < 1) {
+    ctx->err = "dm_reset_lattice: counts[0] * counts[1] * counts[2] must equal particles_per_env";
+    return DM_ERR_ARG;
+  }
+  if (spec->origin_draws < 0 || spec->origin_draws > 3 || spec->material < 0 || spec->material >= ctx->nmat ||
+      spec->group < 0 || (ctx->P.G > 0 ? spec->group >= ctx->P.G : spec->group > 0)) {
+    ctx->err = "dm_reset_lattice: origin_draws must be 0..3 and material / group in range";
+    return DM_ERR_ARG;
+  }
+  if (ctx->poisoned && ctx->h_flags->err_key == ~0ull) ctx->poisoned = false;
+  // scratch in the (idle) particle-cotangent buffer: mask, groups, deltas, flags
+  unsigned char* base = reinterpret_cast<unsigned char*>(ctx->part);
+  double* d_delta = reinterpret_cast<double*>(base);
+  int* d_flag = reinterpret_cast<int*>(base + (size_t)E * 3 * sizeof(double));
+  int* d_group = d_flag + E;
+  unsigned char* d_mask = reinterpret_cast<unsigned char*>(d_group + N);
+  const unsigned char* m = mask;
+  const int* g = pgroup;
+  if (!dev) {
+    if (mask) DM_CUDA(cudaMemcpyAsync(d_mask, mask, E, cudaMemcpyHostToDevice, ctx->stream));
+    if (pgroup) DM_CUDA(cudaMemcpyAsync(d_group, pgroup, (size_t)N * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    m = mask ? d_mask : nullptr;
+    g = pgroup ? d_group : nullptr;
+  }
+  DM_CUDA(cudaMemsetAsync(d_flag, 0, (size_t)E * sizeof(int), ctx->stream));
+  DM_CUDA(cudaMemsetAsync(d_delta, 0, (size_t)E * 3 * sizeof(double), ctx->stream));
+  // the unmasked envs' current state becomes the new initial state
+  const StateView S0 = store_view(ctx, 0);
+  const StateView cur = fwd_state(ctx, ctx->steps * ctx->cfg.substeps);
+  if (mask && cur.f != S0.f) {
+    DM_CUDA(cudaMemcpyAsync(S0.f, cur.f, state_floats(ctx) * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream));
+    DM_CUDA(cudaMemcpyAsync(S0.attr, cur.attr, ctx->Ntot * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  ResetSpec R;
+  for (int a = 0; a < 3; ++a) {
+    R.org[a] = spec->origin[a];
+    R.sp[a] = spec->spacing[a];
+    R.cnt[a] = spec->counts[a];
+  }
+  R.odraws = spec->origin_draws;
+  R.olo = spec->origin_lo;
+  R.ohi = spec->origin_hi;
+  R.jlo = spec->jitter_lo;
+  R.jhi = spec->jitter_hi;
+  R.sigma = spec->velocity_sigma;
+  R.material = spec->material;
+  R.group = spec->group;
+  double* od = odelta ? (dev ? odelta : d_delta) : nullptr;
+  k_reset_lattice<<<ctx->grid_tiles, 256, 0, ctx->stream>>>(R, E, N, seed, env_offset, m, g, od, d_flag, S0);
+  k_reset_normals_seq<<<(E + 127) / 128, 128, 0, ctx->stream>>>(R, E, N, seed, env_offset, d_flag, S0);
+  ctx->launches += 2;
+  if (odelta && !dev)
+    DM_CUDA(cudaMemcpyAsync(odelta, d_delta, (size_t)E * 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->steps = 0;
+  ctx->bwd_t = -1;
+  ctx->poisoned = false;
+  const int rc = reset_flags(ctx);  // synchronises the stream
+  if (rc != DM_OK) return rc;
+  DM_CUDA(cudaGetLastError());
+  return DM_OK;
+}
+}  // namespace
+
+int dm_reset_lattice(DmContext* ctx, const DmLatticeReset* spec, unsigned long long seed, int env_offset,
+                     const unsigned char* env_mask, const int* particle_group, double* origin_delta) {
+  return reset_lattice_impl(ctx, spec, seed, env_offset, env_mask, particle_group, origin_delta, false);
+}
+int dm_reset_lattice_device(DmContext* ctx, const DmLatticeReset* spec, unsigned long long seed, int env_offset,
+                            const unsigned char* env_mask, const int* particle_group, double* origin_delta) {
+  return reset_lattice_impl(ctx, spec, seed, env_offset, env_mask, particle_group, origin_delta, true);
+}
+
 int dm_get_state(DmContext* ctx, float* x, float* v, float* F, float* C) {
   if (!ctx || !ctx->store) return DM_ERR_ARG;
   return get_state_impl(ctx, x, v, F, C, cudaMemcpyDeviceToHost);

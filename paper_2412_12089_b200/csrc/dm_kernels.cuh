@@ -1448,6 +1448,104 @@ __global__ void __launch_bounds__(256) k_obs_adj(DevParams P, StateView S, const
   }
 }
 
+// ============================ device-side reset ============================
+// RngStream (rng.hpp:11-55): key = mix(seed ^ phi (stream + 1)); the k-th
+// draw is mix(key ^ mix(k)), so every particle addresses its own draws.
+__device__ __forceinline__ unsigned long long sm64_mix(unsigned long long z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double rng_double(unsigned long long key, unsigned long long k) {
+  return (double)(sm64_mix(key ^ sm64_mix(k)) >> 11) * 0x1.0p-53;
+}
+__device__ __forceinline__ double rng_uniform(unsigned long long key, unsigned long long k, double lo, double hi) {
+  return __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), rng_double(key, k)));
+}
+__device__ __forceinline__ double box_muller(double u1, double u2) {
+  return __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(6.283185307179586476925286766559, u2)));
+}
+
+struct ResetSpec {
+  double org[3], sp[3];
+  int cnt[3], odraws;
+  double olo, ohi, jlo, jhi, sigma;
+  int material, group;
+};
+
+// One thread per particle of a masked env.  A stream whose Box-Muller u1
+// draw is 0 (probability 2^-53 per draw) is flagged for the exact sequential
+// redraw of k_reset_normals_seq.
+__global__ void k_reset_lattice(ResetSpec R, int E, int N, unsigned long long seed, int env_offset,
+                                const unsigned char* __restrict__ mask, const int* __restrict__ pgroup,
+                                double* __restrict__ odelta, int* __restrict__ seq_flag, StateView S) {
+  const size_t tot = (size_t)E * N;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
+    const int e = (int)(i / N), p = (int)(i % N);
+    if (mask && !mask[e]) continue;
+    const unsigned long long key =
+        sm64_mix(seed ^ (0x9e3779b97f4a7c15ULL * ((unsigned long long)(env_offset + e) + 1ULL)));
+    double d[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if (a < R.odraws) d[a] = rng_uniform(key, (unsigned long long)a + 1, R.olo, R.ohi);
+    if (odelta && p == 0)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) odelta[(size_t)e * 3 + a] = d[a];
+    const int ijk[3] = {p / (R.cnt[1] * R.cnt[2]), (p / R.cnt[2]) % R.cnt[1], p % R.cnt[2]};
+    const bool jit = R.jhi > R.jlo;
+    unsigned long long ctr = (unsigned long long)R.odraws;
+    double x[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      x[a] = __dadd_rn(__dadd_rn(R.org[a], d[a]), __dmul_rn(__dadd_rn((double)ijk[a], 0.5), R.sp[a]));
+      if (jit) x[a] = __dadd_rn(x[a], rng_uniform(key, ctr + 3ULL * p + a + 1, R.jlo, R.jhi));
+    }
+    if (jit) ctr += 3ULL * N;
+    double v[3] = {0.0, 0.0, 0.0};
+    if (R.sigma != 0.0) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const unsigned long long m = 3ULL * p + a;
+        const double u1 = rng_double(key, ctr + 2 * m + 1), u2 = rng_double(key, ctr + 2 * m + 2);
+        if (u1 <= 0.0) seq_flag[e] = 1;
+        v[a] = __dmul_rn(R.sigma, box_muller(u1, u2));
+      }
+    }
+    const size_t o = i;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      S.c(a, o) = __double2float_rn(x[a]);
+      S.c(3 + a, o) = __double2float_rn(v[a]);
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      S.c(6 + q, o) = (q % 4 == 0) ? 1.f : 0.f;
+      S.c(15 + q, o) = 0.f;
+    }
+    const uint32_t g = pgroup ? (uint32_t)pgroup[p] : (uint32_t)R.group;
+    S.attr[o] = (uint32_t)p | (((uint32_t)R.material & 0xF) << 20) | ((g & 0xFF) << 24);
+  }
+}
+
+// Exact sequential Box-Muller redraw (rng.hpp:35-43: u1 is redrawn while
+// u1 <= 0, shifting the stream) for the flagged envs; one thread per env.
+__global__ void k_reset_normals_seq(ResetSpec R, int E, int N, unsigned long long seed, int env_offset,
+                                    const int* __restrict__ seq_flag, StateView S) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E || !seq_flag[e]) return;
+  const unsigned long long key =
+      sm64_mix(seed ^ (0x9e3779b97f4a7c15ULL * ((unsigned long long)(env_offset + e) + 1ULL)));
+  unsigned long long ctr = (unsigned long long)R.odraws + (R.jhi > R.jlo ? 3ULL * N : 0ULL);
+  for (int m = 0; m < 3 * N; ++m) {
+    double u1 = rng_double(key, ++ctr);
+    const double u2 = rng_double(key, ++ctr);
+    while (u1 <= 0.0) u1 = rng_double(key, ++ctr);
+    S.c(3 + m % 3, (size_t)e * N + m / 3) = __double2float_rn(__dmul_rn(R.sigma, box_muller(u1, u2)));
+  }
+}
+
 // ============================ layout conversion ============================
 // host visit order (AoS per env) <-> SoA physical order
 __global__ void k_aos_to_soa(int Ntot, const float* __restrict__ x, const float* __restrict__ v,

@@ -155,7 +155,7 @@ class SapoTrainer:
             for g in o.param_groups:
                 g["lr"] = self.base_lr[1] * frac
         E, H = self.E, self.H
-        alpha = float(self.log_alpha.exp())
+        alpha = float(self.log_alpha.detach().exp())
         # ---- rollout (collect_rollout, algo.hpp:121-191) ----
         self.sim.set_state(self.x0, self.v0, self.F0, self.C0, self.mat, self.grp)
         torch.cuda.synchronize()
@@ -216,7 +216,7 @@ class SapoTrainer:
         self.alpha_opt.zero_grad(set_to_none=True)
         self.log_alpha.grad = torch.tensor(alpha * gap, device=self.dev)
         self.alpha_opt.step()
-        alpha = float(self.log_alpha.exp())
+        alpha = float(self.log_alpha.detach().exp())
         # ---- critics: soft TD(lambda) targets + K full-batch passes (algo.hpp:243-327) ----
         with torch.no_grad():
             obs_all = self.obs[:, :, 7:7 + 64].detach()  # [H+1, E, 64]

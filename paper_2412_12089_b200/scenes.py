@@ -174,6 +174,46 @@ def lattice(org, counts, spacing):
     return np.asarray(org, dtype=np.float64) + pts * np.asarray(spacing, dtype=np.float64)
 
 
+def lattice_reset_spec(origin, counts, spacing, origin_draws=0, origin_range=(0.0, 0.0), jitter=(0.0, 0.0),
+                       velocity_sigma=0.0, material=0, group=0):
+    """Reset descriptor of a seeded lattice env (include/diffmpm.h DmLatticeReset)."""
+    return {"origin": tuple(float(a) for a in origin), "counts": tuple(int(c) for c in counts),
+            "spacing": tuple(float(a) for a in spacing), "origin_draws": int(origin_draws),
+            "origin_range": tuple(float(a) for a in origin_range), "jitter": tuple(float(a) for a in jitter),
+            "velocity_sigma": float(velocity_sigma), "material": int(material), "group": int(group)}
+
+
+def lattice_reset_host(spec, seed, env_offset, n_envs):
+    """Host generator of dm_reset_lattice (the device kernel restates it
+    bit-for-bit): per env the stream RngStream(seed, env_offset + e) draws the
+    origin offsets, then per-particle jitter (3 per particle), then Box-Muller
+    velocities (env.hpp:66-96, mpm.hpp:371-395, rng.hpp:11-55).  Returns
+    x [E,N,3] (float64), v [E,N,3], origin deltas [E,3]."""
+    cnt = spec["counts"]
+    N = cnt[0] * cnt[1] * cnt[2]
+    i, j, k = np.meshgrid(np.arange(cnt[0]), np.arange(cnt[1]), np.arange(cnt[2]), indexing="ij")
+    ijk = np.stack([i.ravel(), j.ravel(), k.ravel()], axis=1).astype(np.float64)
+    lo, hi = spec["origin_range"]
+    jlo, jhi = spec["jitter"]
+    xs, vs, ds = [], [], []
+    for e in range(n_envs):
+        r = RngStream(seed, env_offset + e)
+        d = np.zeros(3)
+        nd = spec["origin_draws"]
+        if nd:
+            d[:nd] = r.uniform(lo, hi, nd)
+        x = (np.asarray(spec["origin"]) + d) + (ijk + 0.5) * np.asarray(spec["spacing"])
+        if jhi > jlo:
+            x = x + r.uniform(jlo, jhi, 3 * N).reshape(N, 3)
+        v = np.zeros((N, 3))
+        if spec["velocity_sigma"] != 0.0:
+            v = spec["velocity_sigma"] * r.normals(3 * N).reshape(N, 3)
+        xs.append(x)
+        vs.append(v)
+        ds.append(d)
+    return np.stack(xs), np.stack(vs), np.stack(ds)
+
+
 def kmeans_groups(pts, k, rng: RngStream, iters=20):
     """Seeded Lloyd k-means over rest positions; init = k distinct draws."""
     n = pts.shape[0]
@@ -210,16 +250,10 @@ def config1(seed=0, n_envs=1, env_offset=0, n_sub=50):
     cell jitter, 32^3 grid, fixed-corotated E=1e4 nu=0.3 rho=1, sticky box,
     dt=1e-4, 50 substeps, v0 ~ N(0, 0.5) per particle, loss |com - (0.5,0.4,0.5)|^2."""
     dx = 1.0 / 32
-    base = lattice((0.3, 0.3, 0.3), (16, 16, 16), (0.2 / 16,) * 3)
-    N = base.shape[0]
-    xs, vs = [], []
-    for e in range(n_envs):
-        r = RngStream(seed, env_offset + e)
-        jit = r.uniform(-0.25 * dx, 0.25 * dx, 3 * N).reshape(N, 3)
-        xs.append(base + jit)
-        vs.append(0.5 * r.normals(3 * N).reshape(N, 3))
-    x = np.stack(xs)
-    v = np.stack(vs)
+    spec = lattice_reset_spec((0.3, 0.3, 0.3), (16, 16, 16), (0.2 / 16,) * 3, jitter=(-0.25 * dx, 0.25 * dx),
+                              velocity_sigma=0.5)
+    x, v, _ = lattice_reset_host(spec, seed, env_offset, n_envs)
+    N = x.shape[1]
     mats = [{"kind": "fixed_corotated", "E": 1e4, "nu": 0.3, "rho": 1.0, "volume": 0.2 ** 3 / N}]
     sim = {"dims": (32, 32, 32), "dx": dx, "dt": 1e-4, "gravity": GRAVITY, "boundary": "sticky",
            "alpha_c": 100.0, "mu_b": 0.0}
@@ -227,7 +261,7 @@ def config1(seed=0, n_envs=1, env_offset=0, n_sub=50):
                  {"kind": "com_target", "target": (0.5, 0.4, 0.5)},
                  x, v, _identity_F(n_envs, N), np.zeros((n_envs, N, 9)),
                  np.zeros((n_envs, N), np.int32), np.zeros((n_envs, N), np.int32),
-                 np.zeros((n_envs, 1, 1)), Task(), 0, env_offset)
+                 np.zeros((n_envs, 1, 1)), Task(), 0, env_offset, {"reset": spec, "seed": seed})
 
 
 def config2(seed=0, n_envs=32, env_offset=0, n_ctrl=32, n_sub=16):
@@ -242,6 +276,7 @@ def config2(seed=0, n_envs=32, env_offset=0, n_ctrl=32, n_sub=16):
     org = (0.5 - size[0] / 2, 0.5 - size[1] / 2, 3.5 * dx)
     base = lattice(org, cnt, (h, h, h))
     N = base.shape[0]
+    spec = lattice_reset_spec(org, cnt, (h, h, h))
     groups = kmeans_groups(base, 8, RngStream(seed, 1 << 40))
     acts = np.stack([RngStream(seed, env_offset + e).uniform(-1.0, 1.0, n_ctrl * 8).reshape(n_ctrl, 8)
                      for e in range(n_envs)])
@@ -254,7 +289,7 @@ def config2(seed=0, n_envs=32, env_offset=0, n_ctrl=32, n_sub=16):
     return Scene("cfg2_softjumper", n_envs, N, sim, mats, [], n_ctrl, n_sub, {"kind": "neg_mean_z"},
                  x, np.zeros((n_envs, N, 3)), _identity_F(n_envs, N), np.zeros((n_envs, N, 9)),
                  np.zeros((n_envs, N), np.int32), np.broadcast_to(groups, (n_envs, N)).astype(np.int32).copy(),
-                 acts, ActuationTask(8), 0, env_offset)
+                 acts, ActuationTask(8), 0, env_offset, {"reset": spec, "seed": seed, "particle_group": groups})
 
 
 def config3(seed=0, n_envs=256, env_offset=0, n_ctrl=24, n_sub=20, n_per_env=30000):
@@ -311,14 +346,13 @@ def config4(seed=0, n_envs=1024, env_offset=0, n_ctrl=16, n_sub=32, lattice_coun
     half = 0.15
     cnt = np.array(lattice_counts)
     spacing = np.array([2 * half, 2 * half, half]) / cnt
-    xs, c0 = [], []
-    for e in range(n_envs):
-        r = RngStream(seed, env_offset + e)
-        jit = r.uniform(-0.01, 0.01, 2)
-        c = np.array([0.5 + jit[0], 0.5 + jit[1], 0.15 + half])  # cavity center; floor at z=0.15
-        c0.append(c)
-        xs.append(lattice((c[0] - half, c[1] - half, 0.15), cnt, spacing))
-    x = np.stack(xs)
+    # per env the lattice origin (and the container) is offset by two draws
+    # U[-0.01, 0.01) from the env's stream; cavity floor at z = 0.15
+    spec = lattice_reset_spec((0.5 - half, 0.5 - half, 0.15), cnt, spacing, origin_draws=2,
+                              origin_range=(-0.01, 0.01))
+    x, _, d = lattice_reset_host(spec, seed, env_offset, n_envs)
+    org = np.asarray(spec["origin"]) + d
+    c0 = [np.array([o[0] + half, o[1] + half, 0.15 + half]) for o in org]  # cavity center
     N = x.shape[1]
     acts = np.stack([RngStream(seed, env_offset + e).uniform(-1.0, 1.0, 2 + n_ctrl * 3)[2:].reshape(n_ctrl, 3)
                      for e in range(n_envs)])
@@ -334,7 +368,8 @@ def config4(seed=0, n_envs=1024, env_offset=0, n_ctrl=16, n_sub=32, lattice_coun
             "tier_threshold": 0.02, "tier_low": 1.0, "tier_high": 2.0}
     return Scene("cfg4_fluidmove", n_envs, N, sim, mats, cols, n_ctrl, n_sub, loss,
                  x, np.zeros((n_envs, N, 3)), _identity_F(n_envs, N), np.zeros((n_envs, N, 9)),
-                 np.zeros((n_envs, N), np.int32), np.zeros((n_envs, N), np.int32), acts, task, 0, env_offset)
+                 np.zeros((n_envs, N), np.int32), np.zeros((n_envs, N), np.int32), acts, task, 0, env_offset,
+                 {"reset": spec, "seed": seed})
 
 
 CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4}

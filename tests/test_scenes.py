@@ -96,3 +96,38 @@ def test_loss_gradient_fd_and_torch(spec):
         assert abs(d[idx] - fd) < 1e-5 * max(1, abs(fd))
     Lt, dt = loss_and_dobs_torch(spec, torch.tensor(obs))
     assert np.allclose(Lt.numpy(), L) and np.allclose(dt.numpy(), d, atol=1e-6)
+
+
+def test_lattice_reset_host_matches_direct_restatement():
+    """scenes.lattice_reset_host (the host twin of the device reset
+    dm_reset_lattice) against a direct restatement of the draws: cfg1's
+    jittered lattice + Box-Muller velocities and cfg4's origin-offset lattice,
+    bit for bit (env.hpp:66-96, mpm.hpp:371-395, rng.hpp:11-55)."""
+    from paper_2412_12089_b200.rng import RngStream
+    dx = 1.0 / 32
+    sc = scenes.config1(seed=7, n_envs=2, env_offset=3)
+    base = scenes.lattice((0.3, 0.3, 0.3), (16, 16, 16), (0.2 / 16,) * 3)
+    N = base.shape[0]
+    for e in range(2):
+        r = RngStream(7, 3 + e)
+        jit = r.uniform(-0.25 * dx, 0.25 * dx, 3 * N).reshape(N, 3)
+        assert np.array_equal(sc.x[e], base + jit)
+        assert np.array_equal(sc.v[e], 0.5 * r.normals(3 * N).reshape(N, 3))
+    sc4 = scenes.config4(seed=2, n_envs=3, n_ctrl=2, n_sub=4, lattice_counts=(4, 4, 2))
+    half = 0.15
+    for e in range(3):
+        r = RngStream(2, e)
+        d = r.uniform(-0.01, 0.01, 2)
+        org = np.array([0.5 - half, 0.5 - half, 0.15]) + np.array([d[0], d[1], 0.0])
+        assert np.array_equal(sc4.x[e], scenes.lattice(org, (4, 4, 2), np.array([0.3, 0.3, 0.15]) / (4, 4, 2)))
+        assert np.allclose(sc4.task.center0[e][:2], org[:2] + half, rtol=0, atol=1e-15)
+
+
+def test_lattice_reset_draw_order_shares_the_action_stream():
+    """cfg4: the origin draws come first in the env's stream, the per-step
+    actions continue after them (one stream per env, env.hpp:71)."""
+    from paper_2412_12089_b200.rng import RngStream
+    sc = scenes.config4(seed=5, n_envs=2, n_ctrl=3, n_sub=4, lattice_counts=(4, 4, 2))
+    for e in range(2):
+        u = RngStream(5, e).uniform(-1.0, 1.0, 2 + 9)
+        assert np.array_equal(sc.actions[e], u[2:].reshape(3, 3))
