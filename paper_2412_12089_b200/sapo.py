@@ -27,6 +27,7 @@ import torch.nn as nn
 import torch.nn.functional as Fn
 
 from . import api, scenes
+from .rng import RngStream
 
 K_LOG_SQRT_2PI = 0.9189385332046727
 
@@ -90,6 +91,7 @@ class SapoTrainer:
                  hidden=(256, 256, 256), dist=None, device=0, gamma=0.99, lam=0.95, actor_lr=2e-3, critic_lr=5e-4,
                  alpha_lr=5e-3, init_alpha=1.0, total_iterations=100):
         self.dist = dist
+        self.seed, self.env_offset = seed, env_offset
         self.dev = torch.device("cuda", device)
         self.scene = scenes.config2(seed=seed, n_envs=n_envs, env_offset=env_offset, n_ctrl=horizon, n_sub=n_sub)
         self.scene.extra["obs_groups"] = 8
@@ -124,6 +126,12 @@ class SapoTrainer:
         self.noise_gen = torch.Generator(device=self.dev).manual_seed(seed * 1000003 + env_offset)
         self.obs = torch.zeros((self.H + 1, self.E, self.od), device=self.dev)
         self.stream = torch.cuda.ExternalStream(self.sim.stream_ptr, device=self.dev)
+
+    def env_rng(self, i):
+        """(key, counter) of env i's RngStream(seed, global index) (env.hpp:71):
+        the config-2 reset draws nothing from it."""
+        r = RngStream(self.seed, self.env_offset + i)
+        return int(r.key), int(r.counter)
 
     # ---- collectives (NCCL) ----
     def _allreduce_grads(self, params):
@@ -233,8 +241,8 @@ class SapoTrainer:
                 self._allreduce_grads(list(c.parameters()))
                 torch.nn.utils.clip_grad_norm_(c.parameters(), 0.5)
                 opt.step()
-                closs += float(lc)
+                closs += float(lc.detach())
         self.iter += 1
         ret_mean = self._allreduce_scalar(float(ret.detach().sum())) / self.n_global
-        return {"actor_loss": self._allreduce_scalar(float(loss)), "critic_loss": closs / 2, "return_mean": ret_mean,
+        return {"actor_loss": self._allreduce_scalar(float(loss.detach())), "critic_loss": closs / 2, "return_mean": ret_mean,
                 "alpha": alpha, "entropy_mean": gap + self.ent_target, "grad_norm": float(gnorm)}

@@ -104,3 +104,28 @@ def test_sapo_iteration_runs():
     assert s1["grad_norm"] > 0
     moved = sum(float((p - q).abs().sum()) for p, q in zip(tr.actor.parameters(), p0))
     assert moved > 0
+
+
+def test_sapo_checkpoint_resume_bitwise(tmp_path):
+    """Trainer persistence in the DSIMCKPT container (checkpoint_io.hpp:140-205):
+    run 2 iterations, save, run 2 more; a fresh trainer restored from the file
+    runs the same 2 iterations bit for bit (test_cli.cpp:130-151)."""
+    import torch
+    from paper_2412_12089_b200 import ckpt
+    from paper_2412_12089_b200.sapo import SapoTrainer
+    kw = dict(seed=1, n_envs=3, horizon=3, n_sub=4, critic_passes=2, hidden=(32, 32, 32))
+    a = SapoTrainer(**kw)
+    a.iteration()
+    a.iteration()
+    path = str(tmp_path / "trainer.ckpt")
+    ckpt.save_checkpoint(ckpt.snapshot_trainer(a), path)
+    ra = [a.iteration(), a.iteration()]
+    torch.manual_seed(123)  # different network init: parameters must come from the file
+    b = SapoTrainer(**kw)
+    ckpt.restore_trainer(b, ckpt.load_checkpoint(path))
+    rb = [b.iteration(), b.iteration()]
+    assert ra == rb
+    for p, q in zip(list(a.actor.parameters()) + list(a.critics.parameters()),
+                    list(b.actor.parameters()) + list(b.critics.parameters())):
+        assert torch.equal(p, q)
+    assert float(a.log_alpha) == float(b.log_alpha) and a.iter == b.iter == 4
