@@ -918,8 +918,11 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
 // cotangents (sorted position) and a 6^3 block of node-velocity cotangents.
 // The next chunk's gathered (x, F) loads are in flight during the current
 // chunk's scatter.
+#ifndef DM_G2PADJ_MINB
+#define DM_G2PADJ_MINB 3
+#endif
 template <int LAW, int NM>
-__global__ void __launch_bounds__(kWarps * 32, 3) k_g2p_adj(DevParams P, StateView S, StateView Sn, const float* __restrict__ adj_in,
+__global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevParams P, StateView S, StateView Sn, const float* __restrict__ adj_in,
                                                          size_t astride, const int* __restrict__ perm,
                                                          const int* __restrict__ tile_start,
                                                          const int* __restrict__ tile_count,

@@ -492,8 +492,11 @@ DM_HD_NOINLINE v3<R> collider_query_vjp(const Col<R>& col, v3<R> p, R dbar, v3<R
       const v3<R> hc = mk3(col.half.x, col.half.y, col.half.z + R(1));
       const BoxQ<R> bo = box_query(ro, ho);
       const BoxQ<R> bc = box_query(rc, hc);
-      if (bo.d >= -bc.d) return box_query_vjp(bo, ro, dbar, nbar);
-      return box_query_vjp(bc, rc, -dbar, -nbar);
+      // one inlined vjp on the active branch (outer box, or the cavity with
+      // negated cotangents) keeps the code compact
+      const bool outer = bo.d >= -bc.d;
+      const R sg = outer ? R(1) : R(-1);
+      return box_query_vjp(outer ? bo : bc, outer ? ro : rc, sg * dbar, nbar * sg);
     }
   }
 }
