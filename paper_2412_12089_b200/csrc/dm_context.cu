@@ -102,7 +102,8 @@ bool dalloc(DmContext* ctx, T** p, size_t n) {
   return true;
 }
 
-size_t state_floats(const DmContext* c) { return 24 * c->Ntot; }
+// state buffers hold 24 floats per particle, Ntot rounded up to 32 (AoSoA blocks)
+size_t state_floats(const DmContext* c) { return 24 * ((c->Ntot + 31) / 32 * 32); }
 
 StateView view(float* f, uint32_t* a, size_t stride) {
   StateView s;
@@ -436,7 +437,7 @@ int get_state_impl(DmContext* ctx, float* x, float* v, float* F, float* C, cudaM
   const int s = ctx->steps * ctx->cfg.substeps;
   const StateView S = fwd_state(ctx, s);
   float* out = ctx->adj[1];
-  k_soa_to_aos<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>((int)N, ctx->P.N, S.f, S.attr, N, out,
+  k_soa_to_aos<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>((int)N, ctx->P.N, S.f, S.attr, N, 1, out,
                                                                      out + 3 * N, out + 6 * N, out + 15 * N);
   ++ctx->launches;
   if (x) DM_CUDA(cudaMemcpyAsync(x, out, 3 * N * sizeof(float), kind, ctx->stream));
@@ -612,7 +613,7 @@ int backward_end(DmContext* ctx, float* dx0, float* dv0, float* dF0, float* dC0,
   const size_t N = ctx->Ntot;
   float* out = ctx->adj[cur ^ 1];
   const StateView S0 = store_view(ctx, 0);
-  k_soa_to_aos<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>((int)N, ctx->P.N, ctx->adj[cur], S0.attr, N, out,
+  k_soa_to_aos<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>((int)N, ctx->P.N, ctx->adj[cur], S0.attr, N, 0, out,
                                                                      out + 3 * N, out + 6 * N, out + 15 * N);
   ++ctx->launches;
   if (dx0) DM_CUDA(cudaMemcpyAsync(dx0, out, 3 * N * sizeof(float), kout, ctx->stream));
@@ -762,18 +763,18 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   const int Kc = P.K > 0 ? P.K : 1, Gc = P.G > 0 ? P.G : 1;
   ctx->n_store = cfg->max_steps * cfg->substeps / ck + 1;
   bool ok = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) == cudaSuccess;
-  ok = ok && dalloc(ctx, &ctx->store, (size_t)ctx->n_store * 24 * N) &&
+  ok = ok && dalloc(ctx, &ctx->store, (size_t)ctx->n_store * state_floats(ctx)) &&
        dalloc(ctx, &ctx->store_attr, (size_t)ctx->n_store * N);
-  if (ck > 1) ok = ok && dalloc(ctx, &ctx->seg, (size_t)(ck - 1) * 24 * N) && dalloc(ctx, &ctx->seg_attr, (size_t)(ck - 1) * N);
+  if (ck > 1) ok = ok && dalloc(ctx, &ctx->seg, (size_t)(ck - 1) * state_floats(ctx)) && dalloc(ctx, &ctx->seg_attr, (size_t)(ck - 1) * N);
   if (ck > 1)
     for (int i = 0; i < 2; ++i)
-      ok = ok && dalloc(ctx, &ctx->scratch[i], 24 * N) && dalloc(ctx, &ctx->scratch_attr[i], N);
+      ok = ok && dalloc(ctx, &ctx->scratch[i], state_floats(ctx)) && dalloc(ctx, &ctx->scratch_attr[i], N);
   ok = ok && dalloc(ctx, &ctx->adj[0], 24 * N) && dalloc(ctx, &ctx->adj[1], 24 * N) && dalloc(ctx, &ctx->part, 12 * N);
   ok = ok && dalloc(ctx, &ctx->keys, N) && dalloc(ctx, &ctx->ptile, N) &&
        dalloc(ctx, &ctx->perm_all, (size_t)ck * N) && dalloc(ctx, &ctx->tstart_all, (size_t)ck * TT) &&
        dalloc(ctx, &ctx->tcount_all, (size_t)ck * TT) && dalloc(ctx, &ctx->active_all, (size_t)ck * TT) &&
        dalloc(ctx, &ctx->abase_all, (size_t)ck * P.E) && dalloc(ctx, &ctx->acount_all, (size_t)ck * P.E) &&
-       dalloc(ctx, &ctx->nact_all, (size_t)ck) && dalloc(ctx, &ctx->tail, 24 * N) && dalloc(ctx, &ctx->tail_attr, N);
+       dalloc(ctx, &ctx->nact_all, (size_t)ck) && dalloc(ctx, &ctx->tail, state_floats(ctx)) && dalloc(ctx, &ctx->tail_attr, N);
   const size_t NN = (size_t)P.E * P.dims[0] * P.dims[1] * P.dims[2];
   ok = ok && dalloc(ctx, &ctx->gmp, NN) && dalloc(ctx, &ctx->gv, NN) && dalloc(ctx, &ctx->gmb, NN);
   ok = ok && dalloc(ctx, &ctx->blocks, TT * kExt3) && dalloc(ctx, &ctx->ablocks, TT * kExt3) &&

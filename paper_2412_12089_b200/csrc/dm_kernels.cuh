@@ -50,11 +50,27 @@ struct DevParams {
   ColShape shape[4];
 };
 
+// Particle-state layout: DM_AOSOA (default) stores blocks of 32 particles
+// with their 24 fields contiguous ([i/32][24][32]: a warp's access to one
+// field is one 128-byte segment, a particle's state one 3 KB region);
+// otherwise plain SoA [24][Ntot].  Allocations round Ntot up to 32.
+#ifndef DM_AOSOA
+#define DM_AOSOA 1
+#endif
+__host__ __device__ __forceinline__ size_t state_index(int comp, size_t i, size_t stride) {
+#if DM_AOSOA
+  (void)stride;
+  return ((i >> 5) * 24 + comp) * 32 + (i & 31);
+#else
+  return comp * stride + i;
+#endif
+}
+
 struct StateView {
   float* f;
   uint32_t* attr;
   size_t stride;
-  __device__ __forceinline__ float& c(int comp, size_t i) const { return f[comp * stride + i]; }
+  __device__ __forceinline__ float& c(int comp, size_t i) const { return f[state_index(comp, i, stride)]; }
 };
 
 struct DevFlags {
@@ -1127,7 +1143,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
     // particle-side cotangents at the sorted slot, and the perm index itself)
     auto stage = [&](int c0, int src) {
 #pragma unroll
-      for (int f = 0; f < 24; ++f) cp_async4(sg + f * 32 + lane, S.f + f * S.stride + src);
+      for (int f = 0; f < 24; ++f) cp_async4(sg + f * 32 + lane, &S.c(f, src));
       cp_async4(sg + 24 * 32 + lane, S.attr + src);
 #pragma unroll
       for (int f = 0; f < 12; ++f) cp_async4(sg + (25 + f) * 32 + lane, part + f * astride + row + c0 + lane);
@@ -1573,7 +1589,7 @@ __global__ void k_aos_to_soa(int Ntot, const float* __restrict__ x, const float*
 
 // physical SoA -> canonical AoS (original order within each env)
 __global__ void k_soa_to_aos(int Ntot, int N, const float* __restrict__ f, const uint32_t* __restrict__ attr,
-                             size_t stride, float* __restrict__ x, float* __restrict__ v, float* __restrict__ F,
+                             size_t stride, int state_layout, float* __restrict__ x, float* __restrict__ v, float* __restrict__ F,
                              float* __restrict__ C) {
   const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (i >= (size_t)Ntot) return;
@@ -1581,13 +1597,13 @@ __global__ void k_soa_to_aos(int Ntot, int N, const float* __restrict__ f, const
   const size_t o = e * N + (attr[i] & 0xFFFFFu);
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    if (x) x[3 * o + a] = f[a * stride + i];
-    if (v) v[3 * o + a] = f[(3 + a) * stride + i];
+    if (x) x[3 * o + a] = f[state_layout ? state_index(a, i, stride) : a * stride + i];
+    if (v) v[3 * o + a] = f[state_layout ? state_index(3 + a, i, stride) : (3 + a) * stride + i];
   }
 #pragma unroll
   for (int q = 0; q < 9; ++q) {
-    if (F) F[9 * o + q] = f[(6 + q) * stride + i];
-    if (C) C[9 * o + q] = f[(15 + q) * stride + i];
+    if (F) F[9 * o + q] = f[state_layout ? state_index(6 + q, i, stride) : (6 + q) * stride + i];
+    if (C) C[9 * o + q] = f[state_layout ? state_index(15 + q, i, stride) : (15 + q) * stride + i];
   }
 }
 
