@@ -539,7 +539,7 @@ int backward_begin(DmContext* ctx, const float* dfx, const float* dfv, const flo
         dfC ? stg + 15 * N : nullptr, Sf.attr, A, N);
     ++ctx->launches;
   } else {
-    DM_CUDA(cudaMemsetAsync(A, 0, 24 * N * sizeof(float), ctx->stream));
+    DM_CUDA(cudaMemsetAsync(A, 0, state_floats(ctx) * sizeof(float), ctx->stream));
   }
   ctx->bwd_t = T - 1;
   return DM_OK;
@@ -613,7 +613,7 @@ int backward_end(DmContext* ctx, float* dx0, float* dv0, float* dF0, float* dC0,
   const size_t N = ctx->Ntot;
   float* out = ctx->adj[cur ^ 1];
   const StateView S0 = store_view(ctx, 0);
-  k_soa_to_aos<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>((int)N, ctx->P.N, ctx->adj[cur], S0.attr, N, 0, out,
+  k_soa_to_aos<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>((int)N, ctx->P.N, ctx->adj[cur], S0.attr, N, 1, out,
                                                                      out + 3 * N, out + 6 * N, out + 15 * N);
   ++ctx->launches;
   if (dx0) DM_CUDA(cudaMemcpyAsync(dx0, out, 3 * N * sizeof(float), kout, ctx->stream));
@@ -769,7 +769,8 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   if (ck > 1)
     for (int i = 0; i < 2; ++i)
       ok = ok && dalloc(ctx, &ctx->scratch[i], state_floats(ctx)) && dalloc(ctx, &ctx->scratch_attr[i], N);
-  ok = ok && dalloc(ctx, &ctx->adj[0], 24 * N) && dalloc(ctx, &ctx->adj[1], 24 * N) && dalloc(ctx, &ctx->part, 12 * N);
+  ok = ok && dalloc(ctx, &ctx->adj[0], state_floats(ctx)) && dalloc(ctx, &ctx->adj[1], state_floats(ctx)) &&
+       dalloc(ctx, &ctx->part, state_floats(ctx) / 2);
   ok = ok && dalloc(ctx, &ctx->keys, N) && dalloc(ctx, &ctx->ptile, N) &&
        dalloc(ctx, &ctx->perm_all, (size_t)ck * N) && dalloc(ctx, &ctx->tstart_all, (size_t)ck * TT) &&
        dalloc(ctx, &ctx->tcount_all, (size_t)ck * TT) && dalloc(ctx, &ctx->active_all, (size_t)ck * TT) &&

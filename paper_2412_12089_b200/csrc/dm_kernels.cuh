@@ -66,6 +66,20 @@ __host__ __device__ __forceinline__ size_t state_index(int comp, size_t i, size_
 #endif
 }
 
+// Adjoint buffers share the layout: the state cotangent (24 fields) like the
+// state, the particle-side partial cotangents (12 fields) in blocks of 32 x 12.
+__host__ __device__ __forceinline__ size_t adj_index(int comp, size_t i, size_t stride) {
+  return state_index(comp, i, stride);
+}
+__host__ __device__ __forceinline__ size_t part_index(int comp, size_t i, size_t stride) {
+#if DM_AOSOA
+  (void)stride;
+  return ((i >> 5) * 12 + comp) * 32 + (i & 31);
+#else
+  return comp * stride + i;
+#endif
+}
+
 struct StateView {
   float* f;
   uint32_t* attr;
@@ -991,13 +1005,13 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
           const float4 q = vw[((lb[0] + i) * kExt + (lb[1] + j)) * kExt + lb[2] + k];
           return mk3(q.x, q.y, q.z);
         };
-        v3<float> xb = mk3(adj_in[0 * astride + dst], adj_in[1 * astride + dst], adj_in[2 * astride + dst]);
-        v3<float> vb = mk3(adj_in[3 * astride + dst], adj_in[4 * astride + dst], adj_in[5 * astride + dst]);
+        v3<float> xb = mk3(adj_in[adj_index(0, dst, astride)], adj_in[adj_index(1, dst, astride)], adj_in[adj_index(2, dst, astride)]);
+        v3<float> vb = mk3(adj_in[adj_index(3, dst, astride)], adj_in[adj_index(4, dst, astride)], adj_in[adj_index(5, dst, astride)]);
         m3<float> Fb, Cb;
 #pragma unroll
         for (int q = 0; q < 9; ++q) {
-          Fb.a[q] = adj_in[(6 + q) * astride + dst];
-          Cb.a[q] = adj_in[(15 + q) * astride + dst];
+          Fb.a[q] = adj_in[adj_index(6 + q, dst, astride)];
+          Cb.a[q] = adj_in[adj_index(15 + q, dst, astride)];
         }
         v3<float> xp, gq;
         m3<float> Fp, Bd;
@@ -1012,11 +1026,11 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
 #pragma unroll
         for (int m = 0; m < NM; ++m)
           if (m == mi) mub[m] += mu_l;
-        part[0 * astride + dst] = xp.x;
-        part[1 * astride + dst] = xp.y;
-        part[2 * astride + dst] = xp.z;
+        part[part_index(0, dst, astride)] = xp.x;
+        part[part_index(1, dst, astride)] = xp.y;
+        part[part_index(2, dst, astride)] = xp.z;
 #pragma unroll
-        for (int q = 0; q < 9; ++q) part[(3 + q) * astride + dst] = Fp.a[q];
+        for (int q = 0; q < 9; ++q) part[part_index(3 + q, dst, astride)] = Fp.a[q];
         stage_payload(pw + lane * kPay, (lb[0] * kExt + lb[1]) * kExt + lb[2], sc, 0.f, gq, Bd);
       }
       __syncwarp();
@@ -1146,7 +1160,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
       for (int f = 0; f < 24; ++f) cp_async4(sg + f * 32 + lane, &S.c(f, src));
       cp_async4(sg + 24 * 32 + lane, S.attr + src);
 #pragma unroll
-      for (int f = 0; f < 12; ++f) cp_async4(sg + (25 + f) * 32 + lane, part + f * astride + row + c0 + lane);
+      for (int f = 0; f < 12; ++f) cp_async4(sg + (25 + f) * 32 + lane, part + part_index(f, row + c0 + lane, astride));
       sg[37 * 32 + lane] = __int_as_float(src);
     };
     int s1 = 32 + lane < cnt ? perm[row + 32 + lane] : 0;  // perm two chunks ahead, parity slots
@@ -1211,16 +1225,16 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
 #pragma unroll
       for (int q = 0; q < NG; ++q)
         if (q == gi) actb[q] += ac_l;
-      adj_out[0 * astride + src] = xb.x;
-      adj_out[1 * astride + src] = xb.y;
-      adj_out[2 * astride + src] = xb.z;
-      adj_out[3 * astride + src] = vb.x;
-      adj_out[4 * astride + src] = vb.y;
-      adj_out[5 * astride + src] = vb.z;
+      adj_out[adj_index(0, src, astride)] = xb.x;
+      adj_out[adj_index(1, src, astride)] = xb.y;
+      adj_out[adj_index(2, src, astride)] = xb.z;
+      adj_out[adj_index(3, src, astride)] = vb.x;
+      adj_out[adj_index(4, src, astride)] = vb.y;
+      adj_out[adj_index(5, src, astride)] = vb.z;
 #pragma unroll
       for (int q = 0; q < 9; ++q) {
-        adj_out[(6 + q) * astride + src] = Fb.a[q];
-        adj_out[(15 + q) * astride + src] = Cb.a[q];
+        adj_out[adj_index(6 + q, src, astride)] = Fb.a[q];
+        adj_out[adj_index(15 + q, src, astride)] = Cb.a[q];
       }
     }
 #pragma unroll
@@ -1418,7 +1432,7 @@ __global__ void __launch_bounds__(256) k_obs_adj(DevParams P, StateView S, const
       }
     }
 #pragma unroll
-    for (int a = 0; a < 3; ++a) adj[a * astride + base + p] += (float)g[a];
+    for (int a = 0; a < 3; ++a) adj[adj_index(a, base + p, astride)] += (float)g[a];
   }
   if (spill) {
     gcx = block_sum(gcx, sh);
@@ -1458,10 +1472,10 @@ __global__ void __launch_bounds__(256) k_obs_adj(DevParams P, StateView S, const
       for (int a = 0; a < 3; ++a) {
         double gx = og[a] / n;
         if (a == 2) gx += og[6] * 2.0 * ((double)S.c(2, i) - mz) / n;
-        adj[a * astride + i] += (float)gx;
+        adj[adj_index(a, i, astride)] += (float)gx;
         double gv = og[3 + a] / n;
         if (vn > 0.0) gv += og[7] * vv[a] / (vn * n);
-        adj[(3 + a) * astride + i] += (float)gv;
+        adj[adj_index(3 + a, i, astride)] += (float)gv;
       }
     }
   }
@@ -1617,13 +1631,13 @@ __global__ void k_aos_to_soa_perm(int Ntot, int N, const float* __restrict__ x, 
   const size_t o = e * N + (attr[i] & 0xFFFFFu);
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    f[a * stride + i] = x ? x[3 * o + a] : 0.f;
-    f[(3 + a) * stride + i] = v ? v[3 * o + a] : 0.f;
+    f[adj_index(a, i, stride)] = x ? x[3 * o + a] : 0.f;
+    f[adj_index(3 + a, i, stride)] = v ? v[3 * o + a] : 0.f;
   }
 #pragma unroll
   for (int q = 0; q < 9; ++q) {
-    f[(6 + q) * stride + i] = F ? F[9 * o + q] : 0.f;
-    f[(15 + q) * stride + i] = C ? C[9 * o + q] : 0.f;
+    f[adj_index(6 + q, i, stride)] = F ? F[9 * o + q] : 0.f;
+    f[adj_index(15 + q, i, stride)] = C ? C[9 * o + q] : 0.f;
   }
 }
 
