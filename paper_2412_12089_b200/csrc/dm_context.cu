@@ -102,8 +102,8 @@ bool dalloc(DmContext* ctx, T** p, size_t n) {
   return true;
 }
 
-// state buffers hold 24 floats per particle, Ntot rounded up to 32 (AoSoA blocks)
-size_t state_floats(const DmContext* c) { return 24 * ((c->Ntot + 31) / 32 * 32); }
+// state buffers hold 24 floats per particle, Ntot rounded up to the AoSoA block
+size_t state_floats(const DmContext* c) { return 24 * ((c->Ntot + kAB - 1) / kAB * kAB); }
 
 StateView view(float* f, uint32_t* a, size_t stride) {
   StateView s;

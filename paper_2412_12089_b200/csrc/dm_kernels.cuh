@@ -57,10 +57,14 @@ struct DevParams {
 #ifndef DM_AOSOA
 #define DM_AOSOA 1
 #endif
+#ifndef DM_AOSOA_LOG2
+#define DM_AOSOA_LOG2 5  // particles per block = 32
+#endif
+constexpr size_t kAB = (size_t)1 << DM_AOSOA_LOG2;
 __host__ __device__ __forceinline__ size_t state_index(int comp, size_t i, size_t stride) {
 #if DM_AOSOA
   (void)stride;
-  return ((i >> 5) * 24 + comp) * 32 + (i & 31);
+  return ((i >> DM_AOSOA_LOG2) * 24 + comp) * kAB + (i & (kAB - 1));
 #else
   return comp * stride + i;
 #endif
@@ -74,7 +78,7 @@ __host__ __device__ __forceinline__ size_t adj_index(int comp, size_t i, size_t 
 __host__ __device__ __forceinline__ size_t part_index(int comp, size_t i, size_t stride) {
 #if DM_AOSOA
   (void)stride;
-  return ((i >> 5) * 12 + comp) * 32 + (i & 31);
+  return ((i >> DM_AOSOA_LOG2) * 12 + comp) * kAB + (i & (kAB - 1));
 #else
   return comp * stride + i;
 #endif
