@@ -272,13 +272,19 @@ def run_ours(args, scene, rank, world, local, dist):
     hcvo = [np.ascontiguousarray(pinned(cvo[:, t, :K])) for t in range(T)] if K else None
     hact = [np.ascontiguousarray(pinned(act[:, t, :G])) for t in range(T)] if G else None
 
+    # pinned output buffers for the host backward (D2H at full DMA rate)
+    hout = {"x": pinned(np.zeros((E, N, 3))), "v": pinned(np.zeros((E, N, 3))), "F": pinned(np.zeros((E, N, 9))),
+            "C": pinned(np.zeros((E, N, 9))), "cvo": pinned(np.zeros((T, E, K, 9))) if K else None,
+            "act": pinned(np.zeros((T, E, G))) if G else None,
+            "E": np.zeros((E, batch.n_materials), np.float64)}
+
     def rollout_host():
         batch.set_state(hx, hv, hF, hC, hmat, hgrp)
         obs = np.zeros((T, E, 7), np.float32)
         for t in range(T):
             obs[t] = batch.step(hcvo[t] if K else None, hact[t] if G else None)
         _, dobs = loss_and_dobs(scene.loss, np.transpose(obs, (1, 0, 2)))
-        return batch.backward(dobs=np.ascontiguousarray(np.transpose(dobs, (1, 0, 2)), dtype=np.float32))
+        return batch.backward(dobs=np.ascontiguousarray(np.transpose(dobs, (1, 0, 2)), dtype=np.float32), out=hout)
 
     h2d = (hx.nbytes + hv.nbytes + hF.nbytes + hC.nbytes + hmat.nbytes + hgrp.nbytes +
            (sum(a.nbytes for a in hcvo) if K else 0) + (sum(a.nbytes for a in hact) if G else 0) + T * E * 7 * 4)

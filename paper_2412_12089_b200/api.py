@@ -300,6 +300,13 @@ class MpmBatch:
         cotangents.  Returns a dict of cotangents (numpy) or fills torch `out`."""
         T = self.tape_steps
         dfinal = dfinal or {}
+        if out is not None and not any(_is_dev(a) for a in out.values()):
+            # host path into caller-provided (e.g. pinned) numpy buffers
+            d = _f32(dobs) if dobs is not None else None
+            fin = [_f32(dfinal.get(k)) for k in ("x", "v", "F", "C")]
+            self._check(self._L.dm_backward(self._h, _ptr(d), *(_ptr(a) for a in fin),
+                                            *(_ptr(out.get(k)) for k in ("x", "v", "F", "C", "cvo", "act", "E"))))
+            return out
         if out is not None:
             args = [out.get(k) for k in ("x", "v", "F", "C", "cvo", "act", "E")]
             self._check(self._L.dm_backward_device(self._h, _ptr(dobs), *(_ptr(dfinal.get(k)) for k in ("x", "v", "F", "C")),

@@ -96,6 +96,22 @@ def test_sort_bit_exact(seed):
         assert np.array_equal(perm[e], O.stable_sort(k_ref))
 
 
+def test_sort_bit_exact_wide_histograms():
+    """More than 65535 particles per env: the bin kernel switches from 16-bit
+    to 32-bit per-warp histograms / cursors; clustered positions put many
+    particles in one tile (long runs, full cursors)."""
+    rng = np.random.default_rng(11)
+    sim = dict(SIM16, dims=(48, 48, 48), dx=1 / 48)
+    n = 70000
+    st = random_block(rng, n, 0.3, 0.36)
+    b = gpu_batch(sim, [LAWS["fluid"]], [], [st], 1, 1)
+    b.set_state(stack([st], "x"), stack([st], "v"), stack([st], "F"), stack([st], "C"))
+    keys, perm = b.debug_sort()
+    k_ref = O.bin_keys(sim, st["x"].astype(np.float32))
+    assert np.array_equal(keys[0], k_ref)
+    assert np.array_equal(perm[0], O.stable_sort(k_ref))
+
+
 # ---------------- forward parity ----------------
 
 @pytest.mark.parametrize("law", list(LAWS))
