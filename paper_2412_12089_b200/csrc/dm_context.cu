@@ -50,6 +50,8 @@ struct DmContext {
   int *perm_all = nullptr, *tstart_all = nullptr, *tcount_all = nullptr;
   int *abase_all = nullptr, *acount_all = nullptr, *nact_all = nullptr;
   int4* active_all = nullptr;
+  int4* work_all = nullptr;
+  int* ord_all = nullptr;
   // per active tile (by slot) 6^3 grid blocks of the replayed substeps:
   // velocity and (mass, momentum), read by the adjoint substep instead of
   // re-running bin / p2g / grid
@@ -175,7 +177,9 @@ struct Slot {
   int* perm;
   int* tile_start;
   int* tile_count;
-  int4* active;
+  int4* active;  // env-ordered (k_bin)
+  int4* work;    // largest-first (k_order_*): the tile kernels' schedule
+  int* ord;      // bucket counters of k_order_*
   int* env_abase;
   int* env_acount;
   int* nact;
@@ -193,6 +197,8 @@ Slot slot(DmContext* c, int q) {
   s.tile_start = c->tstart_all + (size_t)q * TT;
   s.tile_count = c->tcount_all + (size_t)q * TT;
   s.active = c->active_all + (size_t)q * TT;
+  s.work = c->work_all + (size_t)q * TT;
+  s.ord = c->ord_all + (size_t)q * 2 * kOrdBuckets;
   s.env_abase = c->abase_all + (size_t)q * c->P.E;
   s.env_acount = c->acount_all + (size_t)q * c->P.E;
   s.nact = c->nact_all + q;
@@ -212,9 +218,13 @@ void launch_bin(DmContext* c, const StateView& S, const Slot& q, int sub, int ch
     k_bin<int><<<c->P.E, 32 * c->bin_warps, (size_t)c->bin_warps * c->P.Tn * 4, c->stream>>>(
         c->P, S, c->keys, c->ptile, q.tile_start, q.tile_count, q.active, q.env_abase, q.env_acount, c->flags, q.nact,
         sub, check_vmax);
+  cudaMemsetAsync(q.ord, 0, 2 * kOrdBuckets * sizeof(int), c->stream);
+  k_order_hist<<<64, 256, 0, c->stream>>>(q.active, q.nact, q.ord);
+  k_order_scatter<<<(unsigned)((c->P.E * c->P.Tn + 2047) / 2048), 256, 0, c->stream>>>(q.active, q.nact, q.ord, q.work);
+  c->launches += 2;
   wq_reset(c);
   k_cellsort<<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, c->ptile, q.perm, c->keys, q.tile_start,
-                                                           q.tile_count, q.active, q.nact, c->flags, c->wq);
+                                                           q.tile_count, q.work, q.nact, c->flags, c->wq);
   ++c->launches;
   PROF_END(c, 0);
   ++c->launches;
@@ -229,7 +239,7 @@ void launch_p2g(DmContext* c, const StateView& S, const Slot& q, int t, int sub)
   wq_reset(c);
   PROF_BEGIN(c, 1);
 #define L_P2G(LW)                                                                                               \
-  k_p2g<LW><<<c->grid_tiles, kWarps * 32, kP2gSmem, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.active, \
+  k_p2g<LW><<<c->grid_tiles, kWarps * 32, kP2gSmem, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.work, \
                                                           step_act(c, t), c->blocks, c->flags, q.nact, sub, c->wq)
   DM_LAW_DISPATCH(c, L_P2G);
 #undef L_P2G
@@ -257,7 +267,7 @@ void launch_grid(DmContext* c, const Slot& q, int t) {
   wq_reset(c);
   PROF_BEGIN(c, 9);
 #define L_GRID(MC, CK)                                                                                        \
-  k_grid<MC, CK><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.active, step_cvo(c, t), \
+  k_grid<MC, CK><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work, step_cvo(c, t), \
                                                                c->blocks, c->gmp, c->gv, q.nact, c->wq)
   DM_GRID_DISPATCH(c, L_GRID);
 #undef L_GRID
@@ -270,7 +280,7 @@ void launch_g2p(DmContext* c, const StateView& S, const StateView& So, const Slo
   PROF_BEGIN(c, 2);
 #define L_G2P(LW)                                                                                                \
   k_g2p<LW><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, q.perm, q.tile_start, q.tile_count,        \
-                                                          q.active, c->gv, c->flags, q.nact, sub, c->gmp,         \
+                                                          q.work, c->gv, c->flags, q.nact, sub, c->gmp,         \
                                                           dump ? q.gvb : nullptr, dump ? q.gmpb : nullptr, c->wq)
   DM_LAW_DISPATCH(c, L_G2P);
 #undef L_G2P
@@ -291,11 +301,11 @@ template <int LAW, int NG>
 void launch_p2g_adj(DmContext* c, const StateView& S, const Slot& q, int t, float* adj_out) {
   wq_reset(c);
   if (c->P.nmat == 1)
-    k_p2g_adj<LAW, NG, 1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.active,
+    k_p2g_adj<LAW, NG, 1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.work,
                                                               step_act(c, t), c->gmb, c->part, adj_out, c->Ntot,
                                                               c->tile_acc, q.nact, c->wq);
   else
-  k_p2g_adj<LAW, NG, 4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.active,
+  k_p2g_adj<LAW, NG, 4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.work,
                                                               step_act(c, t), c->gmb, c->part, adj_out, c->Ntot,
                                                               c->tile_acc, q.nact, c->wq);
 }
@@ -309,11 +319,11 @@ void backward_substep(DmContext* c, const StateView& S, const StateView& Sn, int
 #define L_G2PA(LW)                                                                                            \
   if (c->P.nmat == 1)                                                                                          \
     k_g2p_adj<LW, 1><<<c->grid_tiles, kWarps * 32, kG2pAdjSmem, c->stream>>>(c->P, S, Sn, adj_in, c->Ntot, q.perm, \
-                                                              q.tile_start, q.tile_count, q.active, q.gvb,  \
+                                                              q.tile_start, q.tile_count, q.work, q.gvb,  \
                                                               c->ablocks, c->part, c->tile_acc, q.nact, c->wq); \
   else                                                                                                         \
     k_g2p_adj<LW, 4><<<c->grid_tiles, kWarps * 32, kG2pAdjSmem, c->stream>>>(c->P, S, Sn, adj_in, c->Ntot, q.perm, \
-                                                              q.tile_start, q.tile_count, q.active, q.gvb,  \
+                                                              q.tile_start, q.tile_count, q.work, q.gvb,  \
                                                               c->ablocks, c->part, c->tile_acc, q.nact, c->wq)
   DM_LAW_DISPATCH(c, L_G2PA);
 #undef L_G2PA
@@ -322,7 +332,7 @@ void backward_substep(DmContext* c, const StateView& S, const StateView& Sn, int
   wq_reset(c);
   PROF_BEGIN(c, 10);
 #define L_GRIDA(MC, CK)                                                                                   \
-  k_grid_adj<MC, CK><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.active,        \
+  k_grid_adj<MC, CK><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work,        \
                                                                    step_cvo(c, t), c->ablocks, q.gmpb,   \
                                                                    c->gmb, c->tile_acc, q.nact, c->wq)
   DM_GRID_DISPATCH(c, L_GRIDA);
@@ -691,8 +701,10 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
     // 16-bit histogram words when a warp's count and an env's cursor fit
     ctx->bin_u16 = P.N <= 65535;
     const size_t wb = ctx->bin_u16 ? 2 : 4;
+    // one CTA per env: with fewer envs than two per SM, wider CTAs
+    const int max_nw = P.E < 296 ? 32 : 16;
     int nw = (int)((160 * 1024) / ((size_t)P.Tn * wb));
-    nw = nw > 16 ? 16 : nw;
+    nw = nw > max_nw ? max_nw : nw;
     if (nw < 1) return fail("dm_create: grid too large for the bin kernel");
     ctx->bin_warps = nw;
     cudaFuncSetAttribute(k_bin<unsigned short>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(nw * P.Tn * 2));
@@ -774,6 +786,7 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   ok = ok && dalloc(ctx, &ctx->keys, N) && dalloc(ctx, &ctx->ptile, N) &&
        dalloc(ctx, &ctx->perm_all, (size_t)ck * N) && dalloc(ctx, &ctx->tstart_all, (size_t)ck * TT) &&
        dalloc(ctx, &ctx->tcount_all, (size_t)ck * TT) && dalloc(ctx, &ctx->active_all, (size_t)ck * TT) &&
+       dalloc(ctx, &ctx->work_all, (size_t)ck * TT) && dalloc(ctx, &ctx->ord_all, (size_t)ck * 2 * kOrdBuckets) &&
        dalloc(ctx, &ctx->abase_all, (size_t)ck * P.E) && dalloc(ctx, &ctx->acount_all, (size_t)ck * P.E) &&
        dalloc(ctx, &ctx->nact_all, (size_t)ck) && dalloc(ctx, &ctx->tail, state_floats(ctx)) && dalloc(ctx, &ctx->tail_attr, N);
   const size_t NN = (size_t)P.E * P.dims[0] * P.dims[1] * P.dims[2];
@@ -811,7 +824,7 @@ void dm_destroy(DmContext* ctx) {
   void* ptrs[] = {ctx->store,     ctx->store_attr, ctx->seg,       ctx->seg_attr,   ctx->scratch[0], ctx->scratch[1],
                   ctx->scratch_attr[0], ctx->scratch_attr[1], ctx->adj[0], ctx->adj[1], ctx->part, ctx->keys,
                   ctx->perm_all,  ctx->ptile, ctx->tstart_all, ctx->tcount_all, ctx->abase_all, ctx->acount_all,
-                  ctx->active_all, ctx->nact_all, ctx->tail, ctx->tail_attr, ctx->gvb_pool, ctx->gmpb_pool,
+                  ctx->active_all, ctx->work_all, ctx->ord_all, ctx->nact_all, ctx->tail, ctx->tail_attr, ctx->gvb_pool, ctx->gmpb_pool,
                   ctx->blocks,    ctx->ablocks,    ctx->tile_acc,   ctx->gmp, ctx->gv, ctx->gmb,   ctx->flags, ctx->wq, ctx->cvo_tape,  ctx->act_tape,
                   ctx->obs_tape,  ctx->dobs_buf, ctx->gcvo,       ctx->gact,       ctx->gmu,        ctx->glam};
   for (void* p : ptrs)

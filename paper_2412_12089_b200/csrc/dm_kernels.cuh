@@ -234,12 +234,12 @@ __device__ __forceinline__ void store_state(const StateView& S, size_t i, v3<flo
 // CT: histogram / cursor word (unsigned short when particles per env fit in
 // 16 bits: half the shared memory, twice the resident CTAs).
 template <class CT>
-__global__ void __launch_bounds__(512) k_bin(DevParams P, StateView S, int* keys, int* perm, int* tile_start,
+__global__ void __launch_bounds__(1024) k_bin(DevParams P, StateView S, int* keys, int* perm, int* tile_start,
                                              int* tile_count, int4* active, int* env_abase, int* env_acount,
                                              DevFlags* flags, int* nact, int substep, int check_vmax) {
   extern __shared__ __align__(16) unsigned char bin_smem[];
   CT* cnt = reinterpret_cast<CT*>(bin_smem);  // [nw][Tn]
-  __shared__ int s_part[512 / 32 + 1][2];
+  __shared__ int s_part[1024 / 32 + 1][2];
   __shared__ int s_base;
   const int e = blockIdx.x;
   const int nw = blockDim.x >> 5;
@@ -350,6 +350,62 @@ __global__ void __launch_bounds__(512) k_bin(DevParams P, StateView S, int* keys
     if (p < p1) perm[base + pos + rank] = (int)(base + p);
     __syncwarp();
   }
+}
+
+// ---- work order: active tiles by descending particle count ----
+// The tile kernels take tiles from a work list ordered largest-first (16
+// buckets of 64 particles), so the dynamic scheduler ends on small tiles
+// (longest-processing-time-first).  Only the schedule depends on the order:
+// every tile's result is order-independent, and the replay and the adjoint of
+// a substep share their slot's list, so the work index also names the tile's
+// stored grid blocks consistently.  ord[0..15]: bucket counts, ord[16..31]:
+// bucket cursors (zeroed before k_order_hist).
+constexpr int kOrdBuckets = 16;
+__device__ __forceinline__ int ord_bucket(int count) {
+  const int b = count >> 6;
+  return kOrdBuckets - 1 - (b < kOrdBuckets - 1 ? b : kOrdBuckets - 1);  // 0 = largest
+}
+
+__global__ void __launch_bounds__(256) k_order_hist(const int4* __restrict__ active, const int* nact, int* ord) {
+  __shared__ int h[kOrdBuckets];
+  if (threadIdx.x < kOrdBuckets) h[threadIdx.x] = 0;
+  __syncthreads();
+  const int n = *(const volatile int*)nact;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    atomicAdd(&h[ord_bucket(active[i].w)], 1);
+  __syncthreads();
+  if (threadIdx.x < kOrdBuckets && h[threadIdx.x]) atomicAdd(&ord[threadIdx.x], h[threadIdx.x]);
+}
+
+__global__ void __launch_bounds__(256) k_order_scatter(const int4* __restrict__ active, const int* nact,
+                                                       int* ord, int4* __restrict__ work) {
+  __shared__ int h[kOrdBuckets], base[kOrdBuckets];
+  if (threadIdx.x < kOrdBuckets) h[threadIdx.x] = 0;
+  __syncthreads();
+  const int n = *(const volatile int*)nact;
+  const int i0 = blockIdx.x * blockDim.x * 8, i1 = min(n, i0 + (int)blockDim.x * 8);
+  int4 d[8];
+  int b[8], r[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = i0 + k * blockDim.x + threadIdx.x;
+    b[k] = -1;
+    if (i < i1) {
+      d[k] = active[i];
+      b[k] = ord_bucket(d[k].w);
+      r[k] = atomicAdd(&h[b[k]], 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < kOrdBuckets) {
+    int start = 0;
+    for (int q = 0; q < threadIdx.x; ++q) start += ord[q];
+    base[threadIdx.x] = h[threadIdx.x] ? start + atomicAdd(&ord[kOrdBuckets + threadIdx.x], h[threadIdx.x]) : 0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (b[k] >= 0) work[base[b[k]] + r[k]] = d[k];
 }
 
 // Second sort level: within every active tile, a stable counting sort by the
