@@ -263,12 +263,12 @@ void launch_p2g(DmContext* c, const StateView& S, const Slot& q, int t, int sub)
     LAUNCH(4, -1);                                        \
   }
 
-void launch_grid(DmContext* c, const Slot& q, int t) {
+void launch_grid(DmContext* c, const Slot& q, int t, bool dump) {
   wq_reset(c);
   PROF_BEGIN(c, 9);
 #define L_GRID(MC, CK)                                                                                        \
   k_grid<MC, CK><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work, step_cvo(c, t), \
-                                                               c->blocks, c->gmp, c->gv, q.nact, c->wq)
+                                                               c->blocks, dump ? c->gmp : nullptr, c->gv, q.nact, c->wq)
   DM_GRID_DISPATCH(c, L_GRID);
 #undef L_GRID
   PROF_END(c, 9);
@@ -293,7 +293,7 @@ void forward_substep(DmContext* c, const StateView& S, const StateView& So, int 
   const Slot q = slot(c, qi);
   launch_bin(c, S, q, sub, check_vmax);
   launch_p2g(c, S, q, t, sub);
-  launch_grid(c, q, t);
+  launch_grid(c, q, t, dump);
   launch_g2p(c, S, So, q, t, sub, dump);
 }
 

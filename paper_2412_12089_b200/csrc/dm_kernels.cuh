@@ -901,7 +901,7 @@ __global__ void __launch_bounds__(kWarps * 32, 6) k_grid(DevParams P, const int*
       const float4 mm = sum_blocks(P, nm, blocks, nbr, e, tc, i);
       const v3<float> v = node_update<float, MAXC, CK>(G, cols, P.K, g, mm.x, mk3(mm.y, mm.z, mm.w));
       const size_t n = node_lin(P, e, g);
-      gmp[n] = mm;
+      if (gmp) gmp[n] = mm;  // (mass, momentum) only when the replay dumps them
       gv[n] = make_float4(v.x, v.y, v.z, 0.f);
     }
   }
