@@ -564,7 +564,22 @@ template <bool HASM>
 __device__ __forceinline__ void run_add(float4* __restrict__ blk, RunAcc& ra, int off, float fi, float fj,
                                         const PayLane& p) {
   if (p.lb != ra.cur) {
-    run_flush(blk, ra, off);
+    if (HASM && p.lb == ra.cur + 1) {
+      // next cell in z (the sort's innermost order): the run's nodes k = 1, 2
+      // are the new run's k = 0, 1 -- flush only node k = 0 and shift
+      // (P2G only: measured slower in the G2P adjoint)
+      float4 b = blk[ra.cur + off];
+      b.x += ra.acc[0].x;
+      b.y += ra.acc[0].y;
+      b.z += ra.acc[0].z;
+      b.w += ra.acc[0].w;
+      blk[ra.cur + off] = b;
+      ra.acc[0] = ra.acc[1];
+      ra.acc[1] = ra.acc[2];
+      ra.acc[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      run_flush(blk, ra, off);
+    }
     ra.cur = p.lb;
   }
   // node (i, j, kk) value: b + kk a  (b = q + Ad_0 i + Ad_1 j, a = Ad_2)
