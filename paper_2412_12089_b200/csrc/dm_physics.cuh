@@ -501,6 +501,81 @@ DM_HD_NOINLINE v3<R> collider_query_vjp(const Col<R>& col, v3<R> p, R dbar, v3<R
   }
 }
 
+// Query record for a compile-time collider kind (CK >= 0): the node update
+// adjoint queries the SDF once and reuses the record for the forward
+// recompute, the coupling adjoint and the SDF adjoint (previously three
+// queries per node).  Same arithmetic as collider_query /
+// collider_query_vjp, so the results are bitwise unchanged.
+template <class R>
+struct ColRec {
+  R d, sg, r;
+  v3<R> n, rel;
+  BoxQ<R> b;
+  CylQ<R> cy;
+};
+
+template <class R, int CK>
+DM_HD void collider_query_rec(const Col<R>& col, v3<R> p, ColRec<R>& q) {
+  const v3<R> rel = p - col.c;
+  if (CK == kPlane) {
+    q.d = dot(rel, col.nrm);
+    q.n = col.nrm;
+  } else if (CK == kSphere) {
+    q.r = r_sqrt(dot(rel, rel) + R(1e-18));
+    q.d = q.r - col.radius;
+    q.n = rel * (R(1) / q.r);
+  } else if (CK == kBox) {
+    q.b = box_query(rel, col.half);
+    q.rel = rel;
+    q.d = q.b.d;
+    q.n = q.b.n;
+  } else if (CK == kCylinder) {
+    q.cy = cyl_query(col, rel);
+    q.d = q.cy.d;
+    q.n = q.cy.n;
+  } else {  // hollow open-top box
+    const R th = col.thickness;
+    const v3<R> ro = mk3(rel.x, rel.y, rel.z + R(0.5) * th);
+    const v3<R> ho = mk3(col.half.x + th, col.half.y + th, col.half.z + R(0.5) * th);
+    const v3<R> rc = mk3(rel.x, rel.y, rel.z - R(1));
+    const v3<R> hc = mk3(col.half.x, col.half.y, col.half.z + R(1));
+    const BoxQ<R> bo = box_query(ro, ho);
+    const BoxQ<R> bc = box_query(rc, hc);
+    const bool outer = bo.d >= -bc.d;
+    q.b = outer ? bo : bc;
+    q.rel = outer ? ro : rc;
+    q.sg = outer ? R(1) : R(-1);
+    q.d = outer ? bo.d : -bc.d;
+    q.n = outer ? bo.n : -bc.n;
+  }
+}
+
+template <class R, int CK>
+DM_HD v3<R> collider_query_vjp_rec(const Col<R>& col, const ColRec<R>& q, R dbar, v3<R> nbar) {
+  if (CK == kPlane) return col.nrm * dbar;
+  if (CK == kSphere) return q.n * dbar + (nbar - q.n * dot(q.n, nbar)) * (R(1) / q.r);
+  if (CK == kBox) return box_query_vjp(q.b, q.rel, dbar, nbar);
+  if (CK == kCylinder) return cyl_query_vjp(q.cy, dbar, nbar);
+  return box_query_vjp(q.b, q.rel, q.sg * dbar, nbar * q.sg);
+}
+
+// collide / collide_vjp on a query record (same arithmetic as below).
+template <class R>
+DM_HD v3<R> collide_rec(const Col<R>& col, R alpha_c, R mu_b, v3<R> node, v3<R> v, const ColRec<R>& q) {
+  const R d = q.d;
+  const v3<R> n = q.n;
+  const R s = d < R(0) ? R(1) : r_exp(-alpha_c * r_max(d, R(0)));
+  const v3<R> vcol = col.vel + cross(col.om, node - col.c);
+  const v3<R> rel = v - vcol;
+  const R vn = dot(rel, n);
+  if (!(vn < R(0))) return v;
+  const v3<R> tang = rel - n * vn;
+  const R tnorm = r_sqrt(dot(tang, tang) + R(1e-18));
+  const R keep = r_max(R(1) - mu_b * r_max(-vn, R(0)) / tnorm, R(0));
+  const v3<R> vproj = vcol + tang * keep + n * r_max(vn, R(0));
+  return v * (R(1) - s) + vproj * s;
+}
+
 // ======================= grid node update =======================
 
 struct Coupling {
@@ -583,6 +658,61 @@ DM_HD_NOINLINE v3<R> collide_vjp(const Col<R>& col, R alpha_c, R mu_b, v3<R> nod
   return vb;
 }
 
+template <class R, int CK>
+DM_HD v3<R> collide_vjp_rec(const Col<R>& col, R alpha_c, R mu_b, v3<R> node, v3<R> v, v3<R> vb_out, const ColRec<R>& q, v3<R>& cbar,
+                        v3<R>& velbar, v3<R>& ombar) {
+  const R d = q.d;
+  const v3<R> n = q.n;
+  const v3<R> r = node - col.c;
+  const v3<R> vcol = col.vel + cross(col.om, r);
+  const v3<R> rel = v - vcol;
+  const R vn = dot(rel, n);
+  if (!(vn < R(0))) return vb_out;
+  const R s = d < R(0) ? R(1) : r_exp(-alpha_c * r_max(d, R(0)));
+  const v3<R> tang = rel - n * vn;
+  const R tnorm = r_sqrt(dot(tang, tang) + R(1e-18));
+  const R m = r_max(-vn, R(0));
+  const R kk = R(1) - mu_b * m / tnorm;
+  const R keep = r_max(kk, R(0));
+  const v3<R> vproj = vcol + tang * keep + n * r_max(vn, R(0));
+  // v' = v (1 - s) + vproj s
+  v3<R> vb = vb_out * (R(1) - s);
+  const R sb = dot(vproj - v, vb_out);
+  const v3<R> vpb = vb_out * s;
+  v3<R> vcolb = vpb;
+  v3<R> tangb = vpb * keep;
+  const R keepb = dot(tang, vpb);
+  v3<R> nb = zero3<R>();  // n * max(vn, 0): vn < 0 here -> no contribution
+  R vnb = R(0);
+  if (kk > R(0)) {
+    const R mb = -keepb * mu_b / tnorm;
+    const R tnb = keepb * mu_b * m / (tnorm * tnorm);
+    tangb += tang * (tnb / tnorm);
+    if (-vn > R(0)) vnb -= mb;
+  }
+  // tang = rel - n vn
+  v3<R> relb = tangb;
+  nb -= tangb * vn;
+  vnb -= dot(n, tangb);
+  // vn = rel . n
+  relb += n * vnb;
+  nb += rel * vnb;
+  // rel = v - vcol
+  vb += relb;
+  vcolb -= relb;
+  // s = exp(-alpha max(d, 0)) for d >= 0
+  R db = R(0);
+  if (!(d < R(0)) && d > R(0)) db = -alpha_c * s * sb;
+  // vcol = vel + om x r
+  velbar += vcolb;
+  ombar += cross(r, vcolb);
+  const v3<R> rb = cross(vcolb, col.om);
+  cbar -= rb;
+  // query
+  cbar -= collider_query_vjp_rec<R, CK>(col, q, db, nb);
+  return vb;
+}
+
 template <class R>
 struct NodeCtx {
   int dims[3];
@@ -647,6 +777,30 @@ DM_HD void node_update_vjp(const NodeCtx<R>& g, const Col<R>* cols, int ncol, co
   v0.y += g.dt * g.gravity.y;
   v0.z += g.dt * g.gravity.z;
   const v3<R> node = mk3(R(idx[0]) * g.dx, R(idx[1]) * g.dx, R(idx[2]) * g.dx);
+  if (CK >= 0 && MAXC == 1) {  // dispatched only for batches with exactly one collider
+    // one compile-time collider: one SDF query per node (query record)
+    ColRec<R> q;
+    collider_query_rec<R, CK>(cols[0], node, q);
+    v3<R> vfin = collide_rec(cols[0], g.alpha_c, g.mu_b, node, v0, q);
+    const int mask = boundary_apply(g, idx, vfin);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if (mask & (1 << a)) vb[a] = R(0);
+    v3<R> cb = zero3<R>(), velb = zero3<R>(), omb = zero3<R>();
+    vb = collide_vjp_rec<R, CK>(cols[0], g.alpha_c, g.mu_b, node, v0, vb, q, cb, velb, omb);
+    cgrad[0] += cb.x;
+    cgrad[1] += cb.y;
+    cgrad[2] += cb.z;
+    cgrad[3] += velb.x;
+    cgrad[4] += velb.y;
+    cgrad[5] += velb.z;
+    cgrad[6] += omb.x;
+    cgrad[7] += omb.y;
+    cgrad[8] += omb.z;
+    momb = vb * inv;
+    massb = -dot(vb, mom) * inv * inv;
+    return;
+  }
   v3<R> vs[MAXC + 1];
   vs[0] = v0;
   const int nc = ncol < MAXC ? ncol : MAXC;
