@@ -862,19 +862,33 @@ __device__ __forceinline__ int owned_nodes(const DevParams& P, const NodeMasks& 
 
 __device__ __forceinline__ float4 sum_blocks(const DevParams& P, const NodeMasks& nm, const float4* __restrict__ blocks,
                                              unsigned nbr, int e, const int tc[3], int i) {
+  // all (<= 8) covering blocks' loads are issued before the fixed-order sum
+  // (ascending tile order = lexicographic (rx, ry, rz), as the cover mask bits)
+  (void)nm;
   const int l[3] = {i / 36, (i / 6) % 6, i % 6};
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (unsigned m = nbr & nm.cand[i]; m; m &= m - 1u) {
-    const int bit = __ffs(m) - 1;
-    const int rx = bit / 9 - 1, ry = (bit / 3) % 3 - 1, rz = bit % 3 - 1;
-    const int st = ((tc[0] + rx) * P.td[1] + (tc[1] + ry)) * P.td[2] + (tc[2] + rz);
-    const int lx = l[0] - 4 * rx, ly = l[1] - 4 * ry, lz = l[2] - 4 * rz;
-    const float4 b = blocks[((size_t)e * P.Tn + st) * kExt3 + (lx * kExt + ly) * kExt + lz];
-    acc.x += b.x;
-    acc.y += b.y;
-    acc.z += b.z;
-    acc.w += b.w;
+  int lo[3], hi[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) cand_range(l[d], lo[d], hi[d]);
+  float4 v[8];
+  bool ok[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int rx = lo[0] + (c >> 2), ry = lo[1] + ((c >> 1) & 1), rz = lo[2] + (c & 1);
+    ok[c] = rx <= hi[0] && ry <= hi[1] && rz <= hi[2] && ((nbr >> ((rx + 1) * 9 + (ry + 1) * 3 + (rz + 1))) & 1u);
+    if (ok[c]) {
+      const int st = ((tc[0] + rx) * P.td[1] + (tc[1] + ry)) * P.td[2] + (tc[2] + rz);
+      v[c] = blocks[((size_t)e * P.Tn + st) * kExt3 + ((l[0] - 4 * rx) * kExt + (l[1] - 4 * ry)) * kExt + (l[2] - 4 * rz)];
+    }
   }
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    if (ok[c]) {
+      acc.x += v[c].x;
+      acc.y += v[c].y;
+      acc.z += v[c].z;
+      acc.w += v[c].w;
+    }
   return acc;
 }
 
@@ -887,7 +901,7 @@ __device__ __forceinline__ size_t node_lin(const DevParams& P, int e, const int 
 // (mpm.hpp:256-305 + extensions), write (mass, momentum) and velocity to the
 // dense per-env grid.
 template <int MAXC, int CK>
-__global__ void __launch_bounds__(kWarps * 32, 6) k_grid(DevParams P, const int* __restrict__ tile_count,
+__global__ void __launch_bounds__(kWarps * 32, 5) k_grid(DevParams P, const int* __restrict__ tile_count,
                                                       const int4* __restrict__ active, const float* __restrict__ cvo,
                                                       const float4* __restrict__ blocks, float4* __restrict__ gmp,
                                                       float4* __restrict__ gv, const int* nact, int* __restrict__ wq) {
