@@ -488,6 +488,7 @@ int step_impl(DmContext* ctx, const float* cvo, const float* act, float* obs, cu
   const int S = ctx->cfg.substeps;
   for (int q = 0; q < S; ++q) {
     const int s = t * S + q;
+    ctx->P.fiso = s > 0;  // every state but the initial one is a G2P output
     forward_substep(ctx, fwd_state(ctx, s), fwd_state(ctx, s + 1), t, q, q == 0, 0, false);
   }
   float* o = ctx->obs_tape + (size_t)t * E * ctx->od;
@@ -594,11 +595,13 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
     for (int q = 0; q < ck; ++q) {
       const int s = s0 + q;
       const StateView So = q + 1 < ck ? seg_state(ctx, s0, s + 1) : view(ctx->tail, ctx->tail_attr, ctx->Ntot);
+      ctx->P.fiso = s > 0;
       forward_substep(ctx, seg_state(ctx, s0, s), So, t, s - t * S, 0, q, true);
     }
     for (int q = ck - 1; q >= 0; --q) {
       const int s = s0 + q;
       const StateView Sn = q + 1 < ck ? seg_state(ctx, s0, s + 1) : view(ctx->tail, ctx->tail_attr, ctx->Ntot);
+      ctx->P.fiso = s > 0;
       backward_substep(ctx, seg_state(ctx, s0, s), Sn, t, q, ctx->adj[cur], ctx->adj[cur ^ 1]);
       cur ^= 1;
     }

@@ -46,6 +46,7 @@ struct DevParams {
   int boundary;
   float alpha_c, mu_b;
   int K, G, nmat;
+  int fiso;  // input state's F isotropic (fluid: every g2p output, F = J^(1/3) I)
   Law<float> law[4];
   ColShape shape[4];
 };
@@ -189,25 +190,39 @@ __device__ __forceinline__ void load_cols(const DevParams& P, const float* cvo_e
   }
 }
 
-__device__ __forceinline__ void load_state(const StateView& S, size_t i, float x[3], v3<float>& v, m3<float>& F,
-                                           m3<float>& C) {
+// F of the state.  The fluid projection (mpm.hpp:207) makes every G2P output
+// F exactly J^(1/3) I (off-diagonals stored as +0), so for a fluid batch and
+// a state produced by G2P (P.fiso) one word is read instead of nine; the
+// reconstructed matrix holds the identical values.
+template <int LAW>
+__device__ __forceinline__ void load_F(const StateView& S, size_t i, m3<float>& F, int fiso) {
+  if (LAW == kFluid && fiso) {
+    const float sF = S.c(6, i);
+    F = mdiag(sF, sF, sF);
+  } else {
 #pragma unroll
-  for (int a = 0; a < 3; ++a) x[a] = S.c(a, i);
-  v = mk3(S.c(3, i), S.c(4, i), S.c(5, i));
-#pragma unroll
-  for (int q = 0; q < 9; ++q) {
-    F.a[q] = S.c(6 + q, i);
-    C.a[q] = S.c(15 + q, i);
+    for (int q = 0; q < 9; ++q) F.a[q] = S.c(6 + q, i);
   }
 }
 
-// G2P and its adjoint only read x and F of the start-of-substep state
-// (v and C are outputs): 48 B instead of 96 B per particle.
-__device__ __forceinline__ void load_xF(const StateView& S, size_t i, float x[3], m3<float>& F) {
+template <int LAW = -1>
+__device__ __forceinline__ void load_state(const StateView& S, size_t i, float x[3], v3<float>& v, m3<float>& F,
+                                           m3<float>& C, int fiso = 0) {
 #pragma unroll
   for (int a = 0; a < 3; ++a) x[a] = S.c(a, i);
+  v = mk3(S.c(3, i), S.c(4, i), S.c(5, i));
+  load_F<LAW>(S, i, F, fiso);
 #pragma unroll
-  for (int q = 0; q < 9; ++q) F.a[q] = S.c(6 + q, i);
+  for (int q = 0; q < 9; ++q) C.a[q] = S.c(15 + q, i);
+}
+
+// G2P and its adjoint only read x and F of the start-of-substep state
+// (v and C are outputs): 48 B (fluid after the first substep: 16 B).
+template <int LAW = -1>
+__device__ __forceinline__ void load_xF(const StateView& S, size_t i, float x[3], m3<float>& F, int fiso = 0) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) x[a] = S.c(a, i);
+  load_F<LAW>(S, i, F, fiso);
 }
 
 __device__ __forceinline__ void store_state(const StateView& S, size_t i, v3<float> x, v3<float> v, const m3<float>& F,
@@ -718,8 +733,9 @@ struct PState {
   uint32_t at;
 };
 
-__device__ __forceinline__ void load_pstate(const StateView& S, int src, PState& p) {
-  load_state(S, src, p.x, p.v, p.F, p.C);
+template <int LAW>
+__device__ __forceinline__ void load_pstate(const StateView& S, int src, PState& p, int fiso) {
+  load_state<LAW>(S, src, p.x, p.v, p.F, p.C, fiso);
   p.at = S.attr[src];
 }
 
@@ -749,7 +765,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_p2g(DevParams P, StateView S
     // perm indices two chunks ahead in two parity slots (no register moves
     // between chunks, so a refill never waits on the load it replaces)
     PState ps;
-    if (lane < cnt) load_pstate(S, prow[lane], ps);
+    if (lane < cnt) load_pstate<LAW>(S, prow[lane], ps, P.fiso);
     int s1 = 32 + lane < cnt ? prow[32 + lane] : 0;
     int s0 = 64 + lane < cnt ? prow[64 + lane] : 0;
     scatter_zero(bw, lane);
@@ -773,7 +789,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_p2g(DevParams P, StateView S
       }
       __syncwarp();
       // software pipeline: issue the next chunk's loads before this chunk's scatter
-      if (c0 + 32 + lane < cnt) load_pstate(S, s_next, ps);
+      if (c0 + 32 + lane < cnt) load_pstate<LAW>(S, s_next, ps, P.fiso);
       s_next = c0 + 96 + lane < cnt ? prow[c0 + 96 + lane] : 0;
       scatter_runs<true>(bw, pw, min(32, cnt - c0), lane, ra);
     };
@@ -980,7 +996,7 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
     uint32_t ata = 0, atb = 0;
     if (lane < cnt) {
       const int src = perm[row + lane];
-      load_xF(S, src, xa, Fa);
+      load_xF<LAW>(S, src, xa, Fa, P.fiso);
       ata = S.attr[src];
     }
     int s1 = lane + 32 < cnt ? perm[row + lane + 32] : 0;
@@ -1013,14 +1029,14 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
     };
     for (int c0 = 0; c0 < cnt; c0 += 64) {
       if (c0 + 32 + lane < cnt) {  // chunk c0 + 32 -> buffer b
-        load_xF(S, s1, xb, Fb);
+        load_xF<LAW>(S, s1, xb, Fb, P.fiso);
         atb = S.attr[s1];
       }
       s1 = c0 + 96 + lane < cnt ? perm[row + c0 + 96 + lane] : 0;
       body(c0, xa, Fa, ata);
       if (c0 + 32 >= cnt) break;
       if (c0 + 64 + lane < cnt) {  // chunk c0 + 64 -> buffer a
-        load_xF(S, s0, xa, Fa);
+        load_xF<LAW>(S, s0, xa, Fa, P.fiso);
         ata = S.attr[s0];
       }
       s0 = c0 + 128 + lane < cnt ? perm[row + c0 + 128 + lane] : 0;
@@ -1071,7 +1087,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
     uint32_t at = 0;
     if (lane < cnt) {
       const int src = perm[row + lane];
-      load_xF(S, src, x, F);
+      load_xF<LAW>(S, src, x, F, P.fiso);
       at = S.attr[src];
     }
     int s1 = 32 + lane < cnt ? perm[row + 32 + lane] : 0;  // perm two chunks ahead, parity slots
@@ -1124,7 +1140,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
       }
       __syncwarp();
       if (c0 + 32 + lane < cnt) {
-        load_xF(S, s_next, x, F);
+        load_xF<LAW>(S, s_next, x, F, P.fiso);
         at = S.attr[s_next];
       }
       s_next = c0 + 96 + lane < cnt ? perm[row + c0 + 96 + lane] : 0;
@@ -1246,7 +1262,8 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
     // particle-side cotangents at the sorted slot, and the perm index itself)
     auto stage = [&](int c0, int src) {
 #pragma unroll
-      for (int f = 0; f < 24; ++f) cp_async4(sg + f * 32 + lane, &S.c(f, src));
+      for (int f = 0; f < 24; ++f)
+        if (!(LAW == kFluid && P.fiso && f > 6 && f < 15)) cp_async4(sg + f * 32 + lane, &S.c(f, src));
       cp_async4(sg + 24 * 32 + lane, S.attr + src);
 #pragma unroll
       for (int f = 0; f < 12; ++f) cp_async4(sg + (25 + f) * 32 + lane, part + part_index(f, row + c0 + lane, astride));
@@ -1278,6 +1295,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
           C.a[q] = sg[(15 + q) * 32 + lane];
           Fb.a[q] = sg[(28 + q) * 32 + lane];
         }
+        if (LAW == kFluid && P.fiso) F = mdiag(F.a[0], F.a[0], F.a[0]);
         at = __float_as_uint(sg[24 * 32 + lane]);
         xb = mk3(sg[25 * 32 + lane], sg[26 * 32 + lane], sg[27 * 32 + lane]);
         src = __float_as_int(sg[37 * 32 + lane]);
