@@ -447,7 +447,8 @@ int get_state_impl(DmContext* ctx, float* x, float* v, float* F, float* C, cudaM
   const int s = ctx->steps * ctx->cfg.substeps;
   const StateView S = fwd_state(ctx, s);
   float* out = ctx->adj[1];
-  k_soa_to_aos<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>((int)N, ctx->P.N, S.f, S.attr, N, 1, out,
+  const int fiso = ctx->law == kFluid && s > 0;  // a fluid G2P output stores F(0,0) only
+  k_soa_to_aos<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>((int)N, ctx->P.N, S.f, S.attr, N, 1, fiso, out,
                                                                      out + 3 * N, out + 6 * N, out + 15 * N);
   ++ctx->launches;
   if (x) DM_CUDA(cudaMemcpyAsync(x, out, 3 * N * sizeof(float), kind, ctx->stream));
@@ -626,7 +627,7 @@ int backward_end(DmContext* ctx, float* dx0, float* dv0, float* dF0, float* dC0,
   const size_t N = ctx->Ntot;
   float* out = ctx->adj[cur ^ 1];
   const StateView S0 = store_view(ctx, 0);
-  k_soa_to_aos<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>((int)N, ctx->P.N, ctx->adj[cur], S0.attr, N, 1, out,
+  k_soa_to_aos<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>((int)N, ctx->P.N, ctx->adj[cur], S0.attr, N, 1, 0, out,
                                                                      out + 3 * N, out + 6 * N, out + 15 * N);
   ++ctx->launches;
   if (dx0) DM_CUDA(cudaMemcpyAsync(dx0, out, 3 * N * sizeof(float), kout, ctx->stream));
@@ -899,6 +900,10 @@ int reset_lattice_impl(DmContext* ctx, const DmLatticeReset* spec, unsigned long
   if (mask && cur.f != S0.f) {
     DM_CUDA(cudaMemcpyAsync(S0.f, cur.f, state_floats(ctx) * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream));
     DM_CUDA(cudaMemcpyAsync(S0.attr, cur.attr, ctx->Ntot * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+    if (ctx->law == kFluid) {  // the kept envs' F becomes a general initial state
+      k_fiso_expand<<<ctx->grid_tiles, 256, 0, ctx->stream>>>(ctx->Ntot, S0);
+      ++ctx->launches;
+    }
   }
   ResetSpec R;
   for (int a = 0; a < 3; ++a) {

@@ -225,6 +225,9 @@ __device__ __forceinline__ void load_xF(const StateView& S, size_t i, float x[3]
   load_F<LAW>(S, i, F, fiso);
 }
 
+// A fluid G2P output stores only F(0,0) (F = J^(1/3) I); readers of such a
+// state reconstruct the rest (load_F, k_soa_to_aos, k_fiso_expand).
+template <int LAW = -1>
 __device__ __forceinline__ void store_state(const StateView& S, size_t i, v3<float> x, v3<float> v, const m3<float>& F,
                                             const m3<float>& C) {
   S.c(0, i) = x.x;
@@ -235,7 +238,7 @@ __device__ __forceinline__ void store_state(const StateView& S, size_t i, v3<flo
   S.c(5, i) = v.z;
 #pragma unroll
   for (int q = 0; q < 9; ++q) {
-    S.c(6 + q, i) = F.a[q];
+    if (LAW != kFluid || q == 0) S.c(6 + q, i) = F.a[q];
     S.c(15 + q, i) = C.a[q];
   }
 }
@@ -1024,7 +1027,7 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
       g2p_particle_sep(law_of<LAW>(P, attr_mat(at)), T, sc, getv, xn, v, C, F, &bad_adv, &bad_det);
       if (bad_adv) report(flags, e, substep, 1, attr_index(at), 0, kErrG2PInterior);
       if (bad_det) report(flags, e, substep, 1, attr_index(at), attr_mat(at), kErrDetF);
-      store_state(Sout, dst, xn, v, F, C);
+      store_state<LAW>(Sout, dst, xn, v, F, C);
       Sout.attr[dst] = at;
     };
     for (int c0 = 0; c0 < cnt; c0 += 64) {
@@ -1588,6 +1591,16 @@ __global__ void __launch_bounds__(256) k_obs_adj(DevParams P, StateView S, const
   }
 }
 
+// Fills F = F(0,0) I for every particle of a fluid G2P-produced state (makes
+// it a general state again: used when it becomes a new initial state).
+__global__ void k_fiso_expand(size_t Ntot, StateView S) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < Ntot; i += (size_t)gridDim.x * blockDim.x) {
+    const float sF = S.c(6, i);
+#pragma unroll
+    for (int q = 1; q < 9; ++q) S.c(6 + q, i) = (q % 4 == 0) ? sF : 0.f;
+  }
+}
+
 // ============================ device-side reset ============================
 // RngStream (rng.hpp:11-55): key = mix(seed ^ phi (stream + 1)); the k-th
 // draw is mix(key ^ mix(k)), so every particle addresses its own draws.
@@ -1710,7 +1723,7 @@ __global__ void k_aos_to_soa(int Ntot, const float* __restrict__ x, const float*
 
 // physical SoA -> canonical AoS (original order within each env)
 __global__ void k_soa_to_aos(int Ntot, int N, const float* __restrict__ f, const uint32_t* __restrict__ attr,
-                             size_t stride, int state_layout, float* __restrict__ x, float* __restrict__ v, float* __restrict__ F,
+                             size_t stride, int state_layout, int fiso, float* __restrict__ x, float* __restrict__ v, float* __restrict__ F,
                              float* __restrict__ C) {
   const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (i >= (size_t)Ntot) return;
@@ -1723,7 +1736,8 @@ __global__ void k_soa_to_aos(int Ntot, int N, const float* __restrict__ f, const
   }
 #pragma unroll
   for (int q = 0; q < 9; ++q) {
-    if (F) F[9 * o + q] = f[state_layout ? state_index(6 + q, i, stride) : (6 + q) * stride + i];
+    if (F) F[9 * o + q] = fiso ? (q % 4 == 0 ? f[state_index(6, i, stride)] : 0.f)
+                               : f[state_layout ? state_index(6 + q, i, stride) : (6 + q) * stride + i];
     if (C) C[9 * o + q] = f[state_layout ? state_index(15 + q, i, stride) : (15 + q) * stride + i];
   }
 }
