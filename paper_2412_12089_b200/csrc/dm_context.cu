@@ -6,6 +6,7 @@
 // (algo.hpp:79-104).
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -705,10 +706,26 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
     // 16-bit histogram words when a warp's count and an env's cursor fit
     ctx->bin_u16 = P.N <= 65535;
     const size_t wb = ctx->bin_u16 ? 2 : 4;
-    // one CTA per env: with fewer envs than two per SM, wider CTAs
-    const int max_nw = P.E < 296 ? 32 : 16;
-    int nw = (int)((160 * 1024) / ((size_t)P.Tn * wb));
-    nw = nw > max_nw ? max_nw : nw;
+    // One CTA per env, nw warps each: pick nw minimising waves x (work per
+    // warp) = ceil(E / (SMs x CTAs per SM)) / nw, CTAs per SM bounded by the
+    // per-warp histograms (shared memory) and 64 resident warps.
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device);
+    const int max_smem = (int)((160 * 1024) / ((size_t)P.Tn * wb));  // warps per CTA by histogram size
+    int nw = 0;
+    double best = 1e30;
+    for (int w = 1; w <= 32 && w <= max_smem; ++w) {
+      const size_t shm = (size_t)w * P.Tn * wb + 1024;
+      int per_sm = (int)((227 * 1024) / shm);
+      per_sm = per_sm < 64 / w ? per_sm : 64 / w;
+      if (per_sm < 1) continue;
+      const double waves = std::ceil((double)P.E / ((double)sms * per_sm));
+      const double cost = waves / w;
+      if (cost < best - 1e-12) {
+        best = cost;
+        nw = w;
+      }
+    }
     if (nw < 1) return fail("dm_create: grid too large for the bin kernel");
     ctx->bin_warps = nw;
     cudaFuncSetAttribute(k_bin<unsigned short>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(nw * P.Tn * 2));
