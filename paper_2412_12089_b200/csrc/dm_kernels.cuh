@@ -139,7 +139,6 @@ __device__ __forceinline__ Law<float> law_of(const DevParams& P, int mi) {
   if (LAW >= 0) L.kind = LAW;
   return L;
 }
-constexpr int kLawBlocks(int law) { return (law == kFluid || law == kNeoHookean) ? 6 : 4; }
 #ifndef DM_G2P_MINB
 #define DM_G2P_MINB 4
 #endif
