@@ -4,8 +4,10 @@
 Metric (BASELINE.json): particle-substeps/s of forward + full adjoint over a
 checkpointed substep tape.  Default workload = config 4 (FluidMove-like:
 1,024 envs x 16,384 particles, 48^3 grid, 16 control steps x 32 substeps),
-the configuration BASELINE.json shards over 1/2/4/8 GPUs (strong scaling:
-the 1,024 envs are split across ranks, no simulator collective).
+the configuration BASELINE.json shards over 1/2/4/8 GPUs.  Envs are
+independent partitions (no simulator collective), so by default every rank
+simulates config 4's 1,024 envs (global env index rank * 1024 + e): weak
+scaling; `--strong` splits the 1,024 envs across the ranks instead.
 
 One step = one whole rollout: set the initial state, 16 recorded control
 steps (512 substeps), loss over the per-step observables, backward through
@@ -53,6 +55,7 @@ def parse():
     p.add_argument("--envs", type=int, default=0, help="override total envs (default: the config's)")
     p.add_argument("--ctrl", type=int, default=0, help="override control steps")
     p.add_argument("--checkpoint-every", type=int, default=-1)
+    p.add_argument("--strong", action="store_true", help="split the config's envs across ranks (default: weak scaling)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--profile-out", default="")
@@ -211,7 +214,8 @@ def run_reference(args, scene, rank, dist):
     v = float(np.mean(vals))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * scene.n_per_env * nt / v,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
             "config": {"workload": scene.name, "sample": desc},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": nt, "kind": "reference", "sample": desc},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -365,7 +369,8 @@ def run_ours(args, scene, rank, world, local, dist):
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if args.strong else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": scene.name, "envs": E * world, "particles_per_env": N, "control_steps": T,
                    "substeps_per_step": S, "grid": list(scene.sim["dims"]), "checkpoint_every": ck or S,
@@ -441,7 +446,13 @@ def main():
     total = args.envs or {1: 1, 2: 32, 3: 256, 4: 1024, 5: 512}[args.config]
     if args.config == 5:
         args.config = 2  # the reference arm times config 5's simulator (config 2 physics)
-    per = total // world if args.impl == "ours" else min(total, cpu_threads())
+    # weak scaling (default): every rank simulates the config's envs, global
+    # env index = rank * per + e (independent partitions, no simulator
+    # collective); --strong splits the config's envs across the ranks
+    if args.impl == "ours":
+        per = total // world if args.strong else total
+    else:
+        per = min(total, cpu_threads())
     kw = {"n_envs": per, "env_offset": rank * per if args.impl == "ours" else 0}
     if args.ctrl:
         kw["n_ctrl"] = args.ctrl
