@@ -314,6 +314,23 @@ def run_ours(args, scene, rank, world, local, dist):
     barrier(dist)
     prof = batch.profile(False)
     ms_rank = ev0.elapsed_time(ev1) / args.steps
+
+    # forward only (the rollout without the backward), same device timing
+    def forward_device():
+        batch.set_state(x0, v0, F0, C0, mat, grp)
+        for t in range(T):
+            batch.step(None if cvo_d is None else cvo_d[t], None if act_d is None else act_d[t], obs_d[t])
+
+    forward_device()
+    barrier(dist)
+    torch.cuda.synchronize()
+    ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev2.record(stream)
+    for _ in range(args.steps):
+        forward_device()
+    ev3.record(stream)
+    torch.cuda.synchronize()
+    fwd_ms = max_over_ranks(dist, ev2.elapsed_time(ev3) / args.steps)
     launches = (batch.launches - launches0) // args.steps
     ms = max_over_ranks(dist, ms_rank)
     value = units_rank * world / (ms / 1e3)
@@ -381,6 +398,8 @@ def run_ours(args, scene, rank, world, local, dist):
                      "peak_source": peak_src,
                      "alg_bytes_per_particle": ALG_BYTES[dom], "kernel_share": dom_ms / total_prof,
                      "path_alg_gbs": path_gbs, "path_frac": path_gbs / hbm},
+        "forward_only": {"value": units_rank * world / (fwd_ms / 1e3), "unit": UNIT, "ms_per_step": fwd_ms,
+                         "note": "the same rollout without the backward (north_star: forward and forward+backward)"},
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
