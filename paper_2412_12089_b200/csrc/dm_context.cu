@@ -59,6 +59,10 @@ struct DmContext {
   float4 *gvb_pool = nullptr, *gmpb_pool = nullptr;
   size_t blk_cap = 0;
   int max_active_seen = 0;
+  // the step that filled the tape kept its segment (states + artifacts) from
+  // the forward pass, so the backward skips that segment's replay
+  int kept_t = -1;
+  bool kept_ok = false;
   float* tail = nullptr;  // replay output of a segment's last substep
   uint32_t* tail_attr = nullptr;
   float4 *blocks = nullptr, *ablocks = nullptr;
@@ -282,7 +286,7 @@ void launch_g2p(DmContext* c, const StateView& S, const StateView& So, const Slo
 #define L_G2P(LW)                                                                                                \
   k_g2p<LW><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, q.perm, q.tile_start, q.tile_count,        \
                                                           q.work, c->gv, c->flags, q.nact, sub, c->gmp,         \
-                                                          dump ? q.gvb : nullptr, dump ? q.gmpb : nullptr, c->wq)
+                                                          dump ? q.gvb : nullptr, dump ? q.gmpb : nullptr, c->wq, (int)c->blk_cap)
   DM_LAW_DISPATCH(c, L_G2P);
 #undef L_G2P
   PROF_END(c, 2);
@@ -436,6 +440,8 @@ int set_state_impl(DmContext* ctx, const float* x, const float* v, const float* 
   ++ctx->launches;
   ctx->steps = 0;
   ctx->bwd_t = -1;
+  ctx->kept_t = -1;
+  ctx->kept_ok = false;
   ctx->poisoned = false;
   const int rc = reset_flags(ctx);
   if (rc != DM_OK) return rc;
@@ -457,6 +463,23 @@ int get_state_impl(DmContext* ctx, float* x, float* v, float* F, float* C, cudaM
   if (F) DM_CUDA(cudaMemcpyAsync(F, out + 6 * N, 9 * N * sizeof(float), kind, ctx->stream));
   if (C) DM_CUDA(cudaMemcpyAsync(C, out + 15 * N, 9 * N * sizeof(float), kind, ctx->stream));
   DM_CUDA(cudaStreamSynchronize(ctx->stream));
+  return DM_OK;
+}
+
+// Allocates the per-slot grid-block pools for `need` active tiles.
+int ensure_blk_pool(DmContext* ctx, size_t need) {
+  if (ctx->blk_cap >= need) return DM_OK;
+  if (ctx->gvb_pool) cudaFree(ctx->gvb_pool);
+  if (ctx->gmpb_pool) cudaFree(ctx->gmpb_pool);
+  ctx->bytes -= 2 * ctx->blk_cap * ctx->ck * kExt3 * sizeof(float4);
+  ctx->gvb_pool = ctx->gmpb_pool = nullptr;
+  ctx->blk_cap = 0;
+  if (!dalloc(ctx, &ctx->gvb_pool, need * ctx->ck * kExt3) || !dalloc(ctx, &ctx->gmpb_pool, need * ctx->ck * kExt3)) {
+    ctx->err = "out of device memory for the replay grid blocks";
+    ctx->kept_ok = false;
+    return DM_ERR_CUDA;
+  }
+  ctx->blk_cap = need;
   return DM_OK;
 }
 
@@ -488,10 +511,29 @@ int step_impl(DmContext* ctx, const float* cvo, const float* act, float* obs, cu
       DM_CUDA(cudaMemsetAsync(const_cast<float*>(step_act(ctx, t)), 0, (size_t)E * G * sizeof(float), ctx->stream));
   }
   const int S = ctx->cfg.substeps;
+  // The step that fills the tape keeps its segment (one segment per control
+  // step): intermediate states into the segment buffer, sort and grid blocks
+  // into the per-substep slots, exactly as the replay would produce them.
+  // (sized from the earlier steps' largest active-tile count plus a margin;
+  // tiles beyond it are not dumped and the step is then replayed as usual)
+  bool keep = ctx->ck == S && S > 1 && t == ctx->cfg.max_steps - 1 && ctx->max_active_seen > 0;
+  if (keep) {
+    const size_t want = (size_t)ctx->max_active_seen + ctx->max_active_seen / 4 + 64;
+    if (ensure_blk_pool(ctx, want) != DM_OK) {
+      keep = false;  // not enough memory to keep it: replay in the backward
+      ctx->err.clear();
+    }
+  }
+  ctx->kept_t = -1;
+  ctx->kept_ok = false;
   for (int q = 0; q < S; ++q) {
     const int s = t * S + q;
     ctx->P.fiso = s > 0;  // every state but the initial one is a G2P output
-    forward_substep(ctx, fwd_state(ctx, s), fwd_state(ctx, s + 1), t, q, q == 0, 0, false);
+    if (keep)
+      forward_substep(ctx, seg_state(ctx, t * S, s), q + 1 < S ? seg_state(ctx, t * S, s + 1) : fwd_state(ctx, s + 1),
+                      t, q, q == 0, q, true);
+    else
+      forward_substep(ctx, fwd_state(ctx, s), fwd_state(ctx, s + 1), t, q, q == 0, 0, false);
   }
   float* o = ctx->obs_tape + (size_t)t * E * ctx->od;
   PROF_BEGIN(ctx, 6);
@@ -503,6 +545,10 @@ int step_impl(DmContext* ctx, const float* cvo, const float* act, float* obs, cu
   const int rc = check_flags(ctx, true);
   if (rc != DM_OK) return rc;
   ctx->steps = t + 1;
+  if (keep && (size_t)ctx->max_active_seen <= ctx->blk_cap) {  // every tile's blocks fit the pool
+    ctx->kept_t = t;
+    ctx->kept_ok = true;
+  }
   return DM_OK;
 }
 
@@ -517,20 +563,12 @@ int backward_begin(DmContext* ctx, const float* dfx, const float* dfv, const flo
     return DM_ERR_ARG;
   }
   {
-    // grid-block pool for one replayed segment: exactly the forward pass's
+    // grid-block pool for one replayed segment: at least the forward pass's
     // largest active-tile count (the replay is bit-identical to it)
     const size_t need = (size_t)(ctx->max_active_seen > 0 ? ctx->max_active_seen : 1);
     if (ctx->blk_cap < need) {
-      if (ctx->gvb_pool) cudaFree(ctx->gvb_pool);
-      if (ctx->gmpb_pool) cudaFree(ctx->gmpb_pool);
-      ctx->bytes -= 2 * ctx->blk_cap * ctx->ck * kExt3 * sizeof(float4);
-      ctx->gvb_pool = ctx->gmpb_pool = nullptr;
-      ctx->blk_cap = 0;
-      if (!dalloc(ctx, &ctx->gvb_pool, need * ctx->ck * kExt3) || !dalloc(ctx, &ctx->gmpb_pool, need * ctx->ck * kExt3)) {
-        ctx->err = "backward: out of device memory for the replay grid blocks";
-        return DM_ERR_CUDA;
-      }
-      ctx->blk_cap = need;
+      ctx->kept_ok = false;  // a reallocated pool loses the kept segment's blocks
+      if (ensure_blk_pool(ctx, need) != DM_OK) return DM_ERR_CUDA;
     }
   }
   DM_CUDA(cudaMemsetAsync(ctx->gcvo, 0, (size_t)T * E * Kc * 9 * sizeof(double), ctx->stream));
@@ -591,10 +629,11 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
     PROF_END(ctx, 7);
     ++ctx->launches;
   }
+  const bool kept = t == ctx->kept_t && ctx->kept_ok;  // the forward kept this step's segment
   for (int s0 = s_end - ck; s0 >= t * S; s0 -= ck) {
     // replay the segment's forward (tape.hpp:229-233), keeping every
     // substep's sort and grid blocks for its adjoint
-    for (int q = 0; q < ck; ++q) {
+    for (int q = 0; q < ck && !kept; ++q) {
       const int s = s0 + q;
       const StateView So = q + 1 < ck ? seg_state(ctx, s0, s + 1) : view(ctx->tail, ctx->tail_attr, ctx->Ntot);
       ctx->P.fiso = s > 0;
@@ -602,7 +641,9 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
     }
     for (int q = ck - 1; q >= 0; --q) {
       const int s = s0 + q;
-      const StateView Sn = q + 1 < ck ? seg_state(ctx, s0, s + 1) : view(ctx->tail, ctx->tail_attr, ctx->Ntot);
+      const StateView Sn = q + 1 < ck ? seg_state(ctx, s0, s + 1)
+                       : kept ? store_view(ctx, (s + 1) / ck)
+                              : view(ctx->tail, ctx->tail_attr, ctx->Ntot);
       ctx->P.fiso = s > 0;
       backward_substep(ctx, seg_state(ctx, s0, s), Sn, t, q, ctx->adj[cur], ctx->adj[cur ^ 1]);
       cur ^= 1;
@@ -610,6 +651,7 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
   }
   ctx->bwd_cur = cur;
   ctx->bwd_t = t - 1;
+  if (!kept) ctx->kept_ok = false;  // a replay overwrote the segment buffer and slots
   int rc = DM_OK;
   if (dcvo_t && ctx->P.K > 0)
     rc = copy_out_f32(ctx, dcvo_t, ctx->gcvo + (size_t)t * E * Kc * 9, (size_t)E * Kc * 9, kout);
@@ -944,6 +986,8 @@ int reset_lattice_impl(DmContext* ctx, const DmLatticeReset* spec, unsigned long
     DM_CUDA(cudaMemcpyAsync(odelta, d_delta, (size_t)E * 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   ctx->steps = 0;
   ctx->bwd_t = -1;
+  ctx->kept_t = -1;
+  ctx->kept_ok = false;
   ctx->poisoned = false;
   const int rc = reset_flags(ctx);  // synchronises the stream
   if (rc != DM_OK) return rc;
@@ -1061,6 +1105,7 @@ int dm_observe_device(DmContext* ctx, const float* cvo, float* obs) {
 int dm_debug_sort(DmContext* ctx, int* keys, int* perm) {
   if (!ctx || !ctx->store) return DM_ERR_ARG;
   const int s = ctx->steps * ctx->cfg.substeps;
+  ctx->kept_ok = false;  // slot 0 is overwritten
   launch_bin(ctx, fwd_state(ctx, s), slot(ctx, 0), 0, 0);
   const size_t N = ctx->Ntot;
   std::vector<int> p(N);

@@ -974,7 +974,8 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
                                                      const int* __restrict__ tile_count, const int4* __restrict__ active,
                                                      const float4* __restrict__ gv, DevFlags* flags, const int* nact,
                                                      int substep, const float4* __restrict__ gmp,
-                                                     float4* __restrict__ out_gv, float4* __restrict__ out_gmp, int* __restrict__ wq) {
+                                                     float4* __restrict__ out_gv, float4* __restrict__ out_gmp, int* __restrict__ wq,
+                                                     int dump_cap) {
   __shared__ __align__(16) float4 vg[kWarps][2][kExt3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_active = *(const volatile int*)nact;
@@ -1006,7 +1007,7 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
     cp_async_wait<1>();  // this tile's grid has landed
     __syncwarp();
     float4* vw = vg[warp][buf];
-    if (out_gv) {  // segment replay: keep the tile's grid for the adjoint substep
+    if (out_gv && a < dump_cap) {  // segment replay: keep the tile's grid for the adjoint substep
       for (int i = lane; i < kExt3; i += 32) out_gv[(size_t)a * kExt3 + i] = vw[i];
       load_tile_grid(P, gmp, e, o, out_gmp + (size_t)a * kExt3, lane);
     }
