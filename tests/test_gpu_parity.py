@@ -263,3 +263,18 @@ def test_cfg4_env_matches_oracle():
                                   loss=sc.loss)
         assert np.allclose(out["obs"][:, e, :3], obs_ref[:, :3], rtol=1e-5, atol=1e-6)
         assert np.allclose(out["obs"][:, e, 3:], obs_ref[:, 3:], rtol=1e-3, atol=1e-7)
+
+
+def test_kept_last_segment_equals_replay_bitwise():
+    """The step that fills the tape keeps its segment from the forward pass
+    and the backward skips its replay; a context with spare tape capacity
+    replays it.  Gradients and states are bit-identical (fluid: the one-word
+    F storage is exercised too)."""
+    sc = scenes.config4(seed=5, n_envs=3, n_ctrl=2, n_sub=6, lattice_counts=(8, 8, 4))
+    out = []
+    for spare in (0, 1):
+        b = api.from_scene(sc, max_steps=sc.n_ctrl + spare)
+        out.append(api.run_scene(b, sc))
+        b.close()
+    for k in ("obs", "x", "v", "F", "C", "cvo", "E"):
+        assert np.array_equal(out[0][k], out[1][k]), k
