@@ -746,7 +746,10 @@ __device__ __forceinline__ void load_pstate(const StateView& S, int src, PState&
 // into the warp's 6^3 shared block (lanes = stencil nodes), write the block.
 // The next chunk's state loads are in flight during the current scatter.
 template <int LAW>
-__global__ void __launch_bounds__(kWarps * 32, 4) k_p2g(DevParams P, StateView S, const int* __restrict__ perm,
+#ifndef DM_P2G_MINB
+#define DM_P2G_MINB 4
+#endif
+__global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, StateView S, const int* __restrict__ perm,
                                                      const int* __restrict__ tile_start,
                                                      const int* __restrict__ tile_count, const int4* __restrict__ active,
                                                      const float* __restrict__ act, float4* __restrict__ blocks,
