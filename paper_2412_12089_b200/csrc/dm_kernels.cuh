@@ -923,7 +923,10 @@ __device__ __forceinline__ size_t node_lin(const DevParams& P, int e, const int 
 // (mpm.hpp:256-305 + extensions), write (mass, momentum) and velocity to the
 // dense per-env grid.
 template <int MAXC, int CK>
-__global__ void __launch_bounds__(kWarps * 32, 5) k_grid(DevParams P, const int* __restrict__ tile_count,
+#ifndef DM_GRID_MINB
+#define DM_GRID_MINB 5
+#endif
+__global__ void __launch_bounds__(kWarps * 32, DM_GRID_MINB) k_grid(DevParams P, const int* __restrict__ tile_count,
                                                       const int4* __restrict__ active, const float* __restrict__ cvo,
                                                       const float4* __restrict__ blocks, float4* __restrict__ gmp,
                                                       float4* __restrict__ gv, const int* nact, int* __restrict__ wq) {
