@@ -216,12 +216,14 @@ struct Svd {
   R s[3];
 };
 
+// Returns whether it rotated (a sweep without any rotation leaves g, v
+// unchanged, so later sweeps would too: svd3 stops there, bit-identically).
 template <class R>
-DM_HD void jacobi_rot(m3<R>& g, m3<R>& v, int p, int q) {
+DM_HD bool jacobi_rot(m3<R>& g, m3<R>& v, int p, int q) {
   const R a = g(0, p) * g(0, p) + g(1, p) * g(1, p) + g(2, p) * g(2, p);
   const R b = g(0, q) * g(0, q) + g(1, q) * g(1, q) + g(2, q) * g(2, q);
   const R c = g(0, p) * g(0, q) + g(1, p) * g(1, q) + g(2, p) * g(2, q);
-  if (r_abs(c) <= R(1e-30) + R(sizeof(R) == 4 ? 1e-8 : 1e-17) * r_sqrt(a * b)) return;
+  if (r_abs(c) <= R(1e-30) + R(sizeof(R) == 4 ? 1e-8 : 1e-17) * r_sqrt(a * b)) return false;
   const R zeta = (b - a) / (R(2) * c);
   const R t = (zeta >= R(0) ? R(1) : R(-1)) / (r_abs(zeta) + r_sqrt(R(1) + zeta * zeta));
   const R cs = R(1) / r_sqrt(R(1) + t * t);
@@ -235,6 +237,7 @@ DM_HD void jacobi_rot(m3<R>& g, m3<R>& v, int p, int q) {
     v(r, p) = cs * vp - sn * vq;
     v(r, q) = sn * vp + cs * vq;
   }
+  return true;
 }
 
 template <class R>
@@ -242,9 +245,10 @@ DM_HD Svd<R> svd3(const m3<R>& f) {
   m3<R> g = f, v = meye<R>();
   const int sweeps = sizeof(R) == 4 ? 6 : 12;
   for (int s = 0; s < sweeps; ++s) {
-    jacobi_rot(g, v, 0, 1);
-    jacobi_rot(g, v, 0, 2);
-    jacobi_rot(g, v, 1, 2);
+    bool rot = jacobi_rot(g, v, 0, 1);
+    rot = jacobi_rot(g, v, 0, 2) || rot;
+    rot = jacobi_rot(g, v, 1, 2) || rot;
+    if (!rot) break;  // converged: the remaining sweeps would not change g or v
   }
   if (det(v) < R(0)) {
 #pragma unroll
