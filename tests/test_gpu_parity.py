@@ -322,3 +322,17 @@ def test_gradient_parity_mixed_materials():
     for m in range(2):
         if abs(ref["E"][m]) > 0:
             assert abs(g["grad"]["E"][0, m] - ref["E"][m]) <= 3e-3 * abs(ref["E"][m]), m
+
+
+def test_gradient_parity_many_actuation_groups():
+    """12 actuation groups (the 16-group adjoint instantiation)."""
+    rng = np.random.default_rng(23)
+    st = to_f32_state(random_block(rng, 160, 0.42, 0.58, groups=12))
+    sim = dict(SIM16, dt=2e-4)
+    act = rng.uniform(-1, 1, (2, 12))
+    loss = {"kind": "var_z"}
+    ref = O.rollout_grad(sim, [LAWS["neo_hookean"]], [], st, 2, 4, loss, act=act, seg=1)
+    g = gpu_rollout(sim, [LAWS["neo_hookean"]], [], [st], 2, 4, act=act, loss=loss, grad=True)
+    _grad_check(g, ref)
+    a, r = g["grad"]["act"][:, 0], ref["act"]
+    assert cosine(a.ravel(), r.ravel()) >= 0.999 and rel_l2(a.ravel(), r.ravel()) <= 1e-3
