@@ -1,22 +1,28 @@
 // sm_100a kernels for the batched MLS-MPM substep and its adjoint.
 //
 // Layout:
-//   particle state  SoA fp32 [24][Ntot]: x(3) v(3) F(9, row-major) C(9),
-//                   env-major; plus one packed u32 attribute per particle
-//                   (original index | material | actuation group)
+//   particle state  AoSoA fp32, blocks of 32 particles x 24 fields
+//                   (x 3, v 3, F 9 row-major, C 9), env-major; plus one packed
+//                   u32 attribute per particle (original index | material |
+//                   actuation group).  Fluid G2P outputs store F(0,0) only.
 //   bins            4x4x4-cell tiles; per env a dense table of tile start /
-//                   count into the env's stably sorted particle order
+//                   count into the env's stably sorted particle order, an
+//                   env-ordered active-tile list and a largest-first work list
 //   grid            per active tile a 6x6x6 node block (fp32 mass, momentum)
 //                   accumulated in shared memory and written once; a node's
 //                   value is the sum of the (<= 8) blocks that cover it, taken
 //                   in ascending tile order, so every transfer is
 //                   deterministic and atomic-free
 //
-// One warp owns one tile.  Constitutive / per-particle math runs with lanes =
-// particles; the stencil scatter runs with lanes = the 27 stencil nodes,
-// serially over the chunk's particles, so shared-memory accumulation needs no
-// atomics and has a fixed order (bit-reproducible replays: the recompute-on-
-// backward contract of tape.hpp:234-241).
+// Persistent warps take tiles from the work list through a per-launch atomic
+// counter; one warp owns one tile at a time.  Constitutive / per-particle
+// math runs with lanes = particles; the stencil scatter runs with lanes = the
+// 27 stencil nodes (3 groups x 9 columns), serially over each group's
+// segment of the staged chunk, so shared-memory accumulation needs no atomics
+// and has a fixed order (bit-reproducible replays: the recompute-on-backward
+// contract of tape.hpp:234-241).  Particle and grid loads are software
+// pipelined (next chunk in flight during the current one; cp.async for tile
+// grids and the P2G-adjoint staging).
 #pragma once
 
 #include <cstdint>
