@@ -223,11 +223,30 @@ DM_HD bool jacobi_rot(m3<R>& g, m3<R>& v, int p, int q) {
   const R a = g(0, p) * g(0, p) + g(1, p) * g(1, p) + g(2, p) * g(2, p);
   const R b = g(0, q) * g(0, q) + g(1, q) * g(1, q) + g(2, q) * g(2, q);
   const R c = g(0, p) * g(0, q) + g(1, p) * g(1, q) + g(2, p) * g(2, q);
-  if (r_abs(c) <= R(1e-30) + R(sizeof(R) == 4 ? 1e-8 : 1e-17) * r_sqrt(a * b)) return false;
-  const R zeta = (b - a) / (R(2) * c);
-  const R t = (zeta >= R(0) ? R(1) : R(-1)) / (r_abs(zeta) + r_sqrt(R(1) + zeta * zeta));
-  const R cs = R(1) / r_sqrt(R(1) + t * t);
-  const R sn = cs * t;
+  R cs, sn;
+#ifdef __CUDA_ARCH__
+  if constexpr (sizeof(R) == 4) {
+    // fp32 on the device: the same rotation from MUFU rsqrt/rcp instead of
+    // three IEEE sqrt and three IEEE divides.  |c| <= 1e-8 sqrt(ab) is
+    // tested squared; t = sgn(b-a) 2c / (|b-a| + sqrt((b-a)^2 + 4c^2)) is
+    // the smaller root of t^2 + 2 zeta t - 1 = 0, zeta = (b-a)/(2c).
+    if (c * c <= 1e-16f * a * b) return false;
+    const float d = b - a, s2 = d * d + 4.f * c * c;
+    const float den = fabsf(d) + s2 * rsqrtf(s2);
+    const float t = __fdividef(d >= 0.f ? 2.f * c : -2.f * c, den);
+    const float q = 1.f + t * t;
+    const float c0 = rsqrtf(q);
+    cs = c0 * fmaf(-0.5f * q * c0, c0, 1.5f);  // one Newton step: V stays orthonormal to ~1 ulp
+    sn = cs * t;
+  } else
+#endif
+  {
+    if (r_abs(c) <= R(1e-30) + R(sizeof(R) == 4 ? 1e-8 : 1e-17) * r_sqrt(a * b)) return false;
+    const R zeta = (b - a) / (R(2) * c);
+    const R t = (zeta >= R(0) ? R(1) : R(-1)) / (r_abs(zeta) + r_sqrt(R(1) + zeta * zeta));
+    cs = R(1) / r_sqrt(R(1) + t * t);
+    sn = cs * t;
+  }
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
     const R gp = g(r, p), gq = g(r, q);
