@@ -63,10 +63,11 @@ DM_HD Hencky<R> hencky(const m3<R>& f, R cy) {
   for (int i = 0; i < 3; ++i) h.dev[i] = h.eps[i] - h.m;
   h.N = r_sqrt(h.dev[0] * h.dev[0] + h.dev[1] * h.dev[1] + h.dev[2] * h.dev[2] + R(1e-30));
   const R dgamma = h.N - cy;
+  const R iN = R(1) / h.N;
   h.yield = dgamma > R(0);
-  h.k = cy / h.N;
+  h.k = cy * iN;
   if (h.yield) {
-    const R s = dgamma / h.N;
+    const R s = dgamma * iN;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       h.epsp[i] = h.eps[i] - h.dev[i] * s;
@@ -145,25 +146,26 @@ template <class R>
 DM_HD m3<R> hencky_stress_vjp(const Svd<R>& sv, const R e[3], R mu, R lam, const m3<R>& Pbar, R* mubar,
                               R* lambar) {
   const R tr = e[0] + e[1] + e[2];
+  const R is[3] = {R(1) / sv.s[0], R(1) / sv.s[1], R(1) / sv.s[2]};
   R phi[3], jd[3][3];
 #pragma unroll
-  for (int i = 0; i < 3; ++i) phi[i] = (R(2) * mu * e[i] + lam * tr) / sv.s[i];
+  for (int i = 0; i < 3; ++i) phi[i] = (R(2) * mu * e[i] + lam * tr) * is[i];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j)
-      jd[i][j] = ((i == j ? R(2) * mu : R(0)) + lam) / (sv.s[j] * sv.s[i]) - (i == j ? phi[i] / sv.s[i] : R(0));
+      jd[i][j] = ((i == j ? R(2) * mu : R(0)) + lam) * (is[j] * is[i]) - (i == j ? phi[i] * is[i] : R(0));
   auto dd = [&](int i, int j) {
     const R L = log_dd(sv.s[i], sv.s[j]);
-    return (R(2) * mu * (sv.s[j] * L - e[j]) - lam * tr) / (sv.s[i] * sv.s[j]);
+    return (R(2) * mu * (sv.s[j] * L - e[j]) - lam * tr) * (is[i] * is[j]);
   };
   const m3<R> ghat = ut_m_v(sv, Pbar);
   if (mubar) {
     R mb = R(0), lb = R(0);
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      mb += ghat(i, i) * R(2) * e[i] / sv.s[i];
-      lb += ghat(i, i) * tr / sv.s[i];
+      mb += ghat(i, i) * R(2) * e[i] * is[i];
+      lb += ghat(i, i) * tr * is[i];
     }
     *mubar += mb;
     *lambar += lb;
@@ -175,13 +177,14 @@ DM_HD m3<R> hencky_stress_vjp(const Svd<R>& sv, const R e[3], R mu, R lam, const
 template <class R>
 DM_HD m3<R> hencky_project_vjp(const Hencky<R>& h, R mu, R cy, const m3<R>& Fpbar, R* mubar) {
   R jd[3][3];
-  const R N2 = h.N * h.N;
+  const R iN = R(1) / h.N, kn2 = h.k * iN * iN;
+  const R is[3] = {R(1) / h.sv.s[0], R(1) / h.sv.s[1], R(1) / h.sv.s[2]};
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      const R de = R(1.0 / 3.0) + h.k * ((i == j ? R(1) : R(0)) - R(1.0 / 3.0)) - h.k * h.dev[i] * h.dev[j] / N2;
-      jd[i][j] = h.sigp[i] * de / h.sv.s[j];
+      const R de = R(1.0 / 3.0) + h.k * ((i == j ? R(1) : R(0)) - R(1.0 / 3.0)) - kn2 * h.dev[i] * h.dev[j];
+      jd[i][j] = h.sigp[i] * de * is[j];
     }
   auto dd = [&](int i, int j) {
     const R L = log_dd(h.sv.s[i], h.sv.s[j]);
@@ -194,8 +197,8 @@ DM_HD m3<R> hencky_project_vjp(const Hencky<R>& h, R mu, R cy, const m3<R>& Fpba
     // c_y = sigma_y / (c mu): d c_y / d mu = -c_y / mu; d e'_i / d c_y = dev_i / N
     R s = R(0);
 #pragma unroll
-    for (int i = 0; i < 3; ++i) s += ghat(i, i) * h.sigp[i] * h.dev[i] / h.N;
-    *mubar += s * (-cy / mu);
+    for (int i = 0; i < 3; ++i) s += ghat(i, i) * h.sigp[i] * h.dev[i];
+    *mubar += s * iN * (-cy / mu);
   }
   return isotropic_vjp(h.sv, ghat, h.sigp, jd, dd(0, 1), dd(0, 2), dd(1, 2));
 }
@@ -211,12 +214,17 @@ DM_HD void law_stress_vjp(const Law<R>& L, const m3<R>& F, R act, const m3<R>& P
       const Svd<R> sv = svd3(F);
       const m3<R> Rot = mul_bt(sv.u, sv.v);
       const m3<R> ph = ut_m_v(sv, Pbar);
+      // skew part: wr(i, j) = -wr(j, i) = (ph(i, j) - ph(j, i)) / (s_i + s_j)
+      const R w01 = (ph(0, 1) - ph(1, 0)) / (sv.s[0] + sv.s[1]);
+      const R w02 = (ph(0, 2) - ph(2, 0)) / (sv.s[0] + sv.s[2]);
+      const R w12 = (ph(1, 2) - ph(2, 1)) / (sv.s[1] + sv.s[2]);
       m3<R> wr = mzero<R>();
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j)
-          if (i != j) wr(i, j) = (ph(i, j) - ph(j, i)) / (sv.s[i] + sv.s[j]);
+      wr(0, 1) = w01;
+      wr(1, 0) = -w01;
+      wr(0, 2) = w02;
+      wr(2, 0) = -w02;
+      wr(1, 2) = w12;
+      wr(2, 1) = -w12;
       const m3<R> dR = u_m_vt(sv, wr);
       const m3<R> cof = cofactor(F);
       Fbar += (Pbar - dR) * (R(2) * L.mu) + cof * (L.lam * ddot(cof, Pbar)) +
