@@ -752,10 +752,35 @@ __device__ __forceinline__ void load_pstate(const StateView& S, int src, PState&
 // Per active tile: stage particle payloads (lanes = particles), scatter runs
 // into the warp's 6^3 shared block (lanes = stencil nodes), write the block.
 // The next chunk's state loads are in flight during the current scatter.
-template <int LAW>
+
+// Drives a per-chunk body (32 particles; chunk k + 1's perm index sits in
+// parity slot (k + 1) & 1; the body loads that chunk and returns chunk
+// k + 3's index for the slot).  Two call sites per iteration suit the short
+// fluid body; the other laws take one call site with the slot selected by
+// parity (the SVD bodies are 3-4x larger and ran 14-70 % faster as a single
+// copy; as a plain lambda called twice they were outlined onto an 880-byte
+// stack).
+template <bool TWO, class Body>
+__device__ __forceinline__ void chunk_loop(Body& body, int cnt, int& s0, int& s1) {
+  if constexpr (TWO) {
+    for (int c0 = 0; c0 < cnt; c0 += 64) {
+      s1 = body(c0, s1);
+      if (c0 + 32 >= cnt) break;
+      s0 = body(c0 + 32, s0);
+    }
+  } else {
+    for (int c0 = 0, k = 0; c0 < cnt; c0 += 32, ++k) {
+      const int sn = body(c0, (k & 1) ? s0 : s1);
+      s0 = (k & 1) ? sn : s0;
+      s1 = (k & 1) ? s1 : sn;
+    }
+  }
+}
+
 #ifndef DM_P2G_MINB
 #define DM_P2G_MINB 4
 #endif
+template <int LAW>
 __global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, StateView S, const int* __restrict__ perm,
                                                      const int* __restrict__ tile_start,
                                                      const int* __restrict__ tile_count, const int4* __restrict__ active,
@@ -783,7 +808,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, S
     scatter_zero(bw, lane);
     RunAcc ra;
     run_reset(ra);
-    auto chunk = [&](int c0, int& s_next) {
+    auto chunk = [&](int c0, int s_next) __attribute__((always_inline)) -> int {
       if (c0 + lane < cnt) {
         Stencil<float> sc;
         make_stencil(ps.x, P.inv_dx, (double)P.dx, P.dims, sc);
@@ -802,14 +827,11 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, S
       __syncwarp();
       // software pipeline: issue the next chunk's loads before this chunk's scatter
       if (c0 + 32 + lane < cnt) load_pstate<LAW>(S, s_next, ps, P.fiso);
-      s_next = c0 + 96 + lane < cnt ? prow[c0 + 96 + lane] : 0;
+      const int s_new = c0 + 96 + lane < cnt ? prow[c0 + 96 + lane] : 0;
       scatter_runs<true>(bw, pw, min(32, cnt - c0), lane, ra);
+      return s_new;
     };
-    for (int c0 = 0; c0 < cnt; c0 += 64) {
-      chunk(c0, s1);
-      if (c0 + 32 >= cnt) break;
-      chunk(c0 + 32, s0);
-    }
+    chunk_loop<LAW == kFluid>(chunk, cnt, s0, s1);
     scatter_store(bw, lane, ra, blocks + tix * kExt3);
   }
 }
@@ -1116,7 +1138,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
     run_reset(ra);
     cp_async_wait<0>();
     __syncwarp();
-    auto chunk = [&](int c0, int& s_next) {
+    auto chunk = [&](int c0, int s_next) __attribute__((always_inline)) -> int {
       if (c0 + lane < cnt) {
         const size_t dst = row + c0 + lane;
         Stencil<float> sc;
@@ -1159,14 +1181,11 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
         load_xF<LAW>(S, s_next, x, F, P.fiso);
         at = S.attr[s_next];
       }
-      s_next = c0 + 96 + lane < cnt ? perm[row + c0 + 96 + lane] : 0;
+      const int s_new = c0 + 96 + lane < cnt ? perm[row + c0 + 96 + lane] : 0;
       scatter_runs<false>(aw, pw, min(32, cnt - c0), lane, ra);
+      return s_new;
     };
-    for (int c0 = 0; c0 < cnt; c0 += 64) {
-      chunk(c0, s1);
-      if (c0 + 32 >= cnt) break;
-      chunk(c0 + 32, s0);
-    }
+    chunk_loop<LAW == kFluid>(chunk, cnt, s0, s1);
     scatter_store(aw, lane, ra, ablocks + tix * kExt3);
 #pragma unroll
     for (int m = 0; m < NM; ++m)
