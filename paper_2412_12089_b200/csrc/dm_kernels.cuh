@@ -815,7 +815,12 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, S
         const Law<float> L = law_of<LAW>(P, attr_mat(ps.at));
         const float av = act ? act[e * P.G + min(attr_group(ps.at), P.G - 1)] : 0.f;
         bool bad = false;
-        const m3<float> A = p2g_affine(L, T, ps.F, ps.C, av, &bad);
+        // fluid with an isotropic F (fiso): a literal-zero diagonal F lets the
+        // compiler drop the off-diagonal work (same values: the products with
+        // the zeros vanish exactly)
+        const m3<float> A = (LAW == kFluid && P.fiso)
+                                ? p2g_affine(L, T, mdiag(ps.F.a[0], ps.F.a[0], ps.F.a[0]), ps.C, av, &bad)
+                                : p2g_affine(L, T, ps.F, ps.C, av, &bad);
         if (bad) report(flags, e, substep, 0, attr_index(ps.at), attr_mat(ps.at), kErrDetF);
         v3<float> q;
         m3<float> Ad;
@@ -1165,7 +1170,11 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
         m3<float> Cn;
 #pragma unroll
         for (int q = 0; q < 9; ++q) Cn.a[q] = Sn.c(15 + q, dst);
-        g2p_vjp_given(law_of<LAW>(P, mi), T, sc, getv, F, vn, Cn, xb, vb, Cb, Fb, xp, Fp, gq, Bd, mu_l);
+        if (LAW == kFluid && P.fiso)  // literal-zero diagonal F (see k_p2g)
+          g2p_vjp_given(law_of<LAW>(P, mi), T, sc, getv, mdiag(F.a[0], F.a[0], F.a[0]), vn, Cn, xb, vb, Cb, Fb, xp, Fp,
+                        gq, Bd, mu_l);
+        else
+          g2p_vjp_given(law_of<LAW>(P, mi), T, sc, getv, F, vn, Cn, xb, vb, Cb, Fb, xp, Fp, gq, Bd, mu_l);
 #pragma unroll
         for (int m = 0; m < NM; ++m)
           if (m == mi) mub[m] += mu_l;
@@ -1357,7 +1366,11 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
       const int mi = attr_mat(at), gi = min(attr_group(at), P.G > 0 ? P.G - 1 : 0);
       const float av = act ? act[e * P.G + gi] : 0.f;
       float mu_l = 0.f, la_l = 0.f, ac_l = 0.f;
-      p2g_vjp_sep(law_of<LAW>(P, mi), T, sc, getmb, v, F, C, av, xb, vb, Fb, Cb, mu_l, la_l, ac_l);
+      if (LAW == kFluid && P.fiso)  // literal-zero diagonal F (see k_p2g)
+        p2g_vjp_sep(law_of<LAW>(P, mi), T, sc, getmb, v, mdiag(F.a[0], F.a[0], F.a[0]), C, av, xb, vb, Fb, Cb, mu_l,
+                    la_l, ac_l);
+      else
+        p2g_vjp_sep(law_of<LAW>(P, mi), T, sc, getmb, v, F, C, av, xb, vb, Fb, Cb, mu_l, la_l, ac_l);
 #pragma unroll
       for (int m = 0; m < NM; ++m)
         if (m == mi) {
