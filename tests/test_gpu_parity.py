@@ -336,3 +336,29 @@ def test_gradient_parity_many_actuation_groups():
     _grad_check(g, ref)
     a, r = g["grad"]["act"][:, 0], ref["act"]
     assert cosine(a.ravel(), r.ravel()) >= 0.999 and rel_l2(a.ravel(), r.ravel()) <= 1e-3
+
+
+# ---------------- chunk boundaries inside one tile ----------------
+
+@pytest.mark.parametrize("law", ["fluid", "elastoplastic", "fixed_corotated"])
+@pytest.mark.parametrize("n", [1, 31, 32, 33, 64, 65, 97, 130])
+def test_one_tile_chunk_counts(law, n):
+    """Every particle in one 4^3-cell tile (base cells 4..7 per axis): the
+    tile kernels walk it in 32-particle chunks with the perm index of chunk
+    k + 1 in parity slot (k + 1) & 1 (two call sites per iteration for fluid,
+    one parity-selected site for the SVD laws) -- counts around the chunk
+    boundaries, forward and gradients against the oracle."""
+    rng = np.random.default_rng(1000 + n)
+    st = to_f32_state(random_block(rng, n, 0.29, 0.52))
+    ref, _, _ = O.rollout(SIM16, [LAWS[law]], [], st, 1, 1)
+    g = gpu_rollout(SIM16, [LAWS[law]], [], [st], 1, 1)["state"]
+    for k in "xvFC":
+        assert field_rel(g[k][0], ref[k], n) <= 1e-5, k
+    loss = {"kind": "var_z"}
+    refg = O.rollout_grad(SIM16, [LAWS[law]], [], st, 2, 3, loss, seg=1)
+    gg = gpu_rollout(SIM16, [LAWS[law]], [], [st], 2, 3, loss=loss, grad=True)
+    for k in "xvFC":
+        a, r = gg["grad"][k][0], refg[k]
+        if np.linalg.norm(r) < 1e-12:
+            continue
+        assert cosine(a, r) >= 0.999 and rel_l2(a, r) <= 1e-3, (k, cosine(a, r), rel_l2(a, r))
