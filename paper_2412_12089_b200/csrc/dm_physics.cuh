@@ -86,13 +86,16 @@ DM_HD Hencky<R> hencky(const m3<R>& f, R cy) {
 // First Piola stress for the P2G (mpm.hpp:212-217 extended).  For the
 // elastoplastic law P is evaluated at the projected strain as the reference
 // does (mpm.hpp:189-196).  *bad set when det F <= 0.
+// memo (optional): receives the SVD / Hencky record of F for the SVD laws,
+// which law_stress_vjp then reuses instead of decomposing F again.
 template <class R>
-DM_HD m3<R> law_stress(const Law<R>& L, const m3<R>& F, R act, bool* bad) {
+DM_HD m3<R> law_stress(const Law<R>& L, const m3<R>& F, R act, bool* bad, Hencky<R>* memo = nullptr) {
   const R J = det(F);
   if (!(J > R(0))) *bad = true;
   switch (L.kind) {
     case kFixedCorotated: {
       const Svd<R> sv = svd3(F);
+      if (memo) memo->sv = sv;
       const m3<R> Rot = mul_bt(sv.u, sv.v);
       return (F - Rot) * (R(2) * L.mu) + cofactor(F) * (L.lam * (J - R(1)));
     }
@@ -109,6 +112,7 @@ DM_HD m3<R> law_stress(const Law<R>& L, const m3<R>& F, R act, bool* bad) {
     }
     case kElastoplastic: {
       const Hencky<R> h = hencky(F, L.cy);
+      if (memo) *memo = h;
       const R tr2 = h.epsp[0] + h.epsp[1] + h.epsp[2];
       R ps[3];
 #pragma unroll
@@ -206,12 +210,12 @@ DM_HD m3<R> hencky_project_vjp(const Hencky<R>& h, R mu, R cy, const m3<R>& Fpba
 // Fbar += (dP/dF)^T Pbar; also mu/lambda/actuation cotangents.
 template <class R>
 DM_HD void law_stress_vjp(const Law<R>& L, const m3<R>& F, R act, const m3<R>& Pbar, m3<R>& Fbar, R& mubar,
-                          R& lambar, R& actbar) {
+                          R& lambar, R& actbar, const Hencky<R>* memo = nullptr) {
   const R J = det(F);
   switch (L.kind) {
     case kFixedCorotated: {
       // P = 2 mu (F - R) + lam (J - 1) cof F ; self-adjoint Hessian
-      const Svd<R> sv = svd3(F);
+      const Svd<R> sv = memo ? memo->sv : svd3(F);
       const m3<R> Rot = mul_bt(sv.u, sv.v);
       const m3<R> ph = ut_m_v(sv, Pbar);
       // skew part: wr(i, j) = -wr(j, i) = (ph(i, j) - ph(j, i)) / (s_i + s_j)
@@ -251,7 +255,7 @@ DM_HD void law_stress_vjp(const Law<R>& L, const m3<R>& F, R act, const m3<R>& P
       return;
     }
     case kElastoplastic: {
-      const Hencky<R> h = hencky(F, L.cy);
+      const Hencky<R> h = memo ? *memo : hencky(F, L.cy);
       if (!h.yield) {
         Fbar += hencky_stress_vjp(h.sv, h.eps, L.mu, L.lam, Pbar, &mubar, &lambar);
       } else {

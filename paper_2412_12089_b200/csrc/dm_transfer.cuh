@@ -407,7 +407,8 @@ DM_HD void p2g_vjp_sep(const Law<R>& L, const TransferCtx<R>& t, const Stencil<R
                        const m3<R>& F, const m3<R>& C, R act, v3<R>& xb, v3<R>& vb, m3<R>& Fb, m3<R>& Cb, R& mubar,
                        R& lambar, R& actbar) {
   bool bad = false;
-  const m3<R> P = law_stress(L, F, act, &bad);
+  Hencky<R> memo;  // the SVD laws' decomposition of F, reused by law_stress_vjp
+  const m3<R> P = law_stress(L, F, act, &bad, &memo);
   m3<R> tau = mul_bt(P, F);
   const bool visc = L.kind == kFluid && L.visc != R(0);
   const m3<R> Cs = C + transpose(C);
@@ -475,7 +476,7 @@ DM_HD void p2g_vjp_sep(const Law<R>& L, const TransferCtx<R>& t, const Stencil<R
   }
   const m3<R> Pb = taub * F;
   Fb += mul_at(taub, P);
-  law_stress_vjp(L, F, act, Pb, Fb, mubar, lambar, actbar);
+  law_stress_vjp(L, F, act, Pb, Fb, mubar, lambar, actbar, &memo);
 }
 
 }  // namespace dm
