@@ -212,6 +212,9 @@ Slot slot(DmContext* c, int q) {
   return s;
 }
 
+#ifndef DM_CS_GRID
+#define DM_CS_GRID 2  // k_cellsort is light (32 registers): twice the tile kernels' resident warps
+#endif
 void launch_bin(DmContext* c, const StateView& S, const Slot& q, int sub, int check_vmax) {
   cudaMemsetAsync(q.nact, 0, sizeof(int), c->stream);
   PROF_BEGIN(c, 0);
@@ -228,7 +231,7 @@ void launch_bin(DmContext* c, const StateView& S, const Slot& q, int sub, int ch
   k_order_scatter<<<(unsigned)((c->P.E * c->P.Tn + 2047) / 2048), 256, 0, c->stream>>>(q.active, q.nact, q.ord, q.work);
   c->launches += 2;
   wq_reset(c);
-  k_cellsort<<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, c->ptile, q.perm, c->keys, q.tile_start,
+  k_cellsort<<<c->grid_tiles * DM_CS_GRID, kWarps * 32, 0, c->stream>>>(c->P, S, c->ptile, q.perm, c->keys, q.tile_start,
                                                            q.tile_count, q.work, q.nact, c->flags, c->wq);
   ++c->launches;
   PROF_END(c, 0);
