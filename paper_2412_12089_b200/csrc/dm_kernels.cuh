@@ -756,10 +756,10 @@ __device__ __forceinline__ void load_pstate(const StateView& S, int src, PState&
 // Drives a per-chunk body (32 particles; chunk k + 1's perm index sits in
 // parity slot (k + 1) & 1; the body loads that chunk and returns chunk
 // k + 3's index for the slot).  Two call sites per iteration suit the short
-// fluid body; the other laws take one call site with the slot selected by
-// parity (the SVD bodies are 3-4x larger and ran 14-70 % faster as a single
-// copy; as a plain lambda called twice they were outlined onto an 880-byte
-// stack).
+// bodies (fluid; neo-Hookean in k_p2g: -8 %, but +2 % in k_g2p_adj); the
+// SVD laws take one call site with the slot selected by parity (their bodies
+// are 3-4x larger and ran 14-70 % faster as a single copy; as a plain lambda
+// called twice they were outlined onto an 880-byte stack).
 template <bool TWO, class Body>
 __device__ __forceinline__ void chunk_loop(Body& body, int cnt, int& s0, int& s1) {
   if constexpr (TWO) {
@@ -836,7 +836,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, S
       scatter_runs<true>(bw, pw, min(32, cnt - c0), lane, ra);
       return s_new;
     };
-    chunk_loop<LAW == kFluid>(chunk, cnt, s0, s1);
+    chunk_loop<LAW == kFluid || LAW == kNeoHookean>(chunk, cnt, s0, s1);
     scatter_store(bw, lane, ra, blocks + tix * kExt3);
   }
 }
