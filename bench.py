@@ -258,12 +258,17 @@ def run_ours(args, scene, rank, world, local, dist):
            "E": torch.empty((E, batch.n_materials), dtype=torch.float64, device=dev)}
     torch.cuda.synchronize()
 
+    stream = torch.cuda.ExternalStream(batch.stream_ptr, device=dev)
+
     def rollout_device():
-        batch.set_state(x0, v0, F0, C0, mat, grp)
-        for t in range(T):
-            batch.step(None if cvo_d is None else cvo_d[t], None if act_d is None else act_d[t], obs_d[t])
-        _, dobs = loss_and_dobs_torch(scene.loss, obs_d.transpose(0, 1))
-        batch.backward(dobs=dobs.transpose(0, 1).contiguous(), out=out)
+        # the loss reads obs_d and writes dobs: on the context stream, ordered
+        # with the simulator's kernels (no host synchronisation in the step)
+        with torch.cuda.stream(stream):
+            batch.set_state(x0, v0, F0, C0, mat, grp)
+            for t in range(T):
+                batch.step(None if cvo_d is None else cvo_d[t], None if act_d is None else act_d[t], obs_d[t])
+            _, dobs = loss_and_dobs_torch(scene.loss, obs_d.transpose(0, 1))
+            batch.backward(dobs=dobs.transpose(0, 1).contiguous(), out=out)
 
     # host (pinned) buffers for the end-to-end arm
     def pinned(a, dtype=np.float32):
@@ -294,7 +299,6 @@ def run_ours(args, scene, rank, world, local, dist):
            (sum(a.nbytes for a in hcvo) if K else 0) + (sum(a.nbytes for a in hact) if G else 0) + T * E * 7 * 4)
     d2h = T * E * 7 * 4 + E * N * 24 * 4 + (T * E * K * 9 * 4 if K else 0) + (T * E * G * 4 if G else 0) + E * 8 * batch.n_materials
 
-    stream = torch.cuda.ExternalStream(batch.stream_ptr, device=dev)
     units_rank = E * N * T * S
     # warm-up
     for _ in range(args.warmup):
@@ -317,9 +321,11 @@ def run_ours(args, scene, rank, world, local, dist):
 
     # forward only (the rollout without the backward), same device timing
     def forward_device():
-        batch.set_state(x0, v0, F0, C0, mat, grp)
-        for t in range(T):
-            batch.step(None if cvo_d is None else cvo_d[t], None if act_d is None else act_d[t], obs_d[t])
+        with torch.cuda.stream(stream):
+            batch.set_state(x0, v0, F0, C0, mat, grp)
+            for t in range(T):
+                batch.step(None if cvo_d is None else cvo_d[t], None if act_d is None else act_d[t], obs_d[t])
+            batch.sync()  # forward errors / CFL of the rollout (the backward would read them)
 
     forward_device()
     barrier(dist)

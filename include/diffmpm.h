@@ -182,6 +182,23 @@ int dm_reset_lattice(DmContext* ctx, const DmLatticeReset* spec, unsigned long l
 int dm_reset_lattice_device(DmContext* ctx, const DmLatticeReset* spec, unsigned long long seed, int env_offset,
                             const unsigned char* env_mask, const int* particle_group, double* origin_delta);
 
+/* Synchronises the context stream and reports what the device recorded
+ * since the last synchronising call: the first error in substep order
+ * (mpm.hpp:156-158, 169, 205, 338-339) and one CFL warning per violating
+ * control step (mpm.hpp:355-361, stderr).  Host-pointer entry points do this
+ * after every control step; the *_device entry points do not synchronise, so
+ * their device-detected errors surface at the next synchronising call
+ * (dm_sync, dm_get_state*, dm_observe*, dm_backward*). */
+int dm_sync(DmContext* ctx);
+
+/* Test hook for the replay verification (Tape::backward_segment,
+ * tape.hpp:234-241; test_tape.cpp:311-323): while replaying control step
+ * `step` in the backward pass, flip the lowest mantissa bit of particle
+ * `particle`'s x in env `env` -- a non-deterministic forward.  The backward
+ * then fails with "checkpoint replay: non-deterministic forward (exit value
+ * k changed)".  step = -1 disables it. */
+int dm_debug_inject(DmContext* ctx, int step, int env, int particle);
+
 /* Parity hooks: bin keys / stable permutation of the
  * current state (per env, local indices) and the current physical order's
  * original particle ids. */

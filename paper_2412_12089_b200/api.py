@@ -85,6 +85,8 @@ _SIGS = {
     "dm_observe_device": (C.c_int, [_P] * 3),
     "dm_reset_lattice": (C.c_int, [_P, C.POINTER(DmLatticeReset), C.c_ulonglong, C.c_int, _P, _P, _P]),
     "dm_reset_lattice_device": (C.c_int, [_P, C.POINTER(DmLatticeReset), C.c_ulonglong, C.c_int, _P, _P, _P]),
+    "dm_sync": (C.c_int, [_P]),
+    "dm_debug_inject": (C.c_int, [_P, C.c_int, C.c_int, C.c_int]),
 }
 
 PROF_CLASSES = ("bin", "p2g", "g2p", "g2p_adj", "p2g_adj", "env_reduce", "obs", "obs_adj", "layout", "grid",
@@ -373,6 +375,26 @@ class MpmBatch:
                "E": np.zeros((self.E, self.n_materials), np.float64)}
         self._check(self._L.dm_backward_end(self._h, *(_ptr(res[k]) for k in ("x", "v", "F", "C", "E"))))
         return res
+
+    def sync(self):
+        """Synchronise the context stream and raise what the device recorded
+        since the last synchronising call (dm_sync): the *_device entry points
+        report device-detected errors and CFL warnings lazily."""
+        self._check(self._L.dm_sync(self._h))
+
+    def debug_inject(self, step: int, env: int = 0, particle: int = 0):
+        """Test hook (dm_debug_inject): make the backward's replay of control
+        step `step` non-deterministic (one ulp of one particle's x)."""
+        self._check(self._L.dm_debug_inject(self._h, step, env, particle))
+
+    def torch_stream(self):
+        """The context stream as a torch stream: run torch work that produces
+        or consumes *_device buffers under ``with torch.cuda.stream(...)`` so
+        it is ordered with the simulator's kernels (no host synchronisation)."""
+        import torch
+        if getattr(self, "_tstream", None) is None:
+            self._tstream = torch.cuda.ExternalStream(self.stream_ptr)
+        return self._tstream
 
     def profile(self, enable: bool = True):
         """Returns {class: (ms, launches)} accumulated since the last call and

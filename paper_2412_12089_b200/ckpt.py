@@ -120,10 +120,10 @@ def _unflat(params, arr):
 def _put_opt(c, prefix, opt, params):
     """detail::put_opt (checkpoint_io.hpp:115-120): AdamW moments + step."""
     st = [opt.state.get(p, {}) for p in params]
-    if all("exp_avg" in s for s in st):
-        c[prefix + ".m"] = _flat([s["exp_avg"] for s in st])
-        c[prefix + ".v"] = _flat([s["exp_avg_sq"] for s in st])
-        step = int(float(st[0]["step"]))
+    if all("m" in s for s in st):  # sapo.AdamWRef: moments m, v and the step count (nets.hpp:289-290)
+        c[prefix + ".m"] = _flat([s["m"] for s in st])
+        c[prefix + ".v"] = _flat([s["v"] for s in st])
+        step = int(opt.step_count)
     else:
         c[prefix + ".m"] = np.zeros(0)
         c[prefix + ".v"] = np.zeros(0)
@@ -146,14 +146,14 @@ def _get_opt(c, prefix, opt, params):
         raise CheckpointError("checkpoint: optimizer moment shapes disagree in '" + prefix + "'")
     step = unpack_u64(expect(c, prefix + ".step", 1)[0])
     opt.state.clear()
+    opt.step_count = step
     if m.size:
         o = 0
         for p in params:
             k = p.numel()
             opt.state[p] = {
-                "step": torch.tensor(float(step), dtype=torch.float32),
-                "exp_avg": torch.as_tensor(m[o:o + k], dtype=p.dtype, device=p.device).view_as(p).clone(),
-                "exp_avg_sq": torch.as_tensor(v[o:o + k], dtype=p.dtype, device=p.device).view_as(p).clone()}
+                "m": torch.as_tensor(m[o:o + k], dtype=p.dtype, device=p.device).view_as(p).clone(),
+                "v": torch.as_tensor(v[o:o + k], dtype=p.dtype, device=p.device).view_as(p).clone()}
             o += k
 
 

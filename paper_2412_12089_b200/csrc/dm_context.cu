@@ -8,6 +8,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -80,6 +81,13 @@ struct DmContext {
   DevFlags* h_flags = nullptr;
   float *cvo_tape = nullptr, *act_tape = nullptr, *obs_tape = nullptr;
   double *gcvo = nullptr, *gact = nullptr, *gmu = nullptr, *glam = nullptr;
+  float *obs_cvo = nullptr, *obs_out = nullptr;  // dm_observe's pose and output (never the tape's slots)
+  float* f32_stage = nullptr;                    // fp32 cotangent staging (device)
+  double* dE_dev = nullptr;                      // [E][nmat]
+  unsigned* vmax_hist = nullptr;                 // per recorded step: max |v| component at its start (CFL)
+  int cfl_checked = 0;                           // steps whose CFL word the host has read
+  unsigned long long* replay_bad = nullptr;      // replay-verification word (k_replay_check)
+  int inj_step = -1, inj_env = 0, inj_particle = 0;  // dm_debug_inject
   // optional per-kernel-class CUDA-event timing (bench roofline)
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -104,7 +112,11 @@ namespace {
 template <class T>
 bool dalloc(DmContext* ctx, T** p, size_t n) {
   if (n == 0) n = 1;
-  if (cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)) != cudaSuccess) return false;
+  if (cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)) != cudaSuccess) {
+    cudaGetLastError();  // a failed allocation must not poison later error checks
+    *p = nullptr;
+    return false;
+  }
   ctx->bytes += n * sizeof(T);
   return true;
 }
@@ -373,8 +385,8 @@ std::string fmt_error(DmContext* c, unsigned long long key) {
   const int code = (int)(key & 0xF);
   const int axis = (int)((key >> 4) & 3);
   const unsigned particle = (unsigned)((key >> 6) & 0xFFFFFF);
-  const int sub = (int)((key >> 32) & 0x3FF);
-  const int env = (int)((key >> 42) & 0xFFFF);
+  const int env = (int)((key >> 32) & 0xFFFF);
+  const int sub = (int)((key >> 48) & 0xFFFF);
   char buf[256];
   if (code == kErrP2GInterior) {
     std::snprintf(buf, sizeof(buf), "mpm: particle %u outside grid interior (axis %d) [env %d, substep %d]", particle,
@@ -392,10 +404,20 @@ std::string fmt_error(DmContext* c, unsigned long long key) {
   return buf;
 }
 
-// Reads the device flags after a control step; returns DM_OK or the error.
-int check_flags(DmContext* ctx, bool cfl) {
+// Synchronises the stream and reads the device flags: errors recorded by
+// any launch since the last read (the first one in substep order) and the
+// CFL word of every control step recorded since (mpm.hpp:355-361: checked
+// once per mpm_step on the velocities at its entry; one warning per
+// violating step).  Host entry points call it after every control step;
+// the *_device entry points only at the points that synchronise anyway.
+int check_flags(DmContext* ctx) {
   prof_flush(ctx);
+  const int n_cfl = ctx->steps - ctx->cfl_checked;
+  std::vector<unsigned> vh(n_cfl > 0 ? n_cfl : 0);
   DM_CUDA(cudaMemcpyAsync(ctx->h_flags, ctx->flags, sizeof(DevFlags), cudaMemcpyDeviceToHost, ctx->stream));
+  if (n_cfl > 0)
+    DM_CUDA(cudaMemcpyAsync(vh.data(), ctx->vmax_hist + ctx->cfl_checked, n_cfl * sizeof(unsigned),
+                            cudaMemcpyDeviceToHost, ctx->stream));
   DM_CUDA(cudaStreamSynchronize(ctx->stream));
   DM_CUDA(cudaGetLastError());
   if (ctx->h_flags->max_active > ctx->max_active_seen) ctx->max_active_seen = ctx->h_flags->max_active;
@@ -404,13 +426,14 @@ int check_flags(DmContext* ctx, bool cfl) {
     ctx->poisoned = true;
     return DM_ERR_RUNTIME;
   }
-  if (cfl) {
+  for (int i = 0; i < n_cfl; ++i) {
     float vmax;
-    std::memcpy(&vmax, &ctx->h_flags->vmax_bits, sizeof(float));
+    std::memcpy(&vmax, &vh[i], sizeof(float));
     if ((double)vmax * ctx->cfg.dt >= ctx->cfg.dx)
       std::fprintf(stderr, "mpm_step: CFL violated (max|v| dt = %g >= dx = %g)\n", (double)vmax * ctx->cfg.dt,
                    ctx->cfg.dx);
   }
+  if (n_cfl > 0) ctx->cfl_checked = ctx->steps;
   return DM_OK;
 }
 
@@ -442,6 +465,7 @@ int set_state_impl(DmContext* ctx, const float* x, const float* v, const float* 
                                                                      ctx->P.N, S0);
   ++ctx->launches;
   ctx->steps = 0;
+  ctx->cfl_checked = 0;
   ctx->bwd_t = -1;
   ctx->kept_t = -1;
   ctx->kept_ok = false;
@@ -519,9 +543,15 @@ int step_impl(DmContext* ctx, const float* cvo, const float* act, float* obs, cu
   // into the per-substep slots, exactly as the replay would produce them.
   // (sized from the earlier steps' largest active-tile count plus a margin;
   // tiles beyond it are not dumped and the step is then replayed as usual)
-  bool keep = ctx->ck == S && S > 1 && t == ctx->cfg.max_steps - 1 && ctx->max_active_seen > 0;
+  bool keep = ctx->ck == S && S > 1 && t == ctx->cfg.max_steps - 1;
+  if (keep && kout == cudaMemcpyDeviceToDevice) {  // the device path reads the flags lazily: refresh them
+    const int rc = check_flags(ctx);
+    if (rc != DM_OK) return rc;
+  }
+  keep = keep && ctx->max_active_seen > 0;
   if (keep) {
-    const size_t want = (size_t)ctx->max_active_seen + ctx->max_active_seen / 4 + 64;
+    size_t want = (size_t)ctx->max_active_seen + ctx->max_active_seen / 4 + 64;
+    if (std::getenv("DIFFMPM_DEBUG_FAIL_KEEP_POOL")) want = (size_t)1 << 40;  // test hook: the pool cannot be allocated
     if (ensure_blk_pool(ctx, want) != DM_OK) {
       keep = false;  // not enough memory to keep it: replay in the backward
       ctx->err.clear();
@@ -529,15 +559,18 @@ int step_impl(DmContext* ctx, const float* cvo, const float* act, float* obs, cu
   }
   ctx->kept_t = -1;
   ctx->kept_ok = false;
+  DM_CUDA(cudaMemsetAsync(&ctx->flags->vmax_bits, 0, sizeof(unsigned), ctx->stream));  // this step's CFL word
   for (int q = 0; q < S; ++q) {
     const int s = t * S + q;
     ctx->P.fiso = s > 0;  // every state but the initial one is a G2P output
     if (keep)
       forward_substep(ctx, seg_state(ctx, t * S, s), q + 1 < S ? seg_state(ctx, t * S, s + 1) : fwd_state(ctx, s + 1),
-                      t, q, q == 0, q, true);
+                      t, s, q == 0, q, true);
     else
-      forward_substep(ctx, fwd_state(ctx, s), fwd_state(ctx, s + 1), t, q, q == 0, 0, false);
+      forward_substep(ctx, fwd_state(ctx, s), fwd_state(ctx, s + 1), t, s, q == 0, 0, false);
   }
+  DM_CUDA(cudaMemcpyAsync(ctx->vmax_hist + t, &ctx->flags->vmax_bits, sizeof(unsigned), cudaMemcpyDeviceToDevice,
+                          ctx->stream));
   float* o = ctx->obs_tape + (size_t)t * E * ctx->od;
   PROF_BEGIN(ctx, 6);
   k_obs<<<E, 256, 0, ctx->stream>>>(ctx->P, fwd_state(ctx, (t + 1) * S), step_cvo(ctx, t), (float)ctx->cfg.spill_half,
@@ -545,9 +578,14 @@ int step_impl(DmContext* ctx, const float* cvo, const float* act, float* obs, cu
   PROF_END(ctx, 6);
   ++ctx->launches;
   if (obs) DM_CUDA(cudaMemcpyAsync(obs, o, (size_t)E * ctx->od * sizeof(float), kout, ctx->stream));
-  const int rc = check_flags(ctx, true);
-  if (rc != DM_OK) return rc;
   ctx->steps = t + 1;
+  if (kout != cudaMemcpyDeviceToDevice) {  // host path: errors and the CFL warning of this step now
+    const int rc = check_flags(ctx);
+    if (rc != DM_OK) {
+      ctx->steps = t;
+      return rc;
+    }
+  }
   if (keep && (size_t)ctx->max_active_seen <= ctx->blk_cap) {  // every tile's blocks fit the pool
     ctx->kept_t = t;
     ctx->kept_ok = true;
@@ -565,6 +603,11 @@ int backward_begin(DmContext* ctx, const float* dfx, const float* dfv, const flo
     ctx->err = "backward: no recorded steps";
     return DM_ERR_ARG;
   }
+  {  // forward errors (lazily read on the device path) surface before the backward
+    const int rc = check_flags(ctx);
+    if (rc != DM_OK) return rc;
+  }
+  DM_CUDA(cudaMemsetAsync(ctx->replay_bad, 0xFF, sizeof(unsigned long long), ctx->stream));
   {
     // grid-block pool for one replayed segment: at least the forward pass's
     // largest active-tile count (the replay is bit-identical to it)
@@ -599,14 +642,14 @@ int backward_begin(DmContext* ctx, const float* dfx, const float* dfv, const flo
   return DM_OK;
 }
 
-// Converts an fp64 device array to fp32 into dst (host or device).
+// Converts an fp64 device array to fp32 on the device, into dst (device:
+// directly; host: through the device staging buffer and an async copy).
 int copy_out_f32(DmContext* ctx, float* dst, const double* src, size_t n, cudaMemcpyKind kout) {
-  std::vector<double> h(n);
-  DM_CUDA(cudaMemcpyAsync(h.data(), src, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-  DM_CUDA(cudaStreamSynchronize(ctx->stream));
-  std::vector<float> f(h.begin(), h.end());
-  DM_CUDA(cudaMemcpy(dst, f.data(), n * sizeof(float),
-                     kout == cudaMemcpyDeviceToDevice ? cudaMemcpyHostToDevice : cudaMemcpyHostToHost));
+  float* d = kout == cudaMemcpyDeviceToDevice ? dst : ctx->f32_stage;
+  k_f64_to_f32<<<(unsigned)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024), 256, 0, ctx->stream>>>(n, src, d);
+  ++ctx->launches;
+  if (d != dst) DM_CUDA(cudaMemcpyAsync(dst, d, n * sizeof(float), kout, ctx->stream));
+  DM_CUDA(cudaGetLastError());
   return DM_OK;
 }
 
@@ -640,7 +683,16 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
       const int s = s0 + q;
       const StateView So = q + 1 < ck ? seg_state(ctx, s0, s + 1) : view(ctx->tail, ctx->tail_attr, ctx->Ntot);
       ctx->P.fiso = s > 0;
-      forward_substep(ctx, seg_state(ctx, s0, s), So, t, s - t * S, 0, q, true);
+      forward_substep(ctx, seg_state(ctx, s0, s), So, t, s, 0, q, true);
+    }
+    if (!kept) {
+      // the replayed exit must equal the stored checkpoint bitwise (tape.hpp:234-241)
+      const StateView tl = view(ctx->tail, ctx->tail_attr, ctx->Ntot);
+      if (ctx->inj_step == t)  // dm_debug_inject: a non-deterministic forward
+        k_debug_flip<<<(ctx->P.N + 255) / 256, 256, 0, ctx->stream>>>(ctx->P, tl, ctx->inj_env, ctx->inj_particle);
+      k_replay_check<<<ctx->grid_tiles, 256, 0, ctx->stream>>>(ctx->P, tl, store_view(ctx, (s0 + ck) / ck),
+                                                                ctx->law == kFluid, nullptr, ctx->replay_bad);
+      ctx->launches += 1 + (ctx->inj_step == t);
     }
     for (int q = ck - 1; q >= 0; --q) {
       const int s = s0 + q;
@@ -660,6 +712,8 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
     rc = copy_out_f32(ctx, dcvo_t, ctx->gcvo + (size_t)t * E * Kc * 9, (size_t)E * Kc * 9, kout);
   if (rc == DM_OK && dact_t && ctx->P.G > 0)
     rc = copy_out_f32(ctx, dact_t, ctx->gact + (size_t)t * E * Gc, (size_t)E * Gc, kout);
+  if (rc == DM_OK && kout != cudaMemcpyDeviceToDevice && (dcvo_t || dact_t))
+    DM_CUDA(cudaStreamSynchronize(ctx->stream));  // host outputs are complete on return
   return rc;
 }
 
@@ -681,20 +735,25 @@ int backward_end(DmContext* ctx, float* dx0, float* dv0, float* dF0, float* dC0,
   if (dF0) DM_CUDA(cudaMemcpyAsync(dF0, out + 6 * N, 9 * N * sizeof(float), kout, ctx->stream));
   if (dC0) DM_CUDA(cudaMemcpyAsync(dC0, out + 15 * N, 9 * N * sizeof(float), kout, ctx->stream));
   if (dE) {
-    std::vector<double> mu((size_t)E * 4), la((size_t)E * 4);
-    DM_CUDA(cudaMemcpyAsync(mu.data(), ctx->gmu, mu.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    DM_CUDA(cudaMemcpyAsync(la.data(), ctx->glam, la.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    DM_CUDA(cudaStreamSynchronize(ctx->stream));
-    std::vector<double> g((size_t)E * ctx->nmat);
-    for (int e = 0; e < E; ++e)
-      for (int m = 0; m < ctx->nmat; ++m)
-        g[(size_t)e * ctx->nmat + m] = mu[e * 4 + m] * ctx->dmu_dE[m] + la[e * 4 + m] * ctx->dlam_dE[m];
-    DM_CUDA(cudaMemcpy(dE, g.data(), g.size() * sizeof(double),
-                       kout == cudaMemcpyDeviceToDevice ? cudaMemcpyHostToDevice : cudaMemcpyHostToHost));
+    double* d = kout == cudaMemcpyDeviceToDevice ? dE : ctx->dE_dev;
+    k_dE<<<(E * ctx->nmat + 127) / 128, 128, 0, ctx->stream>>>(E, ctx->nmat, ctx->gmu, ctx->glam, ctx->P, d);
+    ++ctx->launches;
+    if (d != dE) DM_CUDA(cudaMemcpyAsync(dE, d, (size_t)E * ctx->nmat * sizeof(double), kout, ctx->stream));
   }
-  DM_CUDA(cudaStreamSynchronize(ctx->stream));
+  unsigned long long bad = ~0ull;
+  DM_CUDA(cudaMemcpyAsync(&bad, ctx->replay_bad, sizeof(bad), cudaMemcpyDeviceToHost, ctx->stream));
   ctx->bwd_t = -1;
-  return check_flags(ctx, false);
+  const int rc = check_flags(ctx);  // synchronises
+  if (rc != DM_OK) return rc;
+  if (bad != ~0ull) {
+    // Tape::backward_segment's text (tape.hpp:238-240); k indexes the env's
+    // segment exit values in visit order
+    ctx->err = "checkpoint replay: non-deterministic forward (exit value " + std::to_string(bad & 0xFFFFFFFFFFull) +
+               " changed) [env " + std::to_string(bad >> 40) + "]";
+    ctx->poisoned = true;
+    return DM_ERR_RUNTIME;
+  }
+  return DM_OK;
 }
 
 int backward_impl(DmContext* ctx, const float* dobs, const float* dfx, const float* dfv, const float* dfF,
@@ -807,6 +866,8 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
     L.vol = (float)M.volume;
     L.dmu_dE = (float)ctx->dmu_dE[m];
     L.dlam_dE = (float)ctx->dlam_dE[m];
+    P.dmu_dE[m] = ctx->dmu_dE[m];
+    P.dlam_dE[m] = ctx->dlam_dE[m];
     ctx->law_kind[m] = M.kind;
   }
   ctx->law = mats[0].kind;
@@ -866,6 +927,10 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
        dalloc(ctx, &ctx->gcvo, (size_t)cfg->max_steps * P.E * Kc * 9) &&
        dalloc(ctx, &ctx->gact, (size_t)cfg->max_steps * P.E * Gc) && dalloc(ctx, &ctx->gmu, (size_t)P.E * 4) &&
        dalloc(ctx, &ctx->glam, (size_t)P.E * 4);
+  ok = ok && dalloc(ctx, &ctx->obs_cvo, (size_t)P.E * Kc * 9) && dalloc(ctx, &ctx->obs_out, (size_t)P.E * ctx->od) &&
+       dalloc(ctx, &ctx->f32_stage, (size_t)P.E * (Kc * 9 > Gc ? Kc * 9 : Gc)) &&
+       dalloc(ctx, &ctx->dE_dev, (size_t)P.E * num_materials) && dalloc(ctx, &ctx->vmax_hist, (size_t)cfg->max_steps) &&
+       dalloc(ctx, &ctx->replay_bad, 1);
   ok = ok && cudaMallocHost(reinterpret_cast<void**>(&ctx->h_flags), sizeof(DevFlags)) == cudaSuccess;
   if (!ok) {
     char buf[160];
@@ -892,7 +957,8 @@ void dm_destroy(DmContext* ctx) {
                   ctx->perm_all,  ctx->ptile, ctx->tstart_all, ctx->tcount_all, ctx->abase_all, ctx->acount_all,
                   ctx->active_all, ctx->work_all, ctx->ord_all, ctx->nact_all, ctx->tail, ctx->tail_attr, ctx->gvb_pool, ctx->gmpb_pool,
                   ctx->blocks,    ctx->ablocks,    ctx->tile_acc,   ctx->gmp, ctx->gv, ctx->gmb,   ctx->flags, ctx->wq, ctx->cvo_tape,  ctx->act_tape,
-                  ctx->obs_tape,  ctx->dobs_buf, ctx->gcvo,       ctx->gact,       ctx->gmu,        ctx->glam};
+                  ctx->obs_tape,  ctx->dobs_buf, ctx->gcvo,       ctx->gact,       ctx->gmu,        ctx->glam,
+                  ctx->obs_cvo,   ctx->obs_out,  ctx->f32_stage,  ctx->dE_dev,     ctx->vmax_hist,  ctx->replay_bad};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
@@ -988,6 +1054,7 @@ int reset_lattice_impl(DmContext* ctx, const DmLatticeReset* spec, unsigned long
   if (odelta && !dev)
     DM_CUDA(cudaMemcpyAsync(odelta, d_delta, (size_t)E * 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   ctx->steps = 0;
+  ctx->cfl_checked = 0;
   ctx->bwd_t = -1;
   ctx->kept_t = -1;
   ctx->kept_ok = false;
@@ -1077,20 +1144,37 @@ int dm_backward_end_device(DmContext* ctx, float* dx0, float* dv0, float* dF0, f
 }
 int dm_obs_dim(const DmContext* ctx) { return ctx ? ctx->od : DM_OBS_DIM; }
 
+int dm_sync(DmContext* ctx) {
+  if (!ctx || !ctx->store) return DM_ERR_ARG;
+  if (ctx->poisoned) return DM_ERR_RUNTIME;
+  return check_flags(ctx);
+}
+
+int dm_debug_inject(DmContext* ctx, int step, int env, int particle) {
+  if (!ctx || !ctx->store) return DM_ERR_ARG;
+  if (env < 0 || env >= ctx->P.E || particle < 0 || particle >= ctx->P.N) {
+    ctx->err = "dm_debug_inject: env / particle out of range";
+    return DM_ERR_ARG;
+  }
+  ctx->inj_step = step;
+  ctx->inj_env = env;
+  ctx->inj_particle = particle;
+  return DM_OK;
+}
+
 static int observe_impl(DmContext* ctx, const float* cvo, float* obs, cudaMemcpyKind kin, cudaMemcpyKind kout) {
   if (!ctx || !ctx->store) return DM_ERR_ARG;
   if (ctx->poisoned) return DM_ERR_RUNTIME;
   const int E = ctx->P.E, K = ctx->P.K;
-  // stage the pose in the slot after the last recorded step (unused until the next dm_step)
-  const int t = ctx->steps < ctx->cfg.max_steps ? ctx->steps : ctx->cfg.max_steps - 1;
+  // the pose and the output have their own buffers: the tape's recorded
+  // poses and observables stay untouched (a later backward reads the poses)
   DevParams P = ctx->P;
   if (K > 0 && cvo)
-    DM_CUDA(cudaMemcpyAsync(const_cast<float*>(step_cvo(ctx, t)), cvo, (size_t)E * K * 9 * sizeof(float), kin,
-                            ctx->stream));
+    DM_CUDA(cudaMemcpyAsync(ctx->obs_cvo, cvo, (size_t)E * K * 9 * sizeof(float), kin, ctx->stream));
   else
     P.K = 0;  // no pose: no spill statistic
-  float* o = ctx->obs_tape + (size_t)t * E * ctx->od;
-  k_obs<<<E, 256, 0, ctx->stream>>>(P, fwd_state(ctx, ctx->steps * ctx->cfg.substeps), step_cvo(ctx, t),
+  float* o = ctx->obs_out;
+  k_obs<<<E, 256, 0, ctx->stream>>>(P, fwd_state(ctx, ctx->steps * ctx->cfg.substeps), ctx->obs_cvo,
                                     (float)ctx->cfg.spill_half, (float)ctx->cfg.spill_temp, ctx->cfg.obs_groups, o,
                                     ctx->od);
   ++ctx->launches;
@@ -1116,7 +1200,7 @@ int dm_debug_sort(DmContext* ctx, int* keys, int* perm) {
   DM_CUDA(cudaMemcpyAsync(p.data(), slot(ctx, 0).perm, N * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   DM_CUDA(cudaStreamSynchronize(ctx->stream));
   for (size_t i = 0; i < N; ++i) perm[i] = p[i] - (int)((i / ctx->P.N) * ctx->P.N);
-  return check_flags(ctx, false);
+  return check_flags(ctx);
 }
 
 }  // extern "C"

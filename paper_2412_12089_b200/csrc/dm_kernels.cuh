@@ -54,6 +54,7 @@ struct DevParams {
   int K, G, nmat;
   int fiso;  // input state's F isotropic (fluid: every g2p output, F = J^(1/3) I)
   Law<float> law[4];
+  double dmu_dE[4], dlam_dE[4];  // Lame derivatives w.r.t. Young's modulus (fp64)
   ColShape shape[4];
 };
 
@@ -108,11 +109,16 @@ __device__ __forceinline__ uint32_t attr_index(uint32_t a) { return a & 0xFFFFFu
 __device__ __forceinline__ int attr_mat(uint32_t a) { return (a >> 20) & 0x3; }
 __device__ __forceinline__ int attr_group(uint32_t a) { return (a >> 24) & 0xFF; }
 
-// error key: env(16) | substep(10) | stage(2) | particle(24) | axis(2) | code(4)
+// error key: substep(16) | env(16) | stage(2) | particle(24) | axis(2) | code(4).
+// The minimum over a launch sequence is the first error in substep order
+// (the reference throws at the first failing substep; within it at the
+// lowest env, the P2G check before the G2P one, and the lowest particle
+// index), so the flags can be read lazily after several control steps.
+// sub = global substep index since the tape start.
 __device__ __forceinline__ void report(DevFlags* fl, int env, int sub, int stage, uint32_t particle, int axis,
                                        int code) {
-  const unsigned long long k = ((unsigned long long)(env & 0xFFFF) << 42) |
-                               ((unsigned long long)(sub & 0x3FF) << 32) | ((unsigned long long)(stage & 3) << 30) |
+  const unsigned long long k = ((unsigned long long)(sub & 0xFFFF) << 48) |
+                               ((unsigned long long)(env & 0xFFFF) << 32) | ((unsigned long long)(stage & 3) << 30) |
                                ((unsigned long long)(particle & 0xFFFFFF) << 6) | ((unsigned long long)(axis & 3) << 4) |
                                (unsigned long long)(code & 0xF);
   atomicMin(&fl->err_key, k);
@@ -1421,20 +1427,26 @@ __global__ void k_env_reduce(DevParams P, const int4* __restrict__ active, const
                              const int* __restrict__ env_acount, const float* __restrict__ tile_acc,
                              double* __restrict__ gcvo_t, double* __restrict__ gact_t, double* __restrict__ gmu,
                              double* __restrict__ glam) {
+  __shared__ double sacc[kNacc];
   const int e = blockIdx.x, f = threadIdx.x;
-  if (f >= kNacc) return;
   const int b = env_abase[e], n = env_acount[e];
   double s = 0.0;
-  for (int i = 0; i < n; ++i) {
-    const int4 et = active[b + i];
-    s += tile_acc[((size_t)et.x * P.Tn + et.y) * kNacc + f];
-  }
+  if (f < kNacc)
+    for (int i = 0; i < n; ++i) {
+      const int4 et = active[b + i];
+      s += tile_acc[((size_t)et.x * P.Tn + et.y) * kNacc + f];
+    }
+  if (f < kNacc) sacc[f] = s;
+  __syncthreads();
+  if (f >= kNacc) return;
+  // dL/dmu has two sources (P2G-adjoint stress term f, G2P-adjoint yield
+  // term f + 8): one thread adds both, in that fixed order
   if (f < 4) {
-    if (f < P.nmat) gmu[e * 4 + f] += s;
+    if (f < P.nmat) gmu[e * 4 + f] += s + sacc[f + 8];
   } else if (f < 8) {
     if (f - 4 < P.nmat) glam[e * 4 + f - 4] += s;
   } else if (f < 12) {
-    if (f - 8 < P.nmat) gmu[e * 4 + f - 8] += s;
+    // added by thread f - 8
   } else if (f < 48) {
     const int q = f - 12;
     if (q < P.K * 9) gcvo_t[(size_t)e * P.K * 9 + q] += s;
@@ -1804,6 +1816,64 @@ __global__ void k_aos_to_soa_perm(int Ntot, int N, const float* __restrict__ x, 
   for (int q = 0; q < 9; ++q) {
     f[adj_index(6 + q, i, stride)] = F ? F[9 * o + q] : 0.f;
     f[adj_index(15 + q, i, stride)] = C ? C[9 * o + q] : 0.f;
+  }
+}
+
+// ============================ small device epilogues ============================
+// fp64 -> fp32 cotangent conversion (stays on the device; the host entry
+// points copy the fp32 result out asynchronously).
+__global__ void k_f64_to_f32(size_t n, const double* __restrict__ src, float* __restrict__ dst) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = (float)src[i];
+}
+
+// dL/dE_m = dL/dmu_m dmu/dE + dL/dlam_m dlam/dE per env (MpmMaterial's Lame
+// map, mpm.hpp:33-35; the reference tape cannot produce it).
+__global__ void k_dE(int E, int nmat, const double* __restrict__ gmu, const double* __restrict__ glam, DevParams P,
+                     double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= E * nmat) return;
+  const int e = i / nmat, m = i % nmat;
+  out[i] = gmu[e * 4 + m] * P.dmu_dE[m] + glam[e * 4 + m] * P.dlam_dE[m];
+}
+
+// Replay verification (Tape::backward_segment, tape.hpp:234-241): the
+// segment replay's exit state must equal the stored checkpoint bitwise.  Both
+// are written by the same deterministic G2P in the same sorted order, so
+// physical slots correspond; a mismatch records min over (env << 40 | k)
+// with k the exit value's index in the env's visit order (x 3N, v 3N, F 9N,
+// C 9N; tasks.hpp:203-219).  Fluid G2P outputs store F(0,0) only.  Envs
+// whose state was replaced by an in-tape reset (cut != 0) are skipped.
+__global__ void k_replay_check(DevParams P, StateView R, StateView St, int fluid_iso,
+                               const unsigned char* __restrict__ cut, unsigned long long* __restrict__ bad) {
+  const size_t tot = (size_t)P.E * P.N;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
+    const int e = (int)(i / P.N);
+    if (cut && cut[e]) continue;
+    const uint32_t ar = R.attr[i], as = St.attr[i];
+    const unsigned long long pn = attr_index(as), N = (unsigned long long)P.N;
+    unsigned long long k = ~0ull;
+    if (ar != as) k = 3 * pn;
+    for (int f = 23; f >= 0; --f) {
+      if (fluid_iso && f > 6 && f < 15) continue;
+      if (__float_as_uint(R.c(f, i)) != __float_as_uint(St.c(f, i))) {
+        const unsigned long long kk = f < 3    ? 3 * pn + f
+                                      : f < 6  ? 3 * N + 3 * pn + (f - 3)
+                                      : f < 15 ? 6 * N + 9 * pn + (f - 6)
+                                               : 15 * N + 9 * pn + (f - 15);
+        k = kk < k ? kk : k;
+      }
+    }
+    if (k != ~0ull) atomicMin(bad, ((unsigned long long)e << 40) | k);
+  }
+}
+
+// Test hook (dm_debug_inject): flips the lowest mantissa bit of x of the
+// particle with original index p in env e of state S.
+__global__ void k_debug_flip(DevParams P, StateView S, int e, int p) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.N; i += gridDim.x * blockDim.x) {
+    const size_t j = (size_t)e * P.N + i;
+    if ((int)attr_index(S.attr[j]) == p) S.c(0, j) = __uint_as_float(__float_as_uint(S.c(0, j)) ^ 1u);
   }
 }
 

@@ -44,8 +44,15 @@ class RngStream:
     def doubles(self, n: int) -> np.ndarray:
         return (self.next_u64_block(n) >> np.uint64(11)).astype(np.float64) * _TWO53
 
-    def uniform(self, lo, hi, n: int) -> np.ndarray:
+    def uniform(self, lo, hi, n: int | None = None):
+        """n draws of lo + (hi - lo) u (rng.hpp:27-29); a float when n is None."""
+        if n is None:
+            return float(lo + (hi - lo) * self.doubles(1)[0])
         return lo + (hi - lo) * self.doubles(n)
+
+    def normal(self) -> float:
+        """One Box-Muller cosine draw (rng.hpp:35-43)."""
+        return float(self.normals(1)[0])
 
     def next_double(self) -> float:
         return float(self.doubles(1)[0])
