@@ -145,12 +145,29 @@ void stencil_base(const SimParams& sp, const V3<T>& x, std::size_t p, int base[3
 
 // ---- constitutive laws: first Piola P and the projected F ----
 
+// Gradient-oracle hook.  On the reference tape (oracle/src/ref_capi.cpp) the
+// SVD laws can be recorded as isotropic matrix maps with their exact
+// derivative instead of through Tape::svd3x3, whose adjoint clamps
+// sigma_j^2 - sigma_i^2 to +-1e-9 (svd3.hpp:45-49) and drops the rotation
+// terms at (near-)repeated singular values -- F = I, or the uniaxial strain of
+// a resting body.  Returns false: the literal restatement below.
+// kind: 0 fixed-corotated (fills p), 2 elastoplastic (fills p and f_proj).
+template <class T>
+inline bool iso_law(int kind, const M3<T>& f, const T& mu, const T& lam, const T& c_y, M3<T>& p, M3<T>& f_proj) {
+  (void)kind, (void)f, (void)mu, (void)lam, (void)c_y, (void)p, (void)f_proj;
+  return false;
+}
+
 // Extension (cfg 1): fixed-corotated, P = 2 mu (F - R) + lambda (J - 1) cof(F)
 // with R = U V^T from the SVD (R is a rotation since det F > 0, tape.hpp:172).
 template <class T>
 M3<T> stress_fixed_corotated(const M3<T>& f, const T& mu, const T& lam) {
   const T j = det(f);
   if (value_of(j) <= 0.0) throw std::runtime_error("stress_fixed_corotated: det(F) <= 0");
+  {
+    M3<T> p, fp;
+    if (iso_law(0, f, mu, lam, T(0.0), p, fp)) return p;
+  }
   M3<T> u, vt;
   V3<T> s;
   svd3(f, u, s, vt);
@@ -184,6 +201,10 @@ M3<T> stress_neo_hookean(const M3<T>& f, const T& mu, const T& lam, double k_act
 template <class T>
 M3<T> stress_elastoplastic(const M3<T>& f, const T& mu, const T& lam, const T& c_y, M3<T>& f_proj) {
   if (value_of(det(f)) <= 0.0) throw std::runtime_error("stress_elastoplastic: det(F) <= 0");
+  {
+    M3<T> p;
+    if (iso_law(2, f, mu, lam, c_y, p, f_proj)) return p;
+  }
   M3<T> u, vt;
   V3<T> sig;
   svd3(f, u, sig, vt);

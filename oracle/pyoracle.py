@@ -282,6 +282,16 @@ def ref_grad(sim, mats, cols, state, n_sub, target, seg=0):
     return lo.value, {"x": g[0], "v": g[1], "F": g[2], "C": g[3]}, secs.value
 
 
+def set_svd_adjoint(mode: int) -> int:
+    """SVD-law adjoint of the gradient oracle: 1 (default) records the
+    fixed-corotated / Hencky maps as isotropic-map nodes with their exact
+    derivative; 0 uses the reference's Tape::svd3x3 (svd3.hpp:27-63, clamped
+    at repeated singular values).  Returns the previous mode."""
+    L = lib("ref")
+    L.ref_set_svd_adjoint.restype = C.c_int
+    return int(L.ref_set_svd_adjoint(int(mode)))
+
+
 def rollout_grad(sim, mats, cols, state, n_ctrl, n_sub, loss, act=None, seg=1):
     """Restatement on the reference tape: loss, obs and gradients w.r.t. the
     initial state, per-step collider (center, velocity, omega), per-step

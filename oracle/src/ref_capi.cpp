@@ -28,8 +28,179 @@
 namespace oracle {
 inline void svd3(const M3<diffsim::Value>& f, M3<diffsim::Value>& u, V3<diffsim::Value>& s,
                  M3<diffsim::Value>& vt);
+// SVD-law adjoint of the gradient oracle: 1 = isotropic-map nodes (exact
+// derivative, default), 0 = the reference's Tape::svd3x3 (clamped adjoint).
+inline int g_svd_adjoint = 1;
+inline bool iso_law(int kind, const M3<diffsim::Value>& f, const diffsim::Value& mu, const diffsim::Value& lam,
+                    const diffsim::Value& c_y, M3<diffsim::Value>& p, M3<diffsim::Value>& f_proj);
 }
 #include "oracle/driver.hpp"
+
+// ---- isotropic matrix maps on the reference tape ----
+// Phi(F) = U diag(phi(sigma; prm)) V^T for F = U diag(sigma) V^T (det F > 0,
+// phi symmetric-separable: phi_i = f(sigma_i; symmetric functions of sigma)).
+// The forward derivative (dF^ = U^T dF V):
+//   dPhi^_ii = sum_j dphi_i/dsigma_j dF^_jj
+//   [dPhi^_ij, dPhi^_ji] = [[a, b], [b, a]] [dF^_ij, dF^_ji],  i != j,
+//   a, b = (dd_ij +- (phi_i + phi_j) / (sigma_i + sigma_j)) / 2,
+//   dd_ij = (phi_i - phi_j) / (sigma_i - sigma_j)  ->  dphi_i/dsigma_i - dphi_i/dsigma_j
+// at coinciding singular values (the limit for symmetric-separable phi).
+// Each output is recorded as one linear combination of the 9 entries of F and
+// the law parameters (chains of two-parent Tape::record nodes), with the
+// partials of phi from a scratch tape.  Pinned against central differences of
+// the fp64 forward in tests/test_oracle.py.
+namespace oracle {
+namespace {
+using diffsim::Tape;
+using diffsim::Value;
+
+template <class T>
+void phi_fcr(const T s[3], const T prm[3], bool, T out[3]) {
+  const T J = s[0] * s[1] * s[2];
+  for (int i = 0; i < 3; ++i) out[i] = T(2.0) * prm[0] * (s[i] - T(1.0)) + prm[1] * (J - T(1.0)) * J / s[i];
+}
+
+// Hencky / von Mises (mpm.hpp:165-198): which = 0 -> P's singular values, 1 -> F_proj's
+template <class T, int WHICH>
+void phi_hencky(const T s[3], const T prm[3], bool yield, T out[3]) {
+  T e[3] = {log(s[0]), log(s[1]), log(s[2])};
+  const T third = (e[0] + e[1] + e[2]) * T(1.0 / 3.0);
+  T dev[3] = {e[0] - third, e[1] - third, e[2] - third};
+  T sp[3] = {s[0], s[1], s[2]};
+  if (yield) {
+    const T n = sqrt(dev[0] * dev[0] + dev[1] * dev[1] + dev[2] * dev[2] + T(1e-30));
+    const T k = (n - prm[2]) / n;
+    for (int i = 0; i < 3; ++i) {
+      e[i] = e[i] - dev[i] * k;
+      sp[i] = exp(e[i]);
+    }
+  }
+  const T tr2 = e[0] + e[1] + e[2];
+  for (int i = 0; i < 3; ++i) out[i] = WHICH == 0 ? (T(2.0) * prm[0] * e[i] + prm[1] * tr2) / sp[i] : sp[i];
+}
+
+Value linear_node(Tape* tape, double value, const Value* in, const double* d, int n) {
+  Value acc;
+  bool have = false;
+  int first = -1;
+  for (int i = 0; i < n; ++i) {
+    if (in[i].id < 0 || d[i] == 0.0) continue;
+    if (first < 0) {
+      first = i;
+      continue;
+    }
+    if (!have) {
+      acc = tape->record(value, in[first], d[first], in[i], d[i]);
+      have = true;
+    } else {
+      acc = tape->record(value, acc, 1.0, in[i], d[i]);
+    }
+  }
+  if (have) return acc;
+  if (first >= 0) return tape->record(value, in[first], d[first]);
+  return Value(value);
+}
+
+template <class PhiD, class PhiV>
+void iso_record(const M3<Value>& f, const Value prm[3], bool yield, PhiD phi_d, PhiV phi_v, M3<Value>& out) {
+  Tape* tape = nullptr;
+  for (const Value& e : f.m)
+    if (e.tape) tape = e.tape;
+  for (int m = 0; m < 3; ++m)
+    if (prm[m].tape) tape = prm[m].tape;
+  double fd[9], U[9], S[3], Vt[9], pd[3], phi[3];
+  for (int i = 0; i < 9; ++i) fd[i] = f.m[i].v;
+  for (int m = 0; m < 3; ++m) pd[m] = prm[m].v;
+  svd3x3_values(fd, U, S, Vt);
+  phi_d(S, pd, yield, phi);
+  double J[3][3], K[3][3];  // dphi_i / dsigma_j, dphi_i / dprm_m
+  for (int i = 0; i < 3; ++i) {
+    Tape t;
+    Value sv[3] = {t.var(S[0]), t.var(S[1]), t.var(S[2])};
+    Value pv[3] = {t.var(pd[0]), t.var(pd[1]), t.var(pd[2])};
+    Value o[3];
+    phi_v(sv, pv, yield, o);
+    if (o[i].is_const()) {
+      for (int j = 0; j < 3; ++j) J[i][j] = K[i][j] = 0.0;
+      continue;
+    }
+    t.backward(o[i]);
+    for (int j = 0; j < 3; ++j) {
+      J[i][j] = t.grad(sv[j]);
+      K[i][j] = t.grad(pv[j]);
+    }
+  }
+  double a[3][3] = {}, b[3][3] = {};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      if (i == j) continue;
+      const double ds = S[i] - S[j];
+      const double dd = std::fabs(ds) > 1e-8 * (S[i] + S[j]) ? (phi[i] - phi[j]) / ds : J[i][i] - J[i][j];
+      const double sp = (phi[i] + phi[j]) / (S[i] + S[j]);
+      a[i][j] = 0.5 * (dd + sp);
+      b[i][j] = 0.5 * (dd - sp);
+    }
+  auto uvt = [&](const double D[3][3], double o[9]) {  // U D V^T
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) {
+        double acc = 0.0;
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) acc += U[3 * r + i] * D[i][j] * Vt[3 * j + c];
+        o[3 * r + c] = acc;
+      }
+  };
+  double val[9], jac[9][12];  // output (r,c) x input (9 F entries, 3 parameters)
+  {
+    double D[3][3] = {{phi[0], 0, 0}, {0, phi[1], 0}, {0, 0, phi[2]}};
+    uvt(D, val);
+  }
+  for (int kl = 0; kl < 9; ++kl) {
+    const int k = kl / 3, l = kl % 3;
+    double G[3][3], D[3][3], o[9];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) G[i][j] = U[3 * k + i] * Vt[3 * j + l];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j)
+        D[i][j] = i == j ? J[i][0] * G[0][0] + J[i][1] * G[1][1] + J[i][2] * G[2][2] : a[i][j] * G[i][j] + b[i][j] * G[j][i];
+    uvt(D, o);
+    for (int q = 0; q < 9; ++q) jac[q][kl] = o[q];
+  }
+  for (int m = 0; m < 3; ++m) {
+    double D[3][3] = {{K[0][m], 0, 0}, {0, K[1][m], 0}, {0, 0, K[2][m]}}, o[9];
+    uvt(D, o);
+    for (int q = 0; q < 9; ++q) jac[q][9 + m] = o[q];
+  }
+  Value in[12];
+  for (int i = 0; i < 9; ++i) in[i] = f.m[i];
+  for (int m = 0; m < 3; ++m) in[9 + m] = prm[m];
+  for (int q = 0; q < 9; ++q) out.m[q] = tape ? linear_node(tape, val[q], in, jac[q], 12) : Value(val[q]);
+}
+}  // namespace
+
+inline bool iso_law(int kind, const M3<Value>& f, const Value& mu, const Value& lam, const Value& c_y, M3<Value>& p,
+                    M3<Value>& f_proj) {
+  if (g_svd_adjoint == 0) return false;
+  const Value prm[3] = {mu, lam, c_y};
+  if (kind == 0) {
+    iso_record(f, prm, false, phi_fcr<double>, phi_fcr<Value>, p);
+    return true;
+  }
+  // the yield decision on values, as the restatement's value_of branch (mpm.hpp:182)
+  double fd[9], U[9], S[3], Vt[9];
+  for (int i = 0; i < 9; ++i) fd[i] = f.m[i].v;
+  svd3x3_values(fd, U, S, Vt);
+  const double e[3] = {std::log(S[0]), std::log(S[1]), std::log(S[2])};
+  const double th = (e[0] + e[1] + e[2]) / 3.0;
+  const double dv[3] = {e[0] - th, e[1] - th, e[2] - th};
+  const bool yield = std::sqrt(dv[0] * dv[0] + dv[1] * dv[1] + dv[2] * dv[2] + 1e-30) - c_y.v > 0.0;
+  iso_record(f, prm, yield, phi_hencky<double, 0>, phi_hencky<Value, 0>, p);
+  if (yield)
+    iso_record(f, prm, yield, phi_hencky<double, 1>, phi_hencky<Value, 1>, f_proj);
+  else
+    f_proj = f;
+  return true;
+}
+}  // namespace oracle
 
 namespace oracle {
 inline void svd3(const M3<diffsim::Value>& f, M3<diffsim::Value>& u, V3<diffsim::Value>& s,
@@ -364,6 +535,14 @@ int ref_rollout_grad(const OrSim* sim, const OrMat* mats, int nmat, const OrCol*
     put_err(e.what(), err, errlen);
     return 1;
   }
+}
+
+// SVD-law adjoint of the gradient oracle (ref_rollout_grad): 1 isotropic-map
+// nodes (exact), 0 the reference's Tape::svd3x3.  Returns the previous mode.
+int ref_set_svd_adjoint(int mode) {
+  const int old = oracle::g_svd_adjoint;
+  oracle::g_svd_adjoint = mode;
+  return old;
 }
 
 // reference RngStream draws (rng.hpp:11-55): kind 0 u64, 1 double, 2 normal

@@ -54,6 +54,7 @@ struct DmContext {
   int4* active_all = nullptr;
   int4* work_all = nullptr;
   int* ord_all = nullptr;
+  float4* vref_all = nullptr;  // per slot and env: the substep's reference velocity (k_bin)
   // per active tile (by slot) 6^3 grid blocks of the replayed substeps:
   // velocity and (mass, momentum), read by the adjoint substep instead of
   // re-running bin / p2g / grid
@@ -202,6 +203,7 @@ struct Slot {
   int* nact;
   float4* gvb;   // per-slot grid blocks (replay only)
   float4* gmpb;
+  float4* vref;  // [E] reference velocity of the substep (node_update_rel)
 };
 
 // zeroes the dynamic tile-scheduling counter before a tile kernel
@@ -221,6 +223,7 @@ Slot slot(DmContext* c, int q) {
   s.nact = c->nact_all + q;
   s.gvb = c->gvb_pool ? c->gvb_pool + (size_t)q * c->blk_cap * kExt3 : nullptr;
   s.gmpb = c->gmpb_pool ? c->gmpb_pool + (size_t)q * c->blk_cap * kExt3 : nullptr;
+  s.vref = c->vref_all + (size_t)q * c->P.E;
   return s;
 }
 
@@ -233,11 +236,11 @@ void launch_bin(DmContext* c, const StateView& S, const Slot& q, int sub, int ch
   if (c->bin_u16)
     k_bin<unsigned short><<<c->P.E, 32 * c->bin_warps, (size_t)c->bin_warps * c->P.Tn * 2, c->stream>>>(
         c->P, S, c->keys, c->ptile, q.tile_start, q.tile_count, q.active, q.env_abase, q.env_acount, c->flags, q.nact,
-        sub, check_vmax);
+        sub, check_vmax, q.vref);
   else
     k_bin<int><<<c->P.E, 32 * c->bin_warps, (size_t)c->bin_warps * c->P.Tn * 4, c->stream>>>(
         c->P, S, c->keys, c->ptile, q.tile_start, q.tile_count, q.active, q.env_abase, q.env_acount, c->flags, q.nact,
-        sub, check_vmax);
+        sub, check_vmax, q.vref);
   cudaMemsetAsync(q.ord, 0, 2 * kOrdBuckets * sizeof(int), c->stream);
   k_order_hist<<<64, 256, 0, c->stream>>>(q.active, q.nact, q.ord);
   k_order_scatter<<<(unsigned)((c->P.E * c->P.Tn + 2047) / 2048), 256, 0, c->stream>>>(q.active, q.nact, q.ord, q.work);
@@ -260,7 +263,7 @@ void launch_p2g(DmContext* c, const StateView& S, const Slot& q, int t, int sub)
   PROF_BEGIN(c, 1);
 #define L_P2G(LW)                                                                                               \
   k_p2g<LW><<<c->grid_tiles, kWarps * 32, kP2gSmem, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.work, \
-                                                          step_act(c, t), c->blocks, c->flags, q.nact, sub, c->wq)
+                                                          step_act(c, t), c->blocks, c->flags, q.nact, sub, c->wq, q.vref)
   DM_LAW_DISPATCH(c, L_P2G);
 #undef L_P2G
   PROF_END(c, 1);
@@ -288,7 +291,8 @@ void launch_grid(DmContext* c, const Slot& q, int t, bool dump) {
   PROF_BEGIN(c, 9);
 #define L_GRID(MC, CK)                                                                                        \
   k_grid<MC, CK><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work, step_cvo(c, t), \
-                                                               c->blocks, dump ? c->gmp : nullptr, c->gv, q.nact, c->wq)
+                                                               c->blocks, dump ? c->gmp : nullptr, c->gv, q.nact, c->wq, \
+                                                               q.vref)
   DM_GRID_DISPATCH(c, L_GRID);
 #undef L_GRID
   PROF_END(c, 9);
@@ -301,7 +305,8 @@ void launch_g2p(DmContext* c, const StateView& S, const StateView& So, const Slo
 #define L_G2P(LW)                                                                                                \
   k_g2p<LW><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, q.perm, q.tile_start, q.tile_count,        \
                                                           q.work, c->gv, c->flags, q.nact, sub, c->gmp,         \
-                                                          dump ? q.gvb : nullptr, dump ? q.gmpb : nullptr, c->wq, (int)c->blk_cap)
+                                                          dump ? q.gvb : nullptr, dump ? q.gmpb : nullptr, c->wq, (int)c->blk_cap, \
+                                                          q.vref)
   DM_LAW_DISPATCH(c, L_G2P);
 #undef L_G2P
   PROF_END(c, 2);
@@ -340,11 +345,11 @@ void backward_substep(DmContext* c, const StateView& S, const StateView& Sn, int
   if (c->P.nmat == 1)                                                                                          \
     k_g2p_adj<LW, 1><<<c->grid_tiles, kWarps * 32, kG2pAdjSmem, c->stream>>>(c->P, S, Sn, adj_in, c->Ntot, q.perm, \
                                                               q.tile_start, q.tile_count, q.work, q.gvb,  \
-                                                              c->ablocks, c->part, c->tile_acc, q.nact, c->wq); \
+                                                              c->ablocks, c->part, c->tile_acc, q.nact, c->wq, q.vref); \
   else                                                                                                         \
     k_g2p_adj<LW, 4><<<c->grid_tiles, kWarps * 32, kG2pAdjSmem, c->stream>>>(c->P, S, Sn, adj_in, c->Ntot, q.perm, \
                                                               q.tile_start, q.tile_count, q.work, q.gvb,  \
-                                                              c->ablocks, c->part, c->tile_acc, q.nact, c->wq)
+                                                              c->ablocks, c->part, c->tile_acc, q.nact, c->wq, q.vref)
   DM_LAW_DISPATCH(c, L_G2PA);
 #undef L_G2PA
   PROF_END(c, 3);
@@ -354,7 +359,7 @@ void backward_substep(DmContext* c, const StateView& S, const StateView& Sn, int
 #define L_GRIDA(MC, CK)                                                                                   \
   k_grid_adj<MC, CK><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work,        \
                                                                    step_cvo(c, t), c->ablocks, q.gmpb,   \
-                                                                   c->gmb, c->tile_acc, q.nact, c->wq)
+                                                                   c->gmb, c->tile_acc, q.nact, c->wq, q.vref)
   DM_GRID_DISPATCH(c, L_GRIDA);
 #undef L_GRIDA
   PROF_END(c, 10);
@@ -483,7 +488,7 @@ int get_state_impl(DmContext* ctx, float* x, float* v, float* F, float* C, cudaM
   float* out = ctx->adj[1];
   const int fiso = ctx->law == kFluid && s > 0;  // a fluid G2P output stores F(0,0) only
   k_soa_to_aos<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>((int)N, ctx->P.N, S.f, S.attr, N, 1, fiso, out,
-                                                                     out + 3 * N, out + 6 * N, out + 15 * N);
+                                                                     out + 3 * N, out + 6 * N, out + 15 * N, 1);
   ++ctx->launches;
   if (x) DM_CUDA(cudaMemcpyAsync(x, out, 3 * N * sizeof(float), kind, ctx->stream));
   if (v) DM_CUDA(cudaMemcpyAsync(v, out + 3 * N, 3 * N * sizeof(float), kind, ctx->stream));
@@ -836,6 +841,7 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
     cudaFuncSetAttribute(k_bin<int>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(nw * P.Tn * 4));
   }
   P.dx = (float)cfg->dx;
+  P.dx_lo = (float)(cfg->dx - (double)P.dx);
   P.inv_dx = (float)(1.0 / cfg->dx);
   P.dt = (float)cfg->dt;
   P.boundary = cfg->boundary;
@@ -864,6 +870,9 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
     L.act_k = (float)M.act_strength;
     L.mass = (float)(M.density * M.volume);
     L.vol = (float)M.volume;
+    L.mu64 = mu;
+    L.lam64 = lam;
+    L.cy64 = M.wide_yield ? M.yield_stress / mu : M.yield_stress / (2.0 * mu);
     L.dmu_dE = (float)ctx->dmu_dE[m];
     L.dlam_dE = (float)ctx->dlam_dE[m];
     P.dmu_dE[m] = ctx->dmu_dE[m];
@@ -914,6 +923,7 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
        dalloc(ctx, &ctx->perm_all, (size_t)ck * N) && dalloc(ctx, &ctx->tstart_all, (size_t)ck * TT) &&
        dalloc(ctx, &ctx->tcount_all, (size_t)ck * TT) && dalloc(ctx, &ctx->active_all, (size_t)ck * TT) &&
        dalloc(ctx, &ctx->work_all, (size_t)ck * TT) && dalloc(ctx, &ctx->ord_all, (size_t)ck * 2 * kOrdBuckets) &&
+       dalloc(ctx, &ctx->vref_all, (size_t)ck * P.E) &&
        dalloc(ctx, &ctx->abase_all, (size_t)ck * P.E) && dalloc(ctx, &ctx->acount_all, (size_t)ck * P.E) &&
        dalloc(ctx, &ctx->nact_all, (size_t)ck) && dalloc(ctx, &ctx->tail, state_floats(ctx)) && dalloc(ctx, &ctx->tail_attr, N);
   const size_t NN = (size_t)P.E * P.dims[0] * P.dims[1] * P.dims[2];
@@ -958,7 +968,8 @@ void dm_destroy(DmContext* ctx) {
                   ctx->active_all, ctx->work_all, ctx->ord_all, ctx->nact_all, ctx->tail, ctx->tail_attr, ctx->gvb_pool, ctx->gmpb_pool,
                   ctx->blocks,    ctx->ablocks,    ctx->tile_acc,   ctx->gmp, ctx->gv, ctx->gmb,   ctx->flags, ctx->wq, ctx->cvo_tape,  ctx->act_tape,
                   ctx->obs_tape,  ctx->dobs_buf, ctx->gcvo,       ctx->gact,       ctx->gmu,        ctx->glam,
-                  ctx->obs_cvo,   ctx->obs_out,  ctx->f32_stage,  ctx->dE_dev,     ctx->vmax_hist,  ctx->replay_bad};
+                  ctx->obs_cvo,   ctx->obs_out,  ctx->f32_stage,  ctx->dE_dev,     ctx->vmax_hist,  ctx->replay_bad,
+                  ctx->vref_all};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->h_flags) cudaFreeHost(ctx->h_flags);

@@ -48,6 +48,7 @@ struct DevParams {
   int E, N;                // envs, particles per env
   int dims[3], td[3], Tn;  // grid dims, tile dims, tiles per env
   float dx, inv_dx, dt;
+  float dx_lo;  // dx - (float)dx (node_rel)
   float grav[3];
   int boundary;
   float alpha_c, mu_b;
@@ -175,6 +176,7 @@ __device__ __forceinline__ NodeCtx<float> nctx(const DevParams& P) {
   g.dims[1] = P.dims[1];
   g.dims[2] = P.dims[2];
   g.dx = P.dx;
+  g.dx_lo = P.dx_lo;
   g.dt = P.dt;
   g.gravity = mk3(P.grav[0], P.grav[1], P.grav[2]);
   g.boundary = P.boundary;
@@ -202,10 +204,11 @@ __device__ __forceinline__ void load_cols(const DevParams& P, const float* cvo_e
   }
 }
 
-// F of the state.  The fluid projection (mpm.hpp:207) makes every G2P output
-// F exactly J^(1/3) I (off-diagonals stored as +0), so for a fluid batch and
-// a state produced by G2P (P.fiso) one word is read instead of nine; the
-// reconstructed matrix holds the identical values.
+// The stored deviation D = F - I of the state.  The fluid projection
+// (mpm.hpp:207) makes every G2P output F exactly J^(1/3) I (off-diagonals
+// stored as +0), so for a fluid batch and a state produced by G2P (P.fiso)
+// one word is read instead of nine; the reconstructed matrix holds the
+// identical values.
 template <int LAW>
 __device__ __forceinline__ void load_F(const StateView& S, size_t i, m3<float>& F, int fiso) {
   if (LAW == kFluid && fiso) {
@@ -237,8 +240,9 @@ __device__ __forceinline__ void load_xF(const StateView& S, size_t i, float x[3]
   load_F<LAW>(S, i, F, fiso);
 }
 
-// A fluid G2P output stores only F(0,0) (F = J^(1/3) I); readers of such a
-// state reconstruct the rest (load_F, k_soa_to_aos, k_fiso_expand).
+// The F fields hold the deviation D = F - I (law_stress_fwd).  A fluid G2P
+// output stores only D(0,0) (F = J^(1/3) I, D = (J^(1/3) - 1) I); readers of
+// such a state reconstruct the rest (load_F, k_soa_to_aos, k_fiso_expand).
 template <int LAW = -1>
 __device__ __forceinline__ void store_state(const StateView& S, size_t i, v3<float> x, v3<float> v, const m3<float>& F,
                                             const m3<float>& C) {
@@ -263,10 +267,16 @@ __device__ __forceinline__ void store_state(const StateView& S, size_t i, v3<flo
 // permutation equals std::stable_sort by key.
 // CT: histogram / cursor word (unsigned short when particles per env fit in
 // 16 bits: half the shared memory, twice the resident CTAs).
+// vref[e]: the substep's reference velocity (node_update_rel): the mean
+// velocity of the env's first min(N, 256) particles in physical order, in a
+// fixed summation order (a deterministic function of the state: the replay
+// reproduces it bitwise).
+constexpr int kVrefParticles = 256;
 template <class CT>
 __global__ void __launch_bounds__(1024) k_bin(DevParams P, StateView S, int* keys, int* perm, int* tile_start,
                                              int* tile_count, int4* active, int* env_abase, int* env_acount,
-                                             DevFlags* flags, int* nact, int substep, int check_vmax) {
+                                             DevFlags* flags, int* nact, int substep, int check_vmax,
+                                             float4* __restrict__ vref) {
   extern __shared__ __align__(16) unsigned char bin_smem[];
   CT* cnt = reinterpret_cast<CT*>(bin_smem);  // [nw][Tn]
   __shared__ int s_part[1024 / 32 + 1][2];
@@ -275,6 +285,24 @@ __global__ void __launch_bounds__(1024) k_bin(DevParams P, StateView S, int* key
   const int nw = blockDim.x >> 5;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const size_t base = (size_t)e * P.N;
+  if (wid == 0) {
+    const int nv = P.N < kVrefParticles ? P.N : kVrefParticles;
+    float sx = 0.f, sy = 0.f, sz = 0.f;
+    for (int p = lane; p < nv; p += 32) {
+      sx += S.c(3, base + p);
+      sy += S.c(4, base + p);
+      sz += S.c(5, base + p);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      sx += __shfl_xor_sync(0xffffffffu, sx, o);
+      sy += __shfl_xor_sync(0xffffffffu, sy, o);
+      sz += __shfl_xor_sync(0xffffffffu, sz, o);
+    }
+    const float inv = 1.f / (float)nv;
+    // a non-finite reference (a blown-up particle) would poison every node: use 0
+    const bool ok = isfinite(sx) && isfinite(sy) && isfinite(sz);
+    if (lane == 0) vref[e] = ok ? make_float4(sx * inv, sy * inv, sz * inv, 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   for (int t = threadIdx.x; t < nw * P.Tn; t += blockDim.x) cnt[t] = 0;
   __syncthreads();
   const int chunk = (P.N + nw - 1) / nw;
@@ -791,7 +819,8 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, S
                                                      const int* __restrict__ tile_start,
                                                      const int* __restrict__ tile_count, const int4* __restrict__ active,
                                                      const float* __restrict__ act, float4* __restrict__ blocks,
-                                                     DevFlags* flags, const int* nact, int substep, int* __restrict__ wq) {
+                                                     DevFlags* flags, const int* nact, int substep, int* __restrict__ wq,
+                                                     const float4* __restrict__ vref) {
   extern __shared__ float4 dsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_active = *(const volatile int*)nact;
@@ -805,6 +834,8 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, S
     const int o[3] = {tx * kTile, ty * kTile, tz * kTile};
     const size_t tix = (size_t)e * P.Tn + t;
     const int* prow = perm + (size_t)e * P.N + start;
+    const float4 vr4 = vref[e];
+    const v3<float> vr = mk3(vr4.x, vr4.y, vr4.z);  // momentum relative to the env's reference velocity
     // perm indices two chunks ahead in two parity slots (no register moves
     // between chunks, so a refill never waits on the load it replaces)
     PState ps;
@@ -830,7 +861,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, S
         if (bad) report(flags, e, substep, 0, attr_index(ps.at), attr_mat(ps.at), kErrDetF);
         v3<float> q;
         m3<float> Ad;
-        p2g_payload(A, L.mass, ps.v, sc, P.dx, q, Ad);
+        p2g_payload(A, L.mass, ps.v - vr, sc, P.dx, q, Ad);
         const int lbl = (tile_local(sc.base[0], o[0]) * kExt + tile_local(sc.base[1], o[1])) * kExt +
                         tile_local(sc.base[2], o[2]);
         stage_payload(pw + lane * kPay, lbl, sc, L.mass, q, Ad);
@@ -968,7 +999,8 @@ template <int MAXC, int CK>
 __global__ void __launch_bounds__(kWarps * 32, DM_GRID_MINB) k_grid(DevParams P, const int* __restrict__ tile_count,
                                                       const int4* __restrict__ active, const float* __restrict__ cvo,
                                                       const float4* __restrict__ blocks, float4* __restrict__ gmp,
-                                                      float4* __restrict__ gv, const int* nact, int* __restrict__ wq) {
+                                                      float4* __restrict__ gv, const int* nact, int* __restrict__ wq,
+                                                      const float4* __restrict__ vref) {
   __shared__ short own[kWarps][kExt3];
   __shared__ NodeMasks nm;
   __shared__ Col<float> scol[kWarps][MAXC];
@@ -987,12 +1019,14 @@ __global__ void __launch_bounds__(kWarps * 32, DM_GRID_MINB) k_grid(DevParams P,
     if (lane == 0) load_cols<MAXC>(P, cvo + (size_t)e * P.K * 9, cols);
     __syncwarp();
     const int n_own = owned_nodes(P, nm, nbr, tc, own[warp], lane);
+    const float4 vr4 = vref[e];
+    const v3<float> vr = mk3(vr4.x, vr4.y, vr4.z);
     for (int q = lane; q < n_own; q += 32) {
       const int i = own[warp][q];
       const int l[3] = {i / 36, (i / 6) % 6, i % 6};
       const int g[3] = {tc[0] * kTile + l[0], tc[1] * kTile + l[1], tc[2] * kTile + l[2]};
-      const float4 mm = sum_blocks(P, nm, blocks, nbr, e, tc, i);
-      const v3<float> v = node_update<float, MAXC, CK>(G, cols, P.K, g, mm.x, mk3(mm.y, mm.z, mm.w));
+      const float4 mm = sum_blocks(P, nm, blocks, nbr, e, tc, i);  // (mass, momentum relative to vref)
+      const v3<float> v = node_update_rel<float, MAXC, CK>(G, cols, P.K, g, mm.x, mk3(mm.y, mm.z, mm.w), vr);
       const size_t n = node_lin(P, e, g);
       if (gmp) gmp[n] = mm;  // (mass, momentum) only when the replay dumps them
       gv[n] = make_float4(v.x, v.y, v.z, 0.f);
@@ -1021,7 +1055,7 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
                                                      const float4* __restrict__ gv, DevFlags* flags, const int* nact,
                                                      int substep, const float4* __restrict__ gmp,
                                                      float4* __restrict__ out_gv, float4* __restrict__ out_gmp, int* __restrict__ wq,
-                                                     int dump_cap) {
+                                                     int dump_cap, const float4* __restrict__ vref) {
   __shared__ __align__(16) float4 vg[kWarps][2][kExt3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_active = *(const volatile int*)nact;
@@ -1038,6 +1072,8 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
     const size_t row = (size_t)e * P.N + start;
+    const float4 vr4 = vref[e];
+    const v3<float> vr = mk3(vr4.x, vr4.y, vr4.z);
     // two particle-state buffers (chunks alternate) and perm indices two
     // chunks ahead in parity slots: no register moves between chunks
     float xa[3], xb[3];
@@ -1070,7 +1106,7 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
       v3<float> xn = mk3(x[0], x[1], x[2]), v;
       m3<float> C;
       bool bad_adv = false, bad_det = false;
-      g2p_particle_sep(law_of<LAW>(P, attr_mat(at)), T, sc, getv, xn, v, C, F, &bad_adv, &bad_det);
+      g2p_particle_sep(law_of<LAW>(P, attr_mat(at)), T, sc, getv, xn, v, C, F, &bad_adv, &bad_det, vr);
       if (bad_adv) report(flags, e, substep, 1, attr_index(at), 0, kErrG2PInterior);
       if (bad_det) report(flags, e, substep, 1, attr_index(at), attr_mat(at), kErrDetF);
       store_state<LAW>(Sout, dst, xn, v, F, C);
@@ -1112,7 +1148,8 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
                                                          const int* __restrict__ tile_count,
                                                          const int4* __restrict__ active, const float4* __restrict__ gvb,
                                                          float4* __restrict__ ablocks, float* __restrict__ part,
-                                                         float* __restrict__ tile_acc, const int* nact, int* __restrict__ wq) {
+                                                         float* __restrict__ tile_acc, const int* nact, int* __restrict__ wq,
+                                                         const float4* __restrict__ vref) {
   extern __shared__ float4 dsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TransferCtx<float> T = tctx(P);
@@ -1131,6 +1168,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
     cp_async_commit();
     const size_t tix = (size_t)e * P.Tn + t;
     const size_t row = (size_t)e * P.N + start;
+    const float4 vr4 = vref[e];
     float x[3];
     m3<float> F;
     uint32_t at = 0;
@@ -1155,9 +1193,9 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
         Stencil<float> sc;
         make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
         const int lb[3] = {tile_local(sc.base[0], o[0]), tile_local(sc.base[1], o[1]), tile_local(sc.base[2], o[2])};
-        auto getv = [&](int i, int j, int k) {
+        auto getv = [&](int i, int j, int k) {  // lab-frame node velocity (the grid holds v - vref)
           const float4 q = vw[((lb[0] + i) * kExt + (lb[1] + j)) * kExt + lb[2] + k];
-          return mk3(q.x, q.y, q.z);
+          return mk3(vr4.x + q.x, vr4.y + q.y, vr4.z + q.z);
         };
         v3<float> xb = mk3(adj_in[adj_index(0, dst, astride)], adj_in[adj_index(1, dst, astride)], adj_in[adj_index(2, dst, astride)]);
         v3<float> vb = mk3(adj_in[adj_index(3, dst, astride)], adj_in[adj_index(4, dst, astride)], adj_in[adj_index(5, dst, astride)]);
@@ -1177,10 +1215,10 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
 #pragma unroll
         for (int q = 0; q < 9; ++q) Cn.a[q] = Sn.c(15 + q, dst);
         if (LAW == kFluid && P.fiso)  // literal-zero diagonal F (see k_p2g)
-          g2p_vjp_given(law_of<LAW>(P, mi), T, sc, getv, mdiag(F.a[0], F.a[0], F.a[0]), vn, Cn, xb, vb, Cb, Fb, xp, Fp,
-                        gq, Bd, mu_l);
-        else
-          g2p_vjp_given(law_of<LAW>(P, mi), T, sc, getv, F, vn, Cn, xb, vb, Cb, Fb, xp, Fp, gq, Bd, mu_l);
+          g2p_vjp_given(law_of<LAW>(P, mi), T, sc, getv, mdiag(1.f + F.a[0], 1.f + F.a[0], 1.f + F.a[0]), vn, Cn, xb,
+                        vb, Cb, Fb, xp, Fp, gq, Bd, mu_l);
+        else  // the adjoint linearises at F = I + D (fp32)
+          g2p_vjp_given(law_of<LAW>(P, mi), T, sc, getv, eye_plus(F), vn, Cn, xb, vb, Cb, Fb, xp, Fp, gq, Bd, mu_l);
 #pragma unroll
         for (int m = 0; m < NM; ++m)
           if (m == mi) mub[m] += mu_l;
@@ -1224,7 +1262,8 @@ __global__ void __launch_bounds__(kWarps * 32, DM_GRIDADJ_MINB) k_grid_adj(DevPa
                                                           const int4* __restrict__ active, const float* __restrict__ cvo,
                                                           const float4* __restrict__ ablocks,
                                                           const float4* __restrict__ gmpb, float4* __restrict__ gmb,
-                                                          float* __restrict__ tile_acc, const int* nact, int* __restrict__ wq) {
+                                                          float* __restrict__ tile_acc, const int* nact, int* __restrict__ wq,
+                                                          const float4* __restrict__ vref) {
   __shared__ short own[kWarps][kExt3];
   __shared__ NodeMasks nm;
   __shared__ Col<float> scol[kWarps][MAXC];
@@ -1252,7 +1291,13 @@ __global__ void __launch_bounds__(kWarps * 32, DM_GRIDADJ_MINB) k_grid_adj(DevPa
       const int g[3] = {tc[0] * kTile + l[0], tc[1] * kTile + l[1], tc[2] * kTile + l[2]};
       const float4 vb = sum_blocks(P, nm, ablocks, nbr, e, tc, i);
       const size_t n = node_lin(P, e, g);
-      const float4 mm = gmpb[(size_t)a * kExt3 + i];  // this tile's stored (mass, momentum) block
+      float4 mm = gmpb[(size_t)a * kExt3 + i];  // this tile's stored (mass, momentum relative to vref) block
+      {  // the adjoint linearises in the lab frame: momentum + mass vref
+        const float4 vr4 = vref[e];
+        mm.y += mm.x * vr4.x;
+        mm.z += mm.x * vr4.y;
+        mm.w += mm.x * vr4.z;
+      }
       float mbar;
       v3<float> pbar;
       // adjoint blocks carry (unused, vbar.x, vbar.y, vbar.z) -- emit_contrib layout
@@ -1345,7 +1390,8 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
           C.a[q] = sg[(15 + q) * 32 + lane];
           Fb.a[q] = sg[(28 + q) * 32 + lane];
         }
-        if (LAW == kFluid && P.fiso) F = mdiag(F.a[0], F.a[0], F.a[0]);
+        // the stored deviation D -> F = I + D (fp32; the adjoint's linearisation point)
+        F = (LAW == kFluid && P.fiso) ? mdiag(1.f + F.a[0], 1.f + F.a[0], 1.f + F.a[0]) : eye_plus(F);
         at = __float_as_uint(sg[24 * 32 + lane]);
         xb = mk3(sg[25 * 32 + lane], sg[26 * 32 + lane], sg[27 * 32 + lane]);
         src = __float_as_int(sg[37 * 32 + lane]);
@@ -1648,7 +1694,7 @@ __global__ void __launch_bounds__(256) k_obs_adj(DevParams P, StateView S, const
   }
 }
 
-// Fills F = F(0,0) I for every particle of a fluid G2P-produced state (makes
+// Fills D = D(0,0) I for every particle of a fluid G2P-produced state (makes
 // it a general state again: used when it becomes a new initial state).
 __global__ void k_fiso_expand(size_t Ntot, StateView S) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < Ntot; i += (size_t)gridDim.x * blockDim.x) {
@@ -1731,7 +1777,7 @@ __global__ void k_reset_lattice(ResetSpec R, int E, int N, unsigned long long se
     }
 #pragma unroll
     for (int q = 0; q < 9; ++q) {
-      S.c(6 + q, o) = (q % 4 == 0) ? 1.f : 0.f;
+      S.c(6 + q, o) = 0.f;  // D = F - I = 0
       S.c(15 + q, o) = 0.f;
     }
     const uint32_t g = pgroup ? (uint32_t)pgroup[p] : (uint32_t)R.group;
@@ -1770,7 +1816,7 @@ __global__ void k_aos_to_soa(int Ntot, const float* __restrict__ x, const float*
   }
 #pragma unroll
   for (int q = 0; q < 9; ++q) {
-    S.c(6 + q, i) = F[9 * i + q];
+    S.c(6 + q, i) = (q % 4 == 0) ? F[9 * i + q] - 1.f : F[9 * i + q];  // stored as D = F - I
     S.c(15 + q, i) = C[9 * i + q];
   }
   const uint32_t idx = (uint32_t)(i % N);
@@ -1778,10 +1824,12 @@ __global__ void k_aos_to_soa(int Ntot, const float* __restrict__ x, const float*
   S.attr[i] = idx | ((m & 0xF) << 20) | ((g & 0xFF) << 24);
 }
 
-// physical SoA -> canonical AoS (original order within each env)
+// physical SoA -> canonical AoS (original order within each env).  eye: the
+// F fields hold the stored deviation D (a state: F = I + D) rather than a
+// cotangent (dL/dF = dL/dD, no shift).
 __global__ void k_soa_to_aos(int Ntot, int N, const float* __restrict__ f, const uint32_t* __restrict__ attr,
                              size_t stride, int state_layout, int fiso, float* __restrict__ x, float* __restrict__ v, float* __restrict__ F,
-                             float* __restrict__ C) {
+                             float* __restrict__ C, int eye = 0) {
   const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (i >= (size_t)Ntot) return;
   const size_t e = i / N;
@@ -1793,8 +1841,9 @@ __global__ void k_soa_to_aos(int Ntot, int N, const float* __restrict__ f, const
   }
 #pragma unroll
   for (int q = 0; q < 9; ++q) {
-    if (F) F[9 * o + q] = fiso ? (q % 4 == 0 ? f[state_index(6, i, stride)] : 0.f)
-                               : f[state_layout ? state_index(6 + q, i, stride) : (6 + q) * stride + i];
+    const float e = (eye && q % 4 == 0) ? 1.f : 0.f;
+    if (F) F[9 * o + q] = e + (fiso ? (q % 4 == 0 ? f[state_index(6, i, stride)] : 0.f)
+                                    : f[state_layout ? state_index(6 + q, i, stride) : (6 + q) * stride + i]);
     if (C) C[9 * o + q] = f[state_layout ? state_index(15 + q, i, stride) : (15 + q) * stride + i];
   }
 }

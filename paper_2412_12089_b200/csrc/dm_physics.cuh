@@ -29,6 +29,7 @@ struct Law {
   R mu, lam, cy, visc, act_k;
   R mass, vol;
   R dmu_dE, dlam_dE;
+  double mu64, lam64, cy64;  // fp64 constants of the SVD laws' forward evaluation (law_stress_fwd)
 };
 
 template <class R>
@@ -140,6 +141,128 @@ DM_HD m3<R> law_project(const Law<R>& L, const m3<R>& F, bool* bad) {
     return mdiag(s, s, s);
   }
   return F;
+}
+
+// ---- forward evaluation in deviation form ----
+// The particle state stores D = F - I (fp32): a small strain keeps its
+// relative precision (F itself would round it to 6e-8 absolute, i.e. 6 % of a
+// 1e-6 strain; SURVEY 8(d)'s per-substep 1e-5 gate on a resting elastic body
+// needs ~1e-7).  The forward stress and projection are evaluated from D:
+//   * SVD laws (fixed-corotated, Hencky / von Mises): in fp64 from
+//     F = I + D (exact in fp64) -- an fp32 SVD of I + D loses the strain
+//   * fluid: J - 1 = det(I + D) - 1 expanded in D (det1m), no cancellation
+//   * neo-Hookean: P expanded around F = I (the two O(mu) terms cancel there)
+// The adjoints linearise at F = I + D in fp32 (their terms do not cancel).
+
+// det(I + D) - 1 = tr D + (principal 2x2 minors of D) + det D
+template <class R>
+DM_HD R det1m(const m3<R>& D) {
+  const R m2 = (D(0, 0) * D(1, 1) - D(0, 1) * D(1, 0)) + (D(0, 0) * D(2, 2) - D(0, 2) * D(2, 0)) +
+               (D(1, 1) * D(2, 2) - D(1, 2) * D(2, 1));
+  return (D(0, 0) + D(1, 1) + D(2, 2)) + m2 + det(D);
+}
+
+template <class R>
+DM_HD m3<R> eye_plus(const m3<R>& D) {
+  m3<R> F = D;
+  F(0, 0) += R(1);
+  F(1, 1) += R(1);
+  F(2, 2) += R(1);
+  return F;
+}
+
+template <class R>
+DM_HD Law<double> law64(const Law<R>& L) {
+  Law<double> d;
+  d.kind = L.kind;
+  d.mu = L.mu64;
+  d.lam = L.lam64;
+  d.cy = L.cy64;
+  d.visc = L.visc;
+  d.act_k = L.act_k;
+  d.mass = L.mass;
+  d.vol = L.vol;
+  d.dmu_dE = L.dmu_dE;
+  d.dlam_dE = L.dlam_dE;
+  d.mu64 = L.mu64;
+  d.lam64 = L.lam64;
+  d.cy64 = L.cy64;
+  return d;
+}
+
+template <class R>
+DM_HD m3<double> to64(const m3<R>& a) {
+  m3<double> o;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) o.a[q] = (double)a.a[q];
+  return o;
+}
+template <class R>
+DM_HD m3<R> from64(const m3<double>& a) {
+  m3<R> o;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) o.a[q] = (R)a.a[q];
+  return o;
+}
+
+// First Piola stress from D = F - I (mpm.hpp:212-217 extended; same values as
+// law_stress(I + D) up to rounding).
+template <class R>
+DM_HD m3<R> law_stress_fwd(const Law<R>& L, const m3<R>& D, R act, bool* bad) {
+  const R jm1 = det1m(D);
+  if (!(jm1 > R(-1))) *bad = true;
+  switch (L.kind) {
+    case kFixedCorotated:
+    case kElastoplastic: {
+      bool b = false;
+      const m3<double> P = law_stress(law64(L), eye_plus(to64(D)), (double)act, &b);
+      return from64<R>(P);
+    }
+    case kNeoHookean: {
+      // P = mu (1 - 1/(I_C+1)) F + lam (J - alpha) cof F, alpha = 1 + 3 mu / (4 lam), as
+      // mu [ 3/4 (D + D^T - tr D I - cof D) + (I_C - 3) / (4 (I_C + 1)) F ] + lam (J - 1) cof F
+      const m3<R> F = eye_plus(D);
+      const R trD = D(0, 0) + D(1, 1) + D(2, 2);
+      const R ic3 = R(2) * trD + ddot(D, D);  // I_C - 3
+      const m3<R> cD = cofactor(D);
+      m3<R> S = D + transpose(D) - cD;
+      S(0, 0) -= trD;
+      S(1, 1) -= trD;
+      S(2, 2) -= trD;
+      m3<R> P = S * (R(0.75) * L.mu) + F * (L.mu * ic3 / (R(4) * (ic3 + R(4)))) + cofactor(F) * (L.lam * jm1);
+      const R ka = L.act_k * act;
+      P(0, 0) += ka * F(0, 0);
+      P(1, 0) += ka * F(1, 0);
+      P(2, 0) += ka * F(2, 0);
+      return P;
+    }
+    default:  // fluid
+      return cofactor(eye_plus(D)) * (L.lam * jm1);
+  }
+}
+
+// G2P projection (mpm.hpp:341-344) in deviation form: D' = proj(I + Dn) - I.
+template <class R>
+DM_HD m3<R> law_project_fwd(const Law<R>& L, const m3<R>& Dn, bool* bad) {
+  if (L.kind == kElastoplastic) {
+    const m3<double> Fn = eye_plus(to64(Dn));
+    if (!(det(Fn) > 0.0)) *bad = true;
+    const Hencky<double> h = hencky(Fn, L.cy64);
+    if (!h.yield) return Dn;
+    m3<double> Fp = usv(h.sv, h.sigp[0], h.sigp[1], h.sigp[2]);
+    Fp(0, 0) -= 1.0;
+    Fp(1, 1) -= 1.0;
+    Fp(2, 2) -= 1.0;
+    return from64<R>(Fp);
+  }
+  if (L.kind == kFluid) {
+    // F' = J^(1/3) I  ->  D' = (J^(1/3) - 1) I = expm1(log1p(J - 1) / 3) I
+    const R jm1 = det1m(Dn);
+    if (!(jm1 > R(-1))) *bad = true;
+    const R w = r_expm1(r_log1p(jm1) * R(1.0 / 3.0));
+    return mdiag(w, w, w);
+  }
+  return Dn;  // fixed-corotated, neo-Hookean: no projection (the next P2G checks det F)
 }
 
 // ---- adjoints ----
@@ -303,14 +426,16 @@ struct BoxQ {
   R sgn[3];
 };
 
+// box_query_core: from q = |rel| - half and the signs of rel (callers with
+// a more precise q for an axis pass it directly).
 template <class R>
-DM_HD BoxQ<R> box_query(v3<R> rel, v3<R> half) {
+DM_HD BoxQ<R> box_query_core(const R q[3], const R sg[3]) {
   BoxQ<R> b;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    b.q[a] = r_abs(rel[a]) - half[a];
+    b.q[a] = q[a];
     b.o[a] = r_max(b.q[a], R(0));
-    b.sgn[a] = rel[a] < R(0) ? R(-1) : R(1);
+    b.sgn[a] = sg[a];
   }
   b.outside = r_sqrt(b.o[0] * b.o[0] + b.o[1] * b.o[1] + b.o[2] * b.o[2] + R(1e-18));
   b.out = b.q[0] > R(0) || b.q[1] > R(0) || b.q[2] > R(0);
@@ -329,6 +454,29 @@ DM_HD BoxQ<R> box_query(v3<R> rel, v3<R> half) {
   }
   b.n = mk3(b.n.x * b.sgn[0], b.n.y * b.sgn[1], b.n.z * b.sgn[2]);
   return b;
+}
+
+template <class R>
+DM_HD BoxQ<R> box_query(v3<R> rel, v3<R> half) {
+  R q[3], sg[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    q[a] = r_abs(rel[a]) - half[a];
+    sg[a] = rel[a] < R(0) ? R(-1) : R(1);
+  }
+  return box_query_core(q, sg);
+}
+
+// The open-top hollow box's cavity: a box open at the top (z extent shifted
+// up by 1, rc = rel - e_z, hc = half + e_z); its z face distance
+// |rel.z - 1| - (half.z + 1) = -(rel.z + half.z) for rel.z < 1 is taken
+// directly (the shifted form rounds it to ~6e-8 in fp32, which
+// exp(-alpha_c d) turns into ~6e-6 relative).
+template <class R>
+DM_HD BoxQ<R> cavity_query(v3<R> rel, v3<R> half) {
+  const R q[3] = {r_abs(rel.x) - half.x, r_abs(rel.y) - half.y, -(rel.z + half.z)};
+  const R sg[3] = {rel.x < R(0) ? R(-1) : R(1), rel.y < R(0) ? R(-1) : R(1), R(-1)};
+  return box_query_core(q, sg);
 }
 
 // dbar, nbar -> rel_bar
@@ -431,8 +579,7 @@ DM_HD v3<R> cyl_query_vjp(const CylQ<R>& c, R dbar, v3<R> nbar) {
 // CK >= 0 fixes the collider kind at compile time (the switch folds: small
 // code for single-kind batches); CK = -1 dispatches on col.kind.
 template <class R, int CK = -1>
-DM_HD_NOINLINE void collider_query(const Col<R>& col, v3<R> p, R& d, v3<R>& n) {
-  const v3<R> rel = p - col.c;
+DM_HD_NOINLINE void collider_query_r(const Col<R>& col, v3<R> rel, R& d, v3<R>& n) {
   switch (CK >= 0 ? CK : col.kind) {
     case kPlane:
       d = dot(rel, col.nrm);
@@ -460,10 +607,8 @@ DM_HD_NOINLINE void collider_query(const Col<R>& col, v3<R> p, R& d, v3<R>& n) {
       const R th = col.thickness;
       const v3<R> ro = mk3(rel.x, rel.y, rel.z + R(0.5) * th);
       const v3<R> ho = mk3(col.half.x + th, col.half.y + th, col.half.z + R(0.5) * th);
-      const v3<R> rc = mk3(rel.x, rel.y, rel.z - R(1));
-      const v3<R> hc = mk3(col.half.x, col.half.y, col.half.z + R(1));
       const BoxQ<R> bo = box_query(ro, ho);
-      const BoxQ<R> bc = box_query(rc, hc);
+      const BoxQ<R> bc = cavity_query(rel, col.half);
       if (bo.d >= -bc.d) {
         d = bo.d;
         n = bo.n;
@@ -474,6 +619,11 @@ DM_HD_NOINLINE void collider_query(const Col<R>& col, v3<R> p, R& d, v3<R>& n) {
       return;
     }
   }
+}
+
+template <class R, int CK = -1>
+DM_HD void collider_query(const Col<R>& col, v3<R> p, R& d, v3<R>& n) {
+  collider_query_r<R, CK>(col, p - col.c, d, n);
 }
 
 // Returns pbar (gradient w.r.t. the query point; center gets -pbar).
@@ -503,7 +653,7 @@ DM_HD_NOINLINE v3<R> collider_query_vjp(const Col<R>& col, v3<R> p, R dbar, v3<R
       const v3<R> rc = mk3(rel.x, rel.y, rel.z - R(1));
       const v3<R> hc = mk3(col.half.x, col.half.y, col.half.z + R(1));
       const BoxQ<R> bo = box_query(ro, ho);
-      const BoxQ<R> bc = box_query(rc, hc);
+      const BoxQ<R> bc = cavity_query(rel, col.half);
       // one inlined vjp on the active branch (outer box, or the cavity with
       // negated cotangents) keeps the code compact
       const bool outer = bo.d >= -bc.d;
@@ -552,7 +702,7 @@ DM_HD void collider_query_rec(const Col<R>& col, v3<R> p, ColRec<R>& q) {
     const v3<R> rc = mk3(rel.x, rel.y, rel.z - R(1));
     const v3<R> hc = mk3(col.half.x, col.half.y, col.half.z + R(1));
     const BoxQ<R> bo = box_query(ro, ho);
-    const BoxQ<R> bc = box_query(rc, hc);
+    const BoxQ<R> bc = cavity_query(rel, col.half);
     const bool outer = bo.d >= -bc.d;
     q.b = outer ? bo : bc;
     q.rel = outer ? ro : rc;
@@ -729,6 +879,7 @@ template <class R>
 struct NodeCtx {
   int dims[3];
   R dx, dt;
+  R dx_lo;  // fp32: dx - (float)dx, so node - center = i dx - c rounds once (node_rel)
   v3<R> gravity;
   int boundary;
   R alpha_c, mu_b;
@@ -773,6 +924,88 @@ DM_HD v3<R> node_update(const NodeCtx<R>& g, const Col<R>* cols, int ncol, const
   for (int c = 0; c < ncol && c < MAXC; ++c) v = collide<R, CK>(cols[c], g.alpha_c, g.mu_b, node, v);
   boundary_apply(g, idx, v);
   return v;
+}
+
+// ---- forward node update in a moving frame ----
+// The forward transfers run relative to a per-env reference velocity vref
+// (constant during the substep; k_bin: mean velocity of the env's first
+// particles): P2G accumulates momentum relative to vref, the grid holds
+// dv = v - vref and G2P adds vref back.  Galilean shifts commute with every
+// step (momentum sums, gravity, the lab-frame collider and boundary
+// projections, the B-spline's zero first moment), so the values are the
+// reference's; fp32 then resolves velocity differences between nodes that
+// are orders of magnitude below the common velocity (a settling body: C dx
+// ~ 1e-3 |v| rounds to ~1e-4 relative in the lab frame, SURVEY 8(d)'s
+// per-substep 1e-5 gate).  The adjoints linearise in the lab frame.
+
+// node position minus c, i dx - c with one rounding (dx split in two words):
+// the SDF distance feeds exp(-alpha_c d), which turns a 3e-8 position
+// rounding into ~3e-6 relative at alpha_c = 100.
+template <class R>
+DM_HD v3<R> node_rel(const NodeCtx<R>& g, const int idx[3], v3<R> c) {
+  v3<R> r;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const R i = R(idx[a]);
+#ifdef __CUDA_ARCH__
+    if constexpr (sizeof(R) == 4) {
+      r[a] = fmaf(i, g.dx, fmaf(i, g.dx_lo, -c[a]));
+      continue;
+    }
+#endif
+    r[a] = i * g.dx + (i * g.dx_lo - c[a]);
+  }
+  return r;
+}
+
+// Increment of collide (mpm.hpp:275-294): v_out - v for lab velocity
+// v = vref + dv.  For an approaching node (v_n < 0, max(v_n, 0) = 0):
+// v_out - v = s (v_proj - v) = -s (n v_n + tang (1 - keep)).
+template <class R, int CK = -1>
+DM_HD v3<R> collide_delta(const Col<R>& col, R alpha_c, R mu_b, v3<R> node, v3<R> rel_c, v3<R> vref, v3<R> dv) {
+  R d;
+  v3<R> n;
+  collider_query_r<R, CK>(col, rel_c, d, n);
+  const R s = d < R(0) ? R(1) : r_exp(-alpha_c * r_max(d, R(0)));
+  const v3<R> vcol = col.vel + cross(col.om, node - col.c);
+  const v3<R> rel = (vref - vcol) + dv;
+  const R vn = dot(rel, n);
+  if (!(vn < R(0))) return zero3<R>();
+  const v3<R> tang = rel - n * vn;
+  const R tnorm = r_sqrt(dot(tang, tang) + R(1e-18));
+  const R keep = r_max(R(1) - mu_b * r_max(-vn, R(0)) / tnorm, R(0));
+  return (n * vn + tang * (R(1) - keep)) * (-s);
+}
+
+// node_update (mpm.hpp:256-305) from the momentum relative to vref
+// (momr = mom - mass vref); returns dv = v_new - vref.
+template <class R, int MAXC, int CK = -1>
+DM_HD v3<R> node_update_rel(const NodeCtx<R>& g, const Col<R>* cols, int ncol, const int idx[3], R mass, v3<R> momr,
+                            v3<R> vref) {
+  if (!(mass > R(0))) return zero3<R>() - vref;  // v = 0 (mpm.hpp:265-268)
+  const R inv = R(1) / mass;
+  v3<R> dv = momr * inv;
+  dv.x += g.dt * g.gravity.x;
+  dv.y += g.dt * g.gravity.y;
+  dv.z += g.dt * g.gravity.z;
+  const v3<R> node = mk3(R(idx[0]) * g.dx, R(idx[1]) * g.dx, R(idx[2]) * g.dx);
+  for (int c = 0; c < ncol && c < MAXC; ++c)
+    dv += collide_delta<R, CK>(cols[c], g.alpha_c, g.mu_b, node, node_rel(g, idx, cols[c].c), vref, dv);
+  // domain boundary on the lab-frame velocity (mpm.hpp:296-302)
+  const int bound = 3;
+  if (g.boundary == kSticky) {
+    bool band = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) band = band || idx[a] < bound || idx[a] >= g.dims[a] - bound;
+    if (band) dv = zero3<R>() - vref;
+    return dv;
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const R va = vref[a] + dv[a];
+    if ((idx[a] < bound && va < R(0)) || (idx[a] >= g.dims[a] - bound && va > R(0))) dv[a] = -vref[a];
+  }
+  return dv;
 }
 
 // Node adjoint: from vbar_out to (mass_bar, mom_bar); collider cotangents

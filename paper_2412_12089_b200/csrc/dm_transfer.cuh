@@ -92,12 +92,13 @@ struct TransferCtx {
 // (mpm.hpp:236-239 + viscosity extension).  The node at offset o receives
 //   mass: w_o m,   momentum: w_o (m v + A dpos_o),  dpos_o = (o - fx) dx
 // written as w_o (q + Ad o) with q = m v - A fx dx and Ad = A dx.
+// D = F - I (the stored deviation; law_stress_fwd).
 template <class R>
-DM_HD m3<R> p2g_affine(const Law<R>& L, const TransferCtx<R>& t, const m3<R>& F, const m3<R>& C, R act, bool* bad) {
-  const m3<R> P = law_stress(L, F, act, bad);
-  m3<R> tau = mul_bt(P, F);
+DM_HD m3<R> p2g_affine(const Law<R>& L, const TransferCtx<R>& t, const m3<R>& D, const m3<R>& C, R act, bool* bad) {
+  const m3<R> P = law_stress_fwd(L, D, act, bad);
+  m3<R> tau = P + mul_bt(P, D);  // P F^T
   if (L.kind == kFluid && L.visc != R(0)) {
-    const R jv = det(F) * L.visc;
+    const R jv = (R(1) + det1m(D)) * L.visc;
     tau += (C + transpose(C)) * jv;
   }
   const R kA = -t.dt * L.vol * R(4) * t.inv_dx * t.inv_dx;
@@ -270,11 +271,20 @@ DM_HD void p2g_vjp(const Law<R>& L, const TransferCtx<R>& t, const Stencil<R>& s
 // Factored over the separable weight (w_ijk = wij wz_k, wij = wx_i wy_j):
 //   R_ij = sum_k wz_k v_ijk,  ax[i] = sum_j wij R_ij,  ay[j] = sum_i wij R_ij,
 //   az[k] = wz_k sum_ij wij v_ijk     (~8 FMAs per node instead of 13)
+//
+// Centred on the stencil's middle node velocity v_c: B = sum w (v_n - v_c)
+// (o - fx) dx (the v_c (sum w (o - fx)) dx term is zero -- the quadratic
+// B-spline's first moment -- and is dropped) and v' = v_c + sum w (v_n - v_c).
+// For a near-uniform grid velocity (a body at rest, free fall) the affine
+// matrix is a small difference of O(|v|) sums: uncentred, fp32 rounding of
+// those sums leaves ~1e-7 |v| / dx of noise in C, above the per-substep 1e-5
+// gate when |C| dx << |v|.
 template <class R, class GetV>
 DM_HD void g2p_gather_sep(const Stencil<R>& s, R dx, GetV getv, v3<R>& vnew, m3<R>& B) {
   v3<R> ax[3], ay[3], az[3];
 #pragma unroll
   for (int q = 0; q < 3; ++q) ax[q] = ay[q] = az[q] = zero3<R>();
+  const v3<R> vc = getv(1, 1, 1);
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -283,7 +293,7 @@ DM_HD void g2p_gather_sep(const Stencil<R>& s, R dx, GetV getv, v3<R>& vnew, m3<
       v3<R> r = zero3<R>();
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        const v3<R> g = getv(i, j, k);
+        const v3<R> g = getv(i, j, k) - vc;
         r += g * s.w[2][k];
         az[k] += g * wij;
       }
@@ -292,19 +302,24 @@ DM_HD void g2p_gather_sep(const Stencil<R>& s, R dx, GetV getv, v3<R>& vnew, m3<
     }
 #pragma unroll
   for (int k = 0; k < 3; ++k) az[k] = az[k] * s.w[2][k];
-  vnew = ax[0] + ax[1] + ax[2];
+  const v3<R> dv = ax[0] + ax[1] + ax[2];
+  vnew = vc + dv;
   const v3<R> mc[3] = {ax[1] + ax[2] * R(2), ay[1] + ay[2] * R(2), az[1] + az[2] * R(2)};
 #pragma unroll
   for (int r = 0; r < 3; ++r)
 #pragma unroll
-    for (int c = 0; c < 3; ++c) B(r, c) = (mc[c][r] - vnew[r] * s.fx[c]) * dx;
+    for (int c = 0; c < 3; ++c) B(r, c) = (mc[c][r] - dv[r] * s.fx[c]) * dx;
 }
 
+// Forward G2P in deviation form: D = F - I in, D' = proj(F_new) - I out, with
+// F_new - I = D + dt C (I + D) (no rounding of F_new near I).  getv returns
+// node velocities relative to vref (node_update_rel); v' = vref + gather.
 template <class R, class GetV>
 DM_HD void g2p_particle_sep(const Law<R>& L, const TransferCtx<R>& t, const Stencil<R>& s, GetV getv, v3<R>& x,
-                            v3<R>& v, m3<R>& C, m3<R>& F, bool* bad_adv, bool* bad_det) {
+                            v3<R>& v, m3<R>& C, m3<R>& D, bool* bad_adv, bool* bad_det, v3<R> vref) {
   m3<R> B;
   g2p_gather_sep(s, t.dx, getv, v, B);
+  v = vref + v;
   C = B * (R(4) * t.inv_dx * t.inv_dx);
   x.x += t.dt * v.x;
   x.y += t.dt * v.y;
@@ -314,8 +329,8 @@ DM_HD void g2p_particle_sep(const Law<R>& L, const TransferCtx<R>& t, const Sten
     const R gx = x[a] / t.dx;
     if (!(gx >= R(1.5) && gx <= R(t.dims[a]) - R(2.5))) *bad_adv = true;  // NaN-safe
   }
-  const m3<R> Fnew = (meye<R>() + C * t.dt) * F;
-  F = law_project(L, Fnew, bad_det);
+  const m3<R> Dn = D + (C + C * D) * t.dt;
+  D = law_project_fwd(L, Dn, bad_det);
 }
 
 // d/dfx of sum_n w_n h_n for a per-node scalar h_n, accumulated separably.

@@ -302,7 +302,6 @@ def config3(seed=0, n_envs=256, env_offset=0, n_ctrl=24, n_sub=20, n_per_env=300
     xs = []
     cz = []
     acts = []
-    vol = None
     for e in range(n_envs):
         r = RngStream(seed, env_offset + e)
         semi = 0.12 * r.uniform(0.9, 1.1, 3)
@@ -318,8 +317,9 @@ def config3(seed=0, n_envs=256, env_offset=0, n_ctrl=24, n_sub=20, n_per_env=300
         xs.append(p + center)
         cz.append(center[2] + semi[2] + 0.03 + 0.005)
         acts.append(r.uniform(-1.0, 1.0, n_ctrl * 3).reshape(n_ctrl, 3))  # same stream, after geometry
-        if vol is None:
-            vol = 4.0 / 3.0 * np.pi * semi.prod() / n_per_env
+    # particle volume from the nominal ellipsoid (radius 0.12): the same for
+    # every env, so an env's inputs do not depend on which envs share the batch
+    vol = 4.0 / 3.0 * np.pi * 0.12 ** 3 / n_per_env
     x = np.stack(xs)
     N = n_per_env
     acts = np.stack(acts)

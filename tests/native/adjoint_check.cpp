@@ -34,6 +34,7 @@ Setup make_setup(const OrSim* sim, const OrMat* mats, int nmat) {
     s.t.dims[a] = sim->dims[a];
   }
   s.g.dx = sim->dx;
+  s.g.dx_lo = 0.0;
   s.g.dt = sim->dt;
   s.g.gravity = mk3(sim->gravity[0], sim->gravity[1], sim->gravity[2]);
   s.g.boundary = sim->boundary;
@@ -58,6 +59,9 @@ Setup make_setup(const OrSim* sim, const OrMat* mats, int nmat) {
       L.dlam_dE = nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
     }
     L.cy = m.wide_yield ? m.yield_stress / L.mu : m.yield_stress / (2.0 * L.mu);
+    L.mu64 = L.mu;
+    L.lam64 = L.lam;
+    L.cy64 = L.cy;
     L.visc = m.viscosity;
     L.act_k = m.act_strength;
     L.mass = m.density * m.volume;
@@ -109,7 +113,7 @@ void p2g(const Setup& s, const St& st, int n, const int* mat, const int* grp, co
     }
     bool bad = false;
     const R a = act ? act[grp[p]] : 0.0;
-    const m3<R> A = p2g_affine(L, s.t, F, C, a, &bad);
+    const m3<R> A = p2g_affine(L, s.t, F - meye<R>(), C, a, &bad);  // the device's deviation form D = F - I
     v3<R> q;
     m3<R> Ad;
     p2g_payload(A, L.mass, mk3(st.v[3 * p], st.v[3 * p + 1], st.v[3 * p + 2]), sc, s.t.dx, q, Ad);
@@ -159,7 +163,9 @@ void substep(const Setup& s, St& st, int n, const int* mat, const int* grp, cons
     m3<R> F, C;
     for (int i = 0; i < 9; ++i) F.a[i] = st.F[9 * p + i];
     bool ba = false, bd = false;
-    g2p_particle_sep(s.laws[mat[p]], s.t, sc, getv, x, v, C, F, &ba, &bd);
+    m3<R> D = F - meye<R>();
+    g2p_particle_sep(s.laws[mat[p]], s.t, sc, getv, x, v, C, D, &ba, &bd, zero3<R>());
+    F = D + meye<R>();
     if (ba) throw std::runtime_error("g2p: particle " + std::to_string(p) + " advected outside grid interior");
     for (int a = 0; a < 3; ++a) {
       st.x[3 * p + a] = x[a];
