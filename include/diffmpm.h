@@ -212,6 +212,63 @@ int dm_profile(DmContext* ctx, int enable, double* ms, long long* counts);
 /* Kernel launches issued since the context was created. */
 unsigned long long dm_launch_count(const DmContext* ctx);
 
+/* ---------------- reference tasks (env.hpp, tasks.hpp) ----------------
+ * EnvBatch<Task> (env.hpp:55-117) for the reference's MPM tasks on the GPU
+ * simulator: MiniFluidMove (tasks.hpp:502-645: fluid in a container of four
+ * inward plane walls moved by 2-D actions, reward = tiered distance of the
+ * container to the target minus the smoothed spill) and MiniRollFlat
+ * (tasks.hpp:232-369: an elastoplastic block flattened by a sphere roller
+ * moved by 3-D actions, reward = tiered(mean_z / h_flat) - Var_z).  The
+ * action -> collider maps with their clamps, the per-env task state
+ * (container / roller position), the rewards, the observations (with the
+ * stride-subsampled point cloud) and the auto-reset from each env's own
+ * RngStream(seed, env_offset + i) run behind this ABI; dm_task_backward
+ * returns dL/dactions for L = sum drewards * rewards + sum dobs * obs
+ * through the recorded steps (recompute-on-backward per control step, the
+ * role of step_checkpointed, algo.hpp:79-104).  Gradients do not flow across
+ * an auto-reset (collect_rollout, algo.hpp:171-178).  Actions, rewards and
+ * observations are double, as the reference's EnvBatch. */
+#define DM_TASK_FLUID_MOVE 0
+#define DM_TASK_ROLL_FLAT 1
+typedef struct {
+  int kind;
+  int grid_n, ppc;        /* MPM grid resolution, particles per cell (sample_box) */
+  double dt;              /* control step */
+  int substeps, episode_len, cloud_k;
+  /* MiniFluidMove::Config */
+  double container_half, fill, speed, start_x, start_y, target_x, target_y, spill_temp;
+  /* MiniRollFlat::Config */
+  double block_size, block_height, roller_radius, roller_speed, h_flat, youngs, yield_stress;
+} DmTaskConfig;
+typedef struct DmTask DmTask;
+
+/* The reference's Config{} defaults for a task kind. */
+void dm_task_default_config(int kind, DmTaskConfig* out);
+/* num_envs envs (global indices env_offset + i); horizon = tape capacity in
+ * control steps (a full tape restarts itself when stepping with record = 0). */
+DmTask* dm_task_create(const DmTaskConfig* cfg, int num_envs, int env_offset, int horizon, int device);
+void dm_task_destroy(DmTask* task);
+int dm_task_last_error(const DmTask* task, char* buf, int len);
+/* obs_dim(), act_dim(), particles per env, episode_len() (tasks.hpp). */
+int dm_task_dims(const DmTask* task, int* obs_dim, int* act_dim, int* particles_per_env, int* episode_len);
+/* EnvBatch::reset(seed): every env re-drawn from RngStream(seed, env_offset + i); the tape restarts. */
+int dm_task_reset(DmTask* task, unsigned long long seed);
+/* Task::observe of every env: obs [E][obs_dim]. */
+int dm_task_observe(DmTask* task, double* obs);
+/* EnvBatch::step: actions [E][act_dim] -> rewards [E], dones [E] (either may
+ * be NULL); done envs are reset from their own stream.  record != 0 records
+ * the step on the tape for dm_task_backward. */
+int dm_task_step(DmTask* task, const double* actions, double* rewards, unsigned char* dones, int record);
+/* Backward through the recorded steps t = 0..T-1: drewards [T][E] (may be
+ * NULL), dobs [T+1][E][obs_dim] cotangents of the observations before each
+ * step and after the last (row 0, the reset observation, carries no
+ * gradient; may be NULL) -> dactions [T][E][act_dim].  The tape restarts. */
+int dm_task_backward(DmTask* task, const double* drewards, const double* dobs, double* dactions);
+/* Recorded steps on the tape. */
+int dm_task_tape_steps(const DmTask* task);
+/* The underlying simulator context (device buffers, stream, profiling). */
+DmContext* dm_task_context(DmTask* task);
+
 #ifdef __cplusplus
 }
 #endif

@@ -317,3 +317,46 @@ def rollout_grad(sim, mats, cols, state, n_ctrl, n_sub, loss, act=None, seg=1):
         raise OracleError(err.value.decode())
     return {"loss": lo.value, "obs": obs, "x": g[0], "v": g[1], "F": g[2], "C": g[3], "cvo": gcvo[:, :len(cols)],
             "act": gact[:, :nact], "E": gE[:len(mats)], "seconds": secs.value}
+
+
+# ---- reference tasks (tasks.hpp) ----
+
+TASK_CFG_FIELDS = ("grid_n", "ppc", "dt", "substeps", "episode_len", "cloud_k", "container_half", "fill", "speed",
+                   "start_x", "start_y", "target_x", "target_y", "spill_temp", "block_size", "block_height",
+                   "roller_radius", "roller_speed", "h_flat", "youngs", "yield_stress")
+
+
+def ref_task_dims(kind: int, cfg: dict):
+    L = lib("ref")
+    c = np.ascontiguousarray([float(cfg[k]) for k in TASK_CFG_FIELDS])
+    dims = np.zeros(2, np.int32)
+    err = C.create_string_buffer(512)
+    rc = L.ref_task_rollout(C.c_int(kind), _dp(c), 1, C.c_ulonglong(0), 0, 0, None, None, None, None, None, None,
+                            _ip(dims), err, 512)
+    if rc != 0:
+        raise OracleError(err.value.decode())
+    return int(dims[0]), int(dims[1])
+
+
+def ref_task_rollout(kind: int, cfg: dict, n_envs: int, seed: int, env_offset: int, actions, w_r=None, w_o=None):
+    """The reference's MiniFluidMove (kind 0) / MiniRollFlat (1) stepped as
+    EnvBatch does with the given actions [T, E, A]: rewards [T, E], obs
+    [T+1, E, od]; with weights, dL/dactions of L = sum w_r r + sum w_o obs on
+    the reference tape."""
+    L = lib("ref")
+    od, A = ref_task_dims(kind, cfg)
+    a = np.ascontiguousarray(actions, dtype=np.float64)
+    T = a.shape[0]
+    assert a.shape == (T, n_envs, A)
+    c = np.ascontiguousarray([float(cfg[k]) for k in TASK_CFG_FIELDS])
+    rew = np.zeros((T, n_envs))
+    obs = np.zeros((T + 1, n_envs, od))
+    wr = None if w_r is None else np.ascontiguousarray(w_r, dtype=np.float64)
+    wo = None if w_o is None else np.ascontiguousarray(w_o, dtype=np.float64)
+    da = np.zeros_like(a)
+    err = C.create_string_buffer(512)
+    rc = L.ref_task_rollout(C.c_int(kind), _dp(c), n_envs, C.c_ulonglong(seed), env_offset, T, _dp(a), _dp(rew),
+                            _dp(obs), _dp(wr), _dp(wo), _dp(da), None, err, 512)
+    if rc != 0:
+        raise OracleError(err.value.decode())
+    return rew, obs, (da if wr is not None else None)

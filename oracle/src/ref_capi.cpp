@@ -22,6 +22,8 @@
 #include "diffsim/rng.hpp"
 #include "diffsim/mpm.hpp"
 #include "diffsim/tape.hpp"
+#include "diffsim/env.hpp"
+#include "diffsim/tasks.hpp"
 
 // tape overload of the restatement's SVD hook (mirrors linalg.hpp:173-194)
 #include "oracle/linalg.hpp"
@@ -530,6 +532,159 @@ int ref_rollout_grad(const OrSim* sim, const OrMat* mats, int nmat, const OrCol*
       for (int i = 0; i < n_ctrl * nact; ++i) gact[i] = tape.grad(a_leaves[i]);
     if (gE)
       for (int i = 0; i < nmat; ++i) gE[i] = tape.grad(e_leaves[i]);
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(e.what(), err, errlen);
+    return 1;
+  }
+}
+
+// (4) the reference's own tasks (tasks.hpp) stepped as EnvBatch does
+// (env.hpp:55-117: per-env RngStream(seed, env_offset + i), Task::reset,
+// auto-reset at episode_len) with given actions [T][E][A]: rewards [T][E]
+// and observations [T+1][E][obs_dim] (before each step and after the last;
+// a reset env's next observation is of its reset state).  With w_r != NULL
+// the same rollout is recorded on the reference tape, each step a
+// recompute-on-backward segment (step_checkpointed restated, algo.hpp:79-104),
+// and dact receives dL/dactions of L = sum w_r reward + sum w_o obs (rows
+// t >= 1 of w_o; gradients do not cross a reset, algo.hpp:171-178).
+}  // extern "C"
+namespace {
+template <class Task>
+diffsim::Value task_step_checkpointed(Tape& tape, const Task& task, typename Task::template State<Value>& st,
+                                      const std::vector<Value>& action) {
+  const auto shape = diffsim::env::lower_state<Task>(st);
+  std::vector<Value> inputs;
+  Task::visit(st, [&](Value& v) { inputs.push_back(v); });
+  const std::size_t n_state = inputs.size();
+  inputs.insert(inputs.end(), action.begin(), action.end());
+  auto outs = tape.checkpoint(
+      [&task, shape, n_state](Tape&, std::span<const Value> in) {
+        auto s = Task::template convert<Value, double>(shape);
+        std::size_t i = 0;
+        Task::visit(s, [&](Value& v) { v = in[i++]; });
+        std::vector<Value> act(in.begin() + n_state, in.end());
+        Value r = task.step(s, std::span<const Value>(act));
+        std::vector<Value> out;
+        Task::visit(s, [&](Value& v) { out.push_back(v); });
+        out.push_back(r);
+        return out;
+      },
+      inputs);
+  std::size_t i = 0;
+  Task::visit(st, [&](Value& v) { v = outs[i++]; });
+  return outs.back();
+}
+
+template <class Task>
+void task_rollout(const Task& task, int n_envs, unsigned long long seed, int env_offset, int T,
+                  const double* actions, double* rewards, double* obs, const double* w_r, const double* w_o,
+                  double* dact) {
+  const int A = task.act_dim(), od = task.obs_dim(), L = task.episode_len();
+  for (int i = 0; i < n_envs; ++i) {
+    diffsim::RngStream rng(seed, static_cast<std::uint64_t>(env_offset + i));
+    typename Task::template State<double> s;
+    task.reset(s, rng);
+    auto s0 = s;
+    auto rng0 = rng;
+    int cursor = 0;
+    auto put_obs = [&](int t, const std::vector<double>& o) {
+      for (int k = 0; k < od; ++k) obs[((std::size_t)t * n_envs + i) * od + k] = o[k];
+    };
+    put_obs(0, task.observe(s));
+    for (int t = 0; t < T; ++t) {
+      const double* a = actions + ((std::size_t)t * n_envs + i) * A;
+      const double r = task.step(s, std::span<const double>(a, A));
+      rewards[(std::size_t)t * n_envs + i] = r;
+      if (++cursor >= L) {
+        task.reset(s, rng);
+        cursor = 0;
+      }
+      put_obs(t + 1, task.observe(s));
+    }
+    if (!w_r) continue;
+    Tape tape;
+    rng = rng0;
+    auto st = diffsim::env::lift_state<Task>(tape, s0);
+    cursor = 0;
+    Value total(0.0);
+    std::vector<std::vector<Value>> leaves(T);
+    for (int t = 0; t < T; ++t) {
+      const double* a = actions + ((std::size_t)t * n_envs + i) * A;
+      for (int k = 0; k < A; ++k) leaves[t].push_back(tape.var(a[k]));
+      const Value r = task_step_checkpointed(tape, task, st, leaves[t]);
+      total = total + r * Value(w_r[(std::size_t)t * n_envs + i]);
+      if (++cursor >= L) {  // reset: a fresh (constant-lifted) state
+        auto lowered = diffsim::env::lower_state<Task>(st);
+        task.reset(lowered, rng);
+        st = diffsim::env::lift_state<Task>(tape, lowered);
+        cursor = 0;
+      } else if (w_o) {
+        const auto o = task.observe(st);
+        for (int k = 0; k < od; ++k) total = total + o[k] * Value(w_o[((std::size_t)(t + 1) * n_envs + i) * od + k]);
+      }
+    }
+    if (!total.is_const()) tape.backward(total);
+    for (int t = 0; t < T; ++t)
+      for (int k = 0; k < A; ++k)
+        dact[((std::size_t)t * n_envs + i) * A + k] = total.is_const() ? 0.0 : tape.grad(leaves[t][k]);
+  }
+}
+}  // namespace
+extern "C" {
+
+// cfg: the DmTaskConfig fields as doubles in header order from grid_n:
+// grid_n, ppc, dt, substeps, episode_len, cloud_k, container_half, fill,
+// speed, start_x, start_y, target_x, target_y, spill_temp, block_size,
+// block_height, roller_radius, roller_speed, h_flat, youngs, yield_stress.
+int ref_task_rollout(int kind, const double* cfg, int n_envs, unsigned long long seed, int env_offset, int T,
+                     const double* actions, double* rewards, double* obs, const double* w_r, const double* w_o,
+                     double* dact, int* dims, char* err, int errlen) {
+  try {
+    if (kind == 0) {
+      diffsim::tasks::MiniFluidMove::Config c;
+      c.grid_n = (int)cfg[0];
+      c.ppc = (int)cfg[1];
+      c.dt = cfg[2];
+      c.substeps = (int)cfg[3];
+      c.episode_len = (int)cfg[4];
+      c.cloud_k = (int)cfg[5];
+      c.container_half = cfg[6];
+      c.fill = cfg[7];
+      c.speed = cfg[8];
+      c.start_x = cfg[9];
+      c.start_y = cfg[10];
+      c.target_x = cfg[11];
+      c.target_y = cfg[12];
+      c.spill_temp = cfg[13];
+      diffsim::tasks::MiniFluidMove task(c);
+      if (dims) {
+        dims[0] = task.obs_dim();
+        dims[1] = task.act_dim();
+      }
+      if (T > 0) task_rollout(task, n_envs, seed, env_offset, T, actions, rewards, obs, w_r, w_o, dact);
+    } else {
+      diffsim::tasks::MiniRollFlat::Config c;
+      c.grid_n = (int)cfg[0];
+      c.ppc = (int)cfg[1];
+      c.dt = cfg[2];
+      c.substeps = (int)cfg[3];
+      c.episode_len = (int)cfg[4];
+      c.cloud_k = (int)cfg[5];
+      c.block_size = cfg[14];
+      c.block_height = cfg[15];
+      c.roller_radius = cfg[16];
+      c.roller_speed = cfg[17];
+      c.h_flat = cfg[18];
+      c.youngs = cfg[19];
+      c.yield_stress = cfg[20];
+      diffsim::tasks::MiniRollFlat task(c);
+      if (dims) {
+        dims[0] = task.obs_dim();
+        dims[1] = task.act_dim();
+      }
+      if (T > 0) task_rollout(task, n_envs, seed, env_offset, T, actions, rewards, obs, w_r, w_o, dact);
+    }
     return 0;
   } catch (const std::exception& e) {
     put_err(e.what(), err, errlen);

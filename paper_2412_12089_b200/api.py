@@ -53,6 +53,15 @@ class DmLatticeReset(C.Structure):
                 ("material", C.c_int), ("group", C.c_int)]
 
 
+class DmTaskConfig(C.Structure):
+    _fields_ = [("kind", C.c_int), ("grid_n", C.c_int), ("ppc", C.c_int), ("dt", C.c_double), ("substeps", C.c_int),
+                ("episode_len", C.c_int), ("cloud_k", C.c_int), ("container_half", C.c_double), ("fill", C.c_double),
+                ("speed", C.c_double), ("start_x", C.c_double), ("start_y", C.c_double), ("target_x", C.c_double),
+                ("target_y", C.c_double), ("spill_temp", C.c_double), ("block_size", C.c_double),
+                ("block_height", C.c_double), ("roller_radius", C.c_double), ("roller_speed", C.c_double),
+                ("h_flat", C.c_double), ("youngs", C.c_double), ("yield_stress", C.c_double)]
+
+
 _LIB = None
 
 _P = C.c_void_p
@@ -86,6 +95,17 @@ _SIGS = {
     "dm_reset_lattice": (C.c_int, [_P, C.POINTER(DmLatticeReset), C.c_ulonglong, C.c_int, _P, _P, _P]),
     "dm_reset_lattice_device": (C.c_int, [_P, C.POINTER(DmLatticeReset), C.c_ulonglong, C.c_int, _P, _P, _P]),
     "dm_sync": (C.c_int, [_P]),
+    "dm_task_default_config": (None, [C.c_int, C.POINTER(DmTaskConfig)]),
+    "dm_task_create": (_P, [C.POINTER(DmTaskConfig), C.c_int, C.c_int, C.c_int, C.c_int]),
+    "dm_task_destroy": (None, [_P]),
+    "dm_task_last_error": (C.c_int, [_P, C.c_char_p, C.c_int]),
+    "dm_task_dims": (C.c_int, [_P, _P, _P, _P, _P]),
+    "dm_task_reset": (C.c_int, [_P, C.c_ulonglong]),
+    "dm_task_observe": (C.c_int, [_P, _P]),
+    "dm_task_step": (C.c_int, [_P, _P, _P, _P, C.c_int]),
+    "dm_task_backward": (C.c_int, [_P, _P, _P, _P]),
+    "dm_task_tape_steps": (C.c_int, [_P]),
+    "dm_task_context": (_P, [_P]),
     "dm_debug_inject": (C.c_int, [_P, C.c_int, C.c_int, C.c_int]),
 }
 
@@ -442,3 +462,91 @@ def run_scene(sim_batch: MpmBatch, scene, want_grad=True):
         g = sim_batch.backward(dobs=np.ascontiguousarray(np.transpose(dobs, (1, 0, 2)), dtype=np.float32))
         out.update(g)
     return out
+
+
+TASKS = {"fluid_move": 0, "roll_flat": 1}
+
+
+def task_config(kind: str, **over) -> dict:
+    """The reference task's Config{} defaults (tasks.hpp:241-254, 511-525),
+    with overrides."""
+    L = lib()
+    c = DmTaskConfig()
+    L.dm_task_default_config(TASKS[kind], C.byref(c))
+    d = {f: getattr(c, f) for f, _ in DmTaskConfig._fields_}
+    for k, v in over.items():
+        if k not in d:
+            raise KeyError(k)
+        d[k] = v
+    return d
+
+
+class TaskBatch:
+    """EnvBatch<Task> (env.hpp:55-117) for MiniFluidMove / MiniRollFlat
+    (tasks.hpp) on the GPU simulator (dm_task_* ABI): reset / observe /
+    step(actions) -> rewards, dones with auto-reset / backward(drewards,
+    dobs) -> dL/dactions.  Double precision arrays, as the reference."""
+
+    def __init__(self, cfg: dict, num_envs: int, seed: int = 0, horizon: int = 64, device: int = 0,
+                 env_offset: int = 0):
+        L = lib()
+        c = DmTaskConfig()
+        for f, _ in DmTaskConfig._fields_:
+            setattr(c, f, cfg[f] if f != "kind" or not isinstance(cfg[f], str) else TASKS[cfg[f]])
+        self._L = L
+        self._h = L.dm_task_create(C.byref(c), num_envs, env_offset, horizon, device)
+        if not self._h:
+            raise MemoryError("dm_task_create failed")
+        msg = C.create_string_buffer(1024)
+        if L.dm_task_last_error(self._h, msg, 1024) != 0:
+            text = msg.value.decode()
+            L.dm_task_destroy(self._h)
+            self._h = None
+            raise ValueError(text)
+        dims = [C.c_int(0) for _ in range(4)]
+        L.dm_task_dims(self._h, *(C.byref(d) for d in dims))
+        self.E = num_envs
+        self.obs_dim, self.act_dim, self.particles_per_env, self.episode_len = (int(d.value) for d in dims)
+        self.reset(seed)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.dm_task_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def _check(self, rc):
+        if rc != 0:
+            msg = C.create_string_buffer(1024)
+            self._L.dm_task_last_error(self._h, msg, 1024)
+            raise (ValueError if rc == 1 else RuntimeError)(msg.value.decode())
+
+    def reset(self, seed: int):
+        self._check(self._L.dm_task_reset(self._h, seed))
+
+    def observe(self):
+        o = np.zeros((self.E, self.obs_dim))
+        self._check(self._L.dm_task_observe(self._h, _ptr(o)))
+        return o
+
+    def step(self, actions, record: bool = True):
+        a = np.ascontiguousarray(actions, dtype=np.float64).reshape(self.E, self.act_dim)
+        r = np.zeros(self.E)
+        d = np.zeros(self.E, np.uint8)
+        self._check(self._L.dm_task_step(self._h, _ptr(a), _ptr(r), _ptr(d), int(record)))
+        return r, d.astype(bool)
+
+    @property
+    def tape_steps(self) -> int:
+        return int(self._L.dm_task_tape_steps(self._h))
+
+    def backward(self, drewards=None, dobs=None):
+        T = self.tape_steps
+        dr = None if drewards is None else np.ascontiguousarray(drewards, dtype=np.float64).reshape(T, self.E)
+        do = None if dobs is None else np.ascontiguousarray(dobs, dtype=np.float64).reshape(T + 1, self.E,
+                                                                                             self.obs_dim)
+        da = np.zeros((T, self.E, self.act_dim))
+        self._check(self._L.dm_task_backward(self._h, _ptr(dr), _ptr(do), _ptr(da)))
+        return da

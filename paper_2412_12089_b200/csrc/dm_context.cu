@@ -6,6 +6,7 @@
 // (algo.hpp:79-104).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -89,6 +90,14 @@ struct DmContext {
   int cfl_checked = 0;                           // steps whose CFL word the host has read
   unsigned long long* replay_bad = nullptr;      // replay-verification word (k_replay_check)
   int inj_step = -1, inj_env = 0, inj_particle = 0;  // dm_debug_inject
+  // task layer (dm_task_*): per-step spill centers and their cotangents, and
+  // the envs reset at the end of each recorded step (the gradient is cut there)
+  float* spc_tape = nullptr;     // [max_steps][E][2]
+  double* gspc = nullptr;        // [max_steps][E][2]
+  unsigned char* cut_tape = nullptr;  // [max_steps][E]
+  std::vector<char> cut_any;     // per step: any env reset
+  float* dcloud_buf = nullptr;   // [E][cloud] x cotangent staging
+  int cloud_n = 0, cloud_stride = 1;
   // optional per-kernel-class CUDA-event timing (bench roofline)
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -516,7 +525,7 @@ int ensure_blk_pool(DmContext* ctx, size_t need) {
 }
 
 int step_impl(DmContext* ctx, const float* cvo, const float* act, float* obs, cudaMemcpyKind kin,
-              cudaMemcpyKind kout) {
+              cudaMemcpyKind kout, const float* spc = nullptr) {
   if (ctx->poisoned) {
     if (ctx->err.empty()) ctx->err = "context poisoned by an earlier error";
     return DM_ERR_RUNTIME;
@@ -577,9 +586,18 @@ int step_impl(DmContext* ctx, const float* cvo, const float* act, float* obs, cu
   DM_CUDA(cudaMemcpyAsync(ctx->vmax_hist + t, &ctx->flags->vmax_bits, sizeof(unsigned), cudaMemcpyDeviceToDevice,
                           ctx->stream));
   float* o = ctx->obs_tape + (size_t)t * E * ctx->od;
+  float* spc_t = nullptr;
+  if (spc) {  // task mode: the spill is measured about the post-step container position
+    spc_t = ctx->spc_tape + (size_t)t * E * 2;
+    DM_CUDA(cudaMemcpyAsync(spc_t, spc, (size_t)E * 2 * sizeof(float), kin, ctx->stream));
+  }
+  if (ctx->cut_tape) {
+    DM_CUDA(cudaMemsetAsync(ctx->cut_tape + (size_t)t * E, 0, E, ctx->stream));
+    ctx->cut_any[t] = 0;
+  }
   PROF_BEGIN(ctx, 6);
   k_obs<<<E, 256, 0, ctx->stream>>>(ctx->P, fwd_state(ctx, (t + 1) * S), step_cvo(ctx, t), (float)ctx->cfg.spill_half,
-                                    (float)ctx->cfg.spill_temp, ctx->cfg.obs_groups, o, ctx->od);
+                                    (float)ctx->cfg.spill_temp, ctx->cfg.obs_groups, o, ctx->od, spc_t);
   PROF_END(ctx, 6);
   ++ctx->launches;
   if (obs) DM_CUDA(cudaMemcpyAsync(obs, o, (size_t)E * ctx->od * sizeof(float), kout, ctx->stream));
@@ -658,8 +676,11 @@ int copy_out_f32(DmContext* ctx, float* dst, const double* src, size_t n, cudaMe
   return DM_OK;
 }
 
+// dcloud_t (task layer, host): cotangent of the step's point-cloud
+// observation [E][cloud_n][3]; gspc_t (host): receives the spill-center
+// cotangents [E][2] of a task-mode step.
 int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dact_t, cudaMemcpyKind kin,
-                  cudaMemcpyKind kout) {
+                  cudaMemcpyKind kout, const float* dcloud_t = nullptr, double* gspc_t = nullptr) {
   if (ctx->poisoned) return DM_ERR_RUNTIME;
   if (ctx->bwd_t < 0) {
     ctx->err = "backward_step: no backward in progress (call dm_backward_begin)";
@@ -670,17 +691,20 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
   const size_t N = ctx->Ntot;
   int cur = ctx->bwd_cur;
   const int s_end = (t + 1) * S;
-  if (dobs_t) {
-    DM_CUDA(cudaMemcpyAsync(ctx->dobs_buf, dobs_t, (size_t)E * ctx->od * sizeof(float), kin, ctx->stream));
-    PROF_BEGIN(ctx, 7);
-    k_obs_adj<<<E, 256, 0, ctx->stream>>>(ctx->P, store_view(ctx, s_end / ck), step_cvo(ctx, t),
-                                          (float)ctx->cfg.spill_half, (float)ctx->cfg.spill_temp,
-                                          ctx->cfg.obs_groups, ctx->dobs_buf, ctx->od, ctx->adj[cur], N,
-                                          ctx->gcvo + (size_t)t * E * Kc * 9);
-    PROF_END(ctx, 7);
+  const bool cut = ctx->cut_tape && ctx->cut_any[t];
+  const unsigned char* cut_t = cut ? ctx->cut_tape + (size_t)t * E : nullptr;
+  if (cut) {  // envs reset after this step: no cotangent flows back across the reset (algo.hpp:171-178)
+    k_cut_adj<<<ctx->grid_tiles, 256, 0, ctx->stream>>>(ctx->P, cut_t, ctx->adj[cur], N);
     ++ctx->launches;
   }
+  if (dobs_t) DM_CUDA(cudaMemcpyAsync(ctx->dobs_buf, dobs_t, (size_t)E * ctx->od * sizeof(float), kin, ctx->stream));
+  if (dcloud_t)
+    DM_CUDA(cudaMemcpyAsync(ctx->dcloud_buf, dcloud_t, (size_t)E * ctx->cloud_n * 3 * sizeof(float),
+                            cudaMemcpyHostToDevice, ctx->stream));
   const bool kept = t == ctx->kept_t && ctx->kept_ok;  // the forward kept this step's segment
+  const float* spc_t = ctx->spc_tape && gspc_t ? ctx->spc_tape + (size_t)t * E * 2 : nullptr;
+  if (spc_t) DM_CUDA(cudaMemsetAsync(ctx->gspc + (size_t)t * E * 2, 0, (size_t)E * 2 * sizeof(double), ctx->stream));
+  bool first = true;
   for (int s0 = s_end - ck; s0 >= t * S; s0 -= ck) {
     // replay the segment's forward (tape.hpp:229-233), keeping every
     // substep's sort and grid blocks for its adjoint
@@ -696,8 +720,30 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
       if (ctx->inj_step == t)  // dm_debug_inject: a non-deterministic forward
         k_debug_flip<<<(ctx->P.N + 255) / 256, 256, 0, ctx->stream>>>(ctx->P, tl, ctx->inj_env, ctx->inj_particle);
       k_replay_check<<<ctx->grid_tiles, 256, 0, ctx->stream>>>(ctx->P, tl, store_view(ctx, (s0 + ck) / ck),
-                                                                ctx->law == kFluid, nullptr, ctx->replay_bad);
+                                                                ctx->law == kFluid, s0 + ck == s_end ? cut_t : nullptr,
+                                                                ctx->replay_bad);
       ctx->launches += 1 + (ctx->inj_step == t);
+    }
+    if (first) {
+      // the step's observables are of its end state before any reset: the
+      // replay's exit (== the stored state for envs not reset), or the
+      // stored state of a kept segment (never reset)
+      first = false;
+      const StateView Se = kept ? store_view(ctx, s_end / ck) : view(ctx->tail, ctx->tail_attr, ctx->Ntot);
+      if (dobs_t) {
+        PROF_BEGIN(ctx, 7);
+        k_obs_adj<<<E, 256, 0, ctx->stream>>>(ctx->P, Se, step_cvo(ctx, t), (float)ctx->cfg.spill_half,
+                                              (float)ctx->cfg.spill_temp, ctx->cfg.obs_groups, ctx->dobs_buf, ctx->od,
+                                              ctx->adj[cur], N, ctx->gcvo + (size_t)t * E * Kc * 9, spc_t,
+                                              spc_t ? ctx->gspc + (size_t)t * E * 2 : nullptr);
+        PROF_END(ctx, 7);
+        ++ctx->launches;
+      }
+      if (dcloud_t) {
+        k_cloud_adj<<<ctx->grid_tiles, 256, 0, ctx->stream>>>(ctx->P, Se.attr, ctx->cloud_stride, ctx->cloud_n,
+                                                               ctx->dcloud_buf, nullptr, ctx->adj[cur], N);
+        ++ctx->launches;
+      }
     }
     for (int q = ck - 1; q >= 0; --q) {
       const int s = s0 + q;
@@ -717,7 +763,10 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
     rc = copy_out_f32(ctx, dcvo_t, ctx->gcvo + (size_t)t * E * Kc * 9, (size_t)E * Kc * 9, kout);
   if (rc == DM_OK && dact_t && ctx->P.G > 0)
     rc = copy_out_f32(ctx, dact_t, ctx->gact + (size_t)t * E * Gc, (size_t)E * Gc, kout);
-  if (rc == DM_OK && kout != cudaMemcpyDeviceToDevice && (dcvo_t || dact_t))
+  if (rc == DM_OK && spc_t)
+    DM_CUDA(cudaMemcpyAsync(gspc_t, ctx->gspc + (size_t)t * E * 2, (size_t)E * 2 * sizeof(double),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+  if (rc == DM_OK && kout != cudaMemcpyDeviceToDevice && (dcvo_t || dact_t || gspc_t))
     DM_CUDA(cudaStreamSynchronize(ctx->stream));  // host outputs are complete on return
   return rc;
 }
@@ -870,9 +919,6 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
     L.act_k = (float)M.act_strength;
     L.mass = (float)(M.density * M.volume);
     L.vol = (float)M.volume;
-    L.mu64 = mu;
-    L.lam64 = lam;
-    L.cy64 = M.wide_yield ? M.yield_stress / mu : M.yield_stress / (2.0 * mu);
     L.dmu_dE = (float)ctx->dmu_dE[m];
     L.dlam_dE = (float)ctx->dlam_dE[m];
     P.dmu_dE[m] = ctx->dmu_dE[m];
@@ -969,7 +1015,7 @@ void dm_destroy(DmContext* ctx) {
                   ctx->blocks,    ctx->ablocks,    ctx->tile_acc,   ctx->gmp, ctx->gv, ctx->gmb,   ctx->flags, ctx->wq, ctx->cvo_tape,  ctx->act_tape,
                   ctx->obs_tape,  ctx->dobs_buf, ctx->gcvo,       ctx->gact,       ctx->gmu,        ctx->glam,
                   ctx->obs_cvo,   ctx->obs_out,  ctx->f32_stage,  ctx->dE_dev,     ctx->vmax_hist,  ctx->replay_bad,
-                  ctx->vref_all};
+                  ctx->vref_all,  ctx->spc_tape, ctx->gspc,       ctx->cut_tape,   ctx->dcloud_buf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
@@ -1190,7 +1236,7 @@ static int observe_impl(DmContext* ctx, const float* cvo, float* obs, cudaMemcpy
                                     ctx->od);
   ++ctx->launches;
   DM_CUDA(cudaMemcpyAsync(obs, o, (size_t)E * ctx->od * sizeof(float), kout, ctx->stream));
-  DM_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (kout != cudaMemcpyDeviceToDevice) DM_CUDA(cudaStreamSynchronize(ctx->stream));
   return DM_OK;
 }
 int dm_observe(DmContext* ctx, const float* cvo, float* obs) {
@@ -1215,3 +1261,5 @@ int dm_debug_sort(DmContext* ctx, int* keys, int* perm) {
 }
 
 }  // extern "C"
+
+#include "dm_task.cuh"

@@ -1519,8 +1519,11 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 // (tasks.hpp:286-304, 604-615) followed, when ngr > 0, by pooled statistics of
 // each actuation group g (config 5's 64-d observation): mean x (3), mean v (3),
 // var z (1), mean |v| (1).  fp64 sums in a fixed order (deterministic).
+// spc: optional per-env spill centers [E][2] (a task's post-step container
+// position, tasks.hpp:599-611); nullptr: collider 0's center from cvo.
 __global__ void __launch_bounds__(256) k_obs(DevParams P, StateView S, const float* __restrict__ cvo, float spill_half,
-                                             float spill_temp, int ngr, float* __restrict__ obs, int od) {
+                                             float spill_temp, int ngr, float* __restrict__ obs, int od,
+                                             const float* __restrict__ spc = nullptr) {
   __shared__ double sh[8];
   const int e = blockIdx.x;
   const size_t base = (size_t)e * P.N;
@@ -1533,7 +1536,8 @@ __global__ void __launch_bounds__(256) k_obs(DevParams P, StateView S, const flo
   for (int a = 0; a < 3; ++a) m[a] = block_sum(s[a], sh) / P.N;
   double q[3] = {0.0, 0.0, 0.0}, sp = 0.0;
   const bool spill = P.K > 0 && spill_temp > 0.f;
-  const double cx = spill ? cvo[(size_t)e * P.K * 9 + 0] : 0.0, cy = spill ? cvo[(size_t)e * P.K * 9 + 1] : 0.0;
+  const float* sc = spc ? spc + (size_t)e * 2 : cvo + (size_t)e * P.K * 9;
+  const double cx = spill ? sc[0] : 0.0, cy = spill ? sc[1] : 0.0;
   for (int p = threadIdx.x; p < P.N; p += blockDim.x) {
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -1605,10 +1609,13 @@ __global__ void __launch_bounds__(256) k_obs(DevParams P, StateView S, const flo
 
 // Adds the observable cotangent into the state cotangent (physical order of
 // that state) and the spill's collider-center cotangent into gcvo_t.
+// spc / gspc_t: per-env spill centers and their cotangents (task mode, see
+// k_obs); nullptr: collider 0's center, cotangent into gcvo_t.
 __global__ void __launch_bounds__(256) k_obs_adj(DevParams P, StateView S, const float* __restrict__ cvo,
                                                  float spill_half, float spill_temp, int ngr,
                                                  const float* __restrict__ dobs, int od, float* __restrict__ adj,
-                                                 size_t astride, double* __restrict__ gcvo_t) {
+                                                 size_t astride, double* __restrict__ gcvo_t,
+                                                 const float* __restrict__ spc = nullptr, double* __restrict__ gspc_t = nullptr) {
   __shared__ double sh[8];
   const int e = blockIdx.x;
   const size_t base = (size_t)e * P.N;
@@ -1621,7 +1628,8 @@ __global__ void __launch_bounds__(256) k_obs_adj(DevParams P, StateView S, const
 #pragma unroll
   for (int a = 0; a < 3; ++a) m[a] = block_sum(s[a], sh) / P.N;
   const bool spill = P.K > 0 && spill_temp > 0.f && ob[6] != 0.f;
-  const double cx = spill ? cvo[(size_t)e * P.K * 9 + 0] : 0.0, cy = spill ? cvo[(size_t)e * P.K * 9 + 1] : 0.0;
+  const float* sc = spc ? spc + (size_t)e * 2 : cvo + (size_t)e * P.K * 9;
+  const double cx = spill ? sc[0] : 0.0, cy = spill ? sc[1] : 0.0;
   double gcx = 0.0, gcy = 0.0;
   const double invn = 1.0 / P.N;
   for (int p = threadIdx.x; p < P.N; p += blockDim.x) {
@@ -1651,8 +1659,9 @@ __global__ void __launch_bounds__(256) k_obs_adj(DevParams P, StateView S, const
     gcx = block_sum(gcx, sh);
     gcy = block_sum(gcy, sh);
     if (threadIdx.x == 0) {
-      gcvo_t[(size_t)e * P.K * 9 + 0] += gcx;
-      gcvo_t[(size_t)e * P.K * 9 + 1] += gcy;
+      double* g = spc ? gspc_t + (size_t)e * 2 : gcvo_t + (size_t)e * P.K * 9;
+      g[0] += gcx;
+      g[1] += gcy;
     }
   }
   // pooled group statistics
@@ -1923,6 +1932,74 @@ __global__ void k_debug_flip(DevParams P, StateView S, int e, int p) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.N; i += gridDim.x * blockDim.x) {
     const size_t j = (size_t)e * P.N + i;
     if ((int)attr_index(S.attr[j]) == p) S.c(0, j) = __uint_as_float(__float_as_uint(S.c(0, j)) ^ 1u);
+  }
+}
+
+// ============================ task support ============================
+// Point-cloud observation (tasks.hpp:296-301, 566-569): x of the particles
+// with original index p = 0, stride, 2 stride, ... (p / stride < ncloud),
+// written to out[e * ostride + ooff + 3 (p / stride) + a].
+__global__ void k_cloud(DevParams P, StateView S, int stride, int ncloud, float* __restrict__ out, int ostride,
+                        int ooff) {
+  const size_t tot = (size_t)P.E * P.N;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
+    const int p = (int)attr_index(S.attr[i]);
+    if (p % stride || p / stride >= ncloud) continue;
+    float* o = out + (i / P.N) * ostride + ooff + 3 * (p / stride);
+    o[0] = S.c(0, i);
+    o[1] = S.c(1, i);
+    o[2] = S.c(2, i);
+  }
+}
+
+// Adjoint of k_cloud: dcloud [E][ncloud][3] added into the x cotangent of
+// the state with attributes attr (envs with cut[e] != 0 skipped).
+__global__ void k_cloud_adj(DevParams P, const uint32_t* __restrict__ attr, int stride, int ncloud,
+                            const float* __restrict__ dcloud, const unsigned char* __restrict__ cut,
+                            float* __restrict__ adj, size_t astride) {
+  const size_t tot = (size_t)P.E * P.N;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
+    const int e = (int)(i / P.N);
+    if (cut && cut[e]) continue;
+    const int p = (int)attr_index(attr[i]);
+    if (p % stride || p / stride >= ncloud) continue;
+    const float* d = dcloud + ((size_t)e * ncloud + p / stride) * 3;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) adj[adj_index(a, i, astride)] += d[a];
+  }
+}
+
+// EnvBatch::reset_env (env.hpp:93-96) on the device: masked envs of state S
+// take the task's particle template (x per particle in visit order; v = 0,
+// F = I, C = 0 -- Task::reset copies the sample_box template).
+__global__ void k_task_reset(DevParams P, StateView S, const float* __restrict__ tmpl_x,
+                             const unsigned char* __restrict__ mask, int material) {
+  const size_t tot = (size_t)P.E * P.N;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
+    const int e = (int)(i / P.N), p = (int)(i % P.N);
+    if (!mask[e]) continue;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      S.c(a, i) = tmpl_x[3 * p + a];
+      S.c(3 + a, i) = 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      S.c(6 + q, i) = 0.f;  // D = F - I = 0
+      S.c(15 + q, i) = 0.f;
+    }
+    S.attr[i] = (uint32_t)p | (((uint32_t)material & 0xF) << 20);
+  }
+}
+
+// Zeroes the state cotangent of envs whose state was replaced by a reset
+// (the gradient does not flow across it, algo.hpp:171-178).
+__global__ void k_cut_adj(DevParams P, const unsigned char* __restrict__ cut, float* __restrict__ adj, size_t astride) {
+  const size_t tot = (size_t)P.E * P.N;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
+    if (!cut[i / P.N]) continue;
+#pragma unroll
+    for (int f = 0; f < 24; ++f) adj[adj_index(f, i, astride)] = 0.f;
   }
 }
 

@@ -29,7 +29,6 @@ struct Law {
   R mu, lam, cy, visc, act_k;
   R mass, vol;
   R dmu_dE, dlam_dE;
-  double mu64, lam64, cy64;  // fp64 constants of the SVD laws' forward evaluation (law_stress_fwd)
 };
 
 template <class R>
@@ -148,8 +147,12 @@ DM_HD m3<R> law_project(const Law<R>& L, const m3<R>& F, bool* bad) {
 // relative precision (F itself would round it to 6e-8 absolute, i.e. 6 % of a
 // 1e-6 strain; SURVEY 8(d)'s per-substep 1e-5 gate on a resting elastic body
 // needs ~1e-7).  The forward stress and projection are evaluated from D:
-//   * SVD laws (fixed-corotated, Hencky / von Mises): in fp64 from
-//     F = I + D (exact in fp64) -- an fp32 SVD of I + D loses the strain
+//   * SVD laws (fixed-corotated, Hencky / von Mises): the SVD of F = I + D
+//     from the symmetric eigenproblem of S = F^T F - I = D + D^T + D^T D
+//     (fp32 Jacobi; S and its eigenvalues lambda_i = sigma_i^2 - 1 are
+//     resolved relative to |D|, so eps_i = log1p(lambda_i) / 2 and
+//     sigma_i - 1 = lambda_i / (1 + sigma_i) keep their precision) -- a
+//     one-sided SVD of I + D rounds the singular values to 6e-8 absolute
 //   * fluid: J - 1 = det(I + D) - 1 expanded in D (det1m), no cancellation
 //   * neo-Hookean: P expanded around F = I (the two O(mu) terms cancel there)
 // The adjoints linearise at F = I + D in fp32 (their terms do not cancel).
@@ -171,38 +174,102 @@ DM_HD m3<R> eye_plus(const m3<R>& D) {
   return F;
 }
 
+// SVD of F = I + D with lam_i = s_i^2 - 1 (Svd's s, u, v; v a rotation).
 template <class R>
-DM_HD Law<double> law64(const Law<R>& L) {
-  Law<double> d;
-  d.kind = L.kind;
-  d.mu = L.mu64;
-  d.lam = L.lam64;
-  d.cy = L.cy64;
-  d.visc = L.visc;
-  d.act_k = L.act_k;
-  d.mass = L.mass;
-  d.vol = L.vol;
-  d.dmu_dE = L.dmu_dE;
-  d.dlam_dE = L.dlam_dE;
-  d.mu64 = L.mu64;
-  d.lam64 = L.lam64;
-  d.cy64 = L.cy64;
-  return d;
-}
+struct SvdD {
+  Svd<R> sv;
+  R lam[3];
+};
 
 template <class R>
-DM_HD m3<double> to64(const m3<R>& a) {
-  m3<double> o;
+DM_HD SvdD<R> svd3_dev(const m3<R>& D) {
+  // S = D + D^T + D^T D (symmetric)
+  R S[3][3];
 #pragma unroll
-  for (int q = 0; q < 9; ++q) o.a[q] = (double)a.a[q];
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) S[i][j] = D(i, j) + D(j, i) + (D(0, i) * D(0, j) + D(1, i) * D(1, j) + D(2, i) * D(2, j));
+  m3<R> v = meye<R>();
+  const int sweeps = sizeof(R) == 4 ? 8 : 16;
+  for (int sw = 0; sw < sweeps; ++sw) {
+    bool rot = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int p = k == 2 ? 1 : 0, q = k == 0 ? 1 : 2, r = 3 - p - q;
+      const R apq = S[p][q];
+      const R scale = r_abs(S[p][p]) + r_abs(S[q][q]);
+      // converged at the rounding floor of the pair (fp32: 1e-7)
+      if (!(r_abs(apq) > R(sizeof(R) == 4 ? 1e-7 : 1e-16) * scale + R(1e-35))) continue;
+      rot = true;
+      const R tau = (S[q][q] - S[p][p]) / (R(2) * apq);
+      const R t = (tau >= R(0) ? R(1) : R(-1)) / (r_abs(tau) + r_sqrt(R(1) + tau * tau));
+      const R c = R(1) / r_sqrt(R(1) + t * t), sn = t * c;
+      S[p][p] -= t * apq;
+      S[q][q] += t * apq;
+      S[p][q] = S[q][p] = R(0);
+      const R srp = S[r][p], srq = S[r][q];
+      S[r][p] = S[p][r] = c * srp - sn * srq;
+      S[r][q] = S[q][r] = sn * srp + c * srq;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const R vp = v(i, p), vq = v(i, q);
+        v(i, p) = c * vp - sn * vq;
+        v(i, q) = sn * vp + c * vq;
+      }
+    }
+    if (!rot) break;
+  }
+  if (det(v) < R(0)) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) v(i, 2) = -v(i, 2);
+  }
+  SvdD<R> o;
+  o.sv.v = v;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    o.lam[c] = S[c][c];
+    const R s = r_sqrt(R(1) + S[c][c]);
+    o.sv.s[c] = s;
+    const R inv = s > R(0) ? R(1) / s : R(0);
+    // u_c = F v_c / s_c = (v_c + D v_c) / s_c
+#pragma unroll
+    for (int i = 0; i < 3; ++i) o.sv.u(i, c) = (v(i, c) + (D(i, 0) * v(0, c) + D(i, 1) * v(1, c) + D(i, 2) * v(2, c))) * inv;
+  }
   return o;
 }
+
+// Hencky / von Mises record from the deviation-form SVD (hencky() with
+// eps_i = log1p(lam_i) / 2).
 template <class R>
-DM_HD m3<R> from64(const m3<double>& a) {
-  m3<R> o;
+DM_HD Hencky<R> hencky_dev(const SvdD<R>& sd, R cy) {
+  Hencky<R> h;
+  h.sv = sd.sv;
 #pragma unroll
-  for (int q = 0; q < 9; ++q) o.a[q] = (R)a.a[q];
-  return o;
+  for (int i = 0; i < 3; ++i) h.eps[i] = R(0.5) * r_log1p(sd.lam[i]);
+  const R tr = h.eps[0] + h.eps[1] + h.eps[2];
+  h.m = tr * R(1.0 / 3.0);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) h.dev[i] = h.eps[i] - h.m;
+  h.N = r_sqrt(h.dev[0] * h.dev[0] + h.dev[1] * h.dev[1] + h.dev[2] * h.dev[2] + R(1e-30));
+  const R dgamma = h.N - cy;
+  const R iN = R(1) / h.N;
+  h.yield = dgamma > R(0);
+  h.k = cy * iN;
+  if (h.yield) {
+    const R s = dgamma * iN;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      h.epsp[i] = h.eps[i] - h.dev[i] * s;
+      h.sigp[i] = r_exp(h.epsp[i]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      h.epsp[i] = h.eps[i];
+      h.sigp[i] = h.sv.s[i];
+    }
+  }
+  return h;
 }
 
 // First Piola stress from D = F - I (mpm.hpp:212-217 extended; same values as
@@ -212,11 +279,23 @@ DM_HD m3<R> law_stress_fwd(const Law<R>& L, const m3<R>& D, R act, bool* bad) {
   const R jm1 = det1m(D);
   if (!(jm1 > R(-1))) *bad = true;
   switch (L.kind) {
-    case kFixedCorotated:
+    case kFixedCorotated: {
+      // P = 2 mu (F - R) + lam (J - 1) cof F = U diag(2 mu (s_i - 1) + lam (J - 1) J / s_i) V^T
+      const SvdD<R> sd = svd3_dev(D);
+      const R J = R(1) + jm1;
+      R ph[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+        ph[i] = R(2) * L.mu * (sd.lam[i] / (R(1) + sd.sv.s[i])) + L.lam * jm1 * J / sd.sv.s[i];
+      return usv(sd.sv, ph[0], ph[1], ph[2]);
+    }
     case kElastoplastic: {
-      bool b = false;
-      const m3<double> P = law_stress(law64(L), eye_plus(to64(D)), (double)act, &b);
-      return from64<R>(P);
+      const Hencky<R> h = hencky_dev(svd3_dev(D), L.cy);
+      const R tr2 = h.epsp[0] + h.epsp[1] + h.epsp[2];
+      R ps[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) ps[i] = (R(2) * L.mu * h.epsp[i] + L.lam * tr2) / h.sigp[i];
+      return usv(h.sv, ps[0], ps[1], ps[2]);
     }
     case kNeoHookean: {
       // P = mu (1 - 1/(I_C+1)) F + lam (J - alpha) cof F, alpha = 1 + 3 mu / (4 lam), as
@@ -245,15 +324,15 @@ DM_HD m3<R> law_stress_fwd(const Law<R>& L, const m3<R>& D, R act, bool* bad) {
 template <class R>
 DM_HD m3<R> law_project_fwd(const Law<R>& L, const m3<R>& Dn, bool* bad) {
   if (L.kind == kElastoplastic) {
-    const m3<double> Fn = eye_plus(to64(Dn));
-    if (!(det(Fn) > 0.0)) *bad = true;
-    const Hencky<double> h = hencky(Fn, L.cy64);
+    if (!(det1m(Dn) > R(-1))) *bad = true;
+    const Hencky<R> h = hencky_dev(svd3_dev(Dn), L.cy);
     if (!h.yield) return Dn;
-    m3<double> Fp = usv(h.sv, h.sigp[0], h.sigp[1], h.sigp[2]);
-    Fp(0, 0) -= 1.0;
-    Fp(1, 1) -= 1.0;
-    Fp(2, 2) -= 1.0;
-    return from64<R>(Fp);
+    // D' = U diag(sigma_p - 1) V^T + (U V^T - I)  (yielding: |strain| > c_y, no cancellation issue)
+    m3<R> Dp = usv(h.sv, h.sigp[0] - R(1), h.sigp[1] - R(1), h.sigp[2] - R(1)) + mul_bt(h.sv.u, h.sv.v);
+    Dp(0, 0) -= R(1);
+    Dp(1, 1) -= R(1);
+    Dp(2, 2) -= R(1);
+    return Dp;
   }
   if (L.kind == kFluid) {
     // F' = J^(1/3) I  ->  D' = (J^(1/3) - 1) I = expm1(log1p(J - 1) / 3) I
@@ -426,57 +505,61 @@ struct BoxQ {
   R sgn[3];
 };
 
-// box_query_core: from q = |rel| - half and the signs of rel (callers with
-// a more precise q for an axis pass it directly).
-template <class R>
-DM_HD BoxQ<R> box_query_core(const R q[3], const R sg[3]) {
-  BoxQ<R> b;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    b.q[a] = q[a];
-    b.o[a] = r_max(b.q[a], R(0));
-    b.sgn[a] = sg[a];
-  }
-  b.outside = r_sqrt(b.o[0] * b.o[0] + b.o[1] * b.o[1] + b.o[2] * b.o[2] + R(1e-18));
-  b.out = b.q[0] > R(0) || b.q[1] > R(0) || b.q[2] > R(0);
-  if (b.out) {
-    b.d = b.outside - R(1e-9);
-    b.n = mk3(b.o[0] / b.outside, b.o[1] / b.outside, b.o[2] / b.outside);
-  } else {
-    b.d = r_min(r_max(b.q[0], r_max(b.q[1], b.q[2])), R(0));
-    b.n = zero3<R>();
-    if (b.q[0] >= b.q[1] && b.q[0] >= b.q[2])
-      b.n.x = R(1);
-    else if (b.q[1] >= b.q[2])
-      b.n.y = R(1);
-    else
-      b.n.z = R(1);
-  }
-  b.n = mk3(b.n.x * b.sgn[0], b.n.y * b.sgn[1], b.n.z * b.sgn[2]);
-  return b;
-}
+// Box SDF (mpm.hpp:98-128) from per-axis face offsets q (q_a = |rel_a| -
+// half_a), o = max(q, 0) and the signs of rel, filled by each caller in one
+// pass: a shared helper taking q[] / sg[] arrays, or a second pass over the
+// record, quadrupled the grid adjoint's code (instruction-cache bound,
+// measured: 2k -> 9k instructions).
+#define DM_BOX_QUERY_BODY                                                              \
+  b.outside = r_sqrt(b.o[0] * b.o[0] + b.o[1] * b.o[1] + b.o[2] * b.o[2] + R(1e-18)); \
+  b.out = b.q[0] > R(0) || b.q[1] > R(0) || b.q[2] > R(0);                            \
+  if (b.out) {                                                                        \
+    b.d = b.outside - R(1e-9);                                                        \
+    b.n = mk3(b.o[0] / b.outside, b.o[1] / b.outside, b.o[2] / b.outside);            \
+  } else {                                                                            \
+    b.d = r_min(r_max(b.q[0], r_max(b.q[1], b.q[2])), R(0));                          \
+    b.n = zero3<R>();                                                                 \
+    if (b.q[0] >= b.q[1] && b.q[0] >= b.q[2])                                         \
+      b.n.x = R(1);                                                                   \
+    else if (b.q[1] >= b.q[2])                                                        \
+      b.n.y = R(1);                                                                   \
+    else                                                                              \
+      b.n.z = R(1);                                                                   \
+  }                                                                                   \
+  b.n = mk3(b.n.x * b.sgn[0], b.n.y * b.sgn[1], b.n.z * b.sgn[2])
 
 template <class R>
 DM_HD BoxQ<R> box_query(v3<R> rel, v3<R> half) {
-  R q[3], sg[3];
+  BoxQ<R> b;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    q[a] = r_abs(rel[a]) - half[a];
-    sg[a] = rel[a] < R(0) ? R(-1) : R(1);
+    b.q[a] = r_abs(rel[a]) - half[a];
+    b.o[a] = r_max(b.q[a], R(0));
+    b.sgn[a] = rel[a] < R(0) ? R(-1) : R(1);
   }
-  return box_query_core(q, sg);
+  DM_BOX_QUERY_BODY;
+  return b;
 }
 
 // The open-top hollow box's cavity: a box open at the top (z extent shifted
-// up by 1, rc = rel - e_z, hc = half + e_z); its z face distance
+// up by 1, rc = rel - e_z, hc = half + e_z); its z face offset
 // |rel.z - 1| - (half.z + 1) = -(rel.z + half.z) for rel.z < 1 is taken
 // directly (the shifted form rounds it to ~6e-8 in fp32, which
 // exp(-alpha_c d) turns into ~6e-6 relative).
 template <class R>
 DM_HD BoxQ<R> cavity_query(v3<R> rel, v3<R> half) {
-  const R q[3] = {r_abs(rel.x) - half.x, r_abs(rel.y) - half.y, -(rel.z + half.z)};
-  const R sg[3] = {rel.x < R(0) ? R(-1) : R(1), rel.y < R(0) ? R(-1) : R(1), R(-1)};
-  return box_query_core(q, sg);
+  BoxQ<R> b;
+  b.q[0] = r_abs(rel.x) - half.x;
+  b.q[1] = r_abs(rel.y) - half.y;
+  b.q[2] = -(rel.z + half.z);
+  b.o[0] = r_max(b.q[0], R(0));
+  b.o[1] = r_max(b.q[1], R(0));
+  b.o[2] = r_max(b.q[2], R(0));
+  b.sgn[0] = rel.x < R(0) ? R(-1) : R(1);
+  b.sgn[1] = rel.y < R(0) ? R(-1) : R(1);
+  b.sgn[2] = R(-1);  // sign of rc.z (rel.z < 1 in the domain)
+  DM_BOX_QUERY_BODY;
+  return b;
 }
 
 // dbar, nbar -> rel_bar

@@ -59,9 +59,6 @@ Setup make_setup(const OrSim* sim, const OrMat* mats, int nmat) {
       L.dlam_dE = nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
     }
     L.cy = m.wide_yield ? m.yield_stress / L.mu : m.yield_stress / (2.0 * L.mu);
-    L.mu64 = L.mu;
-    L.lam64 = L.lam;
-    L.cy64 = L.cy;
     L.visc = m.viscosity;
     L.act_k = m.act_strength;
     L.mass = m.density * m.volume;
