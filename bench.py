@@ -5,9 +5,10 @@ Metric (BASELINE.json): particle-substeps/s of forward + full adjoint over a
 checkpointed substep tape.  Default workload = config 4 (FluidMove-like:
 1,024 envs x 16,384 particles, 48^3 grid, 16 control steps x 32 substeps),
 the configuration BASELINE.json shards over 1/2/4/8 GPUs.  Envs are
-independent partitions (no simulator collective), so by default every rank
-simulates config 4's 1,024 envs (global env index rank * 1024 + e): weak
-scaling; `--strong` splits the 1,024 envs across the ranks instead.
+independent partitions (no simulator collective): by default the config's
+1,024 envs are split across the ranks (strong scaling, BASELINE's "sharded
+over 1/2/4/8 GPUs"; rank r owns global envs [r E/N, (r+1) E/N)); `--weak`
+gives every rank the config's full env count instead.
 
 One step = one whole rollout: set the initial state, 16 recorded control
 steps (512 substeps), loss over the per-step observables, backward through
@@ -55,7 +56,7 @@ def parse():
     p.add_argument("--envs", type=int, default=0, help="override total envs (default: the config's)")
     p.add_argument("--ctrl", type=int, default=0, help="override control steps")
     p.add_argument("--checkpoint-every", type=int, default=-1)
-    p.add_argument("--strong", action="store_true", help="split the config's envs across ranks (default: weak scaling)")
+    p.add_argument("--weak", action="store_true", help="every rank simulates the config's envs (default: split them)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--profile-out", default="")
@@ -195,17 +196,47 @@ def reference_sample(scene, n_threads: int, n_sub: int = 1):
     return units, wall, desc
 
 
-def cpu_threads():
+def cpu_info():
+    """(usable host threads, CPU model) of this host."""
     try:
-        return max(1, min(len(os.sched_getaffinity(0)), 16))
+        n = len(os.sched_getaffinity(0))
     except Exception:
-        return max(1, min(os.cpu_count() or 1, 16))
+        n = os.cpu_count() or 1
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return max(1, n), model
+
+
+def cpu_threads(bytes_per_thread=0):
+    """Every host thread, bounded by the memory the per-thread tapes need
+    (one reference tape per worker, tape.hpp:78-79)."""
+    n, _ = cpu_info()
+    if bytes_per_thread > 0:
+        try:
+            import psutil
+            n = max(1, min(n, int(0.8 * psutil.virtual_memory().available // bytes_per_thread)))
+        except Exception:
+            pass
+    return n
+
+
+def ref_tape_bytes(scene):
+    """Peak reference-tape bytes of one worker: ~2,200 nodes x 33 B per
+    particle-substep, one substep segment at a time."""
+    return int(scene.n_per_env * 2200 * 33 * 1.3)
 
 
 def run_reference(args, scene, rank, dist):
     if rank != 0:
         return
-    nt = cpu_threads()
+    nt = cpu_threads(ref_tape_bytes(scene))
     vals = []
     for i in range(args.warmup + args.steps):
         units, wall, desc = reference_sample(scene, nt, 1)
@@ -214,10 +245,11 @@ def run_reference(args, scene, rank, dist):
     v = float(np.mean(vals))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * scene.n_per_env * nt / v,
-            "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": scene.name, "sample": desc},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": nt, "kind": "reference", "sample": desc},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": nt, "kind": "reference", "sample": desc,
+                             "host_threads": cpu_info()[0], "cpu_model": cpu_info()[1]},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -305,7 +337,6 @@ def run_ours(args, scene, rank, world, local, dist):
         rollout_device()
     torch.cuda.synchronize()
     launches0 = batch.launches
-    batch.profile(True)
     barrier(dist)
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -316,8 +347,15 @@ def run_ours(args, scene, rank, world, local, dist):
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier(dist)
-    prof = batch.profile(False)
     ms_rank = ev0.elapsed_time(ev1) / args.steps
+    launches = (batch.launches - launches0) // args.steps
+    # per-kernel-class times from a separate profiled rollout (CUDA events
+    # around every launch on the context stream; not in the timed region)
+    batch.profile(True)
+    rollout_device()
+    torch.cuda.synchronize()
+    prof = batch.profile(False)
+    prof_steps = 1
 
     # forward only (the rollout without the backward), same device timing
     def forward_device():
@@ -337,7 +375,6 @@ def run_ours(args, scene, rank, world, local, dist):
     ev3.record(stream)
     torch.cuda.synchronize()
     fwd_ms = max_over_ranks(dist, ev2.elapsed_time(ev3) / args.steps)
-    launches = (batch.launches - launches0) // args.steps
     ms = max_over_ranks(dist, ms_rank)
     value = units_rank * world / (ms / 1e3)
 
@@ -386,14 +423,15 @@ def run_ours(args, scene, rank, world, local, dist):
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        nt = cpu_threads()
+        nt = cpu_threads(ref_tape_bytes(scene))
         units, wall, desc = reference_sample(scene, nt, 1)
-        cpu = {"value": units / wall, "unit": UNIT, "cores": nt, "kind": "reference", "sample": desc}
+        cpu = {"value": units / wall, "unit": UNIT, "cores": nt, "kind": "reference", "sample": desc,
+               "host_threads": cpu_info()[0], "cpu_model": cpu_info()[1]}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong" if args.strong else "weak",
+        "scaling": "weak" if args.weak else "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": scene.name, "envs": E * world, "particles_per_env": N, "control_steps": T,
                    "substeps_per_step": S, "grid": list(scene.sim["dims"]), "checkpoint_every": ck or S,
@@ -406,7 +444,8 @@ def run_ours(args, scene, rank, world, local, dist):
                      "path_alg_gbs": path_gbs, "path_frac": path_gbs / hbm},
         "forward_only": {"value": units_rank * world / (fwd_ms / 1e3), "unit": UNIT, "ms_per_step": fwd_ms,
                          "note": "the same rollout without the backward (north_star: forward and forward+backward)"},
-        "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
+        "kernel_ms_per_step": {k: v[0] / prof_steps for k, v in prof.items() if v[1]},
+        "kernel_ms_source": "one profiled rollout after the timed region (CUDA events per launch)",
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
@@ -471,13 +510,14 @@ def main():
     total = args.envs or {1: 1, 2: 32, 3: 256, 4: 1024, 5: 512}[args.config]
     if args.config == 5:
         args.config = 2  # the reference arm times config 5's simulator (config 2 physics)
-    # weak scaling (default): every rank simulates the config's envs, global
-    # env index = rank * per + e (independent partitions, no simulator
-    # collective); --strong splits the config's envs across the ranks
+    # strong scaling (default): the config's envs are split across the ranks
+    # (rank r: global envs [r per, (r+1) per), no simulator collective);
+    # --weak: every rank simulates the config's envs
     if args.impl == "ours":
-        per = total // world if args.strong else total
-    else:
-        per = min(total, cpu_threads())
+        per = total if args.weak else total // world
+    else:  # the reference arm: one env per host thread (bounded by the tapes' memory)
+        n_cfg = {1: 4096, 2: 20480, 3: 30000, 4: 16384}[args.config]
+        per = min(total, cpu_threads(int(n_cfg * 2200 * 33 * 1.3)))
     kw = {"n_envs": per, "env_offset": rank * per if args.impl == "ours" else 0}
     if args.ctrl:
         kw["n_ctrl"] = args.ctrl

@@ -158,7 +158,8 @@ int dm_tape_steps(const DmContext* ctx);
  * no host upload at reset.  Per env e (global index env_offset + e), in
  * double precision without contraction, then rounded to fp32:
  *   d_a   = origin_lo + (origin_hi - origin_lo) * u_{a+1}      a < origin_draws (else 0)
- *   x_p,a = (origin_a + d_a) + ((ijk_p,a + 0.5) * spacing_a)  lattice (i, j, k)-major
+ *   x_p,a = (origin_a + d_a) + ((ijk_p,a + 0.5) * spacing_a)  lattice (i, j, k)-major, or with
+ *         size_a > 0 sample_box's (origin_a + d_a) + (size_a * (ijk_p,a + 0.5)) / counts_a
  *   x_p,a += jitter_lo + (jitter_hi - jitter_lo) * u_{D + 3p + a + 1}      if jitter_hi > jitter_lo
  *   v_p,a  = velocity_sigma * normal (Box-Muller cosine, rng.hpp:35-43, draws after the jitter)
  *   F = I, C = 0
@@ -176,6 +177,8 @@ typedef struct {
   double jitter_lo, jitter_hi;
   double velocity_sigma;
   int material, group;
+  double size[3]; /* > 0: sample_box's expression origin_a + (size_a * (ijk_a + 0.5)) / counts_a
+                     (mpm.hpp:386-388) instead of the spacing form */
 } DmLatticeReset;
 int dm_reset_lattice(DmContext* ctx, const DmLatticeReset* spec, unsigned long long seed, int env_offset,
                      const unsigned char* env_mask, const int* particle_group, double* origin_delta);

@@ -360,3 +360,18 @@ def ref_task_rollout(kind: int, cfg: dict, n_envs: int, seed: int, env_offset: i
     if rc != 0:
         raise OracleError(err.value.decode())
     return rew, obs, (da if wr is not None else None)
+
+
+def ref_sample(kind: str, a, b, dx: float, ppc: int, cap: int = 1 << 20):
+    """The reference's sample_box (kind "box": a = org, b = size) /
+    sample_cylinder ("cylinder": a = base center, b = (radius, height))."""
+    L = lib("ref")
+    L.ref_sample.restype = C.c_int
+    aa = np.ascontiguousarray(a, dtype=np.float64)
+    bb = np.ascontiguousarray(list(b) + [0.0] * (3 - len(b)), dtype=np.float64)
+    x = np.zeros((cap, 3))
+    vol = C.c_double(0.0)
+    n = L.ref_sample(0 if kind == "box" else 1, _dp(aa), _dp(bb), C.c_double(dx), ppc, _dp(x), cap, C.byref(vol))
+    if n < 0:
+        raise OracleError("ref_sample: capacity")
+    return x[:n].copy(), vol.value

@@ -692,6 +692,21 @@ int ref_task_rollout(int kind, const double* cfg, int n_envs, unsigned long long
   }
 }
 
+// The reference samplers (mpm.hpp:371-423): kind 0 sample_box(a = org,
+// b = size), 1 sample_cylinder(a = base_center, b = (radius, height, -)).
+// x receives up to cap points; returns the count (or -1).
+int ref_sample(int kind, const double* a, const double* b, double dx, int ppc, double* x, int cap, double* vol) {
+  diffsim::mpm::MpmMaterial m;
+  const auto st = kind == 0 ? diffsim::mpm::sample_box({a[0], a[1], a[2]}, {b[0], b[1], b[2]}, dx, ppc, m, 0)
+                            : diffsim::mpm::sample_cylinder({a[0], a[1], a[2]}, b[0], b[1], dx, ppc, m, 0);
+  const int n = static_cast<int>(st.size());
+  if (n > cap) return -1;
+  for (int p = 0; p < n; ++p)
+    for (int k = 0; k < 3; ++k) x[3 * p + k] = st.x[p][k];
+  if (vol) *vol = n ? st.volume0[0] : 0.0;
+  return n;
+}
+
 // SVD-law adjoint of the gradient oracle (ref_rollout_grad): 1 isotropic-map
 // nodes (exact), 0 the reference's Tape::svd3x3.  Returns the previous mode.
 int ref_set_svd_adjoint(int mode) {

@@ -50,7 +50,7 @@ class DmLatticeReset(C.Structure):
     _fields_ = [("origin", C.c_double * 3), ("spacing", C.c_double * 3), ("counts", C.c_int * 3),
                 ("origin_draws", C.c_int), ("origin_lo", C.c_double), ("origin_hi", C.c_double),
                 ("jitter_lo", C.c_double), ("jitter_hi", C.c_double), ("velocity_sigma", C.c_double),
-                ("material", C.c_int), ("group", C.c_int)]
+                ("material", C.c_int), ("group", C.c_int), ("size", C.c_double * 3)]
 
 
 class DmTaskConfig(C.Structure):
@@ -282,6 +282,7 @@ class MpmBatch:
         r.velocity_sigma = spec.get("velocity_sigma", 0.0)
         r.material = spec.get("material", 0)
         r.group = spec.get("group", 0)
+        r.size[:] = list(spec.get("size", (0.0, 0.0, 0.0)))
         if _is_dev(env_mask) or _is_dev(origin_delta) or _is_dev(particle_group):
             self._check(self._L.dm_reset_lattice_device(self._h, C.byref(r), seed, env_offset, _ptr(env_mask),
                                                         _ptr(particle_group), _ptr(origin_delta)))

@@ -5,6 +5,7 @@
 // (tape.hpp:181-255) driven per control step as step_checkpointed does
 // (algo.hpp:79-104).
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: named ranges for nsys / ncu --nvtx
 
 #include <algorithm>
 #include <cmath>
@@ -108,6 +109,12 @@ struct DmContext {
 };
 
 namespace {
+
+// Scoped NVTX range (ncu --nvtx --nvtx-include / nsys timelines).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 #define DM_CUDA(call)                                                                     \
   do {                                                                                    \
@@ -534,6 +541,7 @@ int step_impl(DmContext* ctx, const float* cvo, const float* act, float* obs, cu
     ctx->err = "tape capacity exceeded (max_steps)";
     return DM_ERR_CAPACITY;
   }
+  NvtxRange nv("dm_step");
   const int t = ctx->steps;
   const int E = ctx->P.E, K = ctx->P.K, G = ctx->P.G;
   if (K > 0) {
@@ -686,6 +694,7 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
     ctx->err = "backward_step: no backward in progress (call dm_backward_begin)";
     return DM_ERR_ARG;
   }
+  NvtxRange nv("dm_backward_step");
   const int t = ctx->bwd_t, S = ctx->cfg.substeps, E = ctx->P.E, ck = ctx->ck;
   const int Kc = ctx->P.K > 0 ? ctx->P.K : 1, Gc = ctx->P.G > 0 ? ctx->P.G : 1;
   const size_t N = ctx->Ntot;
@@ -708,6 +717,7 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
   for (int s0 = s_end - ck; s0 >= t * S; s0 -= ck) {
     // replay the segment's forward (tape.hpp:229-233), keeping every
     // substep's sort and grid blocks for its adjoint
+    if (!kept) nvtxRangePushA("replay");
     for (int q = 0; q < ck && !kept; ++q) {
       const int s = s0 + q;
       const StateView So = q + 1 < ck ? seg_state(ctx, s0, s + 1) : view(ctx->tail, ctx->tail_attr, ctx->Ntot);
@@ -723,6 +733,7 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
                                                                 ctx->law == kFluid, s0 + ck == s_end ? cut_t : nullptr,
                                                                 ctx->replay_bad);
       ctx->launches += 1 + (ctx->inj_step == t);
+      nvtxRangePop();
     }
     if (first) {
       // the step's observables are of its end state before any reset: the
@@ -1094,6 +1105,7 @@ int reset_lattice_impl(DmContext* ctx, const DmLatticeReset* spec, unsigned long
   for (int a = 0; a < 3; ++a) {
     R.org[a] = spec->origin[a];
     R.sp[a] = spec->spacing[a];
+    R.size[a] = spec->size[a];
     R.cnt[a] = spec->counts[a];
   }
   R.odraws = spec->origin_draws;

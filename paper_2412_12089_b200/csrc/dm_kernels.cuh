@@ -1193,9 +1193,9 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
         Stencil<float> sc;
         make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
         const int lb[3] = {tile_local(sc.base[0], o[0]), tile_local(sc.base[1], o[1]), tile_local(sc.base[2], o[2])};
-        auto getv = [&](int i, int j, int k) {  // lab-frame node velocity (the grid holds v - vref)
+        auto getv = [&](int i, int j, int k) {  // node velocity relative to vref (g2p_vjp_given adds vref's part)
           const float4 q = vw[((lb[0] + i) * kExt + (lb[1] + j)) * kExt + lb[2] + k];
-          return mk3(vr4.x + q.x, vr4.y + q.y, vr4.z + q.z);
+          return mk3(q.x, q.y, q.z);
         };
         v3<float> xb = mk3(adj_in[adj_index(0, dst, astride)], adj_in[adj_index(1, dst, astride)], adj_in[adj_index(2, dst, astride)]);
         v3<float> vb = mk3(adj_in[adj_index(3, dst, astride)], adj_in[adj_index(4, dst, astride)], adj_in[adj_index(5, dst, astride)]);
@@ -1216,9 +1216,10 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
         for (int q = 0; q < 9; ++q) Cn.a[q] = Sn.c(15 + q, dst);
         if (LAW == kFluid && P.fiso)  // literal-zero diagonal F (see k_p2g)
           g2p_vjp_given(law_of<LAW>(P, mi), T, sc, getv, mdiag(1.f + F.a[0], 1.f + F.a[0], 1.f + F.a[0]), vn, Cn, xb,
-                        vb, Cb, Fb, xp, Fp, gq, Bd, mu_l);
+                        vb, Cb, Fb, xp, Fp, gq, Bd, mu_l, mk3(vr4.x, vr4.y, vr4.z));
         else  // the adjoint linearises at F = I + D (fp32)
-          g2p_vjp_given(law_of<LAW>(P, mi), T, sc, getv, eye_plus(F), vn, Cn, xb, vb, Cb, Fb, xp, Fp, gq, Bd, mu_l);
+          g2p_vjp_given(law_of<LAW>(P, mi), T, sc, getv, eye_plus(F), vn, Cn, xb, vb, Cb, Fb, xp, Fp, gq, Bd, mu_l,
+                        mk3(vr4.x, vr4.y, vr4.z));
 #pragma unroll
         for (int m = 0; m < NM; ++m)
           if (m == mi) mub[m] += mu_l;
@@ -1733,7 +1734,7 @@ __device__ __forceinline__ double box_muller(double u1, double u2) {
 }
 
 struct ResetSpec {
-  double org[3], sp[3];
+  double org[3], sp[3], size[3];
   int cnt[3], odraws;
   double olo, ohi, jlo, jhi, sigma;
   int material, group;
@@ -1764,7 +1765,10 @@ __global__ void k_reset_lattice(ResetSpec R, int E, int N, unsigned long long se
     double x[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      x[a] = __dadd_rn(__dadd_rn(R.org[a], d[a]), __dmul_rn(__dadd_rn((double)ijk[a], 0.5), R.sp[a]));
+      x[a] = __dadd_rn(__dadd_rn(R.org[a], d[a]),
+                       R.size[a] > 0.0  // sample_box (mpm.hpp:386-388): size * (i + 0.5) / n
+                           ? __ddiv_rn(__dmul_rn(R.size[a], __dadd_rn((double)ijk[a], 0.5)), (double)R.cnt[a])
+                           : __dmul_rn(__dadd_rn((double)ijk[a], 0.5), R.sp[a]));
       if (jit) x[a] = __dadd_rn(x[a], rng_uniform(key, ctr + 3ULL * p + a + 1, R.jlo, R.jhi));
     }
     if (jit) ctr += 3ULL * N;

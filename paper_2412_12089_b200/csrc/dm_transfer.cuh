@@ -357,7 +357,7 @@ struct FxBar {
 template <class R, class GetV>
 DM_HD void g2p_vjp_given(const Law<R>& L, const TransferCtx<R>& t, const Stencil<R>& s, GetV getv, const m3<R>& F,
                          v3<R> vnew, const m3<R>& Cn, v3<R> xb_o, v3<R> vb_o, const m3<R>& Cb_o, const m3<R>& Fb_o,
-                         v3<R>& xb_part, m3<R>& Fb_part, v3<R>& gq, m3<R>& Bd, R& mubar);
+                         v3<R>& xb_part, m3<R>& Fb_part, v3<R>& gq, m3<R>& Bd, R& mubar, v3<R> vref);
 template <class R, class GetV>
 DM_HD void g2p_vjp_sep(const Law<R>& L, const TransferCtx<R>& t, const Stencil<R>& s, GetV getv, const m3<R>& F,
                        v3<R> xb_o, v3<R> vb_o, const m3<R>& Cb_o, const m3<R>& Fb_o, v3<R>& xb_part, m3<R>& Fb_part,
@@ -366,15 +366,19 @@ DM_HD void g2p_vjp_sep(const Law<R>& L, const TransferCtx<R>& t, const Stencil<R
   m3<R> B;
   g2p_gather_sep(s, t.dx, getv, vnew, B);
   const m3<R> Cn = B * (R(4) * t.inv_dx * t.inv_dx);
-  g2p_vjp_given(L, t, s, getv, F, vnew, Cn, xb_o, vb_o, Cb_o, Fb_o, xb_part, Fb_part, gq, Bd, mubar);
+  g2p_vjp_given(L, t, s, getv, F, vnew, Cn, xb_o, vb_o, Cb_o, Fb_o, xb_part, Fb_part, gq, Bd, mubar, zero3<R>());
 }
 
 // g2p_vjp_sep with the forward's G2P outputs (v', C' = the next state's v, C,
-// bit-identical to a re-gather) supplied instead of recomputed.
+// bit-identical to a re-gather) supplied instead of recomputed.  getv may
+// return node velocities relative to vref (node_update_rel): the weight
+// derivatives of the quadratic B-spline sum to 0 and their first moment to 1,
+// so vref's part of sum_n dw_n (v_n . u_n) is vref . bc_axis (9 FMAs instead
+// of adding vref at all 27 nodes).
 template <class R, class GetV>
 DM_HD void g2p_vjp_given(const Law<R>& L, const TransferCtx<R>& t, const Stencil<R>& s, GetV getv, const m3<R>& F,
                          v3<R> vnew, const m3<R>& Cn, v3<R> xb_o, v3<R> vb_o, const m3<R>& Cb_o, const m3<R>& Fb_o,
-                         v3<R>& xb_part, m3<R>& Fb_part, v3<R>& gq, m3<R>& Bd, R& mubar) {
+                         v3<R>& xb_part, m3<R>& Fb_part, v3<R>& gq, m3<R>& Bd, R& mubar, v3<R> vref) {
   const R c4 = R(4) * t.inv_dx * t.inv_dx;
   const m3<R> Ad = meye<R>() + Cn * t.dt;
   const m3<R> Fnew = Ad * F;
@@ -412,7 +416,7 @@ DM_HD void g2p_vjp_given(const Law<R>& L, const TransferCtx<R>& t, const Stencil
       fb.ty[j] += H * s.w[0][i];
     }
   }
-  const v3<R> fxb = fb.result(s) - tmul(Bb, vnew) * t.dx;
+  const v3<R> fxb = fb.result(s) + mk3(dot(vref, bcx), dot(vref, bcy), dot(vref, bcz)) - tmul(Bb, vnew) * t.dx;
   xb_part = mk3(xb_o.x + fxb.x * t.inv_dx, xb_o.y + fxb.y * t.inv_dx, xb_o.z + fxb.z * t.inv_dx);
 }
 

@@ -175,12 +175,38 @@ def lattice(org, counts, spacing):
 
 
 def lattice_reset_spec(origin, counts, spacing, origin_draws=0, origin_range=(0.0, 0.0), jitter=(0.0, 0.0),
-                       velocity_sigma=0.0, material=0, group=0):
-    """Reset descriptor of a seeded lattice env (include/diffmpm.h DmLatticeReset)."""
+                       velocity_sigma=0.0, material=0, group=0, size=None):
+    """Reset descriptor of a seeded lattice env (include/diffmpm.h DmLatticeReset).
+    size: sample_box's box extent -- positions origin + (size (ijk + 0.5)) / counts
+    (mpm.hpp:386-388) instead of origin + (ijk + 0.5) spacing."""
     return {"origin": tuple(float(a) for a in origin), "counts": tuple(int(c) for c in counts),
             "spacing": tuple(float(a) for a in spacing), "origin_draws": int(origin_draws),
             "origin_range": tuple(float(a) for a in origin_range), "jitter": tuple(float(a) for a in jitter),
-            "velocity_sigma": float(velocity_sigma), "material": int(material), "group": int(group)}
+            "velocity_sigma": float(velocity_sigma), "material": int(material), "group": int(group),
+            "size": tuple(float(a) for a in size) if size is not None else (0.0, 0.0, 0.0)}
+
+
+def sample_box(org, size, dx, ppc):
+    """sample_box (mpm.hpp:371-395): lattice with spacing dx / cbrt(ppc),
+    counts round(size / h) (>= 1), positions org + size (i + 0.5) / n in
+    (i, j, k)-major order; returns (x [N, 3], particle volume)."""
+    h = dx / np.cbrt(float(ppc))
+    n = [max(1, int(np.round(s / h))) for s in size]
+    vol = (size[0] / n[0]) * (size[1] / n[1]) * (size[2] / n[2])
+    i, j, k = np.meshgrid(np.arange(n[0]), np.arange(n[1]), np.arange(n[2]), indexing="ij")
+    ijk = np.stack([i.ravel(), j.ravel(), k.ravel()], axis=1).astype(np.float64)
+    x = np.asarray(org, np.float64) + (np.asarray(size, np.float64) * (ijk + 0.5)) / np.asarray(n, np.float64)
+    return x, vol
+
+
+def sample_cylinder(base_center, radius, height, dx, ppc):
+    """sample_cylinder (mpm.hpp:397-423): the sample_box lattice of the
+    cylinder's bounding box, keeping points with rx^2 + ry^2 <= r^2 (box
+    order); returns (x [N, 3], particle volume of the box lattice)."""
+    bc = np.asarray(base_center, np.float64)
+    x, vol = sample_box((bc[0] - radius, bc[1] - radius, bc[2]), (2.0 * radius, 2.0 * radius, height), dx, ppc)
+    rx, ry = x[:, 0] - bc[0], x[:, 1] - bc[1]
+    return x[rx * rx + ry * ry <= radius * radius], vol
 
 
 def lattice_reset_host(spec, seed, env_offset, n_envs):
@@ -196,13 +222,16 @@ def lattice_reset_host(spec, seed, env_offset, n_envs):
     lo, hi = spec["origin_range"]
     jlo, jhi = spec["jitter"]
     xs, vs, ds = [], [], []
+    size = np.asarray(spec.get("size", (0.0, 0.0, 0.0)), np.float64)
     for e in range(n_envs):
         r = RngStream(seed, env_offset + e)
         d = np.zeros(3)
         nd = spec["origin_draws"]
         if nd:
             d[:nd] = r.uniform(lo, hi, nd)
-        x = (np.asarray(spec["origin"]) + d) + (ijk + 0.5) * np.asarray(spec["spacing"])
+        off = np.where(size > 0.0, (size * (ijk + 0.5)) / np.asarray(cnt, np.float64),
+                       (ijk + 0.5) * np.asarray(spec["spacing"]))
+        x = (np.asarray(spec["origin"]) + d) + off
         if jhi > jlo:
             x = x + r.uniform(jlo, jhi, 3 * N).reshape(N, 3)
         v = np.zeros((N, 3))
@@ -251,7 +280,7 @@ def config1(seed=0, n_envs=1, env_offset=0, n_sub=50):
     dt=1e-4, 50 substeps, v0 ~ N(0, 0.5) per particle, loss |com - (0.5,0.4,0.5)|^2."""
     dx = 1.0 / 32
     spec = lattice_reset_spec((0.3, 0.3, 0.3), (16, 16, 16), (0.2 / 16,) * 3, jitter=(-0.25 * dx, 0.25 * dx),
-                              velocity_sigma=0.5)
+                              velocity_sigma=0.5, size=(0.2, 0.2, 0.2))
     x, v, _ = lattice_reset_host(spec, seed, env_offset, n_envs)
     N = x.shape[1]
     mats = [{"kind": "fixed_corotated", "E": 1e4, "nu": 0.3, "rho": 1.0, "volume": 0.2 ** 3 / N}]
@@ -274,9 +303,9 @@ def config2(seed=0, n_envs=32, env_offset=0, n_ctrl=32, n_sub=16):
     cnt = (40, 16, 32)
     size = np.array(cnt) * h
     org = (0.5 - size[0] / 2, 0.5 - size[1] / 2, 3.5 * dx)
-    base = lattice(org, cnt, (h, h, h))
+    base, _ = sample_box(org, tuple(size), dx, 8)  # 2 particles per cell per axis: counts = cnt
     N = base.shape[0]
-    spec = lattice_reset_spec(org, cnt, (h, h, h))
+    spec = lattice_reset_spec(org, cnt, (h, h, h), size=tuple(size))
     groups = kmeans_groups(base, 8, RngStream(seed, 1 << 40))
     acts = np.stack([RngStream(seed, env_offset + e).uniform(-1.0, 1.0, n_ctrl * 8).reshape(n_ctrl, 8)
                      for e in range(n_envs)])
@@ -349,7 +378,7 @@ def config4(seed=0, n_envs=1024, env_offset=0, n_ctrl=16, n_sub=32, lattice_coun
     # per env the lattice origin (and the container) is offset by two draws
     # U[-0.01, 0.01) from the env's stream; cavity floor at z = 0.15
     spec = lattice_reset_spec((0.5 - half, 0.5 - half, 0.15), cnt, spacing, origin_draws=2,
-                              origin_range=(-0.01, 0.01))
+                              origin_range=(-0.01, 0.01), size=(2 * half, 2 * half, half))
     x, _, d = lattice_reset_host(spec, seed, env_offset, n_envs)
     org = np.asarray(spec["origin"]) + d
     c0 = [np.array([o[0] + half, o[1] + half, 0.15 + half]) for o in org]  # cavity center

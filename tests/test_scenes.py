@@ -131,3 +131,20 @@ def test_lattice_reset_draw_order_shares_the_action_stream():
     for e in range(2):
         u = RngStream(5, e).uniform(-1.0, 1.0, 2 + 9)
         assert np.array_equal(sc.actions[e], u[2:].reshape(3, 3))
+
+
+@pytest.mark.skipif(not __import__("pyoracle").have_ref(), reason="oracle/_ref not built (needs /root/reference)")
+def test_samplers_match_reference_bitwise():
+    """scenes.sample_box / sample_cylinder restate mpm.hpp:371-423 with the
+    reference's own expression order: positions and volumes bit-identical."""
+    import pyoracle as O
+    cases = [("box", (0.27, 0.42, 0.1625), (0.16, 0.16, 0.08), 0.05, 8),
+             ("box", (0.3, 0.3, 0.3), (0.2, 0.2, 0.2), 1 / 32, 27),
+             ("box", (0.35, 0.35, 0.15), (0.3, 0.3, 0.15), 1 / 48, 8)]
+    for kind, a, b, dx, ppc in cases:
+        x, vol = scenes.sample_box(a, b, dx, ppc)
+        xr, vr = O.ref_sample(kind, a, b, dx, ppc)
+        assert np.array_equal(x, xr) and vol == vr
+    x, vol = scenes.sample_cylinder((0.5, 0.5, 0.1), 0.08, 0.12, 1 / 40, 8)
+    xr, vr = O.ref_sample("cylinder", (0.5, 0.5, 0.1), (0.08, 0.12), 1 / 40, 8)
+    assert x.shape[0] > 100 and np.array_equal(x, xr) and vol == vr
