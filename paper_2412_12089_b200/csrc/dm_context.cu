@@ -664,7 +664,7 @@ int backward_begin(DmContext* ctx, const float* dfx, const float* dfv, const flo
     if (dfC) DM_CUDA(cudaMemcpyAsync(stg + 15 * N, dfC, 9 * N * sizeof(float), kin, ctx->stream));
     k_aos_to_soa_perm<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>(
         (int)N, ctx->P.N, dfx ? stg : nullptr, dfv ? stg + 3 * N : nullptr, dfF ? stg + 6 * N : nullptr,
-        dfC ? stg + 15 * N : nullptr, Sf.attr, A, N);
+        dfC ? stg + 15 * N : nullptr, Sf.attr, A, N, ctx->law == kFluid);
     ++ctx->launches;
   } else {
     DM_CUDA(cudaMemsetAsync(A, 0, state_floats(ctx) * sizeof(float), ctx->stream));

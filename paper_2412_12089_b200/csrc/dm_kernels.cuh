@@ -81,6 +81,11 @@ __host__ __device__ __forceinline__ size_t state_index(int comp, size_t i, size_
 
 // Adjoint buffers share the layout: the state cotangent (24 fields) like the
 // state, the particle-side partial cotangents (12 fields) in blocks of 32 x 12.
+// kFluidTraceCot: in a fluid context the cotangent of a G2P-produced state's
+// F is stored as its trace (field 6 / part field 3): such an F is J^(1/3) I,
+// so every consumer of its cotangent (the next G2P projection's VJP,
+// tr(F'bar) cof(F_new) / (3 J^(2/3))) reads only the trace.  The initial
+// state (general F) keeps all nine.
 __host__ __device__ __forceinline__ size_t adj_index(int comp, size_t i, size_t stride) {
   return state_index(comp, i, stride);
 }
@@ -1202,7 +1207,9 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
         m3<float> Fb, Cb;
 #pragma unroll
         for (int q = 0; q < 9; ++q) {
-          Fb.a[q] = adj_in[adj_index(6 + q, dst, astride)];
+          // fluid: the cotangent of the (isotropic) next state's F is kept as its trace (kFluidTraceCot)
+          Fb.a[q] = LAW == kFluid ? (q == 0 ? adj_in[adj_index(6, dst, astride)] : 0.f)
+                                  : adj_in[adj_index(6 + q, dst, astride)];
           Cb.a[q] = adj_in[adj_index(15 + q, dst, astride)];
         }
         v3<float> xp, gq;
@@ -1227,7 +1234,11 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
         part[part_index(1, dst, astride)] = xp.y;
         part[part_index(2, dst, astride)] = xp.z;
 #pragma unroll
-        for (int q = 0; q < 9; ++q) part[part_index(3 + q, dst, astride)] = Fp.a[q];
+        if (LAW == kFluid && P.fiso)  // isotropic input F: its cotangent matters only through the trace
+          part[part_index(3, dst, astride)] = Fp.a[0] + Fp.a[4] + Fp.a[8];
+        else
+#pragma unroll
+          for (int q = 0; q < 9; ++q) part[part_index(3 + q, dst, astride)] = Fp.a[q];
         stage_payload(pw + lane * kPay, (lb[0] * kExt + lb[1]) * kExt + lb[2], sc, 0.f, gq, Bd);
       }
       __syncwarp();
@@ -1362,7 +1373,8 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
         if (!(LAW == kFluid && P.fiso && f > 6 && f < 15)) cp_async4(sg + f * 32 + lane, &S.c(f, src));
       cp_async4(sg + 24 * 32 + lane, S.attr + src);
 #pragma unroll
-      for (int f = 0; f < 12; ++f) cp_async4(sg + (25 + f) * 32 + lane, part + part_index(f, row + c0 + lane, astride));
+      for (int f = 0; f < 12; ++f)
+        if (!(LAW == kFluid && P.fiso && f > 3)) cp_async4(sg + (25 + f) * 32 + lane, part + part_index(f, row + c0 + lane, astride));
       sg[37 * 32 + lane] = __int_as_float(src);
     };
     int s1 = 32 + lane < cnt ? perm[row + 32 + lane] : 0;  // perm two chunks ahead, parity slots
@@ -1389,7 +1401,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
         for (int q = 0; q < 9; ++q) {
           F.a[q] = sg[(6 + q) * 32 + lane];
           C.a[q] = sg[(15 + q) * 32 + lane];
-          Fb.a[q] = sg[(28 + q) * 32 + lane];
+          Fb.a[q] = (LAW == kFluid && P.fiso) ? (q == 0 ? sg[28 * 32 + lane] : 0.f) : sg[(28 + q) * 32 + lane];
         }
         // the stored deviation D -> F = I + D (fp32; the adjoint's linearisation point)
         F = (LAW == kFluid && P.fiso) ? mdiag(1.f + F.a[0], 1.f + F.a[0], 1.f + F.a[0]) : eye_plus(F);
@@ -1439,9 +1451,11 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
       adj_out[adj_index(3, src, astride)] = vb.x;
       adj_out[adj_index(4, src, astride)] = vb.y;
       adj_out[adj_index(5, src, astride)] = vb.z;
+      if (LAW == kFluid && P.fiso)  // the trace of an isotropic state's F cotangent (kFluidTraceCot)
+        adj_out[adj_index(6, src, astride)] = Fb.a[0] + Fb.a[4] + Fb.a[8];
 #pragma unroll
       for (int q = 0; q < 9; ++q) {
-        adj_out[adj_index(6 + q, src, astride)] = Fb.a[q];
+        if (!(LAW == kFluid && P.fiso)) adj_out[adj_index(6 + q, src, astride)] = Fb.a[q];
         adj_out[adj_index(15 + q, src, astride)] = Cb.a[q];
       }
     }
@@ -1861,10 +1875,13 @@ __global__ void k_soa_to_aos(int Ntot, int N, const float* __restrict__ f, const
   }
 }
 
-// canonical AoS cotangent -> physical SoA order of the state with attributes attr
+// canonical AoS cotangent -> physical SoA order of the state with attributes
+// attr.  ftrace: a fluid context keeps the cotangent of an isotropic
+// (G2P-produced) state's F as its trace in field 6 (kFluidTraceCot).
 __global__ void k_aos_to_soa_perm(int Ntot, int N, const float* __restrict__ x, const float* __restrict__ v,
                                   const float* __restrict__ F, const float* __restrict__ C,
-                                  const uint32_t* __restrict__ attr, float* __restrict__ f, size_t stride) {
+                                  const uint32_t* __restrict__ attr, float* __restrict__ f, size_t stride,
+                                  int ftrace = 0) {
   const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (i >= (size_t)Ntot) return;
   const size_t e = i / N;
@@ -1876,7 +1893,8 @@ __global__ void k_aos_to_soa_perm(int Ntot, int N, const float* __restrict__ x, 
   }
 #pragma unroll
   for (int q = 0; q < 9; ++q) {
-    f[adj_index(6 + q, i, stride)] = F ? F[9 * o + q] : 0.f;
+    f[adj_index(6 + q, i, stride)] = F ? (ftrace ? (q == 0 ? F[9 * o] + F[9 * o + 4] + F[9 * o + 8] : 0.f) : F[9 * o + q])
+                                       : 0.f;
     f[adj_index(15 + q, i, stride)] = C ? C[9 * o + q] : 0.f;
   }
 }
