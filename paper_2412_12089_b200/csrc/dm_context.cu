@@ -57,6 +57,11 @@ struct DmContext {
   int4* work_all = nullptr;
   int* ord_all = nullptr;
   float4* vref_all = nullptr;  // per slot and env: the substep's reference velocity (k_bin)
+  // sort records: every forward substep's binning kept for the replay (k_rec_save)
+  SortRec rec{};
+  int rec_cap = 0;                  // active / work entries per record
+  std::vector<int> rec_ovf_h;       // per substep, read at backward_begin: 1 = re-bin in the replay
+  void* rec_mem[9] = {};
   // per active tile (by slot) 6^3 grid blocks of the replayed substeps:
   // velocity and (mass, momentum), read by the adjoint substep instead of
   // re-running bin / p2g / grid
@@ -329,10 +334,55 @@ void launch_g2p(DmContext* c, const StateView& S, const StateView& So, const Slo
   ++c->launches;
 }
 
+// Record s of the sort records.
+SortRec rec_at(const DmContext* c, int s) {
+  const size_t TT = (size_t)c->P.E * c->P.Tn;
+  SortRec r;
+  r.perm = c->rec.perm + (size_t)s * c->Ntot;
+  r.tile_count = c->rec.tile_count + (size_t)s * TT;
+  r.active = c->rec.active + (size_t)s * c->rec_cap;
+  r.work = c->rec.work + (size_t)s * c->rec_cap;
+  r.abase = c->rec.abase + (size_t)s * c->P.E;
+  r.acount = c->rec.acount + (size_t)s * c->P.E;
+  r.nact = c->rec.nact + s;
+  r.vref = c->rec.vref + (size_t)s * c->P.E;
+  r.ovf = c->rec.ovf + s;
+  return r;
+}
+
+// Slot qi with the sort artifacts of record s (the grid-block dumps stay the slot's).
+Slot rec_slot(DmContext* c, int qi, int s) {
+  Slot q = slot(c, qi);
+  const SortRec r = rec_at(c, s);
+  q.perm = r.perm;
+  q.tile_count = r.tile_count;
+  q.active = r.active;
+  q.work = r.work;
+  q.env_abase = r.abase;
+  q.env_acount = r.acount;
+  q.nact = r.nact;
+  q.vref = r.vref;
+  return q;
+}
+
+// whether the replay / adjoint of global substep s can use its sort record
+bool rec_usable(const DmContext* c, int s) {
+  return c->rec.perm && s < (int)c->rec_ovf_h.size() && c->rec_ovf_h[s] == 0;
+}
+
+// One forward substep on slot qi.  rec_s >= 0: the replay of substep rec_s
+// with a usable sort record (no binning); record != 0: the forward pass,
+// which saves its binning into the record of substep sub.
 void forward_substep(DmContext* c, const StateView& S, const StateView& So, int t, int sub, int check_vmax, int qi,
-                     bool dump) {
-  const Slot q = slot(c, qi);
-  launch_bin(c, S, q, sub, check_vmax);
+                     bool dump, int rec_s = -1, bool record = false) {
+  const Slot q = rec_s >= 0 ? rec_slot(c, qi, rec_s) : slot(c, qi);
+  if (rec_s < 0) launch_bin(c, S, q, sub, check_vmax);
+  if (record && c->rec.perm) {
+    const size_t TT = (size_t)c->P.E * c->P.Tn;
+    k_rec_save<<<c->grid_tiles, 256, 0, c->stream>>>(c->Ntot, TT, c->P.E, c->rec_cap, q.perm, q.tile_count, q.active,
+                                                     q.work, q.env_abase, q.env_acount, q.nact, q.vref, rec_at(c, sub));
+    ++c->launches;
+  }
   launch_p2g(c, S, q, t, sub);
   launch_grid(c, q, t, dump);
   launch_g2p(c, S, So, q, t, sub, dump);
@@ -353,8 +403,8 @@ void launch_p2g_adj(DmContext* c, const StateView& S, const Slot& q, int t, floa
 
 // Adjoint of one substep from the replay's stored artifacts (slot qi).
 void backward_substep(DmContext* c, const StateView& S, const StateView& Sn, int t, int qi, const float* adj_in,
-                      float* adj_out) {
-  const Slot q = slot(c, qi);
+                      float* adj_out, int rec_s = -1) {
+  const Slot q = rec_s >= 0 ? rec_slot(c, qi, rec_s) : slot(c, qi);
   wq_reset(c);
   PROF_BEGIN(c, 3);
 #define L_G2PA(LW)                                                                                            \
@@ -587,9 +637,9 @@ int step_impl(DmContext* ctx, const float* cvo, const float* act, float* obs, cu
     ctx->P.fiso = s > 0;  // every state but the initial one is a G2P output
     if (keep)
       forward_substep(ctx, seg_state(ctx, t * S, s), q + 1 < S ? seg_state(ctx, t * S, s + 1) : fwd_state(ctx, s + 1),
-                      t, s, q == 0, q, true);
+                      t, s, q == 0, q, true, -1, true);
     else
-      forward_substep(ctx, fwd_state(ctx, s), fwd_state(ctx, s + 1), t, s, q == 0, 0, false);
+      forward_substep(ctx, fwd_state(ctx, s), fwd_state(ctx, s + 1), t, s, q == 0, 0, false, -1, true);
   }
   DM_CUDA(cudaMemcpyAsync(ctx->vmax_hist + t, &ctx->flags->vmax_bits, sizeof(unsigned), cudaMemcpyDeviceToDevice,
                           ctx->stream));
@@ -639,6 +689,10 @@ int backward_begin(DmContext* ctx, const float* dfx, const float* dfv, const flo
     if (rc != DM_OK) return rc;
   }
   DM_CUDA(cudaMemsetAsync(ctx->replay_bad, 0xFF, sizeof(unsigned long long), ctx->stream));
+  if (ctx->rec.perm) {  // which substeps' sort records the replay can use
+    ctx->rec_ovf_h.assign((size_t)T * ctx->cfg.substeps, 1);
+    DM_CUDA(cudaMemcpy(ctx->rec_ovf_h.data(), ctx->rec.ovf, ctx->rec_ovf_h.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  }
   {
     // grid-block pool for one replayed segment: at least the forward pass's
     // largest active-tile count (the replay is bit-identical to it)
@@ -722,7 +776,7 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
       const int s = s0 + q;
       const StateView So = q + 1 < ck ? seg_state(ctx, s0, s + 1) : view(ctx->tail, ctx->tail_attr, ctx->Ntot);
       ctx->P.fiso = s > 0;
-      forward_substep(ctx, seg_state(ctx, s0, s), So, t, s, 0, q, true);
+      forward_substep(ctx, seg_state(ctx, s0, s), So, t, s, 0, q, true, rec_usable(ctx, s) ? s : -1);
     }
     if (!kept) {
       // the replayed exit must equal the stored checkpoint bitwise (tape.hpp:234-241)
@@ -762,7 +816,8 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
                        : kept ? store_view(ctx, (s + 1) / ck)
                               : view(ctx->tail, ctx->tail_attr, ctx->Ntot);
       ctx->P.fiso = s > 0;
-      backward_substep(ctx, seg_state(ctx, s0, s), Sn, t, q, ctx->adj[cur], ctx->adj[cur ^ 1]);
+      backward_substep(ctx, seg_state(ctx, s0, s), Sn, t, q, ctx->adj[cur], ctx->adj[cur ^ 1],
+                       !kept && rec_usable(ctx, s) ? s : -1);
       cur ^= 1;
     }
   }
@@ -1007,6 +1062,32 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   }
   cudaMemsetAsync(ctx->store_attr, 0, N * sizeof(uint32_t), ctx->stream);
   cudaMemsetAsync(ctx->tile_acc, 0, TT * kNacc * sizeof(float), ctx->stream);
+  {
+    // sort records for every substep of the tape, when device memory allows
+    // (DIFFMPM_NO_SORT_RECORDS=1 disables them)
+    const size_t n_sub = (size_t)cfg->max_steps * cfg->substeps;
+    ctx->rec_cap = (int)std::min<size_t>(TT, std::max<size_t>(1024, N / 32));
+    const size_t per = N * 4 + TT * 4 + 2 * (size_t)ctx->rec_cap * 16 + (size_t)P.E * (4 + 4 + 16) + 8;
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    if (!std::getenv("DIFFMPM_NO_SORT_RECORDS") && cfg->substeps > 1 && n_sub * per + (size_t)(6ull << 30) < free_b) {
+      bool r = dalloc(ctx, &ctx->rec.perm, n_sub * N) && dalloc(ctx, &ctx->rec.tile_count, n_sub * TT) &&
+               dalloc(ctx, &ctx->rec.active, n_sub * ctx->rec_cap) && dalloc(ctx, &ctx->rec.work, n_sub * ctx->rec_cap) &&
+               dalloc(ctx, &ctx->rec.abase, n_sub * P.E) && dalloc(ctx, &ctx->rec.acount, n_sub * P.E) &&
+               dalloc(ctx, &ctx->rec.nact, n_sub) && dalloc(ctx, &ctx->rec.vref, n_sub * P.E) &&
+               dalloc(ctx, &ctx->rec.ovf, n_sub);
+      void* m[9] = {ctx->rec.perm, ctx->rec.tile_count, ctx->rec.active, ctx->rec.work, ctx->rec.abase,
+                    ctx->rec.acount, ctx->rec.nact, ctx->rec.vref, ctx->rec.ovf};
+      for (int i = 0; i < 9; ++i) ctx->rec_mem[i] = m[i];
+      if (!r) {  // not enough after all: no records (the replay bins)
+        for (void*& q : ctx->rec_mem)
+          if (q) cudaFree(q), q = nullptr;
+        ctx->rec = SortRec{};
+      } else {
+        cudaMemsetAsync(ctx->rec.ovf, 0xFF, n_sub * sizeof(int), ctx->stream);  // nothing recorded yet
+      }
+    }
+  }
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
   int occ = 0;
@@ -1028,6 +1109,8 @@ void dm_destroy(DmContext* ctx) {
                   ctx->obs_cvo,   ctx->obs_out,  ctx->f32_stage,  ctx->dE_dev,     ctx->vmax_hist,  ctx->replay_bad,
                   ctx->vref_all,  ctx->spc_tape, ctx->gspc,       ctx->cut_tape,   ctx->dcloud_buf};
   for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (void* p : ctx->rec_mem)
     if (p) cudaFree(p);
   if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);

@@ -2025,4 +2025,47 @@ __global__ void k_cut_adj(DevParams P, const unsigned char* __restrict__ cut, fl
   }
 }
 
+// ============================ sort records ============================
+// The forward's binning of substep s (perm, dense tile counts, the active
+// and work lists, per-env ranges, vref) copied into the rollout's record s,
+// so the backward's segment replay reuses it instead of binning again (the
+// replay's state is bit-identical, so is its sort).  Lists longer than the
+// record's capacity set ovf (that substep is re-binned in the replay).
+struct SortRec {
+  int* perm;
+  int* tile_count;
+  int4* active;
+  int4* work;
+  int* abase;
+  int* acount;
+  int* nact;
+  float4* vref;
+  int* ovf;
+};
+__global__ void k_rec_save(size_t Ntot, size_t TT, int E, int cap, const int* __restrict__ perm,
+                           const int* __restrict__ tile_count, const int4* __restrict__ active,
+                           const int4* __restrict__ work, const int* __restrict__ abase, const int* __restrict__ acount,
+                           const int* __restrict__ nact, const float4* __restrict__ vref, SortRec r) {
+  const int n = *nact;
+  const bool fits = n <= cap;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t i0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i0 == 0) {
+    *r.nact = n;
+    *r.ovf = fits ? 0 : 1;
+  }
+  for (size_t i = i0; i < Ntot; i += stride) r.perm[i] = perm[i];
+  for (size_t i = i0; i < TT; i += stride) r.tile_count[i] = tile_count[i];
+  if (fits)
+    for (size_t i = i0; i < (size_t)n; i += stride) {
+      r.active[i] = active[i];
+      r.work[i] = work[i];
+    }
+  for (size_t i = i0; i < (size_t)E; i += stride) {
+    r.abase[i] = abase[i];
+    r.acount[i] = acount[i];
+    r.vref[i] = vref[i];
+  }
+}
+
 }  // namespace dm
