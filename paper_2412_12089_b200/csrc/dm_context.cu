@@ -39,6 +39,7 @@ struct DmContext {
   int n_store = 0;
   unsigned long long launches = 0, bytes = 0;
   int grid_tiles = 148 * 4;
+  bool coop = false;  // CTA-cooperative tiles (small batches; see coop_idx)
 
   float* store = nullptr;  // [n_store][24][Ntot]
   uint32_t* store_attr = nullptr;
@@ -283,7 +284,9 @@ void launch_p2g(DmContext* c, const StateView& S, const Slot& q, int t, int sub)
   wq_reset(c);
   PROF_BEGIN(c, 1);
 #define L_P2G(LW)                                                                                               \
-  k_p2g<LW><<<c->grid_tiles, kWarps * 32, kP2gSmem, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.work, \
+  if (c->coop) k_p2g<LW, true><<<c->grid_tiles, kWarps * 32, kP2gSmem, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.work, \
+                                                          step_act(c, t), c->blocks, c->flags, q.nact, sub, c->wq, q.vref); \
+  else k_p2g<LW, false><<<c->grid_tiles, kWarps * 32, kP2gSmem, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.work, \
                                                           step_act(c, t), c->blocks, c->flags, q.nact, sub, c->wq, q.vref)
   DM_LAW_DISPATCH(c, L_P2G);
 #undef L_P2G
@@ -324,7 +327,11 @@ void launch_g2p(DmContext* c, const StateView& S, const StateView& So, const Slo
   wq_reset(c);
   PROF_BEGIN(c, 2);
 #define L_G2P(LW)                                                                                                \
-  k_g2p<LW><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, q.perm, q.tile_start, q.tile_count,        \
+  if (c->coop) k_g2p<LW, true><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, q.perm, q.tile_start, q.tile_count, \
+                                                          q.work, c->gv, c->flags, q.nact, sub, c->gmp,         \
+                                                          dump ? q.gvb : nullptr, dump ? q.gmpb : nullptr, c->wq, (int)c->blk_cap, \
+                                                          q.vref); \
+  else k_g2p<LW, false><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, q.perm, q.tile_start, q.tile_count,        \
                                                           q.work, c->gv, c->flags, q.nact, sub, c->gmp,         \
                                                           dump ? q.gvb : nullptr, dump ? q.gmpb : nullptr, c->wq, (int)c->blk_cap, \
                                                           q.vref)
@@ -388,17 +395,27 @@ void forward_substep(DmContext* c, const StateView& S, const StateView& So, int 
   launch_g2p(c, S, So, q, t, sub, dump);
 }
 
+template <int LAW, int NG, int NM, bool COOP>
+void launch_p2g_adj_k(DmContext* c, const StateView& S, const Slot& q, int t, float* adj_out) {
+  k_p2g_adj<LAW, NG, NM, COOP><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(
+      c->P, S, q.perm, q.tile_start, q.tile_count, q.work, step_act(c, t), c->gmb, c->part, adj_out, c->Ntot,
+      c->tile_acc, q.nact, c->wq);
+}
+
 template <int LAW, int NG>
 void launch_p2g_adj(DmContext* c, const StateView& S, const Slot& q, int t, float* adj_out) {
   wq_reset(c);
   if (c->P.nmat == 1)
-    k_p2g_adj<LAW, NG, 1><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.work,
-                                                              step_act(c, t), c->gmb, c->part, adj_out, c->Ntot,
-                                                              c->tile_acc, q.nact, c->wq);
+    c->coop ? launch_p2g_adj_k<LAW, NG, 1, true>(c, S, q, t, adj_out) : launch_p2g_adj_k<LAW, NG, 1, false>(c, S, q, t, adj_out);
   else
-  k_p2g_adj<LAW, NG, 4><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.work,
-                                                              step_act(c, t), c->gmb, c->part, adj_out, c->Ntot,
-                                                              c->tile_acc, q.nact, c->wq);
+    c->coop ? launch_p2g_adj_k<LAW, NG, 4, true>(c, S, q, t, adj_out) : launch_p2g_adj_k<LAW, NG, 4, false>(c, S, q, t, adj_out);
+}
+
+template <int LAW, int NM, bool COOP>
+void launch_g2p_adj_k(DmContext* c, const StateView& S, const StateView& Sn, const Slot& q, const float* adj_in) {
+  k_g2p_adj<LAW, NM, COOP><<<c->grid_tiles, kWarps * 32, kG2pAdjSmem, c->stream>>>(
+      c->P, S, Sn, adj_in, c->Ntot, q.perm, q.tile_start, q.tile_count, q.work, q.gvb, c->ablocks, c->part,
+      c->tile_acc, q.nact, c->wq, q.vref);
 }
 
 // Adjoint of one substep from the replay's stored artifacts (slot qi).
@@ -409,13 +426,9 @@ void backward_substep(DmContext* c, const StateView& S, const StateView& Sn, int
   PROF_BEGIN(c, 3);
 #define L_G2PA(LW)                                                                                            \
   if (c->P.nmat == 1)                                                                                          \
-    k_g2p_adj<LW, 1><<<c->grid_tiles, kWarps * 32, kG2pAdjSmem, c->stream>>>(c->P, S, Sn, adj_in, c->Ntot, q.perm, \
-                                                              q.tile_start, q.tile_count, q.work, q.gvb,  \
-                                                              c->ablocks, c->part, c->tile_acc, q.nact, c->wq, q.vref); \
+    c->coop ? launch_g2p_adj_k<LW, 1, true>(c, S, Sn, q, adj_in) : launch_g2p_adj_k<LW, 1, false>(c, S, Sn, q, adj_in); \
   else                                                                                                         \
-    k_g2p_adj<LW, 4><<<c->grid_tiles, kWarps * 32, kG2pAdjSmem, c->stream>>>(c->P, S, Sn, adj_in, c->Ntot, q.perm, \
-                                                              q.tile_start, q.tile_count, q.work, q.gvb,  \
-                                                              c->ablocks, c->part, c->tile_acc, q.nact, c->wq, q.vref)
+    c->coop ? launch_g2p_adj_k<LW, 4, true>(c, S, Sn, q, adj_in) : launch_g2p_adj_k<LW, 4, false>(c, S, Sn, q, adj_in)
   DM_LAW_DISPATCH(c, L_G2PA);
 #undef L_G2PA
   PROF_END(c, 3);
@@ -1006,16 +1019,20 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
     s.thickness = (float)shapes[c].thickness;
   }
   {
-#define DM_SMEM_ATTR(LW)                                                                                   \
-  cudaFuncSetAttribute(k_p2g<LW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kP2gSmem);            \
-  cudaFuncSetAttribute(k_g2p_adj<LW, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kG2pAdjSmem); \
-  cudaFuncSetAttribute(k_g2p_adj<LW, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kG2pAdjSmem)
+#define DM_SMEM_ATTR1(LW, CO)                                                                                 \
+  cudaFuncSetAttribute(k_p2g<LW, CO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kP2gSmem);            \
+  cudaFuncSetAttribute(k_g2p_adj<LW, 1, CO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kG2pAdjSmem); \
+  cudaFuncSetAttribute(k_g2p_adj<LW, 4, CO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kG2pAdjSmem)
+#define DM_SMEM_ATTR(LW) \
+  DM_SMEM_ATTR1(LW, false); \
+  DM_SMEM_ATTR1(LW, true)
     DM_SMEM_ATTR(0);
     DM_SMEM_ATTR(1);
     DM_SMEM_ATTR(2);
     DM_SMEM_ATTR(3);
     DM_SMEM_ATTR(-1);
 #undef DM_SMEM_ATTR
+#undef DM_SMEM_ATTR1
   }
   ctx->Ntot = (size_t)P.E * P.N;
   const size_t N = ctx->Ntot;
@@ -1091,9 +1108,13 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<-1, 16, 4>, kWarps * 32, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<-1, 16, 4, false>, kWarps * 32, 0);
   if (occ < 1) occ = 1;
   ctx->grid_tiles = dev_sms * (occ < 8 ? 8 : occ);
+  // CTA-cooperative tiles when the batch gives each resident warp only a few
+  // chunks (DIFFMPM_COOP=0/1 forces the mode)
+  ctx->coop = N < (size_t)kCoopParticlesPerWarp * ctx->grid_tiles * kWarps;
+  if (const char* f = std::getenv("DIFFMPM_COOP")) ctx->coop = f[0] == '1';
   if (reset_flags(ctx) != DM_OK) return ctx;
   return ctx;
 }

@@ -35,6 +35,7 @@ constexpr int kTile = 4;
 constexpr int kExt = 6;  // tile + quadratic stencil reach
 constexpr int kExt3 = kExt * kExt * kExt;
 constexpr int kWarps = 4;  // warps per CTA in tile kernels
+constexpr int kCoopParticlesPerWarp = 640;  // below this many particles per resident warp: COOP tiles (r02 A/B: cfg4 x128 envs +24 %, x256 -3 %)
 constexpr int kPay = 28;   // payload stride (floats; 7 float4, conflict-free STS.128 / 3-way LDS.128)
 constexpr int kNacc = 64;  // per-tile cotangent accumulators
 constexpr int kAccMu = 0, kAccLam = 4, kAccMuG = 8, kAccCol = 12, kAccAct = 48;
@@ -787,6 +788,77 @@ __device__ __forceinline__ void load_pstate(const StateView& S, int src, PState&
   p.at = S.attr[src];
 }
 
+// ---- cooperative tiles (small batches) ----
+// With few tiles per resident warp (a small env batch: cfg 1, cfg 2, a
+// strong-scaling shard) one warp per tile leaves most of the GPU idle and a
+// launch lasts as long as its largest tile's chunk chain.  COOP kernels let
+// the 4 warps of a CTA share a tile: warp w takes the tile's 32-particle
+// chunks w, w + 4, w + 8, ...  Each warp runs the usual per-chunk code on a
+// virtual particle range: its virtual index v maps to the tile's index
+// coop_idx(v, w); the last (partial) chunk belongs to one warp.  Scatter
+// kernels sum the 4 warps' block copies in a fixed order (deterministic;
+// the replay uses the same mode), gathers need no reduction.
+template <bool COOP>
+__device__ __forceinline__ int coop_idx(int v, int w) {
+  return COOP ? ((((v >> 5) << 2) + w) << 5) + (v & 31) : v;
+}
+template <bool COOP>
+__device__ __forceinline__ int coop_count(int cnt, int w) {
+  if (!COOP) return cnt;
+  const int nc = (cnt + 31) >> 5;
+  if (w >= nc) return 0;
+  const int k = (nc - 1 - w) / 4 + 1;  // chunks w, w + 4, ... below nc
+  return 32 * k - ((((nc - 1) & 3) == w) ? 32 * nc - cnt : 0);
+}
+
+// CTA-level item loop of the COOP kernels: thread 0 takes the next item, the
+// CTA processes it, a barrier closes it.
+template <class Body>
+__device__ __forceinline__ void coop_loop(const int4* __restrict__ work, int* ctr, int n, Body& body) {
+  __shared__ int s_item;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(ctr, 1);
+    __syncthreads();
+    const int a = s_item;
+    if (a >= n) break;
+    body(work[a], a);
+    __syncthreads();
+  }
+}
+
+// Fixed-order sum of the CTA's kWarps x 3 scatter copies (warp w's copies
+// at base + w * wstride, kExt3 apart) into dst, after every warp flushed.
+__device__ __forceinline__ void coop_store_blocks(const float4* __restrict__ base, int wstride,
+                                                  float4* __restrict__ dst) {
+  __syncthreads();
+  for (int i = threadIdx.x; i < kExt3; i += blockDim.x) {
+    float4 acc = base[i];
+#pragma unroll
+    for (int c = 1; c < 3 * kWarps; ++c) {
+      const float4 b = base[(c / 3) * wstride + (c % 3) * kExt3 + i];
+      acc.x += b.x;
+      acc.y += b.y;
+      acc.z += b.z;
+      acc.w += b.w;
+    }
+    dst[i] = acc;
+  }
+}
+
+// Fixed-order CTA sum of a per-warp value (after the warp's butterfly; lane 0 holds it).
+template <class V>
+__device__ __forceinline__ V coop_sum(V v) {
+  __shared__ V s_part[kWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) s_part[warp] = v;
+  __syncthreads();
+  V acc = s_part[0];
+#pragma unroll
+  for (int w = 1; w < kWarps; ++w) acc += s_part[w];
+  return acc;
+}
+
 // ============================ P2G ============================
 // Per active tile: stage particle payloads (lanes = particles), scatter runs
 // into the warp's 6^3 shared block (lanes = stencil nodes), write the block.
@@ -819,7 +891,7 @@ __device__ __forceinline__ void chunk_loop(Body& body, int cnt, int& s0, int& s1
 #ifndef DM_P2G_MINB
 #define DM_P2G_MINB 4
 #endif
-template <int LAW>
+template <int LAW, bool COOP>
 __global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, StateView S, const int* __restrict__ perm,
                                                      const int* __restrict__ tile_start,
                                                      const int* __restrict__ tile_count, const int4* __restrict__ active,
@@ -832,21 +904,22 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, S
   const TransferCtx<float> T = tctx(P);
   float4* bw = dsm + warp * 3 * kExt3;  // 3 group copies of the 6^3 block
   float* pw = reinterpret_cast<float*>(dsm + kWarps * 3 * kExt3) + warp * 32 * kPay;
-  for (TileIter ti(active, wq, n_active, lane); ti.valid(); ti.advance()) {
-    ti.prefetch(active);
-    const int e = ti.cur.x, t = ti.cur.y, start = ti.cur.z, cnt = ti.cur.w;
+  auto tile = [&](const int4 cur) __attribute__((always_inline)) {
+    const int e = cur.x, t = cur.y, start = cur.z;
+    const int cnt = coop_count<COOP>(cur.w, warp);  // this warp's (virtual) particle count
     const int tz = t % P.td[2], ty = (t / P.td[2]) % P.td[1], tx = t / (P.td[2] * P.td[1]);
     const int o[3] = {tx * kTile, ty * kTile, tz * kTile};
     const size_t tix = (size_t)e * P.Tn + t;
     const int* prow = perm + (size_t)e * P.N + start;
+    auto pidx = [&](int v) { return prow[coop_idx<COOP>(v, warp)]; };
     const float4 vr4 = vref[e];
     const v3<float> vr = mk3(vr4.x, vr4.y, vr4.z);  // momentum relative to the env's reference velocity
     // perm indices two chunks ahead in two parity slots (no register moves
     // between chunks, so a refill never waits on the load it replaces)
     PState ps;
-    if (lane < cnt) load_pstate<LAW>(S, prow[lane], ps, P.fiso);
-    int s1 = 32 + lane < cnt ? prow[32 + lane] : 0;
-    int s0 = 64 + lane < cnt ? prow[64 + lane] : 0;
+    if (lane < cnt) load_pstate<LAW>(S, pidx(lane), ps, P.fiso);
+    int s1 = 32 + lane < cnt ? pidx(32 + lane) : 0;
+    int s0 = 64 + lane < cnt ? pidx(64 + lane) : 0;
     scatter_zero(bw, lane);
     RunAcc ra;
     run_reset(ra);
@@ -874,12 +947,26 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, S
       __syncwarp();
       // software pipeline: issue the next chunk's loads before this chunk's scatter
       if (c0 + 32 + lane < cnt) load_pstate<LAW>(S, s_next, ps, P.fiso);
-      const int s_new = c0 + 96 + lane < cnt ? prow[c0 + 96 + lane] : 0;
+      const int s_new = c0 + 96 + lane < cnt ? pidx(c0 + 96 + lane) : 0;
       scatter_runs<true>(bw, pw, min(32, cnt - c0), lane, ra);
       return s_new;
     };
     chunk_loop<LAW == kFluid || LAW == kNeoHookean>(chunk, cnt, s0, s1);
-    scatter_store(bw, lane, ra, blocks + tix * kExt3);
+    if constexpr (COOP) {  // flush, then the CTA sums the 4 warps' copies
+      if (lane < 27) run_flush(bw + (lane / 9) * kExt3, ra, (((lane % 9) / 3) * kExt + lane % 3) * kExt);
+      coop_store_blocks(dsm, 3 * kExt3, blocks + tix * kExt3);
+    } else {
+      scatter_store(bw, lane, ra, blocks + tix * kExt3);
+    }
+  };
+  if constexpr (COOP) {
+    auto item = [&](const int4 cur, int) __attribute__((always_inline)) { tile(cur); };
+    coop_loop(active, wq, n_active, item);
+  } else {
+    for (TileIter ti(active, wq, n_active, lane); ti.valid(); ti.advance()) {
+      ti.prefetch(active);
+      tile(ti.cur);
+    }
   }
 }
 
@@ -1053,7 +1140,7 @@ __device__ __forceinline__ void load_tile_grid(const DevParams& P, const float4*
 // Tile grids are double-buffered in shared memory with cp.async (the next
 // tile's 6^3 velocity block streams in while the current tile computes) and
 // the next chunk's particle loads are issued before the current chunk's math.
-template <int LAW>
+template <int LAW, bool COOP>
 __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams P, StateView S, StateView Sout,
                                                      const int* __restrict__ perm, const int* __restrict__ tile_start,
                                                      const int* __restrict__ tile_count, const int4* __restrict__ active,
@@ -1065,18 +1152,14 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_active = *(const volatile int*)nact;
   const TransferCtx<float> T = tctx(P);
-  TileIter ti(active, wq, n_active, lane);
-  if (ti.valid()) prefetch_tile_grid(P, gv, ti.cur, vg[warp][0], lane);
-  cp_async_commit();
-  for (int buf = 0; ti.valid(); ti.advance(), buf ^= 1) {
-    if (ti.has_next()) prefetch_tile_grid(P, gv, ti.nxt, vg[warp][buf ^ 1], lane);
-    cp_async_commit();
-    ti.prefetch(active);
-    const int a = ti.a;
-    const int e = ti.cur.x, t = ti.cur.y, start = ti.cur.z, cnt = ti.cur.w;
+  // one tile (item a) with its grid block landed in vw
+  auto tile = [&](const int4 cur, const int a, const float4* vw) __attribute__((always_inline)) {
+    const int e = cur.x, t = cur.y, start = cur.z;
+    const int cnt = coop_count<COOP>(cur.w, warp);  // this warp's (virtual) particle count
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
     const size_t row = (size_t)e * P.N + start;
+    auto pidx = [&](int v) { return perm[row + coop_idx<COOP>(v, warp)]; };
     const float4 vr4 = vref[e];
     const v3<float> vr = mk3(vr4.x, vr4.y, vr4.z);
     // two particle-state buffers (chunks alternate) and perm indices two
@@ -1085,22 +1168,19 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
     m3<float> Fa, Fb;
     uint32_t ata = 0, atb = 0;
     if (lane < cnt) {
-      const int src = perm[row + lane];
+      const int src = pidx(lane);
       load_xF<LAW>(S, src, xa, Fa, P.fiso);
       ata = S.attr[src];
     }
-    int s1 = lane + 32 < cnt ? perm[row + lane + 32] : 0;
-    int s0 = lane + 64 < cnt ? perm[row + lane + 64] : 0;
-    cp_async_wait<1>();  // this tile's grid has landed
-    __syncwarp();
-    float4* vw = vg[warp][buf];
-    if (out_gv && a < dump_cap) {  // segment replay: keep the tile's grid for the adjoint substep
+    int s1 = lane + 32 < cnt ? pidx(lane + 32) : 0;
+    int s0 = lane + 64 < cnt ? pidx(lane + 64) : 0;
+    if (out_gv && a < dump_cap && (!COOP || warp == 0)) {  // segment replay: keep the tile's grid for the adjoint
       for (int i = lane; i < kExt3; i += 32) out_gv[(size_t)a * kExt3 + i] = vw[i];
       load_tile_grid(P, gmp, e, o, out_gmp + (size_t)a * kExt3, lane);
     }
     auto body = [&](int c0, const float x[3], m3<float> F, uint32_t at) {
       if (c0 + lane >= cnt) return;
-      const size_t dst = row + c0 + lane;
+      const size_t dst = row + coop_idx<COOP>(c0 + lane, warp);
       Stencil<float> sc;
       make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
       const int lb[3] = {tile_local(sc.base[0], o[0]), tile_local(sc.base[1], o[1]), tile_local(sc.base[2], o[2])};
@@ -1122,19 +1202,41 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
         load_xF<LAW>(S, s1, xb, Fb, P.fiso);
         atb = S.attr[s1];
       }
-      s1 = c0 + 96 + lane < cnt ? perm[row + c0 + 96 + lane] : 0;
+      s1 = c0 + 96 + lane < cnt ? pidx(c0 + 96 + lane) : 0;
       body(c0, xa, Fa, ata);
       if (c0 + 32 >= cnt) break;
       if (c0 + 64 + lane < cnt) {  // chunk c0 + 64 -> buffer a
         load_xF<LAW>(S, s0, xa, Fa, P.fiso);
         ata = S.attr[s0];
       }
-      s0 = c0 + 128 + lane < cnt ? perm[row + c0 + 128 + lane] : 0;
+      s0 = c0 + 128 + lane < cnt ? pidx(c0 + 128 + lane) : 0;
       body(c0 + 32, xb, Fb, atb);
     }
     __syncwarp();  // every lane is done with vw before it is refilled
+  };
+  if constexpr (COOP) {
+    auto item = [&](const int4 cur, int a) __attribute__((always_inline)) {
+      prefetch_tile_grid(P, gv, cur, vg[warp][0], lane);  // each warp its own copy of the tile's grid
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncwarp();
+      tile(cur, a, vg[warp][0]);
+    };
+    coop_loop(active, wq, n_active, item);
+  } else {
+    TileIter ti(active, wq, n_active, lane);
+    if (ti.valid()) prefetch_tile_grid(P, gv, ti.cur, vg[warp][0], lane);
+    cp_async_commit();
+    for (int buf = 0; ti.valid(); ti.advance(), buf ^= 1) {
+      if (ti.has_next()) prefetch_tile_grid(P, gv, ti.nxt, vg[warp][buf ^ 1], lane);
+      cp_async_commit();
+      ti.prefetch(active);
+      cp_async_wait<1>();  // this tile's grid has landed
+      __syncwarp();
+      tile(ti.cur, ti.a, vg[warp][buf]);
+    }
+    cp_async_wait<0>();
   }
-  cp_async_wait<0>();
 }
 
 // ============================ G2P adjoint ============================
@@ -1146,7 +1248,7 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
 #ifndef DM_G2PADJ_MINB
 #define DM_G2PADJ_MINB 3
 #endif
-template <int LAW, int NM>
+template <int LAW, int NM, bool COOP>
 __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevParams P, StateView S, StateView Sn, const float* __restrict__ adj_in,
                                                          size_t astride, const int* __restrict__ perm,
                                                          const int* __restrict__ tile_start,
@@ -1162,10 +1264,9 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
   float4* aw = vw + kExt3;              // 3 group copies of the cotangent block
   float* pw = reinterpret_cast<float*>(dsm + kWarps * 4 * kExt3) + warp * 32 * kPay;
   const int n_active = *(const volatile int*)nact;
-  for (TileIter ti(active, wq, n_active, lane); ti.valid(); ti.advance()) {
-    ti.prefetch(active);
-    const int a = ti.a;
-    const int e = ti.cur.x, t = ti.cur.y, start = ti.cur.z, cnt = ti.cur.w;
+  auto tile = [&](const int4 cur, const int a) __attribute__((always_inline)) {
+    const int e = cur.x, t = cur.y, start = cur.z;
+    const int cnt = coop_count<COOP>(cur.w, warp);  // this warp's (virtual) particle count
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
     // the replayed substep's grid, by slot (asynchronous; overlaps the first loads)
@@ -1173,17 +1274,18 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
     cp_async_commit();
     const size_t tix = (size_t)e * P.Tn + t;
     const size_t row = (size_t)e * P.N + start;
+    auto pidx = [&](int v) { return perm[row + coop_idx<COOP>(v, warp)]; };
     const float4 vr4 = vref[e];
     float x[3];
     m3<float> F;
     uint32_t at = 0;
     if (lane < cnt) {
-      const int src = perm[row + lane];
+      const int src = pidx(lane);
       load_xF<LAW>(S, src, x, F, P.fiso);
       at = S.attr[src];
     }
-    int s1 = 32 + lane < cnt ? perm[row + 32 + lane] : 0;  // perm two chunks ahead, parity slots
-    int s0 = 64 + lane < cnt ? perm[row + 64 + lane] : 0;
+    int s1 = 32 + lane < cnt ? pidx(32 + lane) : 0;  // perm two chunks ahead, parity slots
+    int s0 = 64 + lane < cnt ? pidx(64 + lane) : 0;
     scatter_zero(aw, lane);
     double mub[NM];  // fp64: cancelling per-particle sums (NM = materials)
 #pragma unroll
@@ -1194,7 +1296,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
     __syncwarp();
     auto chunk = [&](int c0, int s_next) __attribute__((always_inline)) -> int {
       if (c0 + lane < cnt) {
-        const size_t dst = row + c0 + lane;
+        const size_t dst = row + coop_idx<COOP>(c0 + lane, warp);
         Stencil<float> sc;
         make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
         const int lb[3] = {tile_local(sc.base[0], o[0]), tile_local(sc.base[1], o[1]), tile_local(sc.base[2], o[2])};
@@ -1233,7 +1335,6 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
         part[part_index(0, dst, astride)] = xp.x;
         part[part_index(1, dst, astride)] = xp.y;
         part[part_index(2, dst, astride)] = xp.z;
-#pragma unroll
         if (LAW == kFluid && P.fiso)  // isotropic input F: its cotangent matters only through the trace
           part[part_index(3, dst, astride)] = Fp.a[0] + Fp.a[4] + Fp.a[8];
         else
@@ -1246,19 +1347,40 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
         load_xF<LAW>(S, s_next, x, F, P.fiso);
         at = S.attr[s_next];
       }
-      const int s_new = c0 + 96 + lane < cnt ? perm[row + c0 + 96 + lane] : 0;
+      const int s_new = c0 + 96 + lane < cnt ? pidx(c0 + 96 + lane) : 0;
       scatter_runs<false>(aw, pw, min(32, cnt - c0), lane, ra);
       return s_new;
     };
     chunk_loop<LAW == kFluid>(chunk, cnt, s0, s1);
-    scatter_store(aw, lane, ra, ablocks + tix * kExt3);
+    if constexpr (COOP) {
+      if (lane < 27) run_flush(aw + (lane / 9) * kExt3, ra, (((lane % 9) / 3) * kExt + lane % 3) * kExt);
+      coop_store_blocks(dsm + kExt3, 4 * kExt3, ablocks + tix * kExt3);
+    } else {
+      scatter_store(aw, lane, ra, ablocks + tix * kExt3);
+    }
 #pragma unroll
     for (int m = 0; m < NM; ++m)
       for (int off = 16; off > 0; off >>= 1) mub[m] += __shfl_xor_sync(0xffffffffu, mub[m], off);
-    if (lane == 0)
+    if constexpr (COOP) {
 #pragma unroll
-      for (int m = 0; m < NM; ++m) tile_acc[tix * kNacc + kAccMuG + m] = (float)mub[m];
+      for (int m = 0; m < NM; ++m) mub[m] = coop_sum(mub[m]);
+      if (threadIdx.x == 0)
+#pragma unroll
+        for (int m = 0; m < NM; ++m) tile_acc[tix * kNacc + kAccMuG + m] = (float)mub[m];
+    } else {
+      if (lane == 0)
+#pragma unroll
+        for (int m = 0; m < NM; ++m) tile_acc[tix * kNacc + kAccMuG + m] = (float)mub[m];
+    }
     __syncwarp();
+  };
+  if constexpr (COOP) {
+    coop_loop(active, wq, n_active, tile);
+  } else {
+    for (TileIter ti(active, wq, n_active, lane); ti.valid(); ti.advance()) {
+      ti.prefetch(active);
+      tile(ti.cur, ti.a);
+    }
   }
 }
 
@@ -1337,7 +1459,7 @@ constexpr int kP2gAdjStage = 38;  // staged words per particle: state 24, attr, 
 #ifndef DM_P2GADJ_MINB
 #define DM_P2GADJ_MINB 3
 #endif
-template <int LAW, int NG, int NM>
+template <int LAW, int NG, int NM, bool COOP>
 __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevParams P, StateView S, const int* __restrict__ perm,
                                                          const int* __restrict__ tile_start,
                                                          const int* __restrict__ tile_count,
@@ -1352,13 +1474,14 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
   const int n_active = *(const volatile int*)nact;
   float4* bw = mb[warp];
   float* sg = stg[warp];
-  for (TileIter ti(active, wq, n_active, lane); ti.valid(); ti.advance()) {
-    ti.prefetch(active);
-    const int e = ti.cur.x, t = ti.cur.y, start = ti.cur.z, cnt = ti.cur.w;
+  auto tile = [&](const int4 cur) __attribute__((always_inline)) {
+    const int e = cur.x, t = cur.y, start = cur.z;
+    const int cnt = coop_count<COOP>(cur.w, warp);  // this warp's (virtual) particle count
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
     const size_t tix = (size_t)e * P.Tn + t;
     const size_t row = (size_t)e * P.N + start;
+    auto pidx = [&](int v) { return perm[row + coop_idx<COOP>(v, warp)]; };
     double mub[NM], lab[NM];  // fp64: cancelling sums (NM = materials)
 #pragma unroll
     for (int m = 0; m < NM; ++m) mub[m] = lab[m] = 0.0;
@@ -1374,16 +1497,16 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
       cp_async4(sg + 24 * 32 + lane, S.attr + src);
 #pragma unroll
       for (int f = 0; f < 12; ++f)
-        if (!(LAW == kFluid && P.fiso && f > 3)) cp_async4(sg + (25 + f) * 32 + lane, part + part_index(f, row + c0 + lane, astride));
+        if (!(LAW == kFluid && P.fiso && f > 3)) cp_async4(sg + (25 + f) * 32 + lane, part + part_index(f, row + coop_idx<COOP>(c0 + lane, warp), astride));
       sg[37 * 32 + lane] = __int_as_float(src);
     };
-    int s1 = 32 + lane < cnt ? perm[row + 32 + lane] : 0;  // perm two chunks ahead, parity slots
-    int s0 = lane < cnt ? perm[row + lane] : 0;
+    int s1 = 32 + lane < cnt ? pidx(32 + lane) : 0;  // perm two chunks ahead, parity slots
+    int s0 = lane < cnt ? pidx(lane) : 0;
     __syncwarp();  // previous tile's readers are done with bw and sg
-    prefetch_tile_grid(P, gmb, ti.cur, bw, lane);
+    prefetch_tile_grid(P, gmb, cur, bw, lane);
     if (lane < cnt) stage(0, s0);
     cp_async_commit();
-    s0 = 64 + lane < cnt ? perm[row + 64 + lane] : 0;
+    s0 = 64 + lane < cnt ? pidx(64 + lane) : 0;
     for (int c0 = 0, k = 0; c0 < cnt; c0 += 32, ++k) {
       cp_async_wait<0>();
       __syncwarp();
@@ -1414,7 +1537,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
       const bool odd = k & 1;
       if (c0 + 32 + lane < cnt) stage(c0 + 32, odd ? s0 : s1);
       cp_async_commit();
-      const int s_new = c0 + 96 + lane < cnt ? perm[row + c0 + 96 + lane] : 0;
+      const int s_new = c0 + 96 + lane < cnt ? pidx(c0 + 96 + lane) : 0;
       s0 = odd ? s_new : s0;
       s1 = odd ? s1 : s_new;
       if (!ok) continue;
@@ -1468,7 +1591,16 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
 #pragma unroll
     for (int q = 0; q < NG; ++q)
       for (int off = 16; off > 0; off >>= 1) actb[q] += __shfl_xor_sync(0xffffffffu, actb[q], off);
-    if (lane == 0) {
+    if constexpr (COOP) {  // fixed-order sum of the 4 warps' partials
+#pragma unroll
+      for (int m = 0; m < NM; ++m) {
+        mub[m] = coop_sum(mub[m]);
+        lab[m] = coop_sum(lab[m]);
+      }
+#pragma unroll
+      for (int q = 0; q < NG; ++q) actb[q] = coop_sum(actb[q]);
+    }
+    if (COOP ? threadIdx.x == 0 : lane == 0) {
       float* ta = tile_acc + tix * kNacc;
 #pragma unroll
       for (int m = 0; m < NM; ++m) {
@@ -1477,6 +1609,18 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
       }
 #pragma unroll
       for (int q = 0; q < NG; ++q) ta[kAccAct + q] = actb[q];
+    }
+  };
+  if constexpr (COOP) {
+    auto item = [&](const int4 cur, int) __attribute__((always_inline)) {
+      tile(cur);
+      cp_async_wait<0>();  // no staging copy outlives the item
+    };
+    coop_loop(active, wq, n_active, item);
+  } else {
+    for (TileIter ti(active, wq, n_active, lane); ti.valid(); ti.advance()) {
+      ti.prefetch(active);
+      tile(ti.cur);
     }
   }
   cp_async_wait<0>();
