@@ -5,6 +5,7 @@
 // (tape.hpp:181-255) driven per control step as step_checkpointed does
 // (algo.hpp:79-104).
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled (driver entry point, no -lcuda)
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: named ranges for nsys / ncu --nvtx
 
 #include <algorithm>
@@ -40,6 +41,7 @@ struct DmContext {
   unsigned long long launches = 0, bytes = 0;
   int grid_tiles = 148 * 4;
   bool coop = false;  // CTA-cooperative tiles (small batches; see coop_idx)
+  CUtensorMap tm_gv, tm_gmb;  // TMA descriptors of the dense node-velocity / (mass, momentum)-cotangent grids
 
   float* store = nullptr;  // [n_store][24][Ntot]
   uint32_t* store_attr = nullptr;
@@ -142,6 +144,32 @@ bool dalloc(DmContext* ctx, T** p, size_t n) {
   }
   ctx->bytes += n * sizeof(T);
   return true;
+}
+
+// TMA descriptor of a dense per-env node grid [E][d0][d1][d2] float4 as a 5-D
+// fp32 tensor (4, d2, d1, d0, E) with a 4 x 6 x 6 x 6 x 1 box: one tile's
+// node block (tma_tile_grid).  The encoder comes from the driver entry point
+// table (no libcuda link).
+bool make_grid_tmap(CUtensorMap* tm, const float4* base, const DevParams& P) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      cudaGetLastError();
+      return false;
+    }
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t d2 = P.dims[2], d1 = P.dims[1], d0 = P.dims[0];
+  const cuuint64_t dims[5] = {4, d2, d1, d0, (cuuint64_t)P.E};
+  const cuuint64_t strides[4] = {16, 16 * d2, 16 * d2 * d1, 16 * d2 * d1 * d0};  // bytes, dims 1..4
+  const cuuint32_t box[5] = {4, kExt, kExt, kExt, 1};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  return encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float4*>(base), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // state buffers hold 24 floats per particle, Ntot rounded up to the AoSoA block
@@ -328,11 +356,11 @@ void launch_g2p(DmContext* c, const StateView& S, const StateView& So, const Slo
   PROF_BEGIN(c, 2);
 #define L_G2P(LW)                                                                                                \
   if (c->coop) k_g2p<LW, true><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, q.perm, q.tile_start, q.tile_count, \
-                                                          q.work, c->gv, c->flags, q.nact, sub, c->gmp,         \
+                                                          q.work, c->tm_gv, c->flags, q.nact, sub, c->gmp,         \
                                                           dump ? q.gvb : nullptr, dump ? q.gmpb : nullptr, c->wq, (int)c->blk_cap, \
                                                           q.vref); \
   else k_g2p<LW, false><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, q.perm, q.tile_start, q.tile_count,        \
-                                                          q.work, c->gv, c->flags, q.nact, sub, c->gmp,         \
+                                                          q.work, c->tm_gv, c->flags, q.nact, sub, c->gmp,         \
                                                           dump ? q.gvb : nullptr, dump ? q.gmpb : nullptr, c->wq, (int)c->blk_cap, \
                                                           q.vref)
   DM_LAW_DISPATCH(c, L_G2P);
@@ -398,7 +426,7 @@ void forward_substep(DmContext* c, const StateView& S, const StateView& So, int 
 template <int LAW, int NG, int NM, bool COOP>
 void launch_p2g_adj_k(DmContext* c, const StateView& S, const Slot& q, int t, float* adj_out) {
   k_p2g_adj<LAW, NG, NM, COOP><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(
-      c->P, S, q.perm, q.tile_start, q.tile_count, q.work, step_act(c, t), c->gmb, c->part, adj_out, c->Ntot,
+      c->P, S, q.perm, q.tile_start, q.tile_count, q.work, step_act(c, t), c->tm_gmb, c->part, adj_out, c->Ntot,
       c->tile_acc, q.nact, c->wq);
 }
 
@@ -1077,6 +1105,8 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
                   ctx->bytes / 1e9);
     return fail(buf);
   }
+  if (!make_grid_tmap(&ctx->tm_gv, ctx->gv, P) || !make_grid_tmap(&ctx->tm_gmb, ctx->gmb, P))
+    return fail("dm_create: TMA descriptor encoding failed (cuTensorMapEncodeTiled)");
   cudaMemsetAsync(ctx->store_attr, 0, N * sizeof(uint32_t), ctx->stream);
   cudaMemsetAsync(ctx->tile_acc, 0, TT * kNacc * sizeof(float), ctx->stream);
   {

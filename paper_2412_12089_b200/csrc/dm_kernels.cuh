@@ -25,6 +25,8 @@
 // grids and the P2G-adjoint staging).
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (TMA descriptors are encoded by the context)
+
 #include <cstdint>
 
 #include "dm_transfer.cuh"
@@ -760,17 +762,59 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// Starts the asynchronous load of tile d's 6^3 block of a dense grid.
-__device__ __forceinline__ void prefetch_tile_grid(const DevParams& P, const float4* __restrict__ grid, int4 d,
-                                                   float4* dst, int lane) {
+// ---- TMA / bulk async copies (sm_90+ async proxy; mbarrier completion) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+// the issuing thread's arrival, expecting `bytes` of async-proxy writes
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// generic-proxy accesses of a buffer are ordered before a following async-proxy write into it
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// 1-D bulk copy global -> shared (UBLKCP), completing on bar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  mbar_expect_tx(bar, bytes);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// 1-D bulk copy shared -> global (bulk async group of the issuing thread)
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+// the issuing thread's bulk stores have finished reading shared memory
+__device__ __forceinline__ void bulk_s2g_read_wait() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_s2g_wait() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+
+// TMA tensor load (UTMALDG) of tile d's 6^3 node block of a dense per-env grid
+// [E][d0][d1][d2] float4, described by the 5-D map tm (4 floats, d2, d1, d0,
+// E; box 4 x 6 x 6 x 6 x 1, dm_context.cu make_grid_tmap).  Nodes past the
+// grid's far faces are zero-filled by the TMA unit (the cp.async path's
+// src-size-0 copies).  One thread issues it; completion lands on bar.
+__device__ __forceinline__ void tma_tile_grid(const DevParams& P, const CUtensorMap* tm, int4 d, float4* dst,
+                                              uint64_t* bar) {
   const int t = d.y;
-  const int o[3] = {(t / (P.td[2] * P.td[1])) * kTile, ((t / P.td[2]) % P.td[1]) * kTile, (t % P.td[2]) * kTile};
-  const size_t eb = (size_t)d.x * P.dims[0] * P.dims[1] * P.dims[2];
-  for (int i = lane; i < kExt3; i += 32) {
-    const int g0 = o[0] + i / 36, g1 = o[1] + (i / 6) % 6, g2 = o[2] + i % 6;
-    const bool in = g0 < P.dims[0] && g1 < P.dims[1] && g2 < P.dims[2];
-    cp_async16(dst + i, in ? grid + eb + ((size_t)g0 * P.dims[1] + g1) * P.dims[2] + g2 : grid, in);
-  }
+  const int o0 = (t / (P.td[2] * P.td[1])) * kTile, o1 = ((t / P.td[2]) % P.td[1]) * kTile, o2 = (t % P.td[2]) * kTile;
+  mbar_expect_tx(bar, kExt3 * (uint32_t)sizeof(float4));
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+      "%6}], [%7];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(0), "r"(o2), "r"(o1), "r"(o0), "r"(d.x), "r"(smem_u32(bar))
+      : "memory");
 }
 
 // Particle state of one chunk slot held in registers (software pipeline:
@@ -1144,12 +1188,19 @@ template <int LAW, bool COOP>
 __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams P, StateView S, StateView Sout,
                                                      const int* __restrict__ perm, const int* __restrict__ tile_start,
                                                      const int* __restrict__ tile_count, const int4* __restrict__ active,
-                                                     const float4* __restrict__ gv, DevFlags* flags, const int* nact,
+                                                     const __grid_constant__ CUtensorMap tm_gv, DevFlags* flags, const int* nact,
                                                      int substep, const float4* __restrict__ gmp,
                                                      float4* __restrict__ out_gv, float4* __restrict__ out_gmp, int* __restrict__ wq,
                                                      int dump_cap, const float4* __restrict__ vref) {
-  __shared__ __align__(16) float4 vg[kWarps][2][kExt3];
+  __shared__ __align__(128) float4 vg[kWarps][2][kExt3];
+  __shared__ uint64_t vbar[kWarps][2];  // TMA completion of vg[w][b]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    mbar_init(&vbar[warp][0]);
+    mbar_init(&vbar[warp][1]);
+    mbar_init_fence();
+  }
+  __syncwarp();
   const int n_active = *(const volatile int*)nact;
   const TransferCtx<float> T = tctx(P);
   // one tile (item a) with its grid block landed in vw
@@ -1175,7 +1226,7 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
     int s1 = lane + 32 < cnt ? pidx(lane + 32) : 0;
     int s0 = lane + 64 < cnt ? pidx(lane + 64) : 0;
     if (out_gv && a < dump_cap && (!COOP || warp == 0)) {  // segment replay: keep the tile's grid for the adjoint
-      for (int i = lane; i < kExt3; i += 32) out_gv[(size_t)a * kExt3 + i] = vw[i];
+      if (lane == 0) bulk_s2g(out_gv + (size_t)a * kExt3, vw, kExt3 * (uint32_t)sizeof(float4));
       load_tile_grid(P, gmp, e, o, out_gmp + (size_t)a * kExt3, lane);
     }
     auto body = [&](int c0, const float x[3], m3<float> F, uint32_t at) {
@@ -1214,29 +1265,37 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
     }
     __syncwarp();  // every lane is done with vw before it is refilled
   };
+  // tile grids arrive by TMA; lane 0 (thread 0 in COOP) issues, after its
+  // bulk dump stores of the buffer's previous tile have read it
+  uint32_t ph = 0;
   if constexpr (COOP) {
     auto item = [&](const int4 cur, int a) __attribute__((always_inline)) {
-      prefetch_tile_grid(P, gv, cur, vg[warp][0], lane);  // each warp its own copy of the tile's grid
-      cp_async_commit();
-      cp_async_wait<0>();
-      __syncwarp();
-      tile(cur, a, vg[warp][0]);
+      if (threadIdx.x == 0) {  // one copy of the tile's grid for the CTA
+        bulk_s2g_read_wait();
+        fence_proxy_async();
+        tma_tile_grid(P, &tm_gv, cur, vg[0][0], &vbar[0][0]);
+      }
+      mbar_wait(&vbar[0][0], ph);
+      ph ^= 1;
+      tile(cur, a, vg[0][0]);
     };
     coop_loop(active, wq, n_active, item);
   } else {
     TileIter ti(active, wq, n_active, lane);
-    if (ti.valid()) prefetch_tile_grid(P, gv, ti.cur, vg[warp][0], lane);
-    cp_async_commit();
+    if (ti.valid() && lane == 0) tma_tile_grid(P, &tm_gv, ti.cur, vg[warp][0], &vbar[warp][0]);
     for (int buf = 0; ti.valid(); ti.advance(), buf ^= 1) {
-      if (ti.has_next()) prefetch_tile_grid(P, gv, ti.nxt, vg[warp][buf ^ 1], lane);
-      cp_async_commit();
+      if (ti.has_next() && lane == 0) {  // the next tile's grid streams in during this tile
+        bulk_s2g_read_wait();
+        fence_proxy_async();
+        tma_tile_grid(P, &tm_gv, ti.nxt, vg[warp][buf ^ 1], &vbar[warp][buf ^ 1]);
+      }
       ti.prefetch(active);
-      cp_async_wait<1>();  // this tile's grid has landed
-      __syncwarp();
+      mbar_wait(&vbar[warp][buf], (ph >> buf) & 1);
+      ph ^= 1u << buf;
       tile(ti.cur, ti.a, vg[warp][buf]);
     }
-    cp_async_wait<0>();
   }
+  if (lane == 0) bulk_s2g_read_wait();  // shared memory outlives the dump stores' reads
 }
 
 // ============================ G2P adjoint ============================
@@ -1257,8 +1316,15 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
                                                          float4* __restrict__ ablocks, float* __restrict__ part,
                                                          float* __restrict__ tile_acc, const int* nact, int* __restrict__ wq,
                                                          const float4* __restrict__ vref) {
-  extern __shared__ float4 dsm[];
+  extern __shared__ __align__(128) float4 dsm[];
+  __shared__ uint64_t vbar[kWarps];  // bulk-copy completion of the warp's vw
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    mbar_init(&vbar[warp]);
+    mbar_init_fence();
+  }
+  __syncwarp();
+  uint32_t ph = 0;
   const TransferCtx<float> T = tctx(P);
   float4* vw = dsm + warp * 4 * kExt3;  // the tile's node velocities
   float4* aw = vw + kExt3;              // 3 group copies of the cotangent block
@@ -1270,8 +1336,10 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
     // the replayed substep's grid, by slot (asynchronous; overlaps the first loads)
-    for (int i = lane; i < kExt3; i += 32) cp_async16(vw + i, gvb + (size_t)a * kExt3 + i, true);
-    cp_async_commit();
+    if (lane == 0) {  // one bulk copy (the previous tile's readers passed its closing __syncwarp)
+      fence_proxy_async();
+      bulk_g2s(vw, gvb + (size_t)a * kExt3, kExt3 * (uint32_t)sizeof(float4), &vbar[warp]);
+    }
     const size_t tix = (size_t)e * P.Tn + t;
     const size_t row = (size_t)e * P.N + start;
     auto pidx = [&](int v) { return perm[row + coop_idx<COOP>(v, warp)]; };
@@ -1292,8 +1360,8 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
     for (int m = 0; m < NM; ++m) mub[m] = 0.0;
     RunAcc ra;
     run_reset(ra);
-    cp_async_wait<0>();
-    __syncwarp();
+    mbar_wait(&vbar[warp], ph);
+    ph ^= 1;
     auto chunk = [&](int c0, int s_next) __attribute__((always_inline)) -> int {
       if (c0 + lane < cnt) {
         const size_t dst = row + coop_idx<COOP>(c0 + lane, warp);
@@ -1464,15 +1532,22 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
                                                          const int* __restrict__ tile_start,
                                                          const int* __restrict__ tile_count,
                                                          const int4* __restrict__ active, const float* __restrict__ act,
-                                                         const float4* __restrict__ gmb, const float* __restrict__ part,
+                                                         const __grid_constant__ CUtensorMap tm_gmb, const float* __restrict__ part,
                                                          float* __restrict__ adj_out, size_t astride,
                                                          float* __restrict__ tile_acc, const int* nact, int* __restrict__ wq) {
-  __shared__ __align__(16) float4 mb[kWarps][kExt3];
+  __shared__ __align__(128) float4 mb[kWarps][kExt3];
+  __shared__ uint64_t mbar[kWarps];  // TMA completion of mb[w]
   __shared__ float stg[kWarps][kP2gAdjStage * 32];  // next chunk: [field][lane]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TransferCtx<float> T = tctx(P);
   const int n_active = *(const volatile int*)nact;
   float4* bw = mb[warp];
+  if (lane == 0) {
+    mbar_init(&mbar[warp]);
+    mbar_init_fence();
+  }
+  __syncwarp();
+  uint32_t ph = 0;
   float* sg = stg[warp];
   auto tile = [&](const int4 cur) __attribute__((always_inline)) {
     const int e = cur.x, t = cur.y, start = cur.z;
@@ -1503,10 +1578,15 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
     int s1 = 32 + lane < cnt ? pidx(32 + lane) : 0;  // perm two chunks ahead, parity slots
     int s0 = lane < cnt ? pidx(lane) : 0;
     __syncwarp();  // previous tile's readers are done with bw and sg
-    prefetch_tile_grid(P, gmb, cur, bw, lane);
+    if (lane == 0) {
+      fence_proxy_async();
+      tma_tile_grid(P, &tm_gmb, cur, bw, &mbar[warp]);
+    }
     if (lane < cnt) stage(0, s0);
     cp_async_commit();
     s0 = 64 + lane < cnt ? pidx(64 + lane) : 0;
+    mbar_wait(&mbar[warp], ph);  // the cotangent block has landed
+    ph ^= 1;
     for (int c0 = 0, k = 0; c0 < cnt; c0 += 32, ++k) {
       cp_async_wait<0>();
       __syncwarp();
