@@ -486,7 +486,7 @@ void backward_substep(DmContext* c, const StateView& S, const StateView& Sn, int
   ++c->launches;
   const int Kc = c->P.K > 0 ? c->P.K : 1;
   PROF_BEGIN(c, 5);
-  k_env_reduce<<<c->P.E, kNacc, 0, c->stream>>>(c->P, q.active, q.env_abase, q.env_acount, c->tile_acc,
+  k_env_reduce<<<c->P.E, kNacc * kRedSlices, 0, c->stream>>>(c->P, q.active, q.env_abase, q.env_acount, c->tile_acc,
                                                 c->gcvo + (size_t)t * c->P.E * Kc * 9,
                                                 c->gact + (size_t)t * c->P.E * (G > 0 ? G : 1), c->gmu, c->glam);
   PROF_END(c, 5);

@@ -1020,15 +1020,24 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, S
 // order and it is computed (owned) by the first active covering tile.
 // nbr: 27-bit activity mask of the 3x3x3 tile neighbourhood (bit = (rx+1)*9 +
 // (ry+1)*3 + (rz+1)).
+// nbt[bit]: the neighbour's block index e * Tn + tile when active, else -1.
 __device__ __forceinline__ unsigned neighbour_mask(const DevParams& P, const int* __restrict__ tile_count, int e,
-                                                   const int tc[3], int lane) {
+                                                   const int tc[3], int lane, int* nbt) {
   bool act = false;
+  __syncwarp();  // the previous tile's readers are done with nbt
   if (lane < 27) {
     const int sx = tc[0] + lane / 9 - 1, sy = tc[1] + (lane / 3) % 3 - 1, sz = tc[2] + lane % 3 - 1;
-    if (sx >= 0 && sx < P.td[0] && sy >= 0 && sy < P.td[1] && sz >= 0 && sz < P.td[2])
-      act = tile_count[(size_t)e * P.Tn + (sx * P.td[1] + sy) * P.td[2] + sz] > 0;
+    int slot = -1;
+    if (sx >= 0 && sx < P.td[0] && sy >= 0 && sy < P.td[1] && sz >= 0 && sz < P.td[2]) {
+      const int st = e * P.Tn + (sx * P.td[1] + sy) * P.td[2] + sz;
+      act = tile_count[st] > 0;
+      slot = act ? st : -1;
+    }
+    nbt[lane] = slot;
   }
-  return __ballot_sync(0xffffffffu, act);
+  const unsigned m = __ballot_sync(0xffffffffu, act);
+  __syncwarp();
+  return m;
 }
 
 // candidate range per axis for local coordinate a in [0, 6): rel in [lo, hi]
@@ -1042,8 +1051,12 @@ __device__ __forceinline__ void cand_range(int a, int& lo, int& hi) {
 // ordered before self.  Ascending bit order = ascending tile order, so
 // iterating the set bits of nbr & cand sums the covering blocks in the fixed
 // order, and a tile owns node i iff nbr & prior == 0.  Built once per CTA.
+// cl[i][0..nc[i]): the covering tiles of node i in ascending order, packed
+// (neighbourhood bit << 8) | (node i's index in that tile's block).
 struct NodeMasks {
   unsigned cand[kExt3], prior[kExt3];
+  unsigned short cl[kExt3][8];
+  unsigned char nc[kExt3];
 };
 
 __device__ __forceinline__ void build_node_masks(NodeMasks& m) {
@@ -1054,14 +1067,18 @@ __device__ __forceinline__ void build_node_masks(NodeMasks& m) {
     for (int d = 0; d < 3; ++d) cand_range(l[d], lo[d], hi[d]);
     unsigned c = 0u, pr = 0u;
     bool before = true;
+    int k = 0;
     for (int rx = lo[0]; rx <= hi[0]; ++rx)
       for (int ry = lo[1]; ry <= hi[1]; ++ry)
         for (int rz = lo[2]; rz <= hi[2]; ++rz) {
-          const unsigned bit = 1u << ((rx + 1) * 9 + (ry + 1) * 3 + (rz + 1));
+          const int code = (rx + 1) * 9 + (ry + 1) * 3 + (rz + 1);
+          const unsigned bit = 1u << code;
           if (rx == 0 && ry == 0 && rz == 0) before = false;
           c |= bit;
           if (before) pr |= bit;
+          m.cl[i][k++] = (unsigned short)((code << 8) | (((l[0] - 4 * rx) * kExt + (l[1] - 4 * ry)) * kExt + (l[2] - 4 * rz)));
         }
+    m.nc[i] = (unsigned char)k;
     m.cand[i] = c;
     m.prior[i] = pr & ~(1u << 13);
   }
@@ -1088,24 +1105,21 @@ __device__ __forceinline__ int owned_nodes(const DevParams& P, const NodeMasks& 
   return n;
 }
 
-__device__ __forceinline__ float4 sum_blocks(const DevParams& P, const NodeMasks& nm, const float4* __restrict__ blocks,
-                                             unsigned nbr, int e, const int tc[3], int i) {
+__device__ __forceinline__ float4 sum_blocks(const NodeMasks& nm, const float4* __restrict__ blocks,
+                                             const int* __restrict__ nbt, int i) {
   // all (<= 8) covering blocks' loads are issued before the fixed-order sum
   // (ascending tile order = lexicographic (rx, ry, rz), as the cover mask bits)
-  (void)nm;
-  const int l[3] = {i / 36, (i / 6) % 6, i % 6};
-  int lo[3], hi[3];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) cand_range(l[d], lo[d], hi[d]);
+  const int k = nm.nc[i];
   float4 v[8];
   bool ok[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
-    const int rx = lo[0] + (c >> 2), ry = lo[1] + ((c >> 1) & 1), rz = lo[2] + (c & 1);
-    ok[c] = rx <= hi[0] && ry <= hi[1] && rz <= hi[2] && ((nbr >> ((rx + 1) * 9 + (ry + 1) * 3 + (rz + 1))) & 1u);
-    if (ok[c]) {
-      const int st = ((tc[0] + rx) * P.td[1] + (tc[1] + ry)) * P.td[2] + (tc[2] + rz);
-      v[c] = blocks[((size_t)e * P.Tn + st) * kExt3 + ((l[0] - 4 * rx) * kExt + (l[1] - 4 * ry)) * kExt + (l[2] - 4 * rz)];
+    ok[c] = false;
+    if (c < k) {
+      const unsigned cc = nm.cl[i][c];
+      const int b = nbt[cc >> 8];
+      ok[c] = b >= 0;
+      if (ok[c]) v[c] = blocks[(size_t)b * kExt3 + (cc & 255u)];
     }
   }
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1139,6 +1153,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_GRID_MINB) k_grid(DevParams P,
                                                       const float4* __restrict__ vref) {
   __shared__ short own[kWarps][kExt3];
   __shared__ NodeMasks nm;
+  __shared__ int nbt[kWarps][27];  // the tile's neighbour block indices (neighbour_mask)
   __shared__ Col<float> scol[kWarps][MAXC];
   build_node_masks(nm);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1149,7 +1164,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_GRID_MINB) k_grid(DevParams P,
     const int4 et = active[a];
     const int e = et.x, t = et.y;
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
-    const unsigned nbr = neighbour_mask(P, tile_count, e, tc, lane);
+    const unsigned nbr = neighbour_mask(P, tile_count, e, tc, lane, nbt[warp]);
     Col<float>* cols = scol[warp];  // the env's colliders, in shared memory (frees registers)
     __syncwarp();
     if (lane == 0) load_cols<MAXC>(P, cvo + (size_t)e * P.K * 9, cols);
@@ -1161,7 +1176,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_GRID_MINB) k_grid(DevParams P,
       const int i = own[warp][q];
       const int l[3] = {i / 36, (i / 6) % 6, i % 6};
       const int g[3] = {tc[0] * kTile + l[0], tc[1] * kTile + l[1], tc[2] * kTile + l[2]};
-      const float4 mm = sum_blocks(P, nm, blocks, nbr, e, tc, i);  // (mass, momentum relative to vref)
+      const float4 mm = sum_blocks(nm, blocks, nbt[warp], i);  // (mass, momentum relative to vref)
       const v3<float> v = node_update_rel<float, MAXC, CK>(G, cols, P.K, g, mm.x, mk3(mm.y, mm.z, mm.w), vr);
       const size_t n = node_lin(P, e, g);
       if (gmp) gmp[n] = mm;  // (mass, momentum) only when the replay dumps them
@@ -1468,6 +1483,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_GRIDADJ_MINB) k_grid_adj(DevPa
                                                           const float4* __restrict__ vref) {
   __shared__ short own[kWarps][kExt3];
   __shared__ NodeMasks nm;
+  __shared__ int nbt[kWarps][27];  // the tile's neighbour block indices (neighbour_mask)
   __shared__ Col<float> scol[kWarps][MAXC];
   build_node_masks(nm);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1478,7 +1494,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_GRIDADJ_MINB) k_grid_adj(DevPa
     const int4 et = active[a];
     const int e = et.x, t = et.y;
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
-    const unsigned nbr = neighbour_mask(P, tile_count, e, tc, lane);
+    const unsigned nbr = neighbour_mask(P, tile_count, e, tc, lane, nbt[warp]);
     Col<float>* cols = scol[warp];  // the env's colliders, in shared memory (frees registers)
     __syncwarp();
     if (lane == 0) load_cols<MAXC>(P, cvo + (size_t)e * P.K * 9, cols);
@@ -1491,7 +1507,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_GRIDADJ_MINB) k_grid_adj(DevPa
       const int i = own[warp][q];
       const int l[3] = {i / 36, (i / 6) % 6, i % 6};
       const int g[3] = {tc[0] * kTile + l[0], tc[1] * kTile + l[1], tc[2] * kTile + l[2]};
-      const float4 vb = sum_blocks(P, nm, ablocks, nbr, e, tc, i);
+      const float4 vb = sum_blocks(nm, ablocks, nbt[warp], i);
       const size_t n = node_lin(P, e, g);
       float4 mm = gmpb[(size_t)a * kExt3 + i];  // this tile's stored (mass, momentum relative to vref) block
       {  // the adjoint linearises in the lab frame: momentum + mass vref
@@ -1706,24 +1722,42 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
   cp_async_wait<0>();
 }
 
-// Per env: sum the env's tile accumulators in tile order into the step's
-// (double) parameter cotangents.
-__global__ void k_env_reduce(DevParams P, const int4* __restrict__ active, const int* __restrict__ env_abase,
+// Per env: sum the env's tile accumulators into the step's (double)
+// parameter cotangents.  kRedSlices contiguous slices of the env's tile list
+// are summed in tile order (4 loads in flight per thread), then the slices in
+// slice order: a fixed order, independent of the schedule.
+constexpr int kRedSlices = 4;
+__global__ void __launch_bounds__(kNacc * kRedSlices) k_env_reduce(DevParams P, const int4* __restrict__ active, const int* __restrict__ env_abase,
                              const int* __restrict__ env_acount, const float* __restrict__ tile_acc,
                              double* __restrict__ gcvo_t, double* __restrict__ gact_t, double* __restrict__ gmu,
                              double* __restrict__ glam) {
+  __shared__ double part[kRedSlices][kNacc];
   __shared__ double sacc[kNacc];
-  const int e = blockIdx.x, f = threadIdx.x;
+  const int e = blockIdx.x, f = threadIdx.x % kNacc, g = threadIdx.x / kNacc;
   const int b = env_abase[e], n = env_acount[e];
+  const int i0 = b + (int)((long long)n * g / kRedSlices), i1 = b + (int)((long long)n * (g + 1) / kRedSlices);
+  auto acc_of = [&](int i) {
+    const int4 et = active[i];
+    return tile_acc[((size_t)et.x * P.Tn + et.y) * kNacc + f];
+  };
   double s = 0.0;
-  if (f < kNacc)
-    for (int i = 0; i < n; ++i) {
-      const int4 et = active[b + i];
-      s += tile_acc[((size_t)et.x * P.Tn + et.y) * kNacc + f];
-    }
-  if (f < kNacc) sacc[f] = s;
+  int i = i0;
+  for (; i + 4 <= i1; i += 4) {
+    const float a0 = acc_of(i), a1 = acc_of(i + 1), a2 = acc_of(i + 2), a3 = acc_of(i + 3);
+    s += a0;
+    s += a1;
+    s += a2;
+    s += a3;
+  }
+  for (; i < i1; ++i) s += acc_of(i);
+  part[g][f] = s;
   __syncthreads();
-  if (f >= kNacc) return;
+  if (g != 0) return;
+  s = part[0][f];
+#pragma unroll
+  for (int q = 1; q < kRedSlices; ++q) s += part[q][f];
+  sacc[f] = s;
+  asm volatile("bar.sync 1, %0;\n" ::"n"(kNacc) : "memory");  // slice 0's threads (2 whole warps) only
   // dL/dmu has two sources (P2G-adjoint stress term f, G2P-adjoint yield
   // term f + 8): one thread adds both, in that fixed order
   if (f < 4) {

@@ -82,11 +82,15 @@ def gpu_rollout(sim, mats, cols, states, n_ctrl, n_sub, act=None, loss=None, gra
 
 # ---------------- binning / sort ----------------
 
-@pytest.mark.parametrize("seed", [0, 1])
-def test_sort_bit_exact(seed):
+@pytest.mark.parametrize("seed,n,E,lo,hi", [(0, 3000, 3, 0.08, 0.92), (1, 3000, 3, 0.08, 0.92),
+                                            (2, 4096, 1, 0.3, 0.5), (3, 20000, 2, 0.2, 0.5), (4, 700, 5, 0.1, 0.9)])
+def test_sort_bit_exact(seed, n, E, lo, hi):
+    """Several batch shapes (particles per warp from ~2 to ~600 chunks of the
+    bin kernel's per-warp histograms): the permutation equals
+    std::stable_sort by key."""
     rng = np.random.default_rng(seed)
     sim = dict(SIM16, dims=(48, 48, 48), dx=1 / 48)
-    states = [random_block(rng, 3000, 0.08, 0.92) for _ in range(3)]
+    states = [random_block(rng, n, lo, hi) for _ in range(E)]
     b = gpu_batch(sim, [LAWS["fluid"]], [], states, 1, 1)
     b.set_state(stack(states, "x"), stack(states, "v"), stack(states, "F"), stack(states, "C"))
     keys, perm = b.debug_sort()
