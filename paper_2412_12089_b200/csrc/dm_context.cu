@@ -146,10 +146,11 @@ bool dalloc(DmContext* ctx, T** p, size_t n) {
   return true;
 }
 
-// TMA descriptor of a dense per-env node grid [E][d0][d1][d2] float4 as a 5-D
-// fp32 tensor (4, d2, d1, d0, E) with a 4 x 6 x 6 x 6 x 1 box: one tile's
-// node block (tma_tile_grid).  The encoder comes from the driver entry point
-// table (no libcuda link).
+// TMA descriptor of a dense per-env node grid [E][d0][d1][d2] float4 as a 4-D
+// fp32 tensor (4 d2, d1, d0, E) with a 24 x 6 x 6 x 1 box: one tile's node
+// block (tma_tile_grid), 96-byte rows (a separate 16-byte node dimension
+// measured slower).  The encoder comes from the driver entry point table (no
+// libcuda link).
 bool make_grid_tmap(CUtensorMap* tm, const float4* base, const DevParams& P) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
@@ -163,11 +164,11 @@ bool make_grid_tmap(CUtensorMap* tm, const float4* base, const DevParams& P) {
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   const cuuint64_t d2 = P.dims[2], d1 = P.dims[1], d0 = P.dims[0];
-  const cuuint64_t dims[5] = {4, d2, d1, d0, (cuuint64_t)P.E};
-  const cuuint64_t strides[4] = {16, 16 * d2, 16 * d2 * d1, 16 * d2 * d1 * d0};  // bytes, dims 1..4
-  const cuuint32_t box[5] = {4, kExt, kExt, kExt, 1};
-  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  return encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float4*>(base), dims, strides, box, estr,
+  const cuuint64_t dims[4] = {4 * d2, d1, d0, (cuuint64_t)P.E};
+  const cuuint64_t strides[3] = {16 * d2, 16 * d2 * d1, 16 * d2 * d1 * d0};  // bytes, dims 1..3
+  const cuuint32_t box[4] = {4 * kExt, kExt, kExt, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float4*>(base), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -426,7 +427,7 @@ void forward_substep(DmContext* c, const StateView& S, const StateView& So, int 
 template <int LAW, int NG, int NM, bool COOP>
 void launch_p2g_adj_k(DmContext* c, const StateView& S, const Slot& q, int t, float* adj_out) {
   k_p2g_adj<LAW, NG, NM, COOP><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(
-      c->P, S, q.perm, q.tile_start, q.tile_count, q.work, step_act(c, t), c->tm_gmb, c->part, adj_out, c->Ntot,
+      c->P, S, q.perm, q.tile_start, q.tile_count, q.work, step_act(c, t), c->gmb, c->tm_gmb, c->part, adj_out, c->Ntot,
       c->tile_acc, q.nact, c->wq);
 }
 

@@ -800,9 +800,23 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void bulk_s2g_read_wait() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_s2g_wait() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
+// cp.async (LDGSTS) load of tile d's 6^3 block of a dense grid, zero-filling
+// nodes past the grid's far faces (src-size 0).
+__device__ __forceinline__ void prefetch_tile_grid(const DevParams& P, const float4* __restrict__ grid, int4 d,
+                                                   float4* dst, int lane) {
+  const int t = d.y;
+  const int o[3] = {(t / (P.td[2] * P.td[1])) * kTile, ((t / P.td[2]) % P.td[1]) * kTile, (t % P.td[2]) * kTile};
+  const size_t eb = (size_t)d.x * P.dims[0] * P.dims[1] * P.dims[2];
+  for (int i = lane; i < kExt3; i += 32) {
+    const int g0 = o[0] + i / 36, g1 = o[1] + (i / 6) % 6, g2 = o[2] + i % 6;
+    const bool in = g0 < P.dims[0] && g1 < P.dims[1] && g2 < P.dims[2];
+    cp_async16(dst + i, in ? grid + eb + ((size_t)g0 * P.dims[1] + g1) * P.dims[2] + g2 : grid, in);
+  }
+}
+
 // TMA tensor load (UTMALDG) of tile d's 6^3 node block of a dense per-env grid
-// [E][d0][d1][d2] float4, described by the 5-D map tm (4 floats, d2, d1, d0,
-// E; box 4 x 6 x 6 x 6 x 1, dm_context.cu make_grid_tmap).  Nodes past the
+// [E][d0][d1][d2] float4, described by the 4-D map tm (4 d2 floats, d1, d0,
+// E; box 24 x 6 x 6 x 1, dm_context.cu make_grid_tmap).  Nodes past the
 // grid's far faces are zero-filled by the TMA unit (the cp.async path's
 // src-size-0 copies).  One thread issues it; completion lands on bar.
 __device__ __forceinline__ void tma_tile_grid(const DevParams& P, const CUtensorMap* tm, int4 d, float4* dst,
@@ -811,9 +825,9 @@ __device__ __forceinline__ void tma_tile_grid(const DevParams& P, const CUtensor
   const int o0 = (t / (P.td[2] * P.td[1])) * kTile, o1 = ((t / P.td[2]) % P.td[1]) * kTile, o2 = (t % P.td[2]) * kTile;
   mbar_expect_tx(bar, kExt3 * (uint32_t)sizeof(float4));
   asm volatile(
-      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
-      "%6}], [%7];\n" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(0), "r"(o2), "r"(o1), "r"(o0), "r"(d.x), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5}], [%6];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(4 * o2), "r"(o1), "r"(o0), "r"(d.x), "r"(smem_u32(bar))
       : "memory");
 }
 
@@ -1332,9 +1346,9 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
                                                          float* __restrict__ tile_acc, const int* nact, int* __restrict__ wq,
                                                          const float4* __restrict__ vref) {
   extern __shared__ __align__(128) float4 dsm[];
-  __shared__ uint64_t vbar[kWarps];  // bulk-copy completion of the warp's vw
+  __shared__ uint64_t vbar[kWarps];  // COOP: bulk-copy completion of the warp's vw
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) {
+  if (COOP && lane == 0) {
     mbar_init(&vbar[warp]);
     mbar_init_fence();
   }
@@ -1351,9 +1365,18 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
     // the replayed substep's grid, by slot (asynchronous; overlaps the first loads)
-    if (lane == 0) {  // one bulk copy (the previous tile's readers passed its closing __syncwarp)
-      fence_proxy_async();
-      bulk_g2s(vw, gvb + (size_t)a * kExt3, kExt3 * (uint32_t)sizeof(float4), &vbar[warp]);
+    // the replayed substep's grid, by slot (asynchronous; overlaps the first
+    // loads): one bulk copy (UBLKCP) in COOP mode, per-lane LDGSTS otherwise
+    // (r02 A/B: the bulk copy is 7 % faster with CTA-shared tiles, 2.5 %
+    // slower with one tile per warp)
+    if constexpr (COOP) {
+      if (lane == 0) {  // the previous tile's readers passed its closing __syncwarp
+        fence_proxy_async();
+        bulk_g2s(vw, gvb + (size_t)a * kExt3, kExt3 * (uint32_t)sizeof(float4), &vbar[warp]);
+      }
+    } else {
+      for (int i = lane; i < kExt3; i += 32) cp_async16(vw + i, gvb + (size_t)a * kExt3 + i, true);
+      cp_async_commit();
     }
     const size_t tix = (size_t)e * P.Tn + t;
     const size_t row = (size_t)e * P.N + start;
@@ -1375,8 +1398,13 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
     for (int m = 0; m < NM; ++m) mub[m] = 0.0;
     RunAcc ra;
     run_reset(ra);
-    mbar_wait(&vbar[warp], ph);
-    ph ^= 1;
+    if constexpr (COOP) {
+      mbar_wait(&vbar[warp], ph);
+      ph ^= 1;
+    } else {
+      cp_async_wait<0>();
+      __syncwarp();
+    }
     auto chunk = [&](int c0, int s_next) __attribute__((always_inline)) -> int {
       if (c0 + lane < cnt) {
         const size_t dst = row + coop_idx<COOP>(c0 + lane, warp);
@@ -1548,23 +1576,28 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
                                                          const int* __restrict__ tile_start,
                                                          const int* __restrict__ tile_count,
                                                          const int4* __restrict__ active, const float* __restrict__ act,
-                                                         const __grid_constant__ CUtensorMap tm_gmb, const float* __restrict__ part,
+                                                         const float4* __restrict__ gmb, const __grid_constant__ CUtensorMap tm_gmb,
+                                                         const float* __restrict__ part,
                                                          float* __restrict__ adj_out, size_t astride,
                                                          float* __restrict__ tile_acc, const int* nact, int* __restrict__ wq) {
   __shared__ __align__(128) float4 mb[kWarps][kExt3];
-  __shared__ uint64_t mbar[kWarps];  // TMA completion of mb[w]
+  __shared__ uint64_t mbar[kWarps];  // COOP: TMA completion of mb[w]
   __shared__ float stg[kWarps][kP2gAdjStage * 32];  // next chunk: [field][lane]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TransferCtx<float> T = tctx(P);
   const int n_active = *(const volatile int*)nact;
-  float4* bw = mb[warp];
-  if (lane == 0) {
+  if (COOP && lane == 0) {
     mbar_init(&mbar[warp]);
     mbar_init_fence();
   }
   __syncwarp();
   uint32_t ph = 0;
   float* sg = stg[warp];
+  // The tile's (mass, momentum) cotangent block: a TMA box load in COOP mode
+  // (r02 A/B: -6 % with CTA-shared tiles), per-lane LDGSTS in the staging
+  // group otherwise (a TMA load, single or double-buffered, was 1.5-3 % slower
+  // with one tile per warp).
+  float4* bw = mb[warp];
   auto tile = [&](const int4 cur) __attribute__((always_inline)) {
     const int e = cur.x, t = cur.y, start = cur.z;
     const int cnt = coop_count<COOP>(cur.w, warp);  // this warp's (virtual) particle count
@@ -1594,15 +1627,21 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
     int s1 = 32 + lane < cnt ? pidx(32 + lane) : 0;  // perm two chunks ahead, parity slots
     int s0 = lane < cnt ? pidx(lane) : 0;
     __syncwarp();  // previous tile's readers are done with bw and sg
-    if (lane == 0) {
-      fence_proxy_async();
-      tma_tile_grid(P, &tm_gmb, cur, bw, &mbar[warp]);
+    if constexpr (COOP) {
+      if (lane == 0) {
+        fence_proxy_async();
+        tma_tile_grid(P, &tm_gmb, cur, bw, &mbar[warp]);
+      }
+    } else {
+      prefetch_tile_grid(P, gmb, cur, bw, lane);
     }
     if (lane < cnt) stage(0, s0);
     cp_async_commit();
     s0 = 64 + lane < cnt ? pidx(64 + lane) : 0;
-    mbar_wait(&mbar[warp], ph);  // the cotangent block has landed
-    ph ^= 1;
+    if constexpr (COOP) {  // the cotangent block has landed
+      mbar_wait(&mbar[warp], ph);
+      ph ^= 1;
+    }
     for (int c0 = 0, k = 0; c0 < cnt; c0 += 32, ++k) {
       cp_async_wait<0>();
       __syncwarp();
