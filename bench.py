@@ -409,14 +409,16 @@ def run_ours(args, scene, rank, world, local, dist):
     achieved = ALG_BYTES[dom] * per_launch_units / (dom_ms / dom_n / 1e3) / 1e9
     total_prof = sum(v[0] for v in prof.values())
     # DRAM traffic of the dominant kernel from the committed ncu --set full
-    # capture (profiles/ncu_summary.json, bytes per particle), per launch here
+    # capture (profiles/ncu_summary_cfg<N>.json, bytes per particle), per launch here
+    # of this config (profiles/ncu_summary_cfg<N>.json; none committed: null)
     traffic, traffic_src = None, None
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+        name = "ncu_summary_cfg%d.json" % args.config
+        with open(os.path.join(ROOT, "profiles", name)) as f:
             ks = json.load(f)
         kinfo = ks["kernels"][dom]
         traffic = kinfo["dram_bytes_per_particle"] * per_launch_units
-        traffic_src = "%s (%s, cfg4 steady state)" % (ks.get("source", "profiles/ncu_summary.json"), kinfo["kernel"])
+        traffic_src = "profiles/%s (%s, %s)" % (name, kinfo["kernel"], ks.get("source", ""))
     except Exception:
         pass
     path_gbs = 480.0 * units_rank / (ms_rank / 1e3) / 1e9

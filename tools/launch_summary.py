@@ -1,27 +1,20 @@
-"""Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv):
-launches, total ms, share and ms/launch per kernel.  usage: python tools/launch_summary.py launches.csv"""
+"""Per-kernel totals of an ncu launch list (--metrics gpu__time_duration.sum --csv).
+
+usage: python tools/launch_summary.py LAUNCHES.csv "HEADER LINE" > SUMMARY.txt"""
+import collections
 import csv
 import sys
-from collections import defaultdict
 
-rows = list(csv.reader(open(sys.argv[1])))
-hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
-h = rows[hi]
-kn, mn, mv = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
-tot, cnt = defaultdict(float), defaultdict(int)
-unit = h.index("Metric Unit") if "Metric Unit" in h else None
-for r in rows[hi + 1:]:
-    if len(r) <= mv or r[mn] != "gpu__time_duration.sum":
-        continue
-    name = r[kn].split("(")[0].replace("void ", "")
-    if not name.startswith("dm::"):
-        name = "torch/other: " + name.split("<")[0][:40]
-    v = float(r[mv].replace(",", ""))
-    u = r[unit] if unit is not None else "ns"
-    ms = v * {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1.0, "msecond": 1.0}.get(u, 1e-6)
-    tot[name] += ms
-    cnt[name] += 1
-T = sum(tot.values())
-print(f"{'kernel':34s} {'launches':>8s} {'total ms':>10s} {'share':>7s} {'ms/launch':>10s}")
-for k in sorted(tot, key=lambda k: -tot[k]):
-    print(f"{k:34s} {cnt[k]:8d} {tot[k]:10.2f} {100 * tot[k] / T:6.1f}% {tot[k] / cnt[k]:10.3f}")
+rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
+h = rows[0]
+ik, iv, iu = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
+agg = collections.defaultdict(list)
+for r in rows[1:]:
+    agg[r[ik].split("(")[0].replace("void ", "")].append(float(r[iv].replace(",", "")) * scale[r[iu]])
+tot = sum(sum(v) for v in agg.values())
+print("# " + (sys.argv[2] if len(sys.argv) > 2 else sys.argv[1]))
+print("# serialised, per-launch cold cache (ncu): shares, not absolute step times")
+print("# %-30s %8s %10s %10s %7s" % ("kernel", "launches", "mean_us", "total_ms", "share"))
+for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
+    print("%-32s %8d %10.1f %10.2f %6.1f%%" % (k[:32], len(v), sum(v) / len(v), sum(v) / 1e3, 100 * sum(v) / tot))
