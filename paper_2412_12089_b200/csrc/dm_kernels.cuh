@@ -280,8 +280,9 @@ __device__ __forceinline__ void store_state(const StateView& S, size_t i, v3<flo
 // fixed summation order (a deterministic function of the state: the replay
 // reproduces it bitwise).
 constexpr int kVrefParticles = 256;
+constexpr int kBinU = 4;  // chunks whose loads k_bin / k_cellsort issue together
 template <class CT>
-__global__ void __launch_bounds__(1024) k_bin(DevParams P, StateView S, int* keys, int* perm, int* tile_start,
+__global__ void __launch_bounds__(1024, 2) k_bin(DevParams P, StateView S, int* keys, int* perm, int* tile_start,
                                              int* tile_count, int4* active, int* env_abase, int* env_acount,
                                              DevFlags* flags, int* nact, int substep, int check_vmax,
                                              float4* __restrict__ vref) {
@@ -317,27 +318,40 @@ __global__ void __launch_bounds__(1024) k_bin(DevParams P, StateView S, int* key
   const int p0 = wid * chunk, p1 = min(P.N, p0 + chunk);
   CT* my = cnt + wid * P.Tn;
   float vmax = 0.f;
-  for (int c0 = p0; c0 < p1; c0 += 32) {
-    const int p = c0 + lane;
-    int key = -1 - lane;
-    if (p < p1) {
-      const size_t i = base + p;
-      float x[3] = {S.c(0, i), S.c(1, i), S.c(2, i)};
-      int b[3];
-      float fx[3];
-      const int bad = stencil_base(x, P.inv_dx, (double)P.dx, P.dims, b, fx);
-      if (bad >= 0) {
-        report(flags, e, substep, 0, attr_index(S.attr[i]), bad, kErrP2GInterior);
+  // kBinU chunks per step: their position loads are all in flight before the
+  // first key is computed (latency-bound at small batches)
+  for (int c0 = p0; c0 < p1; c0 += 32 * kBinU) {
+    float xs[kBinU][3];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) b[a] = b[a] < 1 ? 1 : (b[a] > P.dims[a] - 4 ? P.dims[a] - 4 : b[a]);
-      }
-      key = ((b[0] >> 2) * P.td[1] + (b[1] >> 2)) * P.td[2] + (b[2] >> 2);
-      keys[i] = key * 64 + ((b[0] & 3) * 4 + (b[1] & 3)) * 4 + (b[2] & 3);  // full key: tile * 64 + cell
-      if (check_vmax) vmax = fmaxf(vmax, fmaxf(fabsf(S.c(3, i)), fmaxf(fabsf(S.c(4, i)), fabsf(S.c(5, i)))));
+    for (int u = 0; u < kBinU; ++u) {
+      const int p = c0 + 32 * u + lane;
+      if (p < p1)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) xs[u][a] = S.c(a, base + p);
     }
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    if (p < p1 && lane == __ffs(peers) - 1) my[key] = (CT)(my[key] + __popc(peers));
-    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < kBinU; ++u) {
+      const int p = c0 + 32 * u + lane;
+      if (c0 + 32 * u >= p1) break;
+      int key = -1 - lane;
+      if (p < p1) {
+        const size_t i = base + p;
+        int b[3];
+        float fx[3];
+        const int bad = stencil_base(xs[u], P.inv_dx, (double)P.dx, P.dims, b, fx);
+        if (bad >= 0) {
+          report(flags, e, substep, 0, attr_index(S.attr[i]), bad, kErrP2GInterior);
+#pragma unroll
+          for (int a = 0; a < 3; ++a) b[a] = b[a] < 1 ? 1 : (b[a] > P.dims[a] - 4 ? P.dims[a] - 4 : b[a]);
+        }
+        key = ((b[0] >> 2) * P.td[1] + (b[1] >> 2)) * P.td[2] + (b[2] >> 2);
+        keys[i] = key * 64 + ((b[0] & 3) * 4 + (b[1] & 3)) * 4 + (b[2] & 3);  // full key: tile * 64 + cell
+        if (check_vmax) vmax = fmaxf(vmax, fmaxf(fabsf(S.c(3, i)), fmaxf(fabsf(S.c(4, i)), fabsf(S.c(5, i)))));
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      if (p < p1 && lane == __ffs(peers) - 1) my[key] = (CT)(my[key] + __popc(peers));
+      __syncwarp();
+    }
   }
   if (check_vmax) {
     for (int o = 16; o > 0; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
@@ -401,20 +415,30 @@ __global__ void __launch_bounds__(1024) k_bin(DevParams P, StateView S, int* key
     }
   }
   __syncthreads();
-  for (int c0 = p0; c0 < p1; c0 += 32) {
-    const int p = c0 + lane;
-    const int key = p < p1 ? keys[base + p] >> 6 : -1 - lane;
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    const int leader = __ffs(peers) - 1;
-    const int rank = __popc(peers & ((1u << lane) - 1u));
-    int pos = 0;
-    if (lane == leader && p < p1) {
-      pos = my[key];
-      my[key] = (CT)(pos + __popc(peers));
+  for (int c0 = p0; c0 < p1; c0 += 32 * kBinU) {
+    int ks[kBinU];
+#pragma unroll
+    for (int u = 0; u < kBinU; ++u) {
+      const int p = c0 + 32 * u + lane;
+      ks[u] = p < p1 ? keys[base + p] >> 6 : -1 - lane;
     }
-    pos = __shfl_sync(0xffffffffu, pos, leader);
-    if (p < p1) perm[base + pos + rank] = (int)(base + p);
-    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < kBinU; ++u) {  // in index order: the cursors advance stably
+      if (c0 + 32 * u >= p1) break;
+      const int p = c0 + 32 * u + lane;
+      const int key = ks[u];
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      const int leader = __ffs(peers) - 1;
+      const int rank = __popc(peers & ((1u << lane) - 1u));
+      int pos = 0;
+      if (lane == leader && p < p1) {
+        pos = my[key];
+        my[key] = (CT)(pos + __popc(peers));
+      }
+      pos = __shfl_sync(0xffffffffu, pos, leader);
+      if (p < p1) perm[base + pos + rank] = (int)(base + p);
+      __syncwarp();
+    }
   }
 }
 
@@ -499,12 +523,24 @@ __global__ void __launch_bounds__(kWarps * 32) k_cellsort(DevParams P, StateView
     cnt[lane + 32] = 0;
     __syncwarp();
     auto cell_of = [&](int src) { return keys[src] & 63; };  // k_bin stored the full key
-    for (int c0 = 0; c0 < n; c0 += 32) {
-      const bool ok = c0 + lane < n;
-      const int cell = ok ? cell_of(ptile[base + c0 + lane]) : 64 + lane;
-      const unsigned peers = __match_any_sync(0xffffffffu, cell);
-      if (ok && lane == __ffs(peers) - 1) cnt[cell] += __popc(peers);
-      __syncwarp();
+    // kBinU chunks per step, their dependent (perm -> key) loads in flight together
+    auto load_cells = [&](int c0, int (&src)[kBinU], int (&cell)[kBinU]) __attribute__((always_inline)) {
+#pragma unroll
+      for (int u = 0; u < kBinU; ++u) src[u] = c0 + 32 * u + lane < n ? ptile[base + c0 + 32 * u + lane] : -1;
+#pragma unroll
+      for (int u = 0; u < kBinU; ++u) cell[u] = src[u] >= 0 ? cell_of(src[u]) : 64 + lane;
+    };
+    for (int c0 = 0; c0 < n; c0 += 32 * kBinU) {
+      int src[kBinU], cl[kBinU];
+      load_cells(c0, src, cl);
+#pragma unroll
+      for (int u = 0; u < kBinU; ++u) {
+        if (c0 + 32 * u >= n) break;
+        const bool ok = src[u] >= 0;
+        const unsigned peers = __match_any_sync(0xffffffffu, cl[u]);
+        if (ok && lane == __ffs(peers) - 1) cnt[cl[u]] += __popc(peers);
+        __syncwarp();
+      }
     }
     // exclusive scan over the 64 buckets (2 per lane)
     const int a0 = cnt[2 * lane], a1 = cnt[2 * lane + 1];
@@ -518,21 +554,25 @@ __global__ void __launch_bounds__(kWarps * 32) k_cellsort(DevParams P, StateView
     cnt[2 * lane] = ex;
     cnt[2 * lane + 1] = ex + a0;
     __syncwarp();
-    for (int c0 = 0; c0 < n; c0 += 32) {
-      const bool ok = c0 + lane < n;
-      const int src = ok ? ptile[base + c0 + lane] : 0;
-      const int cell = ok ? cell_of(src) : 64 + lane;
-      const unsigned peers = __match_any_sync(0xffffffffu, cell);
-      const int leader = __ffs(peers) - 1;
-      const int rank = __popc(peers & ((1u << lane) - 1u));
-      int pos = 0;
-      if (ok && lane == leader) {
-        pos = cnt[cell];
-        cnt[cell] = pos + __popc(peers);
+    for (int c0 = 0; c0 < n; c0 += 32 * kBinU) {
+      int src[kBinU], cl[kBinU];
+      load_cells(c0, src, cl);
+#pragma unroll
+      for (int u = 0; u < kBinU; ++u) {  // in index order: stable
+        if (c0 + 32 * u >= n) break;
+        const bool ok = src[u] >= 0;
+        const unsigned peers = __match_any_sync(0xffffffffu, cl[u]);
+        const int leader = __ffs(peers) - 1;
+        const int rank = __popc(peers & ((1u << lane) - 1u));
+        int pos = 0;
+        if (ok && lane == leader) {
+          pos = cnt[cl[u]];
+          cnt[cl[u]] = pos + __popc(peers);
+        }
+        pos = __shfl_sync(0xffffffffu, pos, leader);
+        if (ok) perm[base + pos + rank] = src[u];
+        __syncwarp();
       }
-      pos = __shfl_sync(0xffffffffu, pos, leader);
-      if (ok) perm[base + pos + rank] = src;
-      __syncwarp();
     }
   }
 }
