@@ -41,6 +41,7 @@ struct DmContext {
   unsigned long long launches = 0, bytes = 0;
   int grid_tiles = 148 * 4;
   bool coop = false;  // CTA-cooperative tiles (small batches; see coop_idx)
+  bool grid_coop = false;  // CTA-shared tiles in the grid kernels (tiny batches)
   CUtensorMap tm_gv, tm_gmb;  // TMA descriptors of the dense node-velocity / (mass, momentum)-cotangent grids
 
   float* store = nullptr;  // [n_store][24][Ntot]
@@ -343,7 +344,12 @@ void launch_grid(DmContext* c, const Slot& q, int t, bool dump) {
   wq_reset(c);
   PROF_BEGIN(c, 9);
 #define L_GRID(MC, CK)                                                                                        \
-  k_grid<MC, CK><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work, step_cvo(c, t), \
+  if (c->grid_coop)                                                                                     \
+    k_grid<MC, CK, true><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work, step_cvo(c, t), \
+                                                               c->blocks, dump ? c->gmp : nullptr, c->gv, q.nact, c->wq, \
+                                                               q.vref);                                 \
+  else                                                                                                  \
+    k_grid<MC, CK, false><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work, step_cvo(c, t), \
                                                                c->blocks, dump ? c->gmp : nullptr, c->gv, q.nact, c->wq, \
                                                                q.vref)
   DM_GRID_DISPATCH(c, L_GRID);
@@ -465,7 +471,12 @@ void backward_substep(DmContext* c, const StateView& S, const StateView& Sn, int
   wq_reset(c);
   PROF_BEGIN(c, 10);
 #define L_GRIDA(MC, CK)                                                                                   \
-  k_grid_adj<MC, CK><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work,        \
+  if (c->grid_coop)                                                                                 \
+    k_grid_adj<MC, CK, true><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work,  \
+                                                                   step_cvo(c, t), c->ablocks, q.gmpb,   \
+                                                                   c->gmb, c->tile_acc, q.nact, c->wq, q.vref); \
+  else                                                                                              \
+    k_grid_adj<MC, CK, false><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work, \
                                                                    step_cvo(c, t), c->ablocks, q.gmpb,   \
                                                                    c->gmb, c->tile_acc, q.nact, c->wq, q.vref)
   DM_GRID_DISPATCH(c, L_GRIDA);
@@ -1146,6 +1157,11 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   // chunks (DIFFMPM_COOP=0/1 forces the mode)
   ctx->coop = N < (size_t)kCoopParticlesPerWarp * ctx->grid_tiles * kWarps;
   if (const char* f = std::getenv("DIFFMPM_COOP")) ctx->coop = f[0] == '1';
+  // the grid kernels' tiles are short (owned nodes): sharing them pays only
+  // when there are fewer tiles than warps (r02 A/B: cfg1 grid -25 %, grid_adj
+  // -32 %; neutral at 32 envs; +5 / +11 % at 128 envs)
+  ctx->grid_coop = N < (size_t)kGridCoopParticlesPerWarp * ctx->grid_tiles * kWarps;
+  if (const char* f = std::getenv("DIFFMPM_GRID_COOP")) ctx->grid_coop = f[0] == '1';
   if (reset_flags(ctx) != DM_OK) return ctx;
   return ctx;
 }

@@ -37,6 +37,7 @@ constexpr int kTile = 4;
 constexpr int kExt = 6;  // tile + quadratic stencil reach
 constexpr int kExt3 = kExt * kExt * kExt;
 constexpr int kWarps = 4;  // warps per CTA in tile kernels
+constexpr int kGridCoopParticlesPerWarp = 64;  // the grid kernels' COOP threshold (dm_create)
 constexpr int kCoopParticlesPerWarp = 640;  // below this many particles per resident warp: COOP tiles (r02 A/B: cfg4 x128 envs +24 %, x256 -3 %)
 constexpr int kPay = 28;   // payload stride (floats; 7 float4, conflict-free STS.128 / 3-way LDS.128)
 constexpr int kNacc = 64;  // per-tile cotangent accumulators
@@ -1196,7 +1197,7 @@ __device__ __forceinline__ size_t node_lin(const DevParams& P, int e, const int 
 // Owned nodes of every active tile: sum the covering blocks, update
 // (mpm.hpp:256-305 + extensions), write (mass, momentum) and velocity to the
 // dense per-env grid.
-template <int MAXC, int CK>
+template <int MAXC, int CK, bool COOP>
 #ifndef DM_GRID_MINB
 #define DM_GRID_MINB 5
 #endif
@@ -1213,9 +1214,9 @@ __global__ void __launch_bounds__(kWarps * 32, DM_GRID_MINB) k_grid(DevParams P,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_active = *(const volatile int*)nact;
   const NodeCtx<float> G = nctx(P);
-  for (int a = grab_tile(wq, lane), an = a < n_active ? grab_tile(wq, lane) : n_active; a < n_active;
-       a = an, an = a < n_active ? grab_tile(wq, lane) : n_active) {
-    const int4 et = active[a];
+  // COOP (small batches): the CTA's 4 warps share a tile's owned nodes (each
+  // warp builds the tile's masks itself; node q goes to warp (q / 32) % 4)
+  auto tile = [&](const int4 et) __attribute__((always_inline)) {
     const int e = et.x, t = et.y;
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const unsigned nbr = neighbour_mask(P, tile_count, e, tc, lane, nbt[warp]);
@@ -1226,7 +1227,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_GRID_MINB) k_grid(DevParams P,
     const int n_own = owned_nodes(P, nm, nbr, tc, own[warp], lane);
     const float4 vr4 = vref[e];
     const v3<float> vr = mk3(vr4.x, vr4.y, vr4.z);
-    for (int q = lane; q < n_own; q += 32) {
+    for (int q = COOP ? 32 * warp + lane : lane; q < n_own; q += COOP ? 32 * kWarps : 32) {
       const int i = own[warp][q];
       const int l[3] = {i / 36, (i / 6) % 6, i % 6};
       const int g[3] = {tc[0] * kTile + l[0], tc[1] * kTile + l[1], tc[2] * kTile + l[2]};
@@ -1236,6 +1237,14 @@ __global__ void __launch_bounds__(kWarps * 32, DM_GRID_MINB) k_grid(DevParams P,
       if (gmp) gmp[n] = mm;  // (mass, momentum) only when the replay dumps them
       gv[n] = make_float4(v.x, v.y, v.z, 0.f);
     }
+  };
+  if constexpr (COOP) {
+    auto item = [&](const int4 cur, int) __attribute__((always_inline)) { tile(cur); };
+    coop_loop(active, wq, n_active, item);
+  } else {
+    for (int a = grab_tile(wq, lane), an = a < n_active ? grab_tile(wq, lane) : n_active; a < n_active;
+         a = an, an = a < n_active ? grab_tile(wq, lane) : n_active)
+      tile(active[a]);
   }
 }
 
@@ -1539,7 +1548,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
 // Owned nodes: node-velocity cotangent (sum of the covering adjoint blocks)
 // -> (mass, momentum) cotangents in the dense grid; collider cotangents
 // reduced per tile (each node counted once, by its owner).
-template <int MAXC, int CK>
+template <int MAXC, int CK, bool COOP>
 #ifndef DM_GRIDADJ_MINB
 #define DM_GRIDADJ_MINB 4
 #endif
@@ -1557,9 +1566,8 @@ __global__ void __launch_bounds__(kWarps * 32, DM_GRIDADJ_MINB) k_grid_adj(DevPa
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_active = *(const volatile int*)nact;
   const NodeCtx<float> G = nctx(P);
-  for (int a = grab_tile(wq, lane), an = a < n_active ? grab_tile(wq, lane) : n_active; a < n_active;
-       a = an, an = a < n_active ? grab_tile(wq, lane) : n_active) {
-    const int4 et = active[a];
+  __shared__ float cred[kWarps][MAXC * 9];  // COOP: the warps' collider cotangents, summed in warp order
+  auto tile = [&](const int4 et, const int a) __attribute__((always_inline)) {
     const int e = et.x, t = et.y;
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const unsigned nbr = neighbour_mask(P, tile_count, e, tc, lane, nbt[warp]);
@@ -1571,7 +1579,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_GRIDADJ_MINB) k_grid_adj(DevPa
 #pragma unroll
     for (int q = 0; q < MAXC * 9; ++q) cg[q] = 0.f;
     const int n_own = owned_nodes(P, nm, nbr, tc, own[warp], lane);
-    for (int q = lane; q < n_own; q += 32) {
+    for (int q = COOP ? 32 * warp + lane : lane; q < n_own; q += COOP ? 32 * kWarps : 32) {
       const int i = own[warp][q];
       const int l[3] = {i / 36, (i / 6) % 6, i % 6};
       const int g[3] = {tc[0] * kTile + l[0], tc[1] * kTile + l[1], tc[2] * kTile + l[2]};
@@ -1594,12 +1602,31 @@ __global__ void __launch_bounds__(kWarps * 32, DM_GRIDADJ_MINB) k_grid_adj(DevPa
 #pragma unroll
     for (int q = 0; q < MAXC * 9; ++q)
       for (int off = 16; off > 0; off >>= 1) cg[q] += __shfl_xor_sync(0xffffffffu, cg[q], off);
-    if (lane == 0) {
-      float* ta = tile_acc + ((size_t)e * P.Tn + t) * kNacc;
+    float* ta = tile_acc + ((size_t)e * P.Tn + t) * kNacc;
+    if constexpr (COOP) {
+      if (lane == 0)
 #pragma unroll
-      for (int q = 0; q < MAXC * 9; ++q) ta[kAccCol + q] = cg[q];
+        for (int q = 0; q < MAXC * 9; ++q) cred[warp][q] = cg[q];
+      __syncthreads();
+      if (threadIdx.x < MAXC * 9) {
+        float acc = cred[0][threadIdx.x];
+#pragma unroll
+        for (int w = 1; w < kWarps; ++w) acc += cred[w][threadIdx.x];
+        ta[kAccCol + threadIdx.x] = acc;
+      }
+    } else {
+      if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < MAXC * 9; ++q) ta[kAccCol + q] = cg[q];
     }
     __syncwarp();
+  };
+  if constexpr (COOP) {
+    coop_loop(active, wq, n_active, tile);
+  } else {
+    for (int a = grab_tile(wq, lane), an = a < n_active ? grab_tile(wq, lane) : n_active; a < n_active;
+         a = an, an = a < n_active ? grab_tile(wq, lane) : n_active)
+      tile(active[a], a);
   }
 }
 
