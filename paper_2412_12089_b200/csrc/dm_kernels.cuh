@@ -667,11 +667,14 @@ __device__ __forceinline__ void load_pay(const float* __restrict__ pk, int wi, P
 }
 
 // One particle's contribution to the lane's column run.
+#ifndef DM_RUN_SHIFT
+#define DM_RUN_SHIFT 1
+#endif
 template <bool HASM>
 __device__ __forceinline__ void run_add(float4* __restrict__ blk, RunAcc& ra, int off, float fi, float fj,
                                         const PayLane& p) {
   if (p.lb != ra.cur) {
-    if (HASM && p.lb == ra.cur + 1) {
+    if (DM_RUN_SHIFT && HASM && p.lb == ra.cur + 1) {
       // next cell in z (the sort's innermost order): the run's nodes k = 1, 2
       // are the new run's k = 0, 1 -- flush only node k = 0 and shift
       // (P2G only: measured slower in the G2P adjoint)

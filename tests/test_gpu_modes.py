@@ -1,0 +1,65 @@
+"""The small-batch scheduling modes (GPU, through the C ABI).
+
+dm_create picks CTA-cooperative tiles (`coop`: the 4 warps of a CTA share a
+tile's chunks; `grid_coop`: they share its owned nodes) from the batch size;
+DIFFMPM_COOP / DIFFMPM_GRID_COOP force them.  Every mode must be
+deterministic run to run (the replay verification relies on it) and agree
+with the others up to the fp32 summation order of the per-warp partials.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2412_12089_b200 import api, scenes
+
+pytestmark = pytest.mark.gpu
+
+MODES = [("0", "0"), ("1", "0"), ("1", "1")]
+
+
+def _run(sc, coop, grid_coop):
+    old = {k: os.environ.get(k) for k in ("DIFFMPM_COOP", "DIFFMPM_GRID_COOP")}
+    os.environ["DIFFMPM_COOP"], os.environ["DIFFMPM_GRID_COOP"] = coop, grid_coop
+    try:
+        b = api.from_scene(sc)  # the mode is read when the context is created
+        r1 = api.run_scene(b, sc)
+        r2 = api.run_scene(b, sc)
+        b.close()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    for k in r1:
+        if isinstance(r1[k], np.ndarray):
+            assert np.array_equal(r1[k], r2[k]), (coop, grid_coop, k)
+    return r1
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
+
+
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_modes_deterministic_and_consistent(cfg):
+    kw = {"seed": 3, "n_envs": 3, "n_ctrl": 2}
+    sc = scenes.CONFIGS[cfg](**kw)
+    runs = {m: _run(sc, *m) for m in MODES}
+    ref = runs[("0", "0")]
+    full = lambda r: np.concatenate([np.asarray(r[k], np.float64).ravel() for k in ("x", "v", "F", "C")])
+    for m, r in runs.items():
+        assert _rel(r["obs"], ref["obs"]) <= 1e-4, (m, "obs")
+        # the full per-env state gradient (a field the loss does not depend on,
+        # e.g. dL/dF0 of a centre-of-mass loss, is rounding noise on its own)
+        assert _rel(full(r), full(ref)) <= 1e-4, (m, "dL/dstate", _rel(full(r), full(ref)))
+        scale = np.linalg.norm(full(ref))
+        for k in ("cvo", "act"):
+            if k not in ref:
+                continue
+            if np.linalg.norm(ref[k]) <= 1e-6 * scale:  # the loss does not depend on it: noise
+                assert np.linalg.norm(r[k]) <= 1e-4 * scale, (m, k)
+            else:
+                assert _rel(r[k], ref[k]) <= 1e-4, (m, k, _rel(r[k], ref[k]))

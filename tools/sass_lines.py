@@ -15,6 +15,7 @@ import tempfile
 
 src, fsub = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+depth = int(sys.argv[4]) if len(sys.argv) > 4 else 0  # > 0: also aggregate at this inline depth (1 = kernel level)
 so = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2412_12089_b200", "libdiffmpm.so")
 tmp = tempfile.mkdtemp()
 subprocess.check_call(["cuobjdump", "-xelf", "all", so], cwd=tmp, stdout=subprocess.DEVNULL)
@@ -22,7 +23,7 @@ cub = [os.path.join(tmp, f) for f in os.listdir(tmp) if f.endswith(".cubin")][0]
 dis = subprocess.run(["nvdisasm", "-c", "-gi", cub], capture_output=True, text=True).stdout.splitlines()
 loc_re = re.compile(r'//## File ".*?([^/]+)", line (\d+)(?: inlined at ".*?([^/]+)", line (\d+))?')
 ins_re = re.compile(r"/\*([0-9a-f]{4,})\*/\s+(.*?);")
-inner, outer, text = {}, {}, {}
+inner, outer, text, chain = {}, {}, {}, {}
 infn, cur = False, []
 for ln in dis:
     if ln.startswith("//----") and ".text." in ln:
@@ -41,6 +42,7 @@ for ln in dis:
         if cur:
             inner[off] = cur[0]
             outer[off] = cur[-1]
+            chain[off] = cur[::-1]  # outermost first
         text[off] = m.group(2).strip()
         cur = []
 rows = list(csv.reader(gzip.open(src, "rt")))
@@ -65,6 +67,19 @@ print("total samples %d, warp instructions %.3g" % (tot_s, tot_e))
 print("-- innermost line: samples%, inst%")
 for k, v in agg_i.most_common(top):
     print("%-22s %6.2f%% %6.2f%%" % ("%s:%d" % k, 100 * v / tot_s, 100 * ex_i[k] / max(tot_e, 1)))
+if depth:
+    agg_d, ex_d = collections.Counter(), collections.Counter()
+    last = ("?", 0)
+    for r in rows[2:]:
+        off = int(r[ia], 16) - base
+        ch = chain.get(off)
+        k = ch[min(depth, len(ch)) - 1] if ch else last
+        last = k
+        agg_d[k] += float(r[isamp] or 0)
+        ex_d[k] += float(r[iex] or 0)
+    print("-- inline depth %d: samples%%, inst%%" % depth)
+    for k, v in sorted(agg_d.items(), key=lambda x: -ex_d[x[0]])[:top]:
+        print("%-22s %6.2f%% %6.2f%%" % ("%s:%d" % k, 100 * v / tot_s, 100 * ex_d[k] / max(tot_e, 1)))
 print("-- kernel-level line: samples%")
 for k, v in agg_o.most_common(20):
     print("%-22s %6.2f%%" % ("%s:%d" % k, 100 * v / tot_s))
