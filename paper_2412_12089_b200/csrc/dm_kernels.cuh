@@ -603,8 +603,8 @@ __device__ __forceinline__ void stage_payload(float* __restrict__ pp, int lbl, c
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) w[3 * i + j] = sc.w[0][i] * sc.w[1][j];
-  p4[0] = make_float4(__int_as_float(lbl), m, sc.w[2][0], sc.w[2][1]);
-  p4[1] = make_float4(sc.w[2][2], w[0], w[1], w[2]);
+  p4[0] = make_float4(__int_as_float(lbl), sc.w[2][0], sc.w[2][1], sc.w[2][2]);
+  p4[1] = make_float4(m, w[0], w[1], w[2]);
   p4[2] = make_float4(w[3], w[4], w[5], w[6]);
   p4[3] = make_float4(w[7], w[8], 0.f, 0.f);
   p4[4] = make_float4(q.x, Ad.a[0], Ad.a[1], Ad.a[2]);
@@ -652,14 +652,19 @@ struct PayLane {
   float4 r[3];
 };
 
+// Payload: (label, wz0, wz1, wz2), (m, w_00 .. w_22), (q_a, Ad row a) x 3:
+// the mass-free adjoint scatter reads 5 shared-memory words-groups per
+// particle, P2G 6 (g2p_adj -2.8 %; a register mass for one-material batches
+// made P2G slower, +3.7 %).
+template <bool HASM>
 __device__ __forceinline__ void load_pay(const float* __restrict__ pk, int wi, PayLane& p) {
   const float4* p4 = reinterpret_cast<const float4*>(pk);
   const float4 h = p4[0];
   p.lb = __float_as_int(h.x);
-  p.m = h.y;
-  p.wz[0] = h.z;
-  p.wz[1] = h.w;
-  p.wz[2] = pk[4];
+  p.wz[0] = h.y;
+  p.wz[1] = h.z;
+  p.wz[2] = h.w;
+  p.m = HASM ? pk[4] : 0.f;
   p.wij = pk[wi];
   p.r[0] = p4[4];
   p.r[1] = p4[5];
@@ -723,12 +728,12 @@ __device__ __forceinline__ void scatter_runs(float4* __restrict__ blk3, const fl
     const int k0 = g * kSeg, k1 = min(nv, k0 + kSeg);
     if (k0 < k1) {
       PayLane pa, pb;
-      load_pay(pay + k0 * kPay, wi, pa);
+      load_pay<HASM>(pay + k0 * kPay, wi, pa);
       int k = k0;
       for (; k + 1 < k1; k += 2) {
-        load_pay(pay + (k + 1) * kPay, wi, pb);
+        load_pay<HASM>(pay + (k + 1) * kPay, wi, pb);
         run_add<HASM>(blk, ra, off, fi, fj, pa);
-        if (k + 2 < k1) load_pay(pay + (k + 2) * kPay, wi, pa);
+        if (k + 2 < k1) load_pay<HASM>(pay + (k + 2) * kPay, wi, pa);
         run_add<HASM>(blk, ra, off, fi, fj, pb);
       }
       if (k < k1) run_add<HASM>(blk, ra, off, fi, fj, pa);
