@@ -49,6 +49,12 @@ struct DmContext {
   float* seg = nullptr;  // [ck-1][24][Ntot]
   uint32_t* seg_attr = nullptr;
   float* scratch[2] = {nullptr, nullptr};
+  // elastoplastic batches: the cached stress of every state buffer
+  // (StateView::tau, 6 floats per particle; written by G2P), when memory allows
+  bool tau_on = false;
+  float* tau_store = nullptr;
+  float* tau_scratch[2] = {nullptr, nullptr};
+  float* tau_seg = nullptr;
   uint32_t* scratch_attr[2] = {nullptr, nullptr};
   float* adj[2] = {nullptr, nullptr};  // [24][Ntot]
   float* part = nullptr;               // [12][Ntot]
@@ -185,21 +191,35 @@ StateView view(float* f, uint32_t* a, size_t stride) {
   return s;
 }
 
+size_t tau_floats(const DmContext* c) { return 6 * ((c->Ntot + kAB - 1) / kAB * kAB); }
+
 StateView store_view(DmContext* c, int k) {
-  return view(c->store + (size_t)k * state_floats(c), c->store_attr + (size_t)k * c->Ntot, c->Ntot);
+  StateView v = view(c->store + (size_t)k * state_floats(c), c->store_attr + (size_t)k * c->Ntot, c->Ntot);
+  if (c->tau_on) v.tau = c->tau_store + (size_t)k * tau_floats(c);
+  return v;
 }
 
 // State of global substep index s while running forward.
 StateView fwd_state(DmContext* c, int s) {
   if (s % c->ck == 0) return store_view(c, s / c->ck);
-  return view(c->scratch[s & 1], c->scratch_attr[s & 1], c->Ntot);
+  StateView v = view(c->scratch[s & 1], c->scratch_attr[s & 1], c->Ntot);
+  if (c->tau_on) v.tau = c->tau_scratch[s & 1];
+  return v;
 }
+
+// P2G of global substep s reads the cached stress unless s starts a control
+// step (set_state, resets and the in-tape cut write fresh particles there).
+// The rule does not depend on the checkpoint interval: checkpointed and
+// store-every-substep runs stay bit-identical.
+void set_tauv(DmContext* c, int s) { c->P.tauv = c->tau_on && s % c->cfg.substeps != 0; }
 
 // State of substep s inside the segment starting at s0 during backward.
 StateView seg_state(DmContext* c, int s0, int s) {
   if (s == s0) return store_view(c, s0 / c->ck);
   const int k = s - s0 - 1;
-  return view(c->seg + (size_t)k * state_floats(c), c->seg_attr + (size_t)k * c->Ntot, c->Ntot);
+  StateView v = view(c->seg + (size_t)k * state_floats(c), c->seg_attr + (size_t)k * c->Ntot, c->Ntot);
+  if (c->tau_on) v.tau = c->tau_seg + (size_t)k * tau_floats(c);
+  return v;
 }
 
 int maxc_of(int K) { return K <= 1 ? 1 : 4; }
@@ -688,6 +708,7 @@ int step_impl(DmContext* ctx, const float* cvo, const float* act, float* obs, cu
   for (int q = 0; q < S; ++q) {
     const int s = t * S + q;
     ctx->P.fiso = s > 0;  // every state but the initial one is a G2P output
+    set_tauv(ctx, s);
     if (keep)
       forward_substep(ctx, seg_state(ctx, t * S, s), q + 1 < S ? seg_state(ctx, t * S, s + 1) : fwd_state(ctx, s + 1),
                       t, s, q == 0, q, true, -1, true);
@@ -829,6 +850,7 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
       const int s = s0 + q;
       const StateView So = q + 1 < ck ? seg_state(ctx, s0, s + 1) : view(ctx->tail, ctx->tail_attr, ctx->Ntot);
       ctx->P.fiso = s > 0;
+      set_tauv(ctx, s);
       forward_substep(ctx, seg_state(ctx, s0, s), So, t, s, 0, q, true, rec_usable(ctx, s) ? s : -1);
     }
     if (!kept) {
@@ -1083,6 +1105,7 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   ok = ok && dalloc(ctx, &ctx->store, (size_t)ctx->n_store * state_floats(ctx)) &&
        dalloc(ctx, &ctx->store_attr, (size_t)ctx->n_store * N);
   if (ck > 1) ok = ok && dalloc(ctx, &ctx->seg, (size_t)(ck - 1) * state_floats(ctx)) && dalloc(ctx, &ctx->seg_attr, (size_t)(ck - 1) * N);
+
   if (ck > 1)
     for (int i = 0; i < 2; ++i)
       ok = ok && dalloc(ctx, &ctx->scratch[i], state_floats(ctx)) && dalloc(ctx, &ctx->scratch_attr[i], N);
@@ -1119,6 +1142,22 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   }
   if (!make_grid_tmap(&ctx->tm_gv, ctx->gv, P) || !make_grid_tmap(&ctx->tm_gmb, ctx->gmb, P))
     return fail("dm_create: TMA descriptor encoding failed (cuTensorMapEncodeTiled)");
+  if (ctx->law == kElastoplastic && !std::getenv("DIFFMPM_NO_TAU_CACHE")) {
+    // the stress cache (+25 % of the state memory), when it leaves room for the rest
+    const size_t want = ((size_t)ctx->n_store + (ck > 1 ? ck + 1 : 0)) * tau_floats(ctx) * sizeof(float);
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    if (want + (size_t)(8ull << 30) < free_b) {
+      bool r = dalloc(ctx, &ctx->tau_store, (size_t)ctx->n_store * tau_floats(ctx));
+      if (ck > 1)
+        r = r && dalloc(ctx, &ctx->tau_seg, (size_t)(ck - 1) * tau_floats(ctx)) &&
+            dalloc(ctx, &ctx->tau_scratch[0], tau_floats(ctx)) && dalloc(ctx, &ctx->tau_scratch[1], tau_floats(ctx));
+      ctx->tau_on = r;
+      if (!r)
+        for (float** q : {&ctx->tau_store, &ctx->tau_seg, &ctx->tau_scratch[0], &ctx->tau_scratch[1]})
+          if (*q) cudaFree(*q), *q = nullptr;
+    }
+  }
   cudaMemsetAsync(ctx->store_attr, 0, N * sizeof(uint32_t), ctx->stream);
   cudaMemsetAsync(ctx->tile_acc, 0, TT * kNacc * sizeof(float), ctx->stream);
   {
@@ -1168,7 +1207,8 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
 
 void dm_destroy(DmContext* ctx) {
   if (!ctx) return;
-  void* ptrs[] = {ctx->store,     ctx->store_attr, ctx->seg,       ctx->seg_attr,   ctx->scratch[0], ctx->scratch[1],
+  void* ptrs[] = {ctx->tau_store, ctx->tau_seg, ctx->tau_scratch[0], ctx->tau_scratch[1],
+                  ctx->store,     ctx->store_attr, ctx->seg,       ctx->seg_attr,   ctx->scratch[0], ctx->scratch[1],
                   ctx->scratch_attr[0], ctx->scratch_attr[1], ctx->adj[0], ctx->adj[1], ctx->part, ctx->keys,
                   ctx->perm_all,  ctx->ptile, ctx->tstart_all, ctx->tcount_all, ctx->abase_all, ctx->acount_all,
                   ctx->active_all, ctx->work_all, ctx->ord_all, ctx->nact_all, ctx->tail, ctx->tail_attr, ctx->gvb_pool, ctx->gmpb_pool,

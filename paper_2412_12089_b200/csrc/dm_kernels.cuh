@@ -58,6 +58,7 @@ struct DevParams {
   float alpha_c, mu_b;
   int K, G, nmat;
   int fiso;  // input state's F isotropic (fluid: every g2p output, F = J^(1/3) I)
+  int tauv;  // elastoplastic: the input state carries tau (S.tau), P2G skips the stress SVD
   Law<float> law[4];
   double dmu_dE[4], dlam_dE[4];  // Lame derivatives w.r.t. Young's modulus (fp64)
   ColShape shape[4];
@@ -102,11 +103,16 @@ __host__ __device__ __forceinline__ size_t part_index(int comp, size_t i, size_t
 #endif
 }
 
+// tau (elastoplastic batches, G2P outputs inside a segment): the Kirchhoff
+// stress P F^T of the state's F as the G2P projection computed it, 6
+// symmetric components, AoSoA [N/32][6][32]; nullptr elsewhere.
 struct StateView {
   float* f;
   uint32_t* attr;
   size_t stride;
+  float* tau = nullptr;
   __device__ __forceinline__ float& c(int comp, size_t i) const { return f[state_index(comp, i, stride)]; }
+  __device__ __forceinline__ float& t(int comp, size_t i) const { return tau[((i >> 5) * 6 + comp) * 32 + (i & 31)]; }
 };
 
 struct DevFlags {
@@ -889,9 +895,21 @@ struct PState {
   uint32_t at;
 };
 
+// tauv (elastoplastic, a G2P output inside a segment): the cached stress's 6
+// components go into F.a[0..5] instead of F (P2G needs F only for the stress).
 template <int LAW>
-__device__ __forceinline__ void load_pstate(const StateView& S, int src, PState& p, int fiso) {
-  load_state<LAW>(S, src, p.x, p.v, p.F, p.C, fiso);
+__device__ __forceinline__ void load_pstate(const StateView& S, int src, PState& p, int fiso, int tauv = 0) {
+  if (LAW == kElastoplastic && tauv) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) p.x[a] = S.c(a, src);
+    p.v = mk3(S.c(3, src), S.c(4, src), S.c(5, src));
+#pragma unroll
+    for (int q = 0; q < 6; ++q) p.F.a[q] = S.t(q, src);
+#pragma unroll
+    for (int q = 0; q < 9; ++q) p.C.a[q] = S.c(15 + q, src);
+  } else {
+    load_state<LAW>(S, src, p.x, p.v, p.F, p.C, fiso);
+  }
   p.at = S.attr[src];
 }
 
@@ -1024,7 +1042,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, S
     // perm indices two chunks ahead in two parity slots (no register moves
     // between chunks, so a refill never waits on the load it replaces)
     PState ps;
-    if (lane < cnt) load_pstate<LAW>(S, pidx(lane), ps, P.fiso);
+    if (lane < cnt) load_pstate<LAW>(S, pidx(lane), ps, P.fiso, P.tauv);
     int s1 = 32 + lane < cnt ? pidx(32 + lane) : 0;
     int s0 = 64 + lane < cnt ? pidx(64 + lane) : 0;
     scatter_zero(bw, lane);
@@ -1042,7 +1060,8 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, S
         // the zeros vanish exactly)
         const m3<float> A = (LAW == kFluid && P.fiso)
                                 ? p2g_affine(L, T, mdiag(ps.F.a[0], ps.F.a[0], ps.F.a[0]), ps.C, av, &bad)
-                                : p2g_affine(L, T, ps.F, ps.C, av, &bad);
+                            : (LAW == kElastoplastic && P.tauv) ? p2g_affine_tau(L, T, sym6(ps.F.a), ps.C)
+                                                                : p2g_affine(L, T, ps.F, ps.C, av, &bad);
         if (bad) report(flags, e, substep, 0, attr_index(ps.at), attr_mat(ps.at), kErrDetF);
         v3<float> q;
         m3<float> Ad;
@@ -1053,7 +1072,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, S
       }
       __syncwarp();
       // software pipeline: issue the next chunk's loads before this chunk's scatter
-      if (c0 + 32 + lane < cnt) load_pstate<LAW>(S, s_next, ps, P.fiso);
+      if (c0 + 32 + lane < cnt) load_pstate<LAW>(S, s_next, ps, P.fiso, P.tauv);
       const int s_new = c0 + 96 + lane < cnt ? pidx(c0 + 96 + lane) : 0;
       scatter_runs<true>(bw, pw, min(32, cnt - c0), lane, ra);
       return s_new;
@@ -1328,10 +1347,20 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
       v3<float> xn = mk3(x[0], x[1], x[2]), v;
       m3<float> C;
       bool bad_adv = false, bad_det = false;
-      g2p_particle_sep(law_of<LAW>(P, attr_mat(at)), T, sc, getv, xn, v, C, F, &bad_adv, &bad_det, vr);
+      m3<float> tau;
+      g2p_particle_sep(law_of<LAW>(P, attr_mat(at)), T, sc, getv, xn, v, C, F, &bad_adv, &bad_det, vr,
+                       LAW == kElastoplastic && Sout.tau ? &tau : nullptr);
       if (bad_adv) report(flags, e, substep, 1, attr_index(at), 0, kErrG2PInterior);
       if (bad_det) report(flags, e, substep, 1, attr_index(at), attr_mat(at), kErrDetF);
       store_state<LAW>(Sout, dst, xn, v, F, C);
+      if (LAW == kElastoplastic && Sout.tau) {  // the next P2G's stress (SURVEY 8 "stress source")
+        Sout.t(0, dst) = tau.a[0];
+        Sout.t(1, dst) = tau.a[1];
+        Sout.t(2, dst) = tau.a[2];
+        Sout.t(3, dst) = tau.a[4];
+        Sout.t(4, dst) = tau.a[5];
+        Sout.t(5, dst) = tau.a[8];
+      }
       Sout.attr[dst] = at;
     };
     for (int c0 = 0; c0 < cnt; c0 += 64) {

@@ -303,6 +303,31 @@ DM_HD m3<R> usv(const Svd<R>& sv, R d0, R d1, R d2) {
       o(r, c) = sv.u(r, 0) * d0 * sv.v(c, 0) + sv.u(r, 1) * d1 * sv.v(c, 1) + sv.u(r, 2) * d2 * sv.v(c, 2);
   return o;
 }
+// U diag(d) U^T (symmetric; the 6 upper entries computed, mirrored)
+template <class R>
+DM_HD m3<R> udut(const m3<R>& u, R d0, R d1, R d2) {
+  m3<R> o;
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = r; c < 3; ++c) {
+      o(r, c) = u(r, 0) * d0 * u(c, 0) + u(r, 1) * d1 * u(c, 1) + u(r, 2) * d2 * u(c, 2);
+      o(c, r) = o(r, c);
+    }
+  return o;
+}
+// the symmetric matrix of 6 stored components (xx, xy, xz, yy, yz, zz)
+template <class R>
+DM_HD m3<R> sym6(const R* t) {
+  m3<R> o;
+  o(0, 0) = t[0];
+  o(0, 1) = o(1, 0) = t[1];
+  o(0, 2) = o(2, 0) = t[2];
+  o(1, 1) = t[3];
+  o(1, 2) = o(2, 1) = t[4];
+  o(2, 2) = t[5];
+  return o;
+}
 // U M V^T
 template <class R>
 DM_HD m3<R> u_m_vt(const Svd<R>& sv, const m3<R>& m) {

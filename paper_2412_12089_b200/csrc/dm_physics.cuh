@@ -321,11 +321,20 @@ DM_HD m3<R> law_stress_fwd(const Law<R>& L, const m3<R>& D, R act, bool* bad) {
 }
 
 // G2P projection (mpm.hpp:341-344) in deviation form: D' = proj(I + Dn) - I.
+// tau (elastoplastic): also the Kirchhoff stress P F'^T of the projected F'
+// = U diag(2 mu epsp + lam tr epsp) U^T -- the value the next P2G's
+// stress_elastoplastic(F') has (F' is on or inside the yield surface, so its
+// own return mapping is the identity), from this SVD instead of a new one.
 template <class R>
-DM_HD m3<R> law_project_fwd(const Law<R>& L, const m3<R>& Dn, bool* bad) {
+DM_HD m3<R> law_project_fwd(const Law<R>& L, const m3<R>& Dn, bool* bad, m3<R>* tau = nullptr) {
   if (L.kind == kElastoplastic) {
     if (!(det1m(Dn) > R(-1))) *bad = true;
     const Hencky<R> h = hencky_dev(svd3_dev(Dn), L.cy);
+    if (tau) {
+      const R tr = h.epsp[0] + h.epsp[1] + h.epsp[2];
+      *tau = udut(h.sv.u, R(2) * L.mu * h.epsp[0] + L.lam * tr, R(2) * L.mu * h.epsp[1] + L.lam * tr,
+                  R(2) * L.mu * h.epsp[2] + L.lam * tr);
+    }
     if (!h.yield) return Dn;
     // D' = U diag(sigma_p - 1) V^T + (U V^T - I)  (yielding: |strain| > c_y, no cancellation issue)
     m3<R> Dp = usv(h.sv, h.sigp[0] - R(1), h.sigp[1] - R(1), h.sigp[2] - R(1)) + mul_bt(h.sv.u, h.sv.v);

@@ -105,6 +105,14 @@ DM_HD m3<R> p2g_affine(const Law<R>& L, const TransferCtx<R>& t, const m3<R>& D,
   return tau * kA + C * L.mass;
 }
 
+// p2g_affine from a cached Kirchhoff stress tau = P F^T (elastoplastic: the
+// G2P projection's value, no viscosity term).
+template <class R>
+DM_HD m3<R> p2g_affine_tau(const Law<R>& L, const TransferCtx<R>& t, const m3<R>& tau, const m3<R>& C) {
+  const R kA = -t.dt * L.vol * R(4) * t.inv_dx * t.inv_dx;
+  return tau * kA + C * L.mass;
+}
+
 template <class R>
 DM_HD void p2g_payload(const m3<R>& A, R mass, v3<R> v, const Stencil<R>& s, R dx, v3<R>& q, m3<R>& Ad) {
   const v3<R> f = mk3(s.fx[0] * dx, s.fx[1] * dx, s.fx[2] * dx);
@@ -316,7 +324,8 @@ DM_HD void g2p_gather_sep(const Stencil<R>& s, R dx, GetV getv, v3<R>& vnew, m3<
 // node velocities relative to vref (node_update_rel); v' = vref + gather.
 template <class R, class GetV>
 DM_HD void g2p_particle_sep(const Law<R>& L, const TransferCtx<R>& t, const Stencil<R>& s, GetV getv, v3<R>& x,
-                            v3<R>& v, m3<R>& C, m3<R>& D, bool* bad_adv, bool* bad_det, v3<R> vref) {
+                            v3<R>& v, m3<R>& C, m3<R>& D, bool* bad_adv, bool* bad_det, v3<R> vref,
+                            m3<R>* tau = nullptr) {
   m3<R> B;
   g2p_gather_sep(s, t.dx, getv, v, B);
   v = vref + v;
@@ -330,7 +339,7 @@ DM_HD void g2p_particle_sep(const Law<R>& L, const TransferCtx<R>& t, const Sten
     if (!(gx >= R(1.5) && gx <= R(t.dims[a]) - R(2.5))) *bad_adv = true;  // NaN-safe
   }
   const m3<R> Dn = D + (C + C * D) * t.dt;
-  D = law_project_fwd(L, Dn, bad_det);
+  D = law_project_fwd(L, Dn, bad_det, tau);
 }
 
 // d/dfx of sum_n w_n h_n for a per-node scalar h_n, accumulated separably.
