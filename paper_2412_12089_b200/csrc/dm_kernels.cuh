@@ -75,6 +75,23 @@ struct DevParams {
 #define DM_AOSOA_LOG2 5  // particles per block = 32
 #endif
 constexpr size_t kAB = (size_t)1 << DM_AOSOA_LOG2;
+
+// Bounds checks of the debug build (tools/bounds_check.sh: -DDM_DEBUG_BOUNDS,
+// the GPU suite against it; compute-sanitizer is not available on the pool):
+// a failed check prints the condition and traps, so the test fails loudly.
+#ifdef DM_DEBUG_BOUNDS
+#define DM_CHECK(cond)                                                          \
+  do {                                                                          \
+    if (!(cond)) {                                                              \
+      printf("DM_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond);        \
+      __trap();                                                                 \
+    }                                                                           \
+  } while (0)
+#else
+#define DM_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
 __host__ __device__ __forceinline__ size_t state_index(int comp, size_t i, size_t stride) {
 #if DM_AOSOA
   (void)stride;
@@ -111,8 +128,14 @@ struct StateView {
   uint32_t* attr;
   size_t stride;
   float* tau = nullptr;
-  __device__ __forceinline__ float& c(int comp, size_t i) const { return f[state_index(comp, i, stride)]; }
-  __device__ __forceinline__ float& t(int comp, size_t i) const { return tau[((i >> 5) * 6 + comp) * 32 + (i & 31)]; }
+  __device__ __forceinline__ float& c(int comp, size_t i) const {
+    DM_CHECK(i < stride && comp >= 0 && comp < 24);
+    return f[state_index(comp, i, stride)];
+  }
+  __device__ __forceinline__ float& t(int comp, size_t i) const {
+    DM_CHECK(tau != nullptr && i < stride && comp >= 0 && comp < 6);
+    return tau[((i >> 5) * 6 + comp) * 32 + (i & 31)];
+  }
 };
 
 struct DevFlags {
@@ -629,6 +652,7 @@ __device__ __forceinline__ void run_reset(RunAcc& ra) {
 // Adds the lane's three run sums (nodes (i, j, 0..2) of the run's base) into
 // its group's block copy.
 __device__ __forceinline__ void run_flush(float4* __restrict__ blk, RunAcc& ra, int off) {
+  DM_CHECK(ra.cur >= 0 && ra.cur + off + 2 < kExt3);
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     float4 b = blk[ra.cur + off + k];
@@ -1036,7 +1060,12 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, S
     const int o[3] = {tx * kTile, ty * kTile, tz * kTile};
     const size_t tix = (size_t)e * P.Tn + t;
     const int* prow = perm + (size_t)e * P.N + start;
-    auto pidx = [&](int v) { return prow[coop_idx<COOP>(v, warp)]; };
+    auto pidx = [&](int v) {
+      DM_CHECK(coop_idx<COOP>(v, warp) < cur.w);
+      const int r = prow[coop_idx<COOP>(v, warp)];
+      DM_CHECK(r >= 0 && (size_t)r < (size_t)P.E * P.N);
+      return r;
+    };
     const float4 vr4 = vref[e];
     const v3<float> vr = mk3(vr4.x, vr4.y, vr4.z);  // momentum relative to the env's reference velocity
     // perm indices two chunks ahead in two parity slots (no register moves
@@ -1217,6 +1246,8 @@ __device__ __forceinline__ float4 sum_blocks(const NodeMasks& nm, const float4* 
 }
 
 __device__ __forceinline__ size_t node_lin(const DevParams& P, int e, const int g[3]) {
+  DM_CHECK(e >= 0 && e < P.E && g[0] >= 0 && g[0] < P.dims[0] && g[1] >= 0 && g[1] < P.dims[1] && g[2] >= 0 &&
+           g[2] < P.dims[2]);
   return (size_t)e * P.dims[0] * P.dims[1] * P.dims[2] + ((size_t)g[0] * P.dims[1] + g[1]) * P.dims[2] + g[2];
 }
 
@@ -1315,7 +1346,12 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
     const size_t row = (size_t)e * P.N + start;
-    auto pidx = [&](int v) { return perm[row + coop_idx<COOP>(v, warp)]; };
+    auto pidx = [&](int v) {
+      DM_CHECK(coop_idx<COOP>(v, warp) < cur.w);
+      const int r = perm[row + coop_idx<COOP>(v, warp)];
+      DM_CHECK(r >= 0 && (size_t)r < (size_t)P.E * P.N);
+      return r;
+    };
     const float4 vr4 = vref[e];
     const v3<float> vr = mk3(vr4.x, vr4.y, vr4.z);
     // two particle-state buffers (chunks alternate) and perm indices two
@@ -1466,7 +1502,12 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
     }
     const size_t tix = (size_t)e * P.Tn + t;
     const size_t row = (size_t)e * P.N + start;
-    auto pidx = [&](int v) { return perm[row + coop_idx<COOP>(v, warp)]; };
+    auto pidx = [&](int v) {
+      DM_CHECK(coop_idx<COOP>(v, warp) < cur.w);
+      const int r = perm[row + coop_idx<COOP>(v, warp)];
+      DM_CHECK(r >= 0 && (size_t)r < (size_t)P.E * P.N);
+      return r;
+    };
     const float4 vr4 = vref[e];
     float x[3];
     m3<float> F;
@@ -1709,7 +1750,12 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
     const size_t tix = (size_t)e * P.Tn + t;
     const size_t row = (size_t)e * P.N + start;
-    auto pidx = [&](int v) { return perm[row + coop_idx<COOP>(v, warp)]; };
+    auto pidx = [&](int v) {
+      DM_CHECK(coop_idx<COOP>(v, warp) < cur.w);
+      const int r = perm[row + coop_idx<COOP>(v, warp)];
+      DM_CHECK(r >= 0 && (size_t)r < (size_t)P.E * P.N);
+      return r;
+    };
     double mub[NM], lab[NM];  // fp64: cancelling sums (NM = materials)
 #pragma unroll
     for (int m = 0; m < NM; ++m) mub[m] = lab[m] = 0.0;
