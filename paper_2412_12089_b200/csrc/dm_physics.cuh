@@ -671,7 +671,7 @@ DM_HD v3<R> cyl_query_vjp(const CylQ<R>& c, R dbar, v3<R> nbar) {
 // CK >= 0 fixes the collider kind at compile time (the switch folds: small
 // code for single-kind batches); CK = -1 dispatches on col.kind.
 template <class R, int CK = -1>
-DM_HD_NOINLINE void collider_query_r(const Col<R>& col, v3<R> rel, R& d, v3<R>& n) {
+DM_HD void collider_query_body(const Col<R>& col, v3<R> rel, R& d, v3<R>& n) {
   switch (CK >= 0 ? CK : col.kind) {
     case kPlane:
       d = dot(rel, col.nrm);
@@ -711,6 +711,14 @@ DM_HD_NOINLINE void collider_query_r(const Col<R>& col, v3<R> rel, R& d, v3<R>& 
       return;
     }
   }
+}
+
+// Out-of-line query (small code where several call sites or kinds meet:
+// the adjoint kernels are instruction-cache bound); the forward node update
+// with a compile-time kind inlines collider_query_body instead.
+template <class R, int CK = -1>
+DM_HD_NOINLINE void collider_query_r(const Col<R>& col, v3<R> rel, R& d, v3<R>& n) {
+  collider_query_body<R, CK>(col, rel, d, n);
 }
 
 template <class R, int CK = -1>
@@ -1057,7 +1065,10 @@ template <class R, int CK = -1>
 DM_HD v3<R> collide_delta(const Col<R>& col, R alpha_c, R mu_b, v3<R> node, v3<R> rel_c, v3<R> vref, v3<R> dv) {
   R d;
   v3<R> n;
-  collider_query_r<R, CK>(col, rel_c, d, n);
+  if constexpr (CK >= 0)
+    collider_query_body<R, CK>(col, rel_c, d, n);
+  else
+    collider_query_r<R, CK>(col, rel_c, d, n);
   const R s = d < R(0) ? R(1) : r_exp(-alpha_c * r_max(d, R(0)));
   const v3<R> vcol = col.vel + cross(col.om, node - col.c);
   const v3<R> rel = (vref - vcol) + dv;
