@@ -1330,6 +1330,9 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
                                                      int dump_cap, const float4* __restrict__ vref) {
   __shared__ __align__(128) float4 vg[kWarps][2][kExt3];
   __shared__ uint64_t vbar[kWarps][2];  // TMA completion of vg[w][b]
+  // fluid, isotropic F: a ring of 3 chunk slots per warp (x, F word, attr:
+  // 5 x 32 words each) filled by cp.async two chunks ahead
+  __shared__ float gst[LAW == kFluid ? kWarps : 1][3][5 * 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) {
     mbar_init(&vbar[warp][0]);
@@ -1354,22 +1357,12 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
     };
     const float4 vr4 = vref[e];
     const v3<float> vr = mk3(vr4.x, vr4.y, vr4.z);
-    // two particle-state buffers (chunks alternate) and perm indices two
-    // chunks ahead in parity slots: no register moves between chunks
-    float xa[3], xb[3];
-    m3<float> Fa, Fb;
-    uint32_t ata = 0, atb = 0;
-    if (lane < cnt) {
-      const int src = pidx(lane);
-      load_xF<LAW>(S, src, xa, Fa, P.fiso);
-      ata = S.attr[src];
-    }
-    int s1 = lane + 32 < cnt ? pidx(lane + 32) : 0;
-    int s0 = lane + 64 < cnt ? pidx(lane + 64) : 0;
-    if (out_gv && a < dump_cap && (!COOP || warp == 0)) {  // segment replay: keep the tile's grid for the adjoint
-      if (lane == 0) bulk_s2g(out_gv + (size_t)a * kExt3, vw, kExt3 * (uint32_t)sizeof(float4));
-      load_tile_grid(P, gmp, e, o, out_gmp + (size_t)a * kExt3, lane);
-    }
+    auto dump = [&]() __attribute__((always_inline)) {
+      if (out_gv && a < dump_cap && (!COOP || warp == 0)) {  // segment replay: keep the tile's grid for the adjoint
+        if (lane == 0) bulk_s2g(out_gv + (size_t)a * kExt3, vw, kExt3 * (uint32_t)sizeof(float4));
+        load_tile_grid(P, gmp, e, o, out_gmp + (size_t)a * kExt3, lane);
+      }
+    };
     auto body = [&](int c0, const float x[3], m3<float> F, uint32_t at) {
       if (c0 + lane >= cnt) return;
       const size_t dst = row + coop_idx<COOP>(c0 + lane, warp);
@@ -1399,6 +1392,57 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
       }
       Sout.attr[dst] = at;
     };
+    if (LAW == kFluid && P.fiso) {
+      // staged: chunk k + 2's loads are issued (perm index one chunk earlier)
+      // before chunk k computes -- no state registers held for the prefetch
+      float* ring = &gst[LAW == kFluid ? warp : 0][0][0];
+      auto issue = [&](int c0, int src, int slot) __attribute__((always_inline)) {
+        if (c0 + lane < cnt) {
+          float* d = ring + slot * 160 + lane;
+          cp_async4(d, &S.c(0, src));
+          cp_async4(d + 32, &S.c(1, src));
+          cp_async4(d + 64, &S.c(2, src));
+          cp_async4(d + 96, &S.c(6, src));
+          cp_async4(d + 128, S.attr + src);
+        }
+        cp_async_commit();
+      };
+      const int p0 = lane < cnt ? pidx(lane) : 0;
+      const int p1 = 32 + lane < cnt ? pidx(32 + lane) : 0;
+      int p2 = 64 + lane < cnt ? pidx(64 + lane) : 0;
+      issue(0, p0, 0);
+      issue(32, p1, 1);
+      dump();
+      for (int c0 = 0, slot = 0, nslot = 2; c0 < cnt; c0 += 32) {
+        issue(c0 + 64, p2, nslot);
+        p2 = c0 + 96 + lane < cnt ? pidx(c0 + 96 + lane) : 0;
+        cp_async_wait<2>();  // chunk c0 has landed
+        __syncwarp();
+        const float* sl = ring + slot * 160 + lane;
+        const float x[3] = {sl[0], sl[32], sl[64]};
+        const float f0 = sl[96];
+        body(c0, x, mdiag(f0, f0, f0), __float_as_uint(sl[128]));
+        __syncwarp();  // slot is refilled two chunks later
+        slot = slot == 2 ? 0 : slot + 1;
+        nslot = nslot == 2 ? 0 : nslot + 1;
+      }
+      cp_async_wait<0>();
+      __syncwarp();  // every lane is done with vw before it is refilled
+      return;
+    }
+    // two particle-state buffers (chunks alternate) and perm indices two
+    // chunks ahead in parity slots: no register moves between chunks
+    float xa[3], xb[3];
+    m3<float> Fa, Fb;
+    uint32_t ata = 0, atb = 0;
+    if (lane < cnt) {
+      const int src = pidx(lane);
+      load_xF<LAW>(S, src, xa, Fa, P.fiso);
+      ata = S.attr[src];
+    }
+    int s1 = lane + 32 < cnt ? pidx(lane + 32) : 0;
+    int s0 = lane + 64 < cnt ? pidx(lane + 64) : 0;
+    dump();
     for (int c0 = 0; c0 < cnt; c0 += 64) {
       if (c0 + 32 + lane < cnt) {  // chunk c0 + 32 -> buffer b
         load_xF<LAW>(S, s1, xb, Fb, P.fiso);
