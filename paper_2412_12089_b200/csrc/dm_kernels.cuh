@@ -1320,6 +1320,10 @@ __device__ __forceinline__ void load_tile_grid(const DevParams& P, const float4*
 // Tile grids are double-buffered in shared memory with cp.async (the next
 // tile's 6^3 velocity block streams in while the current tile computes) and
 // the next chunk's particle loads are issued before the current chunk's math.
+#ifndef DM_G2P_RING
+#define DM_G2P_RING 3
+#endif
+constexpr int kG2pRing = DM_G2P_RING;  // 3: k_g2p -7 % vs registers one chunk ahead; 4: same at 1,024 envs, +3 % at 128
 template <int LAW, bool COOP>
 __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams P, StateView S, StateView Sout,
                                                      const int* __restrict__ perm, const int* __restrict__ tile_start,
@@ -1330,9 +1334,9 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
                                                      int dump_cap, const float4* __restrict__ vref) {
   __shared__ __align__(128) float4 vg[kWarps][2][kExt3];
   __shared__ uint64_t vbar[kWarps][2];  // TMA completion of vg[w][b]
-  // fluid, isotropic F: a ring of 3 chunk slots per warp (x, F word, attr:
-  // 5 x 32 words each) filled by cp.async two chunks ahead
-  __shared__ float gst[LAW == kFluid ? kWarps : 1][3][5 * 32];
+  // fluid, isotropic F: a ring of kG2pRing chunk slots per warp (x, F word,
+  // attr: 5 x 32 words each) filled by cp.async kG2pRing - 1 chunks ahead
+  __shared__ float gst[LAW == kFluid ? kWarps : 1][kG2pRing][5 * 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) {
     mbar_init(&vbar[warp][0]);
@@ -1393,8 +1397,8 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
       Sout.attr[dst] = at;
     };
     if (LAW == kFluid && P.fiso) {
-      // staged: chunk k + 2's loads are issued (perm index one chunk earlier)
-      // before chunk k computes -- no state registers held for the prefetch
+      // staged: chunk k + kG2pRing - 1's loads are issued (perm index one
+      // chunk earlier) before chunk k computes -- no state registers held
       float* ring = &gst[LAW == kFluid ? warp : 0][0][0];
       auto issue = [&](int c0, int src, int slot) __attribute__((always_inline)) {
         if (c0 + lane < cnt) {
@@ -1407,24 +1411,22 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
         }
         cp_async_commit();
       };
-      const int p0 = lane < cnt ? pidx(lane) : 0;
-      const int p1 = 32 + lane < cnt ? pidx(32 + lane) : 0;
-      int p2 = 64 + lane < cnt ? pidx(64 + lane) : 0;
-      issue(0, p0, 0);
-      issue(32, p1, 1);
+#pragma unroll
+      for (int r = 0; r < kG2pRing - 1; ++r) issue(32 * r, 32 * r + lane < cnt ? pidx(32 * r + lane) : 0, r);
+      int pn = 32 * (kG2pRing - 1) + lane < cnt ? pidx(32 * (kG2pRing - 1) + lane) : 0;
       dump();
-      for (int c0 = 0, slot = 0, nslot = 2; c0 < cnt; c0 += 32) {
-        issue(c0 + 64, p2, nslot);
-        p2 = c0 + 96 + lane < cnt ? pidx(c0 + 96 + lane) : 0;
-        cp_async_wait<2>();  // chunk c0 has landed
+      for (int c0 = 0, slot = 0, nslot = kG2pRing - 1; c0 < cnt; c0 += 32) {
+        issue(c0 + 32 * (kG2pRing - 1), pn, nslot);
+        pn = c0 + 32 * kG2pRing + lane < cnt ? pidx(c0 + 32 * kG2pRing + lane) : 0;
+        cp_async_wait<kG2pRing - 1>();  // chunk c0 has landed
         __syncwarp();
         const float* sl = ring + slot * 160 + lane;
         const float x[3] = {sl[0], sl[32], sl[64]};
         const float f0 = sl[96];
         body(c0, x, mdiag(f0, f0, f0), __float_as_uint(sl[128]));
-        __syncwarp();  // slot is refilled two chunks later
-        slot = slot == 2 ? 0 : slot + 1;
-        nslot = nslot == 2 ? 0 : nslot + 1;
+        __syncwarp();  // slot is refilled kG2pRing - 1 chunks later
+        slot = slot == kG2pRing - 1 ? 0 : slot + 1;
+        nslot = nslot == kG2pRing - 1 ? 0 : nslot + 1;
       }
       cp_async_wait<0>();
       __syncwarp();  // every lane is done with vw before it is refilled
