@@ -437,11 +437,14 @@ bool rec_usable(const DmContext* c, int s) {
 // which saves its binning into the record of substep sub.
 void forward_substep(DmContext* c, const StateView& S, const StateView& So, int t, int sub, int check_vmax, int qi,
                      bool dump, int rec_s = -1, bool record = false) {
-  const Slot q = rec_s >= 0 ? rec_slot(c, qi, rec_s) : slot(c, qi);
+  Slot q = rec_s >= 0 ? rec_slot(c, qi, rec_s) : slot(c, qi);
+  // the forward pass sorts straight into the record's permutation (always
+  // complete: N entries); k_rec_save copies the rest of the binning
+  if (record && c->rec.perm) q.perm = rec_at(c, sub).perm;
   if (rec_s < 0) launch_bin(c, S, q, sub, check_vmax);
   if (record && c->rec.perm) {
     const size_t TT = (size_t)c->P.E * c->P.Tn;
-    k_rec_save<<<c->grid_tiles, 256, 0, c->stream>>>(c->Ntot, TT, c->P.E, c->rec_cap, q.perm, q.tile_count, q.active,
+    k_rec_save<<<c->grid_tiles, 256, 0, c->stream>>>(c->Ntot, TT, c->P.E, c->rec_cap, nullptr, q.tile_count, q.active,
                                                      q.work, q.env_abase, q.env_acount, q.nact, q.vref, rec_at(c, sub));
     ++c->launches;
   }
@@ -475,8 +478,9 @@ void launch_g2p_adj_k(DmContext* c, const StateView& S, const StateView& Sn, con
 
 // Adjoint of one substep from the replay's stored artifacts (slot qi).
 void backward_substep(DmContext* c, const StateView& S, const StateView& Sn, int t, int qi, const float* adj_in,
-                      float* adj_out, int rec_s = -1) {
-  const Slot q = rec_s >= 0 ? rec_slot(c, qi, rec_s) : slot(c, qi);
+                      float* adj_out, int rec_s = -1, int perm_s = -1) {
+  Slot q = rec_s >= 0 ? rec_slot(c, qi, rec_s) : slot(c, qi);
+  if (perm_s >= 0) q.perm = rec_at(c, perm_s).perm;  // a kept segment: the forward sorted into the record
   wq_reset(c);
   PROF_BEGIN(c, 3);
 #define L_G2PA(LW)                                                                                            \
@@ -892,7 +896,7 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
                               : view(ctx->tail, ctx->tail_attr, ctx->Ntot);
       ctx->P.fiso = s > 0;
       backward_substep(ctx, seg_state(ctx, s0, s), Sn, t, q, ctx->adj[cur], ctx->adj[cur ^ 1],
-                       !kept && rec_usable(ctx, s) ? s : -1);
+                       !kept && rec_usable(ctx, s) ? s : -1, kept && ctx->rec.perm ? s : -1);
       cur ^= 1;
     }
   }
