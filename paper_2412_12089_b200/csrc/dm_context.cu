@@ -438,13 +438,18 @@ bool rec_usable(const DmContext* c, int s) {
 void forward_substep(DmContext* c, const StateView& S, const StateView& So, int t, int sub, int check_vmax, int qi,
                      bool dump, int rec_s = -1, bool record = false) {
   Slot q = rec_s >= 0 ? rec_slot(c, qi, rec_s) : slot(c, qi);
-  // the forward pass sorts straight into the record's permutation (always
-  // complete: N entries); k_rec_save copies the rest of the binning
-  if (record && c->rec.perm) q.perm = rec_at(c, sub).perm;
+  // the forward pass sorts straight into the record's permutation and tile
+  // counts (always complete: N and E x Tn entries); k_rec_save copies the
+  // capacity-limited rest of the binning
+  if (record && c->rec.perm) {
+    const SortRec r = rec_at(c, sub);
+    q.perm = r.perm;
+    q.tile_count = r.tile_count;
+  }
   if (rec_s < 0) launch_bin(c, S, q, sub, check_vmax);
   if (record && c->rec.perm) {
     const size_t TT = (size_t)c->P.E * c->P.Tn;
-    k_rec_save<<<c->grid_tiles, 256, 0, c->stream>>>(c->Ntot, TT, c->P.E, c->rec_cap, nullptr, q.tile_count, q.active,
+    k_rec_save<<<c->grid_tiles, 256, 0, c->stream>>>(c->Ntot, TT, c->P.E, c->rec_cap, nullptr, nullptr, q.active,
                                                      q.work, q.env_abase, q.env_acount, q.nact, q.vref, rec_at(c, sub));
     ++c->launches;
   }
@@ -480,7 +485,10 @@ void launch_g2p_adj_k(DmContext* c, const StateView& S, const StateView& Sn, con
 void backward_substep(DmContext* c, const StateView& S, const StateView& Sn, int t, int qi, const float* adj_in,
                       float* adj_out, int rec_s = -1, int perm_s = -1) {
   Slot q = rec_s >= 0 ? rec_slot(c, qi, rec_s) : slot(c, qi);
-  if (perm_s >= 0) q.perm = rec_at(c, perm_s).perm;  // a kept segment: the forward sorted into the record
+  if (perm_s >= 0) {  // a kept segment: the forward sorted into the record
+    q.perm = rec_at(c, perm_s).perm;
+    q.tile_count = rec_at(c, perm_s).tile_count;
+  }
   wq_reset(c);
   PROF_BEGIN(c, 3);
 #define L_G2PA(LW)                                                                                            \

@@ -2549,7 +2549,8 @@ __global__ void k_rec_save(size_t Ntot, size_t TT, int E, int cap, const int* __
   }
   if (perm)  // nullptr: the sort wrote the record's permutation itself
     for (size_t i = i0; i < Ntot; i += stride) r.perm[i] = perm[i];
-  for (size_t i = i0; i < TT; i += stride) r.tile_count[i] = tile_count[i];
+  if (tile_count)
+    for (size_t i = i0; i < TT; i += stride) r.tile_count[i] = tile_count[i];
   if (fits)
     for (size_t i = i0; i < (size_t)n; i += stride) {
       r.active[i] = active[i];
