@@ -40,7 +40,8 @@ struct DmContext {
   int n_store = 0;
   unsigned long long launches = 0, bytes = 0;
   int grid_tiles = 148 * 4;
-  bool coop = false;  // CTA-cooperative tiles (small batches; see coop_idx)
+  bool coop = false;      // CTA-cooperative tiles in g2p / g2p_adj (small batches; see coop_idx)
+  bool coop_p2g = false;  // ... in p2g / p2g_adj (pays up to larger batches)
   bool grid_coop = false;  // CTA-shared tiles in the grid kernels (tiny batches)
   CUtensorMap tm_gv, tm_gmb;  // TMA descriptors of the dense node-velocity / (mass, momentum)-cotangent grids
 
@@ -334,7 +335,7 @@ void launch_p2g(DmContext* c, const StateView& S, const Slot& q, int t, int sub)
   wq_reset(c);
   PROF_BEGIN(c, 1);
 #define L_P2G(LW)                                                                                               \
-  if (c->coop) k_p2g<LW, true><<<c->grid_tiles, kWarps * 32, kP2gSmem, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.work, \
+  if (c->coop_p2g) k_p2g<LW, true><<<c->grid_tiles, kWarps * 32, kP2gSmem, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.work, \
                                                           step_act(c, t), c->blocks, c->flags, q.nact, sub, c->wq, q.vref); \
   else k_p2g<LW, false><<<c->grid_tiles, kWarps * 32, kP2gSmem, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.work, \
                                                           step_act(c, t), c->blocks, c->flags, q.nact, sub, c->wq, q.vref)
@@ -469,9 +470,9 @@ template <int LAW, int NG>
 void launch_p2g_adj(DmContext* c, const StateView& S, const Slot& q, int t, float* adj_out) {
   wq_reset(c);
   if (c->P.nmat == 1)
-    c->coop ? launch_p2g_adj_k<LAW, NG, 1, true>(c, S, q, t, adj_out) : launch_p2g_adj_k<LAW, NG, 1, false>(c, S, q, t, adj_out);
+    c->coop_p2g ? launch_p2g_adj_k<LAW, NG, 1, true>(c, S, q, t, adj_out) : launch_p2g_adj_k<LAW, NG, 1, false>(c, S, q, t, adj_out);
   else
-    c->coop ? launch_p2g_adj_k<LAW, NG, 4, true>(c, S, q, t, adj_out) : launch_p2g_adj_k<LAW, NG, 4, false>(c, S, q, t, adj_out);
+    c->coop_p2g ? launch_p2g_adj_k<LAW, NG, 4, true>(c, S, q, t, adj_out) : launch_p2g_adj_k<LAW, NG, 4, false>(c, S, q, t, adj_out);
 }
 
 template <int LAW, int NM, bool COOP>
@@ -1207,7 +1208,8 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   // CTA-cooperative tiles when the batch gives each resident warp only a few
   // chunks (DIFFMPM_COOP=0/1 forces the mode)
   ctx->coop = N < (size_t)kCoopParticlesPerWarp * ctx->grid_tiles * kWarps;
-  if (const char* f = std::getenv("DIFFMPM_COOP")) ctx->coop = f[0] == '1';
+  ctx->coop_p2g = N < (size_t)kCoopP2gParticlesPerWarp * ctx->grid_tiles * kWarps;
+  if (const char* f = std::getenv("DIFFMPM_COOP")) ctx->coop = ctx->coop_p2g = f[0] == '1';
   // the grid kernels' tiles are short (owned nodes): sharing them pays only
   // when there are fewer tiles than warps (r02 A/B: cfg1 grid -25 %, grid_adj
   // -32 %; neutral at 32 envs; +5 / +11 % at 128 envs)
