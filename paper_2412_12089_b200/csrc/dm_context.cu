@@ -319,8 +319,13 @@ void launch_bin(DmContext* c, const StateView& S, const Slot& q, int sub, int ch
   k_order_scatter<<<(unsigned)((c->P.E * c->P.Tn + 2047) / 2048), 256, 0, c->stream>>>(q.active, q.nact, q.ord, q.work);
   c->launches += 2;
   wq_reset(c);
-  k_cellsort<<<c->grid_tiles * DM_CS_GRID, kWarps * 32, 0, c->stream>>>(c->P, S, c->ptile, q.perm, c->keys, q.tile_start,
-                                                           q.tile_count, q.work, q.nact, c->flags, c->wq);
+  if (c->coop)  // CTA-shared tiles, like the tile kernels of small batches
+    k_cellsort_coop<<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, c->ptile, q.perm, c->keys, q.work, q.nact,
+                                                                  c->flags, c->wq);
+  else
+    k_cellsort<<<c->grid_tiles * DM_CS_GRID, kWarps * 32, 0, c->stream>>>(c->P, S, c->ptile, q.perm, c->keys,
+                                                                         q.tile_start, q.tile_count, q.work, q.nact,
+                                                                         c->flags, c->wq);
   ++c->launches;
   PROF_END(c, 0);
   ++c->launches;

@@ -1011,6 +1011,93 @@ __device__ __forceinline__ V coop_sum(V v) {
   return acc;
 }
 
+// k_cellsort with CTA-shared tiles (small batches: a tile's chunk chain is
+// the launch's critical path).  Warp w takes the w-th contiguous quarter of
+// the tile (whole chunks), counts it, the CTA scans the 64 buckets in
+// (bucket, warp) order, and each warp scatters its quarter in index order
+// from its cursors: the same stable permutation as k_cellsort.
+__global__ void __launch_bounds__(kWarps * 32) k_cellsort_coop(DevParams P, const int* __restrict__ ptile,
+                                                               int* __restrict__ perm, const int* __restrict__ keys,
+                                                               const int4* __restrict__ active, const int* nact,
+                                                               DevFlags* flags, int* __restrict__ wq) {
+  __shared__ int c64[kWarps][64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_active = *(const volatile int*)nact;
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicMax(&flags->max_active, n_active);
+  auto item = [&](const int4 et, int) __attribute__((always_inline)) {
+    const int n = et.w;
+    const size_t base = (size_t)et.x * P.N + et.z;
+    const int nch = (n + 31) >> 5, per = (nch + kWarps - 1) / kWarps;
+    const int q0 = min(n, warp * per * 32), q1 = min(n, (warp + 1) * per * 32);  // this warp's quarter
+    int* cnt = c64[warp];
+    cnt[lane] = 0;
+    cnt[lane + 32] = 0;
+    __syncwarp();
+    auto load_cells = [&](int c0, int (&src)[kBinU], int (&cell)[kBinU]) __attribute__((always_inline)) {
+#pragma unroll
+      for (int u = 0; u < kBinU; ++u) src[u] = c0 + 32 * u + lane < q1 ? ptile[base + c0 + 32 * u + lane] : -1;
+#pragma unroll
+      for (int u = 0; u < kBinU; ++u) cell[u] = src[u] >= 0 ? (keys[src[u]] & 63) : 64 + lane;
+    };
+    for (int c0 = q0; c0 < q1; c0 += 32 * kBinU) {
+      int src[kBinU], cl[kBinU];
+      load_cells(c0, src, cl);
+#pragma unroll
+      for (int u = 0; u < kBinU; ++u) {
+        if (c0 + 32 * u >= q1) break;
+        const unsigned peers = __match_any_sync(0xffffffffu, cl[u]);
+        if (src[u] >= 0 && lane == __ffs(peers) - 1) cnt[cl[u]] += __popc(peers);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {  // bucket-major exclusive scan of (bucket, warp) counts -> cursors
+      int t0 = 0, t1 = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        t0 += c64[w][2 * lane];
+        t1 += c64[w][2 * lane + 1];
+      }
+      int incl = t0 + t1;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int e0 = incl - t0 - t1, e1 = incl - t1;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        const int a0 = c64[w][2 * lane], a1 = c64[w][2 * lane + 1];
+        c64[w][2 * lane] = e0;
+        c64[w][2 * lane + 1] = e1;
+        e0 += a0;
+        e1 += a1;
+      }
+    }
+    __syncthreads();
+    for (int c0 = q0; c0 < q1; c0 += 32 * kBinU) {
+      int src[kBinU], cl[kBinU];
+      load_cells(c0, src, cl);
+#pragma unroll
+      for (int u = 0; u < kBinU; ++u) {  // in index order: stable
+        if (c0 + 32 * u >= q1) break;
+        const bool ok = src[u] >= 0;
+        const unsigned peers = __match_any_sync(0xffffffffu, cl[u]);
+        const int leader = __ffs(peers) - 1;
+        const int rank = __popc(peers & ((1u << lane) - 1u));
+        int pos = 0;
+        if (ok && lane == leader) {
+          pos = cnt[cl[u]];
+          cnt[cl[u]] = pos + __popc(peers);
+        }
+        pos = __shfl_sync(0xffffffffu, pos, leader);
+        if (ok) perm[base + pos + rank] = src[u];
+        __syncwarp();
+      }
+    }
+  };
+  coop_loop(active, wq, n_active, item);
+}
+
 // ============================ P2G ============================
 // Per active tile: stage particle payloads (lanes = particles), scatter runs
 // into the warp's 6^3 shared block (lanes = stencil nodes), write the block.
