@@ -63,3 +63,39 @@ def test_modes_deterministic_and_consistent(cfg):
                 assert np.linalg.norm(r[k]) <= 1e-4 * scale, (m, k)
             else:
                 assert _rel(r[k], ref[k]) <= 1e-4, (m, k, _rel(r[k], ref[k]))
+
+
+def test_stress_cache_on_off_consistent():
+    """The elastoplastic stress cache (G2P writes P F'^T, the next P2G reads it
+    instead of a new SVD) changes only fp32 rounding: a cfg3 rollout with it
+    and with DIFFMPM_NO_TAU_CACHE=1 agree (states 1e-5, the full per-env
+    gradient 1e-4), and each is deterministic."""
+    sc = scenes.CONFIGS[3](seed=4, n_envs=2, n_ctrl=2)
+
+    def run(no_cache):
+        old = os.environ.get("DIFFMPM_NO_TAU_CACHE")
+        if no_cache:
+            os.environ["DIFFMPM_NO_TAU_CACHE"] = "1"
+        else:
+            os.environ.pop("DIFFMPM_NO_TAU_CACHE", None)
+        try:
+            b = api.from_scene(sc)
+            r1, r2 = api.run_scene(b, sc), api.run_scene(b, sc)
+            st = b.get_state()
+            b.close()
+        finally:
+            if old is None:
+                os.environ.pop("DIFFMPM_NO_TAU_CACHE", None)
+            else:
+                os.environ["DIFFMPM_NO_TAU_CACHE"] = old
+        for k in r1:
+            if isinstance(r1[k], np.ndarray):
+                assert np.array_equal(r1[k], r2[k]), (no_cache, k)
+        return r1, st
+
+    (ra, sa), (rb, sb) = run(False), run(True)
+    for k in "xvFC":
+        assert _rel(sa[k], sb[k]) <= 1e-5, (k, _rel(sa[k], sb[k]))
+    full = lambda r: np.concatenate([np.asarray(r[k], np.float64).ravel() for k in ("x", "v", "F", "C")])
+    assert _rel(full(ra), full(rb)) <= 1e-4, _rel(full(ra), full(rb))
+    assert _rel(ra["cvo"], rb["cvo"]) <= 1e-4
