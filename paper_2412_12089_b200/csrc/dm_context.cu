@@ -79,6 +79,7 @@ struct DmContext {
   float4 *gvb_pool = nullptr, *gmpb_pool = nullptr;
   size_t blk_cap = 0;
   int max_active_seen = 0;
+  int dev_sms = 148;
   // the step that filled the tape kept its segment (states + artifacts) from
   // the forward pass, so the backward skips that segment's replay
   int kept_t = -1;
@@ -303,6 +304,18 @@ Slot slot(DmContext* c, int q) {
 #ifndef DM_CS_GRID
 #define DM_CS_GRID 2  // k_cellsort is light (32 registers): twice the tile kernels' resident warps
 #endif
+// CTAs of a tile kernel: every resident slot (grid_tiles), unless the batch
+// has few active tiles (max_active_seen, known after the first sync): then a
+// CTA per tile in COOP mode (a warp per tile otherwise) with 2x headroom, at
+// least one per SM.  Only the schedule changes (every tile's result is
+// independent of which CTA runs it); idle CTAs cost a prologue and a
+// contended atomic each (cfg1: ~25 of 1,184 CTAs had work).
+int tile_ctas(const DmContext* c, bool coop) {
+  if (c->max_active_seen <= 0) return c->grid_tiles;
+  const long want = coop ? 2L * c->max_active_seen : (2L * c->max_active_seen + kWarps - 1) / kWarps;
+  return (int)std::min<long>(c->grid_tiles, std::max<long>(c->dev_sms, want));
+}
+
 void launch_bin(DmContext* c, const StateView& S, const Slot& q, int sub, int check_vmax) {
   cudaMemsetAsync(q.nact, 0, sizeof(int), c->stream);
   PROF_BEGIN(c, 0);
@@ -320,10 +333,10 @@ void launch_bin(DmContext* c, const StateView& S, const Slot& q, int sub, int ch
   c->launches += 2;
   wq_reset(c);
   if (c->coop)  // CTA-shared tiles, like the tile kernels of small batches
-    k_cellsort_coop<<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, c->ptile, q.perm, c->keys, q.work, q.nact,
+    k_cellsort_coop<<<tile_ctas(c, true), kWarps * 32, 0, c->stream>>>(c->P, c->ptile, q.perm, c->keys, q.work, q.nact,
                                                                   c->flags, c->wq);
   else
-    k_cellsort<<<c->grid_tiles * DM_CS_GRID, kWarps * 32, 0, c->stream>>>(c->P, S, c->ptile, q.perm, c->keys,
+    k_cellsort<<<tile_ctas(c, false) * DM_CS_GRID, kWarps * 32, 0, c->stream>>>(c->P, S, c->ptile, q.perm, c->keys,
                                                                          q.tile_start, q.tile_count, q.work, q.nact,
                                                                          c->flags, c->wq);
   ++c->launches;
@@ -340,9 +353,9 @@ void launch_p2g(DmContext* c, const StateView& S, const Slot& q, int t, int sub)
   wq_reset(c);
   PROF_BEGIN(c, 1);
 #define L_P2G(LW)                                                                                               \
-  if (c->coop_p2g) k_p2g<LW, true><<<c->grid_tiles, kWarps * 32, kP2gSmem, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.work, \
+  if (c->coop_p2g) k_p2g<LW, true><<<tile_ctas(c, true), kWarps * 32, kP2gSmem, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.work, \
                                                           step_act(c, t), c->blocks, c->flags, q.nact, sub, c->wq, q.vref); \
-  else k_p2g<LW, false><<<c->grid_tiles, kWarps * 32, kP2gSmem, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.work, \
+  else k_p2g<LW, false><<<tile_ctas(c, false), kWarps * 32, kP2gSmem, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.work, \
                                                           step_act(c, t), c->blocks, c->flags, q.nact, sub, c->wq, q.vref)
   DM_LAW_DISPATCH(c, L_P2G);
 #undef L_P2G
@@ -371,11 +384,11 @@ void launch_grid(DmContext* c, const Slot& q, int t, bool dump) {
   PROF_BEGIN(c, 9);
 #define L_GRID(MC, CK)                                                                                        \
   if (c->grid_coop)                                                                                     \
-    k_grid<MC, CK, true><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work, step_cvo(c, t), \
+    k_grid<MC, CK, true><<<tile_ctas(c, true), kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work, step_cvo(c, t), \
                                                                c->blocks, dump ? c->gmp : nullptr, c->gv, q.nact, c->wq, \
                                                                q.vref);                                 \
   else                                                                                                  \
-    k_grid<MC, CK, false><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work, step_cvo(c, t), \
+    k_grid<MC, CK, false><<<tile_ctas(c, false), kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work, step_cvo(c, t), \
                                                                c->blocks, dump ? c->gmp : nullptr, c->gv, q.nact, c->wq, \
                                                                q.vref)
   DM_GRID_DISPATCH(c, L_GRID);
@@ -388,11 +401,11 @@ void launch_g2p(DmContext* c, const StateView& S, const StateView& So, const Slo
   wq_reset(c);
   PROF_BEGIN(c, 2);
 #define L_G2P(LW)                                                                                                \
-  if (c->coop) k_g2p<LW, true><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, q.perm, q.tile_start, q.tile_count, \
+  if (c->coop) k_g2p<LW, true><<<tile_ctas(c, true), kWarps * 32, 0, c->stream>>>(c->P, S, So, q.perm, q.tile_start, q.tile_count, \
                                                           q.work, c->tm_gv, c->flags, q.nact, sub, c->gmp,         \
                                                           dump ? q.gvb : nullptr, dump ? q.gmpb : nullptr, c->wq, (int)c->blk_cap, \
                                                           q.vref); \
-  else k_g2p<LW, false><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, S, So, q.perm, q.tile_start, q.tile_count,        \
+  else k_g2p<LW, false><<<tile_ctas(c, false), kWarps * 32, 0, c->stream>>>(c->P, S, So, q.perm, q.tile_start, q.tile_count,        \
                                                           q.work, c->tm_gv, c->flags, q.nact, sub, c->gmp,         \
                                                           dump ? q.gvb : nullptr, dump ? q.gmpb : nullptr, c->wq, (int)c->blk_cap, \
                                                           q.vref)
@@ -466,7 +479,7 @@ void forward_substep(DmContext* c, const StateView& S, const StateView& So, int 
 
 template <int LAW, int NG, int NM, bool COOP>
 void launch_p2g_adj_k(DmContext* c, const StateView& S, const Slot& q, int t, float* adj_out) {
-  k_p2g_adj<LAW, NG, NM, COOP><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(
+  k_p2g_adj<LAW, NG, NM, COOP><<<tile_ctas(c, COOP), kWarps * 32, 0, c->stream>>>(
       c->P, S, q.perm, q.tile_start, q.tile_count, q.work, step_act(c, t), c->gmb, c->tm_gmb, c->part, adj_out, c->Ntot,
       c->tile_acc, q.nact, c->wq);
 }
@@ -482,7 +495,7 @@ void launch_p2g_adj(DmContext* c, const StateView& S, const Slot& q, int t, floa
 
 template <int LAW, int NM, bool COOP>
 void launch_g2p_adj_k(DmContext* c, const StateView& S, const StateView& Sn, const Slot& q, const float* adj_in) {
-  k_g2p_adj<LAW, NM, COOP><<<c->grid_tiles, kWarps * 32, kG2pAdjSmem, c->stream>>>(
+  k_g2p_adj<LAW, NM, COOP><<<tile_ctas(c, COOP), kWarps * 32, kG2pAdjSmem, c->stream>>>(
       c->P, S, Sn, adj_in, c->Ntot, q.perm, q.tile_start, q.tile_count, q.work, q.gvb, c->ablocks, c->part,
       c->tile_acc, q.nact, c->wq, q.vref);
 }
@@ -510,11 +523,11 @@ void backward_substep(DmContext* c, const StateView& S, const StateView& Sn, int
   PROF_BEGIN(c, 10);
 #define L_GRIDA(MC, CK)                                                                                   \
   if (c->grid_coop)                                                                                 \
-    k_grid_adj<MC, CK, true><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work,  \
+    k_grid_adj<MC, CK, true><<<tile_ctas(c, true), kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work,  \
                                                                    step_cvo(c, t), c->ablocks, q.gmpb,   \
                                                                    c->gmb, c->tile_acc, q.nact, c->wq, q.vref); \
   else                                                                                              \
-    k_grid_adj<MC, CK, false><<<c->grid_tiles, kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work, \
+    k_grid_adj<MC, CK, false><<<tile_ctas(c, false), kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work, \
                                                                    step_cvo(c, t), c->ablocks, q.gmpb,   \
                                                                    c->gmb, c->tile_acc, q.nact, c->wq, q.vref)
   DM_GRID_DISPATCH(c, L_GRIDA);
@@ -1210,6 +1223,7 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<-1, 16, 4, false>, kWarps * 32, 0);
   if (occ < 1) occ = 1;
   ctx->grid_tiles = dev_sms * (occ < 8 ? 8 : occ);
+  ctx->dev_sms = dev_sms;
   // CTA-cooperative tiles when the batch gives each resident warp only a few
   // chunks (DIFFMPM_COOP=0/1 forces the mode)
   ctx->coop = N < (size_t)kCoopParticlesPerWarp * ctx->grid_tiles * kWarps;
