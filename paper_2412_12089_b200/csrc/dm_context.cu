@@ -42,6 +42,7 @@ struct DmContext {
   int grid_tiles = 148 * 4;
   bool coop = false;      // CTA-cooperative tiles in g2p / g2p_adj (small batches; see coop_idx)
   bool coop_p2g = false;  // ... in p2g / p2g_adj (pays up to larger batches)
+  int coop_cg = 4;        // COOP group size: warps per tile (4 for tiny batches, else 2)
   bool grid_coop = false;  // CTA-shared tiles in the grid kernels (tiny batches)
   CUtensorMap tm_gv, tm_gmb;  // TMA descriptors of the dense node-velocity / (mass, momentum)-cotangent grids
 
@@ -349,14 +350,23 @@ const float* step_act(DmContext* c, int t) {
   return c->P.G > 0 ? c->act_tape + (size_t)t * c->P.E * c->P.G : nullptr;
 }
 
+template <int LW, bool COOP, int CG>
+void launch_p2g_k(DmContext* c, const StateView& S, const Slot& q, int t, int sub) {
+  k_p2g<LW, COOP, CG><<<tile_ctas(c, COOP), kWarps * 32, kP2gSmem, c->stream>>>(
+      c->P, S, q.perm, q.tile_start, q.tile_count, q.work, step_act(c, t), c->blocks, c->flags, q.nact, sub, c->wq,
+      q.vref);
+}
+
 void launch_p2g(DmContext* c, const StateView& S, const Slot& q, int t, int sub) {
   wq_reset(c);
   PROF_BEGIN(c, 1);
-#define L_P2G(LW)                                                                                               \
-  if (c->coop_p2g) k_p2g<LW, true><<<tile_ctas(c, true), kWarps * 32, kP2gSmem, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.work, \
-                                                          step_act(c, t), c->blocks, c->flags, q.nact, sub, c->wq, q.vref); \
-  else k_p2g<LW, false><<<tile_ctas(c, false), kWarps * 32, kP2gSmem, c->stream>>>(c->P, S, q.perm, q.tile_start, q.tile_count, q.work, \
-                                                          step_act(c, t), c->blocks, c->flags, q.nact, sub, c->wq, q.vref)
+#define L_P2G(LW)                                   \
+  if (!c->coop_p2g)                                 \
+    launch_p2g_k<LW, false, 4>(c, S, q, t, sub);    \
+  else if (c->coop_cg == 2)                         \
+    launch_p2g_k<LW, true, 2>(c, S, q, t, sub);     \
+  else                                              \
+    launch_p2g_k<LW, true, 4>(c, S, q, t, sub)
   DM_LAW_DISPATCH(c, L_P2G);
 #undef L_P2G
   PROF_END(c, 1);
@@ -397,18 +407,24 @@ void launch_grid(DmContext* c, const Slot& q, int t, bool dump) {
   ++c->launches;
 }
 
+template <int LW, bool COOP, int CG>
+void launch_g2p_k(DmContext* c, const StateView& S, const StateView& So, const Slot& q, int sub, bool dump) {
+  k_g2p<LW, COOP, CG><<<tile_ctas(c, COOP), kWarps * 32, 0, c->stream>>>(
+      c->P, S, So, q.perm, q.tile_start, q.tile_count, q.work, c->tm_gv, c->flags, q.nact, sub, c->gmp,
+      dump ? q.gvb : nullptr, dump ? q.gmpb : nullptr, c->wq, (int)c->blk_cap, q.vref);
+}
+
 void launch_g2p(DmContext* c, const StateView& S, const StateView& So, const Slot& q, int t, int sub, bool dump) {
+  (void)t;
   wq_reset(c);
   PROF_BEGIN(c, 2);
-#define L_G2P(LW)                                                                                                \
-  if (c->coop) k_g2p<LW, true><<<tile_ctas(c, true), kWarps * 32, 0, c->stream>>>(c->P, S, So, q.perm, q.tile_start, q.tile_count, \
-                                                          q.work, c->tm_gv, c->flags, q.nact, sub, c->gmp,         \
-                                                          dump ? q.gvb : nullptr, dump ? q.gmpb : nullptr, c->wq, (int)c->blk_cap, \
-                                                          q.vref); \
-  else k_g2p<LW, false><<<tile_ctas(c, false), kWarps * 32, 0, c->stream>>>(c->P, S, So, q.perm, q.tile_start, q.tile_count,        \
-                                                          q.work, c->tm_gv, c->flags, q.nact, sub, c->gmp,         \
-                                                          dump ? q.gvb : nullptr, dump ? q.gmpb : nullptr, c->wq, (int)c->blk_cap, \
-                                                          q.vref)
+#define L_G2P(LW)                                        \
+  if (!c->coop)                                          \
+    launch_g2p_k<LW, false, 4>(c, S, So, q, sub, dump);  \
+  else if (c->coop_cg == 2)                              \
+    launch_g2p_k<LW, true, 2>(c, S, So, q, sub, dump);   \
+  else                                                   \
+    launch_g2p_k<LW, true, 4>(c, S, So, q, sub, dump)
   DM_LAW_DISPATCH(c, L_G2P);
 #undef L_G2P
   PROF_END(c, 2);
@@ -477,9 +493,9 @@ void forward_substep(DmContext* c, const StateView& S, const StateView& So, int 
   launch_g2p(c, S, So, q, t, sub, dump);
 }
 
-template <int LAW, int NG, int NM, bool COOP>
+template <int LAW, int NG, int NM, bool COOP, int CG>
 void launch_p2g_adj_k(DmContext* c, const StateView& S, const Slot& q, int t, float* adj_out) {
-  k_p2g_adj<LAW, NG, NM, COOP><<<tile_ctas(c, COOP), kWarps * 32, 0, c->stream>>>(
+  k_p2g_adj<LAW, NG, NM, COOP, CG><<<tile_ctas(c, COOP), kWarps * 32, 0, c->stream>>>(
       c->P, S, q.perm, q.tile_start, q.tile_count, q.work, step_act(c, t), c->gmb, c->tm_gmb, c->part, adj_out, c->Ntot,
       c->tile_acc, q.nact, c->wq);
 }
@@ -487,15 +503,20 @@ void launch_p2g_adj_k(DmContext* c, const StateView& S, const Slot& q, int t, fl
 template <int LAW, int NG>
 void launch_p2g_adj(DmContext* c, const StateView& S, const Slot& q, int t, float* adj_out) {
   wq_reset(c);
-  if (c->P.nmat == 1)
-    c->coop_p2g ? launch_p2g_adj_k<LAW, NG, 1, true>(c, S, q, t, adj_out) : launch_p2g_adj_k<LAW, NG, 1, false>(c, S, q, t, adj_out);
-  else
-    c->coop_p2g ? launch_p2g_adj_k<LAW, NG, 4, true>(c, S, q, t, adj_out) : launch_p2g_adj_k<LAW, NG, 4, false>(c, S, q, t, adj_out);
+  if (c->P.nmat == 1) {
+    if (!c->coop_p2g) launch_p2g_adj_k<LAW, NG, 1, false, 4>(c, S, q, t, adj_out);
+    else if (c->coop_cg == 2) launch_p2g_adj_k<LAW, NG, 1, true, 2>(c, S, q, t, adj_out);
+    else launch_p2g_adj_k<LAW, NG, 1, true, 4>(c, S, q, t, adj_out);
+  } else {
+    if (!c->coop_p2g) launch_p2g_adj_k<LAW, NG, 4, false, 4>(c, S, q, t, adj_out);
+    else if (c->coop_cg == 2) launch_p2g_adj_k<LAW, NG, 4, true, 2>(c, S, q, t, adj_out);
+    else launch_p2g_adj_k<LAW, NG, 4, true, 4>(c, S, q, t, adj_out);
+  }
 }
 
-template <int LAW, int NM, bool COOP>
+template <int LAW, int NM, bool COOP, int CG>
 void launch_g2p_adj_k(DmContext* c, const StateView& S, const StateView& Sn, const Slot& q, const float* adj_in) {
-  k_g2p_adj<LAW, NM, COOP><<<tile_ctas(c, COOP), kWarps * 32, kG2pAdjSmem, c->stream>>>(
+  k_g2p_adj<LAW, NM, COOP, CG><<<tile_ctas(c, COOP), kWarps * 32, kG2pAdjSmem, c->stream>>>(
       c->P, S, Sn, adj_in, c->Ntot, q.perm, q.tile_start, q.tile_count, q.work, q.gvb, c->ablocks, c->part,
       c->tile_acc, q.nact, c->wq, q.vref);
 }
@@ -510,11 +531,16 @@ void backward_substep(DmContext* c, const StateView& S, const StateView& Sn, int
   }
   wq_reset(c);
   PROF_BEGIN(c, 3);
-#define L_G2PA(LW)                                                                                            \
-  if (c->P.nmat == 1)                                                                                          \
-    c->coop ? launch_g2p_adj_k<LW, 1, true>(c, S, Sn, q, adj_in) : launch_g2p_adj_k<LW, 1, false>(c, S, Sn, q, adj_in); \
-  else                                                                                                         \
-    c->coop ? launch_g2p_adj_k<LW, 4, true>(c, S, Sn, q, adj_in) : launch_g2p_adj_k<LW, 4, false>(c, S, Sn, q, adj_in)
+#define L_G2PA(LW)                                                                                     \
+  if (c->P.nmat == 1) {                                                                                 \
+    if (!c->coop) launch_g2p_adj_k<LW, 1, false, 4>(c, S, Sn, q, adj_in);                               \
+    else if (c->coop_cg == 2) launch_g2p_adj_k<LW, 1, true, 2>(c, S, Sn, q, adj_in);                    \
+    else launch_g2p_adj_k<LW, 1, true, 4>(c, S, Sn, q, adj_in);                                         \
+  } else {                                                                                              \
+    if (!c->coop) launch_g2p_adj_k<LW, 4, false, 4>(c, S, Sn, q, adj_in);                               \
+    else if (c->coop_cg == 2) launch_g2p_adj_k<LW, 4, true, 2>(c, S, Sn, q, adj_in);                    \
+    else launch_g2p_adj_k<LW, 4, true, 4>(c, S, Sn, q, adj_in);                                         \
+  }
   DM_LAW_DISPATCH(c, L_G2PA);
 #undef L_G2PA
   PROF_END(c, 3);
@@ -1112,13 +1138,14 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
     s.thickness = (float)shapes[c].thickness;
   }
   {
-#define DM_SMEM_ATTR1(LW, CO)                                                                                 \
-  cudaFuncSetAttribute(k_p2g<LW, CO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kP2gSmem);            \
-  cudaFuncSetAttribute(k_g2p_adj<LW, 1, CO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kG2pAdjSmem); \
-  cudaFuncSetAttribute(k_g2p_adj<LW, 4, CO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kG2pAdjSmem)
-#define DM_SMEM_ATTR(LW) \
-  DM_SMEM_ATTR1(LW, false); \
-  DM_SMEM_ATTR1(LW, true)
+#define DM_SMEM_ATTR1(LW, CO, CG)                                                                                 \
+  cudaFuncSetAttribute(k_p2g<LW, CO, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kP2gSmem);            \
+  cudaFuncSetAttribute(k_g2p_adj<LW, 1, CO, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kG2pAdjSmem); \
+  cudaFuncSetAttribute(k_g2p_adj<LW, 4, CO, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kG2pAdjSmem)
+#define DM_SMEM_ATTR(LW)        \
+  DM_SMEM_ATTR1(LW, false, 4);  \
+  DM_SMEM_ATTR1(LW, true, 2);   \
+  DM_SMEM_ATTR1(LW, true, 4)
     DM_SMEM_ATTR(0);
     DM_SMEM_ATTR(1);
     DM_SMEM_ATTR(2);
@@ -1220,7 +1247,7 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<-1, 16, 4, false>, kWarps * 32, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<-1, 16, 4, false, 4>, kWarps * 32, 0);
   if (occ < 1) occ = 1;
   ctx->grid_tiles = dev_sms * (occ < 8 ? 8 : occ);
   ctx->dev_sms = dev_sms;
@@ -1234,6 +1261,10 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   // -32 %; neutral at 32 envs; +5 / +11 % at 128 envs)
   ctx->grid_coop = N < (size_t)kGridCoopParticlesPerWarp * ctx->grid_tiles * kWarps;
   if (const char* f = std::getenv("DIFFMPM_GRID_COOP")) ctx->grid_coop = f[0] == '1';
+  // two-warp tile groups unless the batch is tiny (a tile's chunk chain is
+  // then the critical path); DIFFMPM_COOP_CG=2/4 forces it
+  ctx->coop_cg = N < (size_t)kGridCoopParticlesPerWarp * ctx->grid_tiles * kWarps ? 4 : 2;
+  if (const char* f = std::getenv("DIFFMPM_COOP_CG")) ctx->coop_cg = f[0] == '2' ? 2 : 4;
   if (reset_flags(ctx) != DM_OK) return ctx;
   return ctx;
 }

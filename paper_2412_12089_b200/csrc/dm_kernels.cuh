@@ -950,43 +950,57 @@ __device__ __forceinline__ void load_pstate(const StateView& S, int src, PState&
 // coop_idx(v, w); the last (partial) chunk belongs to one warp.  Scatter
 // kernels sum the 4 warps' block copies in a fixed order (deterministic;
 // the replay uses the same mode), gathers need no reduction.
-template <bool COOP>
+// CG (warps per tile group) divides kWarps: CG < kWarps lets a CTA work on
+// kWarps / CG tiles at once (groups synchronise on named barriers).
+template <bool COOP, int CG = kWarps>
 __device__ __forceinline__ int coop_idx(int v, int w) {
-  return COOP ? ((((v >> 5) << 2) + w) << 5) + (v & 31) : v;
+  return COOP ? (((v >> 5) * CG + w) << 5) + (v & 31) : v;
 }
-template <bool COOP>
+template <bool COOP, int CG = kWarps>
 __device__ __forceinline__ int coop_count(int cnt, int w) {
   if (!COOP) return cnt;
   const int nc = (cnt + 31) >> 5;
   if (w >= nc) return 0;
-  const int k = (nc - 1 - w) / 4 + 1;  // chunks w, w + 4, ... below nc
-  return 32 * k - ((((nc - 1) & 3) == w) ? 32 * nc - cnt : 0);
+  const int k = (nc - 1 - w) / CG + 1;  // chunks w, w + CG, ... below nc
+  return 32 * k - ((((nc - 1) % CG) == w) ? 32 * nc - cnt : 0);
+}
+template <int CG>
+__device__ __forceinline__ void group_sync(int g) {
+  if (CG == kWarps)
+    __syncthreads();
+  else
+    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + g), "n"(CG * 32) : "memory");
 }
 
-// CTA-level item loop of the COOP kernels: thread 0 takes the next item, the
-// CTA processes it, a barrier closes it.
-template <class Body>
+// Group-level item loop of the COOP kernels: the group's first thread takes
+// the next item, the group (the CTA when CG = kWarps) processes it, a
+// barrier closes it.
+template <int CG = kWarps, class Body>
 __device__ __forceinline__ void coop_loop(const int4* __restrict__ work, int* ctr, int n, Body& body) {
-  __shared__ int s_item;
+  __shared__ int s_item[kWarps / CG];
+  const int g = (threadIdx.x >> 5) / CG;
+  const int tig = threadIdx.x - g * CG * 32;
   for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(ctr, 1);
-    __syncthreads();
-    const int a = s_item;
+    if (tig == 0) s_item[g] = atomicAdd(ctr, 1);
+    group_sync<CG>(g);
+    const int a = s_item[g];
     if (a >= n) break;
     body(work[a], a);
-    __syncthreads();
+    group_sync<CG>(g);
   }
 }
 
-// Fixed-order sum of the CTA's kWarps x 3 scatter copies (warp w's copies
-// at base + w * wstride, kExt3 apart) into dst, after every warp flushed.
+// Fixed-order sum of the group's CG x 3 scatter copies (warp w's copies at
+// base + w * wstride, kExt3 apart) into dst, after every warp flushed.
+template <int CG = kWarps>
 __device__ __forceinline__ void coop_store_blocks(const float4* __restrict__ base, int wstride,
                                                   float4* __restrict__ dst) {
-  __syncthreads();
-  for (int i = threadIdx.x; i < kExt3; i += blockDim.x) {
+  const int g = (threadIdx.x >> 5) / CG;
+  group_sync<CG>(g);
+  for (int i = threadIdx.x - g * CG * 32; i < kExt3; i += CG * 32) {
     float4 acc = base[i];
 #pragma unroll
-    for (int c = 1; c < 3 * kWarps; ++c) {
+    for (int c = 1; c < 3 * CG; ++c) {
       const float4 b = base[(c / 3) * wstride + (c % 3) * kExt3 + i];
       acc.x += b.x;
       acc.y += b.y;
@@ -997,19 +1011,24 @@ __device__ __forceinline__ void coop_store_blocks(const float4* __restrict__ bas
   }
 }
 
-// Fixed-order CTA sum of a per-warp value (after the warp's butterfly; lane 0 holds it).
-template <class V>
+// Fixed-order group sum of a per-warp value (after the warp's butterfly; lane 0 holds it).
+template <int CG = kWarps, class V>
 __device__ __forceinline__ V coop_sum(V v) {
   __shared__ V s_part[kWarps];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = warp / CG;
+  group_sync<CG>(g);
   if (lane == 0) s_part[warp] = v;
-  __syncthreads();
-  V acc = s_part[0];
+  group_sync<CG>(g);
+  V acc = s_part[g * CG];
 #pragma unroll
-  for (int w = 1; w < kWarps; ++w) acc += s_part[w];
+  for (int w = 1; w < CG; ++w) acc += s_part[g * CG + w];
   return acc;
 }
+// COOP group size CG (warps per tile; the tile kernels' last template
+// parameter, chosen per context): 2 for small batches -- each CTA works on
+// two tiles, half the block copies to combine, shorter barrier waits (r02
+// A/B: cfg2 +12 %, cfg4 at 128 envs +11 %) -- and 4 for tiny ones, where a
+// tile's chunk chain is the critical path (cfg1: CG = 2 was 25 % slower).
 
 // k_cellsort with CTA-shared tiles (small batches: a tile's chunk chain is
 // the launch's critical path).  Warp w takes the w-th contiguous quarter of
@@ -1130,7 +1149,8 @@ __device__ __forceinline__ void chunk_loop(Body& body, int cnt, int& s0, int& s1
 #ifndef DM_P2G_MINB
 #define DM_P2G_MINB 4
 #endif
-template <int LAW, bool COOP>
+
+template <int LAW, bool COOP, int CG>
 __global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, StateView S, const int* __restrict__ perm,
                                                      const int* __restrict__ tile_start,
                                                      const int* __restrict__ tile_count, const int4* __restrict__ active,
@@ -1145,14 +1165,14 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, S
   float* pw = reinterpret_cast<float*>(dsm + kWarps * 3 * kExt3) + warp * 32 * kPay;
   auto tile = [&](const int4 cur) __attribute__((always_inline)) {
     const int e = cur.x, t = cur.y, start = cur.z;
-    const int cnt = coop_count<COOP>(cur.w, warp);  // this warp's (virtual) particle count
+    const int cnt = coop_count<COOP, CG>(cur.w, warp % CG);  // this warp's (virtual) particle count
     const int tz = t % P.td[2], ty = (t / P.td[2]) % P.td[1], tx = t / (P.td[2] * P.td[1]);
     const int o[3] = {tx * kTile, ty * kTile, tz * kTile};
     const size_t tix = (size_t)e * P.Tn + t;
     const int* prow = perm + (size_t)e * P.N + start;
     auto pidx = [&](int v) {
-      DM_CHECK(coop_idx<COOP>(v, warp) < cur.w);
-      const int r = prow[coop_idx<COOP>(v, warp)];
+      DM_CHECK((coop_idx<COOP, CG>(v, warp % CG) < cur.w));
+      const int r = prow[coop_idx<COOP, CG>(v, warp % CG)];
       DM_CHECK(r >= 0 && (size_t)r < (size_t)P.E * P.N);
       return r;
     };
@@ -1199,14 +1219,14 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, S
     chunk_loop<LAW == kFluid || LAW == kNeoHookean>(chunk, cnt, s0, s1);
     if constexpr (COOP) {  // flush, then the CTA sums the 4 warps' copies
       if (lane < 27) run_flush(bw + (lane / 9) * kExt3, ra, (((lane % 9) / 3) * kExt + lane % 3) * kExt);
-      coop_store_blocks(dsm, 3 * kExt3, blocks + tix * kExt3);
+      coop_store_blocks<CG>(dsm + (warp / CG) * CG * 3 * kExt3, 3 * kExt3, blocks + tix * kExt3);
     } else {
       scatter_store(bw, lane, ra, blocks + tix * kExt3);
     }
   };
   if constexpr (COOP) {
     auto item = [&](const int4 cur, int) __attribute__((always_inline)) { tile(cur); };
-    coop_loop(active, wq, n_active, item);
+    coop_loop<CG>(active, wq, n_active, item);
   } else {
     for (TileIter ti(active, wq, n_active, lane); ti.valid(); ti.advance()) {
       ti.prefetch(active);
@@ -1414,7 +1434,7 @@ __device__ __forceinline__ void load_tile_grid(const DevParams& P, const float4*
 #define DM_G2P_RING 3
 #endif
 constexpr int kG2pRing = DM_G2P_RING;  // 3: k_g2p -7 % vs registers one chunk ahead; 4: same at 1,024 envs, +3 % at 128
-template <int LAW, bool COOP>
+template <int LAW, bool COOP, int CG>
 __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams P, StateView S, StateView Sout,
                                                      const int* __restrict__ perm, const int* __restrict__ tile_start,
                                                      const int* __restrict__ tile_count, const int4* __restrict__ active,
@@ -1439,27 +1459,27 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
   // one tile (item a) with its grid block landed in vw
   auto tile = [&](const int4 cur, const int a, const float4* vw) __attribute__((always_inline)) {
     const int e = cur.x, t = cur.y, start = cur.z;
-    const int cnt = coop_count<COOP>(cur.w, warp);  // this warp's (virtual) particle count
+    const int cnt = coop_count<COOP, CG>(cur.w, warp % CG);  // this warp's (virtual) particle count
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
     const size_t row = (size_t)e * P.N + start;
     auto pidx = [&](int v) {
-      DM_CHECK(coop_idx<COOP>(v, warp) < cur.w);
-      const int r = perm[row + coop_idx<COOP>(v, warp)];
+      DM_CHECK((coop_idx<COOP, CG>(v, warp % CG) < cur.w));
+      const int r = perm[row + coop_idx<COOP, CG>(v, warp % CG)];
       DM_CHECK(r >= 0 && (size_t)r < (size_t)P.E * P.N);
       return r;
     };
     const float4 vr4 = vref[e];
     const v3<float> vr = mk3(vr4.x, vr4.y, vr4.z);
     auto dump = [&]() __attribute__((always_inline)) {
-      if (out_gv && a < dump_cap && (!COOP || warp == 0)) {  // segment replay: keep the tile's grid for the adjoint
+      if (out_gv && a < dump_cap && (!COOP || warp % CG == 0)) {  // segment replay: keep the tile's grid for the adjoint
         if (lane == 0) bulk_s2g(out_gv + (size_t)a * kExt3, vw, kExt3 * (uint32_t)sizeof(float4));
         load_tile_grid(P, gmp, e, o, out_gmp + (size_t)a * kExt3, lane);
       }
     };
     auto body = [&](int c0, const float x[3], m3<float> F, uint32_t at) {
       if (c0 + lane >= cnt) return;
-      const size_t dst = row + coop_idx<COOP>(c0 + lane, warp);
+      const size_t dst = row + coop_idx<COOP, CG>(c0 + lane, warp % CG);
       Stencil<float> sc;
       make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
       const int lb[3] = {tile_local(sc.base[0], o[0]), tile_local(sc.base[1], o[1]), tile_local(sc.base[2], o[2])};
@@ -1556,17 +1576,18 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
   // bulk dump stores of the buffer's previous tile have read it
   uint32_t ph = 0;
   if constexpr (COOP) {
+    const int gw = warp - warp % CG;  // the group's first warp: its buffer holds the group's tile grid
     auto item = [&](const int4 cur, int a) __attribute__((always_inline)) {
-      if (threadIdx.x == 0) {  // one copy of the tile's grid for the CTA
+      if (warp == gw && lane == 0) {  // one copy of the tile's grid for the group
         bulk_s2g_read_wait();
         fence_proxy_async();
-        tma_tile_grid(P, &tm_gv, cur, vg[0][0], &vbar[0][0]);
+        tma_tile_grid(P, &tm_gv, cur, vg[gw][0], &vbar[gw][0]);
       }
-      mbar_wait(&vbar[0][0], ph);
+      mbar_wait(&vbar[gw][0], ph);
       ph ^= 1;
-      tile(cur, a, vg[0][0]);
+      tile(cur, a, vg[gw][0]);
     };
-    coop_loop(active, wq, n_active, item);
+    coop_loop<CG>(active, wq, n_active, item);
   } else {
     TileIter ti(active, wq, n_active, lane);
     if (ti.valid() && lane == 0) tma_tile_grid(P, &tm_gv, ti.cur, vg[warp][0], &vbar[warp][0]);
@@ -1594,7 +1615,7 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
 #ifndef DM_G2PADJ_MINB
 #define DM_G2PADJ_MINB 3
 #endif
-template <int LAW, int NM, bool COOP>
+template <int LAW, int NM, bool COOP, int CG>
 __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevParams P, StateView S, StateView Sn, const float* __restrict__ adj_in,
                                                          size_t astride, const int* __restrict__ perm,
                                                          const int* __restrict__ tile_start,
@@ -1619,7 +1640,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
   const int n_active = *(const volatile int*)nact;
   auto tile = [&](const int4 cur, const int a) __attribute__((always_inline)) {
     const int e = cur.x, t = cur.y, start = cur.z;
-    const int cnt = coop_count<COOP>(cur.w, warp);  // this warp's (virtual) particle count
+    const int cnt = coop_count<COOP, CG>(cur.w, warp % CG);  // this warp's (virtual) particle count
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
     // the replayed substep's grid, by slot (asynchronous; overlaps the first loads)
@@ -1639,8 +1660,8 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
     const size_t tix = (size_t)e * P.Tn + t;
     const size_t row = (size_t)e * P.N + start;
     auto pidx = [&](int v) {
-      DM_CHECK(coop_idx<COOP>(v, warp) < cur.w);
-      const int r = perm[row + coop_idx<COOP>(v, warp)];
+      DM_CHECK((coop_idx<COOP, CG>(v, warp % CG) < cur.w));
+      const int r = perm[row + coop_idx<COOP, CG>(v, warp % CG)];
       DM_CHECK(r >= 0 && (size_t)r < (size_t)P.E * P.N);
       return r;
     };
@@ -1670,7 +1691,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
     }
     auto chunk = [&](int c0, int s_next) __attribute__((always_inline)) -> int {
       if (c0 + lane < cnt) {
-        const size_t dst = row + coop_idx<COOP>(c0 + lane, warp);
+        const size_t dst = row + coop_idx<COOP, CG>(c0 + lane, warp % CG);
         Stencil<float> sc;
         make_stencil(x, P.inv_dx, (double)P.dx, P.dims, sc);
         const int lb[3] = {tile_local(sc.base[0], o[0]), tile_local(sc.base[1], o[1]), tile_local(sc.base[2], o[2])};
@@ -1728,7 +1749,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
     chunk_loop<LAW == kFluid>(chunk, cnt, s0, s1);
     if constexpr (COOP) {
       if (lane < 27) run_flush(aw + (lane / 9) * kExt3, ra, (((lane % 9) / 3) * kExt + lane % 3) * kExt);
-      coop_store_blocks(dsm + kExt3, 4 * kExt3, ablocks + tix * kExt3);
+      coop_store_blocks<CG>(dsm + kExt3 + (warp - warp % CG) * 4 * kExt3, 4 * kExt3, ablocks + tix * kExt3);
     } else {
       scatter_store(aw, lane, ra, ablocks + tix * kExt3);
     }
@@ -1737,8 +1758,8 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
       for (int off = 16; off > 0; off >>= 1) mub[m] += __shfl_xor_sync(0xffffffffu, mub[m], off);
     if constexpr (COOP) {
 #pragma unroll
-      for (int m = 0; m < NM; ++m) mub[m] = coop_sum(mub[m]);
-      if (threadIdx.x == 0)
+      for (int m = 0; m < NM; ++m) mub[m] = coop_sum<CG>(mub[m]);
+      if (warp % CG == 0 && lane == 0)
 #pragma unroll
         for (int m = 0; m < NM; ++m) tile_acc[tix * kNacc + kAccMuG + m] = (float)mub[m];
     } else {
@@ -1749,7 +1770,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
     __syncwarp();
   };
   if constexpr (COOP) {
-    coop_loop(active, wq, n_active, tile);
+    coop_loop<CG>(active, wq, n_active, tile);
   } else {
     for (TileIter ti(active, wq, n_active, lane); ti.valid(); ti.advance()) {
       ti.prefetch(active);
@@ -1852,7 +1873,7 @@ constexpr int kP2gAdjStage = 38;  // staged words per particle: state 24, attr, 
 #ifndef DM_P2GADJ_MINB
 #define DM_P2GADJ_MINB 3
 #endif
-template <int LAW, int NG, int NM, bool COOP>
+template <int LAW, int NG, int NM, bool COOP, int CG>
 __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevParams P, StateView S, const int* __restrict__ perm,
                                                          const int* __restrict__ tile_start,
                                                          const int* __restrict__ tile_count,
@@ -1881,14 +1902,14 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
   float4* bw = mb[warp];
   auto tile = [&](const int4 cur) __attribute__((always_inline)) {
     const int e = cur.x, t = cur.y, start = cur.z;
-    const int cnt = coop_count<COOP>(cur.w, warp);  // this warp's (virtual) particle count
+    const int cnt = coop_count<COOP, CG>(cur.w, warp % CG);  // this warp's (virtual) particle count
     const int tc[3] = {t / (P.td[2] * P.td[1]), (t / P.td[2]) % P.td[1], t % P.td[2]};
     const int o[3] = {tc[0] * kTile, tc[1] * kTile, tc[2] * kTile};
     const size_t tix = (size_t)e * P.Tn + t;
     const size_t row = (size_t)e * P.N + start;
     auto pidx = [&](int v) {
-      DM_CHECK(coop_idx<COOP>(v, warp) < cur.w);
-      const int r = perm[row + coop_idx<COOP>(v, warp)];
+      DM_CHECK((coop_idx<COOP, CG>(v, warp % CG) < cur.w));
+      const int r = perm[row + coop_idx<COOP, CG>(v, warp % CG)];
       DM_CHECK(r >= 0 && (size_t)r < (size_t)P.E * P.N);
       return r;
     };
@@ -1907,7 +1928,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
       cp_async4(sg + 24 * 32 + lane, S.attr + src);
 #pragma unroll
       for (int f = 0; f < 12; ++f)
-        if (!(LAW == kFluid && P.fiso && f > 3)) cp_async4(sg + (25 + f) * 32 + lane, part + part_index(f, row + coop_idx<COOP>(c0 + lane, warp), astride));
+        if (!(LAW == kFluid && P.fiso && f > 3)) cp_async4(sg + (25 + f) * 32 + lane, part + part_index(f, row + coop_idx<COOP, CG>(c0 + lane, warp % CG), astride));
       sg[37 * 32 + lane] = __int_as_float(src);
     };
     int s1 = 32 + lane < cnt ? pidx(32 + lane) : 0;  // perm two chunks ahead, parity slots
@@ -2015,13 +2036,13 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
     if constexpr (COOP) {  // fixed-order sum of the 4 warps' partials
 #pragma unroll
       for (int m = 0; m < NM; ++m) {
-        mub[m] = coop_sum(mub[m]);
-        lab[m] = coop_sum(lab[m]);
+        mub[m] = coop_sum<CG>(mub[m]);
+        lab[m] = coop_sum<CG>(lab[m]);
       }
 #pragma unroll
-      for (int q = 0; q < NG; ++q) actb[q] = coop_sum(actb[q]);
+      for (int q = 0; q < NG; ++q) actb[q] = coop_sum<CG>(actb[q]);
     }
-    if (COOP ? threadIdx.x == 0 : lane == 0) {
+    if (COOP ? (warp % CG == 0 && lane == 0) : lane == 0) {
       float* ta = tile_acc + tix * kNacc;
 #pragma unroll
       for (int m = 0; m < NM; ++m) {
@@ -2037,7 +2058,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
       tile(cur);
       cp_async_wait<0>();  // no staging copy outlives the item
     };
-    coop_loop(active, wq, n_active, item);
+    coop_loop<CG>(active, wq, n_active, item);
   } else {
     for (TileIter ti(active, wq, n_active, lane); ti.valid(); ti.advance()) {
       ti.prefetch(active);

@@ -1,8 +1,9 @@
 """The small-batch scheduling modes (GPU, through the C ABI).
 
-dm_create picks CTA-cooperative tiles (`coop`: the 4 warps of a CTA share a
-tile's chunks; `grid_coop`: they share its owned nodes) from the batch size;
-DIFFMPM_COOP / DIFFMPM_GRID_COOP force them.  Every mode must be
+dm_create picks CTA-cooperative tiles (`coop`: a group of 2 or 4 warps of a
+CTA shares a tile's chunks; `grid_coop`: the 4 warps share its owned nodes)
+from the batch size; DIFFMPM_COOP / DIFFMPM_GRID_COOP / DIFFMPM_COOP_CG force
+them.  Every mode must be
 deterministic run to run (the replay verification relies on it) and agree
 with the others up to the fp32 summation order of the per-warp partials.
 """
@@ -15,12 +16,13 @@ from paper_2412_12089_b200 import api, scenes
 
 pytestmark = pytest.mark.gpu
 
-MODES = [("0", "0"), ("1", "0"), ("1", "1")]
+# (COOP, grid COOP, COOP group size in warps)
+MODES = [("0", "0", "4"), ("1", "0", "2"), ("1", "0", "4"), ("1", "1", "4")]
 
 
-def _run(sc, coop, grid_coop):
-    old = {k: os.environ.get(k) for k in ("DIFFMPM_COOP", "DIFFMPM_GRID_COOP")}
-    os.environ["DIFFMPM_COOP"], os.environ["DIFFMPM_GRID_COOP"] = coop, grid_coop
+def _run(sc, coop, grid_coop, cg):
+    old = {k: os.environ.get(k) for k in ("DIFFMPM_COOP", "DIFFMPM_GRID_COOP", "DIFFMPM_COOP_CG")}
+    os.environ["DIFFMPM_COOP"], os.environ["DIFFMPM_GRID_COOP"], os.environ["DIFFMPM_COOP_CG"] = coop, grid_coop, cg
     try:
         b = api.from_scene(sc)  # the mode is read when the context is created
         r1 = api.run_scene(b, sc)
@@ -34,7 +36,7 @@ def _run(sc, coop, grid_coop):
                 os.environ[k] = v
     for k in r1:
         if isinstance(r1[k], np.ndarray):
-            assert np.array_equal(r1[k], r2[k]), (coop, grid_coop, k)
+            assert np.array_equal(r1[k], r2[k]), (coop, grid_coop, cg, k)
     return r1
 
 
@@ -48,7 +50,7 @@ def test_modes_deterministic_and_consistent(cfg):
     kw = {"seed": 3, "n_envs": 3, "n_ctrl": 2}
     sc = scenes.CONFIGS[cfg](**kw)
     runs = {m: _run(sc, *m) for m in MODES}
-    ref = runs[("0", "0")]
+    ref = runs[("0", "0", "4")]
     full = lambda r: np.concatenate([np.asarray(r[k], np.float64).ravel() for k in ("x", "v", "F", "C")])
     for m, r in runs.items():
         assert _rel(r["obs"], ref["obs"]) <= 1e-4, (m, "obs")
