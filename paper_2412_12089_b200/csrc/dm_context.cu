@@ -40,8 +40,8 @@ struct DmContext {
   int n_store = 0;
   unsigned long long launches = 0, bytes = 0;
   int grid_tiles = 148 * 4;
-  bool coop = false;      // CTA-cooperative tiles in g2p / g2p_adj (small batches; see coop_idx)
-  bool coop_p2g = false;  // ... in p2g / p2g_adj (pays up to larger batches)
+  bool coop = false;      // CTA-cooperative tiles in g2p and the cell sort (small batches; see coop_idx)
+  bool coop_p2g = false;  // ... in p2g / p2g_adj / g2p_adj (pays up to larger batches)
   int coop_cg = 4;        // COOP group size: warps per tile (4 for tiny batches, else 2)
   bool grid_coop = false;  // CTA-shared tiles in the grid kernels (tiny batches)
   CUtensorMap tm_gv, tm_gmb;  // TMA descriptors of the dense node-velocity / (mass, momentum)-cotangent grids
@@ -533,11 +533,11 @@ void backward_substep(DmContext* c, const StateView& S, const StateView& Sn, int
   PROF_BEGIN(c, 3);
 #define L_G2PA(LW)                                                                                     \
   if (c->P.nmat == 1) {                                                                                 \
-    if (!c->coop) launch_g2p_adj_k<LW, 1, false, 4>(c, S, Sn, q, adj_in);                               \
+    if (!c->coop_p2g) launch_g2p_adj_k<LW, 1, false, 4>(c, S, Sn, q, adj_in);                           \
     else if (c->coop_cg == 2) launch_g2p_adj_k<LW, 1, true, 2>(c, S, Sn, q, adj_in);                    \
     else launch_g2p_adj_k<LW, 1, true, 4>(c, S, Sn, q, adj_in);                                         \
   } else {                                                                                              \
-    if (!c->coop) launch_g2p_adj_k<LW, 4, false, 4>(c, S, Sn, q, adj_in);                               \
+    if (!c->coop_p2g) launch_g2p_adj_k<LW, 4, false, 4>(c, S, Sn, q, adj_in);                           \
     else if (c->coop_cg == 2) launch_g2p_adj_k<LW, 4, true, 2>(c, S, Sn, q, adj_in);                    \
     else launch_g2p_adj_k<LW, 4, true, 4>(c, S, Sn, q, adj_in);                                         \
   }

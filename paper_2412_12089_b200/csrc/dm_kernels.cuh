@@ -39,8 +39,9 @@ constexpr int kExt3 = kExt * kExt * kExt;
 constexpr int kWarps = 4;  // warps per CTA in tile kernels
 constexpr int kGridCoopParticlesPerWarp = 64;  // the grid kernels' COOP threshold (dm_create)
 constexpr int kCoopParticlesPerWarp = 640;  // below this many particles per resident warp: COOP tiles (r02 A/B: cfg4 x128 envs +24 %, x256 -3 %)
-// the scatter-side pair (p2g, p2g_adj) keeps COOP up to larger batches (r02 A/B
-// at 256 envs: p2g -5 %, p2g_adj -2 %, while g2p / g2p_adj lose 7 % and 6 %)
+// the scatter kernels (p2g, p2g_adj, g2p_adj) keep COOP up to larger batches
+// (r02 A/B at 256 envs, 2-warp groups: g2p_adj -6 % in COOP, g2p +3 %; at
+// 512 envs COOP loses everywhere)
 constexpr int kCoopP2gParticlesPerWarp = 1280;
 constexpr int kPay = 28;   // payload stride (floats; 7 float4, conflict-free STS.128 / 3-way LDS.128)
 constexpr int kNacc = 64;  // per-tile cotangent accumulators
