@@ -195,9 +195,9 @@ __device__ __forceinline__ Law<float> law_of(const DevParams& P, int mi) {
   return L;
 }
 #ifndef DM_G2P_MINB
-#define DM_G2P_MINB 5
+#define DM_G2P_MINB 4
 #endif
-// fluid: 5 CTAs/SM (one-word F loads leave room; measured -4 % vs 4), others 4
+// 4 CTAs/SM (r02, with the staging ring: fluid -1.7 % vs 5; round 1 without it: 5 was 4 % faster)
 constexpr int kG2pBlocks(int law) { return law == kFluid ? DM_G2P_MINB : 4; }
 
 __device__ __forceinline__ TransferCtx<float> tctx(const DevParams& P) {
