@@ -1786,7 +1786,7 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
 // reduced per tile (each node counted once, by its owner).
 template <int MAXC, int CK, bool COOP>
 #ifndef DM_GRIDADJ_MINB
-#define DM_GRIDADJ_MINB 4
+#define DM_GRIDADJ_MINB 5  // r02: 96 B of spills but -8 % on cfg4 (the hollow-box query record), -1 % cfg3, +6 % cfg2
 #endif
 __global__ void __launch_bounds__(kWarps * 32, DM_GRIDADJ_MINB) k_grid_adj(DevParams P, const int* __restrict__ tile_count,
                                                           const int4* __restrict__ active, const float* __restrict__ cvo,
