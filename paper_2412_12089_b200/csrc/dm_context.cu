@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/diffmpm.h"
@@ -98,7 +99,10 @@ struct DmContext {
   int bwd_cur = 0;  // which adj buffer holds the running state cotangent
   float* tile_acc = nullptr;
   DevFlags* flags = nullptr;
-  int* wq = nullptr;  // dynamic tile-scheduling counter
+  bool pdl = false;        // programmatic dependent launch (dm_launch)
+  int* wq = nullptr;       // this launch's tile-scheduling counter (a slot of wq_ring)
+  int* wq_ring = nullptr;  // kWqRing counters, each zeroed by the previous tile kernel
+  unsigned wq_i = 0;
   DevFlags* h_flags = nullptr;
   float *cvo_tape = nullptr, *act_tape = nullptr, *obs_tape = nullptr;
   double *gcvo = nullptr, *gact = nullptr, *gmu = nullptr, *glam = nullptr;
@@ -127,6 +131,21 @@ struct DmContext {
 };
 
 namespace {
+
+// Kernel launch, with programmatic dependent launch when `pdl` (every kernel
+// opens with dm_pdl(), so it may be scheduled while the previous grid
+// drains).  The context enables it for small batches (COOP mode), where the
+// ~2 us launch gap per kernel boundary is a visible share of a substep; on
+// cfg4's 1,024 envs it measured 2 % slower and stays off.
+// DIFFMPM_PDL=0/1 forces it.
+template <class... KA, class... A>
+void dm_launch(dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl, void (*k)(KA...), A&&... args) {
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {grid, block, smem, s, at, pdl ? 1u : 0u};
+  cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
+}
 
 // Scoped NVTX range (ncu --nvtx --nvtx-include / nsys timelines).
 struct NvtxRange {
@@ -282,7 +301,9 @@ struct Slot {
 };
 
 // zeroes the dynamic tile-scheduling counter before a tile kernel
-void wq_reset(DmContext* c) { cudaMemsetAsync(c->wq, 0, sizeof(int), c->stream); }
+// Next tile kernel's counter: the ring slot the previous tile kernel zeroed
+// (wq_clear_next); every wq_reset is followed by exactly one tile kernel.
+void wq_reset(DmContext* c) { c->wq = c->wq_ring + (c->wq_i++ % kWqRing); }
 
 Slot slot(DmContext* c, int q) {
   const size_t TT = (size_t)c->P.E * c->P.Tn;
@@ -317,29 +338,43 @@ int tile_ctas(const DmContext* c, bool coop) {
   return (int)std::min<long>(c->grid_tiles, std::max<long>(c->dev_sms, want));
 }
 
-void launch_bin(DmContext* c, const StateView& S, const Slot& q, int sub, int check_vmax) {
-  cudaMemsetAsync(q.nact, 0, sizeof(int), c->stream);
+// active-tile count (as last seen) up to which one CTA orders the work list
+constexpr int kOrderSmallMax = 4096;
+
+void launch_bin(DmContext* c, const StateView& S, const Slot& q, int sub, int check_vmax,
+                const SortRec* rec = nullptr) {
+  wq_reset(c);  // k_bin totals the active tiles in a zeroed ring slot (no memset node)
   PROF_BEGIN(c, 0);
   if (c->bin_u16)
-    k_bin<unsigned short><<<c->P.E, 32 * c->bin_warps, (size_t)c->bin_warps * c->P.Tn * 2, c->stream>>>(
-        c->P, S, c->keys, c->ptile, q.tile_start, q.tile_count, q.active, q.env_abase, q.env_acount, c->flags, q.nact,
-        sub, check_vmax, q.vref);
+    dm_launch(c->P.E, 32 * c->bin_warps, (size_t)c->bin_warps * c->P.Tn * 2, c->stream, c->pdl, k_bin<unsigned short>, 
+        c->P, S, c->keys, c->ptile, q.tile_start, q.tile_count, q.active, q.env_abase, q.env_acount, c->flags, c->wq,
+        sub, check_vmax, q.vref, q.ord);
   else
-    k_bin<int><<<c->P.E, 32 * c->bin_warps, (size_t)c->bin_warps * c->P.Tn * 4, c->stream>>>(
-        c->P, S, c->keys, c->ptile, q.tile_start, q.tile_count, q.active, q.env_abase, q.env_acount, c->flags, q.nact,
-        sub, check_vmax, q.vref);
-  cudaMemsetAsync(q.ord, 0, 2 * kOrdBuckets * sizeof(int), c->stream);
-  k_order_hist<<<64, 256, 0, c->stream>>>(q.active, q.nact, q.ord);
-  k_order_scatter<<<(unsigned)((c->P.E * c->P.Tn + 2047) / 2048), 256, 0, c->stream>>>(q.active, q.nact, q.ord, q.work);
-  c->launches += 2;
+    dm_launch(c->P.E, 32 * c->bin_warps, (size_t)c->bin_warps * c->P.Tn * 4, c->stream, c->pdl, k_bin<int>, 
+        c->P, S, c->keys, c->ptile, q.tile_start, q.tile_count, q.active, q.env_abase, q.env_acount, c->flags, c->wq,
+        sub, check_vmax, q.vref, q.ord);
+  // the sort record's copy of the binning tables: by the one-CTA order kernel
+  // or the cell sort (rec_copy)
+  const RecSrc rs{q.active, q.work, q.env_abase, q.env_acount, q.nact, q.vref, c->rec_cap, c->P.E};
+  const bool small = c->max_active_seen > 0 && c->max_active_seen <= kOrderSmallMax;
+  const SortRec no_rec{}, rec_cs = rec && !small ? *rec : no_rec;
+  if (small) {  // one CTA orders the list
+    dm_launch(1, 1024, 0, c->stream, c->pdl, k_order_small, q.active, c->wq, q.nact, q.work, rec ? *rec : no_rec, rs);
+    c->launches += 1;
+  } else {
+    dm_launch(64, 256, 0, c->stream, c->pdl, k_order_hist, q.active, c->wq, q.ord, q.nact);
+    dm_launch((unsigned)((c->P.E * c->P.Tn + 2047) / 2048), 256, 0, c->stream, c->pdl, k_order_scatter, q.active, q.nact,
+              q.ord, q.work);
+    c->launches += 2;
+  }
   wq_reset(c);
   if (c->coop)  // CTA-shared tiles, like the tile kernels of small batches
-    k_cellsort_coop<<<tile_ctas(c, true), kWarps * 32, 0, c->stream>>>(c->P, c->ptile, q.perm, c->keys, q.work, q.nact,
-                                                                  c->flags, c->wq);
+    dm_launch(tile_ctas(c, true), kWarps * 32, 0, c->stream, c->pdl, k_cellsort_coop, c->P, c->ptile, q.perm, c->keys, q.work, q.nact,
+                                                                  c->flags, c->wq, rec_cs, rs);
   else
-    k_cellsort<<<tile_ctas(c, false) * DM_CS_GRID, kWarps * 32, 0, c->stream>>>(c->P, S, c->ptile, q.perm, c->keys,
+    dm_launch(tile_ctas(c, false) * DM_CS_GRID, kWarps * 32, 0, c->stream, c->pdl, k_cellsort, c->P, S, c->ptile, q.perm, c->keys,
                                                                          q.tile_start, q.tile_count, q.work, q.nact,
-                                                                         c->flags, c->wq);
+                                                                         c->flags, c->wq, rec_cs, rs);
   ++c->launches;
   PROF_END(c, 0);
   ++c->launches;
@@ -352,7 +387,7 @@ const float* step_act(DmContext* c, int t) {
 
 template <int LW, bool COOP, int CG>
 void launch_p2g_k(DmContext* c, const StateView& S, const Slot& q, int t, int sub) {
-  k_p2g<LW, COOP, CG><<<tile_ctas(c, COOP), kWarps * 32, kP2gSmem, c->stream>>>(
+  dm_launch(tile_ctas(c, COOP), kWarps * 32, kP2gSmem, c->stream, c->pdl, k_p2g<LW, COOP, CG>, 
       c->P, S, q.perm, q.tile_start, q.tile_count, q.work, step_act(c, t), c->blocks, c->flags, q.nact, sub, c->wq,
       q.vref);
 }
@@ -394,11 +429,11 @@ void launch_grid(DmContext* c, const Slot& q, int t, bool dump) {
   PROF_BEGIN(c, 9);
 #define L_GRID(MC, CK)                                                                                        \
   if (c->grid_coop)                                                                                     \
-    k_grid<MC, CK, true><<<tile_ctas(c, true), kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work, step_cvo(c, t), \
+    dm_launch(tile_ctas(c, true), kWarps * 32, 0, c->stream, c->pdl, k_grid<MC, CK, true>, c->P, q.tile_count, q.work, step_cvo(c, t), \
                                                                c->blocks, dump ? c->gmp : nullptr, c->gv, q.nact, c->wq, \
                                                                q.vref);                                 \
   else                                                                                                  \
-    k_grid<MC, CK, false><<<tile_ctas(c, false), kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work, step_cvo(c, t), \
+    dm_launch(tile_ctas(c, false), kWarps * 32, 0, c->stream, c->pdl, k_grid<MC, CK, false>, c->P, q.tile_count, q.work, step_cvo(c, t), \
                                                                c->blocks, dump ? c->gmp : nullptr, c->gv, q.nact, c->wq, \
                                                                q.vref)
   DM_GRID_DISPATCH(c, L_GRID);
@@ -409,7 +444,7 @@ void launch_grid(DmContext* c, const Slot& q, int t, bool dump) {
 
 template <int LW, bool COOP, int CG>
 void launch_g2p_k(DmContext* c, const StateView& S, const StateView& So, const Slot& q, int sub, bool dump) {
-  k_g2p<LW, COOP, CG><<<tile_ctas(c, COOP), kWarps * 32, 0, c->stream>>>(
+  dm_launch(tile_ctas(c, COOP), kWarps * 32, 0, c->stream, c->pdl, k_g2p<LW, COOP, CG>, 
       c->P, S, So, q.perm, q.tile_start, q.tile_count, q.work, c->tm_gv, c->flags, q.nact, sub, c->gmp,
       dump ? q.gvb : nullptr, dump ? q.gmpb : nullptr, c->wq, (int)c->blk_cap, q.vref);
 }
@@ -474,17 +509,21 @@ void forward_substep(DmContext* c, const StateView& S, const StateView& So, int 
                      bool dump, int rec_s = -1, bool record = false) {
   Slot q = rec_s >= 0 ? rec_slot(c, qi, rec_s) : slot(c, qi);
   // the forward pass sorts straight into the record's permutation and tile
-  // counts (always complete: N and E x Tn entries); k_rec_save copies the
-  // capacity-limited rest of the binning
+  // counts (always complete: N and E x Tn entries); the cell sort copies the
+  // capacity-limited rest of the binning (rec_copy; k_rec_save otherwise)
   if (record && c->rec.perm) {
     const SortRec r = rec_at(c, sub);
     q.perm = r.perm;
     q.tile_count = r.tile_count;
   }
-  if (rec_s < 0) launch_bin(c, S, q, sub, check_vmax);
-  if (record && c->rec.perm) {
+  const bool rec_fused = rec_s < 0 && record && c->rec.perm;
+  if (rec_s < 0) {
+    const SortRec r = rec_fused ? rec_at(c, sub) : SortRec{};
+    launch_bin(c, S, q, sub, check_vmax, rec_fused ? &r : nullptr);
+  }
+  if (record && c->rec.perm && !rec_fused) {
     const size_t TT = (size_t)c->P.E * c->P.Tn;
-    k_rec_save<<<c->grid_tiles, 256, 0, c->stream>>>(c->Ntot, TT, c->P.E, c->rec_cap, nullptr, nullptr, q.active,
+    dm_launch(c->grid_tiles, 256, 0, c->stream, c->pdl, k_rec_save, c->Ntot, TT, c->P.E, c->rec_cap, nullptr, nullptr, q.active,
                                                      q.work, q.env_abase, q.env_acount, q.nact, q.vref, rec_at(c, sub));
     ++c->launches;
   }
@@ -495,7 +534,7 @@ void forward_substep(DmContext* c, const StateView& S, const StateView& So, int 
 
 template <int LAW, int NG, int NM, bool COOP, int CG>
 void launch_p2g_adj_k(DmContext* c, const StateView& S, const Slot& q, int t, float* adj_out) {
-  k_p2g_adj<LAW, NG, NM, COOP, CG><<<tile_ctas(c, COOP), kWarps * 32, 0, c->stream>>>(
+  dm_launch(tile_ctas(c, COOP), kWarps * 32, 0, c->stream, c->pdl, k_p2g_adj<LAW, NG, NM, COOP, CG>, 
       c->P, S, q.perm, q.tile_start, q.tile_count, q.work, step_act(c, t), c->gmb, c->tm_gmb, c->part, adj_out, c->Ntot,
       c->tile_acc, q.nact, c->wq);
 }
@@ -516,7 +555,7 @@ void launch_p2g_adj(DmContext* c, const StateView& S, const Slot& q, int t, floa
 
 template <int LAW, int NM, bool COOP, int CG>
 void launch_g2p_adj_k(DmContext* c, const StateView& S, const StateView& Sn, const Slot& q, const float* adj_in) {
-  k_g2p_adj<LAW, NM, COOP, CG><<<tile_ctas(c, COOP), kWarps * 32, kG2pAdjSmem, c->stream>>>(
+  dm_launch(tile_ctas(c, COOP), kWarps * 32, kG2pAdjSmem, c->stream, c->pdl, k_g2p_adj<LAW, NM, COOP, CG>, 
       c->P, S, Sn, adj_in, c->Ntot, q.perm, q.tile_start, q.tile_count, q.work, q.gvb, c->ablocks, c->part,
       c->tile_acc, q.nact, c->wq, q.vref);
 }
@@ -549,11 +588,11 @@ void backward_substep(DmContext* c, const StateView& S, const StateView& Sn, int
   PROF_BEGIN(c, 10);
 #define L_GRIDA(MC, CK)                                                                                   \
   if (c->grid_coop)                                                                                 \
-    k_grid_adj<MC, CK, true><<<tile_ctas(c, true), kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work,  \
+    dm_launch(tile_ctas(c, true), kWarps * 32, 0, c->stream, c->pdl, k_grid_adj<MC, CK, true>, c->P, q.tile_count, q.work,  \
                                                                    step_cvo(c, t), c->ablocks, q.gmpb,   \
                                                                    c->gmb, c->tile_acc, q.nact, c->wq, q.vref); \
   else                                                                                              \
-    k_grid_adj<MC, CK, false><<<tile_ctas(c, false), kWarps * 32, 0, c->stream>>>(c->P, q.tile_count, q.work, \
+    dm_launch(tile_ctas(c, false), kWarps * 32, 0, c->stream, c->pdl, k_grid_adj<MC, CK, false>, c->P, q.tile_count, q.work, \
                                                                    step_cvo(c, t), c->ablocks, q.gmpb,   \
                                                                    c->gmb, c->tile_acc, q.nact, c->wq, q.vref)
   DM_GRID_DISPATCH(c, L_GRIDA);
@@ -575,7 +614,7 @@ void backward_substep(DmContext* c, const StateView& S, const StateView& Sn, int
   ++c->launches;
   const int Kc = c->P.K > 0 ? c->P.K : 1;
   PROF_BEGIN(c, 5);
-  k_env_reduce<<<c->P.E, kNacc * kRedSlices, 0, c->stream>>>(c->P, q.active, q.env_abase, q.env_acount, c->tile_acc,
+  dm_launch(c->P.E, kNacc * kRedSlices, 0, c->stream, c->pdl, k_env_reduce, c->P, q.active, q.env_abase, q.env_acount, c->tile_acc,
                                                 c->gcvo + (size_t)t * c->P.E * Kc * 9,
                                                 c->gact + (size_t)t * c->P.E * (G > 0 ? G : 1), c->gmu, c->glam);
   PROF_END(c, 5);
@@ -661,7 +700,7 @@ int set_state_impl(DmContext* ctx, const float* x, const float* v, const float* 
   if (mat) DM_CUDA(cudaMemcpyAsync(ints, mat, N * sizeof(int), kind, ctx->stream));
   if (grp) DM_CUDA(cudaMemcpyAsync(ints + N, grp, N * sizeof(int), kind, ctx->stream));
   const StateView S0 = store_view(ctx, 0);
-  k_aos_to_soa<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>((int)N, st, st + 3 * N, st + 6 * N, st + 15 * N,
+  dm_launch((unsigned)((N + 255) / 256), 256, 0, ctx->stream, ctx->pdl, k_aos_to_soa, (int)N, st, st + 3 * N, st + 6 * N, st + 15 * N,
                                                                      mat ? ints : nullptr, grp ? ints + N : nullptr,
                                                                      ctx->P.N, S0);
   ++ctx->launches;
@@ -683,7 +722,7 @@ int get_state_impl(DmContext* ctx, float* x, float* v, float* F, float* C, cudaM
   const StateView S = fwd_state(ctx, s);
   float* out = ctx->adj[1];
   const int fiso = ctx->law == kFluid && s > 0;  // a fluid G2P output stores F(0,0) only
-  k_soa_to_aos<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>((int)N, ctx->P.N, S.f, S.attr, N, 1, fiso, out,
+  dm_launch((unsigned)((N + 255) / 256), 256, 0, ctx->stream, ctx->pdl, k_soa_to_aos, (int)N, ctx->P.N, S.f, S.attr, N, 1, fiso, out,
                                                                      out + 3 * N, out + 6 * N, out + 15 * N, 1);
   ++ctx->launches;
   if (x) DM_CUDA(cudaMemcpyAsync(x, out, 3 * N * sizeof(float), kind, ctx->stream));
@@ -785,7 +824,7 @@ int step_impl(DmContext* ctx, const float* cvo, const float* act, float* obs, cu
     ctx->cut_any[t] = 0;
   }
   PROF_BEGIN(ctx, 6);
-  k_obs<<<E, 256, 0, ctx->stream>>>(ctx->P, fwd_state(ctx, (t + 1) * S), step_cvo(ctx, t), (float)ctx->cfg.spill_half,
+  dm_launch(E, 256, 0, ctx->stream, ctx->pdl, k_obs, ctx->P, fwd_state(ctx, (t + 1) * S), step_cvo(ctx, t), (float)ctx->cfg.spill_half,
                                     (float)ctx->cfg.spill_temp, ctx->cfg.obs_groups, o, ctx->od, spc_t);
   PROF_END(ctx, 6);
   ++ctx->launches;
@@ -847,7 +886,7 @@ int backward_begin(DmContext* ctx, const float* dfx, const float* dfv, const flo
     if (dfv) DM_CUDA(cudaMemcpyAsync(stg + 3 * N, dfv, 3 * N * sizeof(float), kin, ctx->stream));
     if (dfF) DM_CUDA(cudaMemcpyAsync(stg + 6 * N, dfF, 9 * N * sizeof(float), kin, ctx->stream));
     if (dfC) DM_CUDA(cudaMemcpyAsync(stg + 15 * N, dfC, 9 * N * sizeof(float), kin, ctx->stream));
-    k_aos_to_soa_perm<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>(
+    dm_launch((unsigned)((N + 255) / 256), 256, 0, ctx->stream, ctx->pdl, k_aos_to_soa_perm, 
         (int)N, ctx->P.N, dfx ? stg : nullptr, dfv ? stg + 3 * N : nullptr, dfF ? stg + 6 * N : nullptr,
         dfC ? stg + 15 * N : nullptr, Sf.attr, A, N, ctx->law == kFluid);
     ++ctx->launches;
@@ -862,7 +901,7 @@ int backward_begin(DmContext* ctx, const float* dfx, const float* dfv, const flo
 // directly; host: through the device staging buffer and an async copy).
 int copy_out_f32(DmContext* ctx, float* dst, const double* src, size_t n, cudaMemcpyKind kout) {
   float* d = kout == cudaMemcpyDeviceToDevice ? dst : ctx->f32_stage;
-  k_f64_to_f32<<<(unsigned)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024), 256, 0, ctx->stream>>>(n, src, d);
+  dm_launch((unsigned)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024), 256, 0, ctx->stream, ctx->pdl, k_f64_to_f32, n, src, d);
   ++ctx->launches;
   if (d != dst) DM_CUDA(cudaMemcpyAsync(dst, d, n * sizeof(float), kout, ctx->stream));
   DM_CUDA(cudaGetLastError());
@@ -888,7 +927,7 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
   const bool cut = ctx->cut_tape && ctx->cut_any[t];
   const unsigned char* cut_t = cut ? ctx->cut_tape + (size_t)t * E : nullptr;
   if (cut) {  // envs reset after this step: no cotangent flows back across the reset (algo.hpp:171-178)
-    k_cut_adj<<<ctx->grid_tiles, 256, 0, ctx->stream>>>(ctx->P, cut_t, ctx->adj[cur], N);
+    dm_launch(ctx->grid_tiles, 256, 0, ctx->stream, ctx->pdl, k_cut_adj, ctx->P, cut_t, ctx->adj[cur], N);
     ++ctx->launches;
   }
   if (dobs_t) DM_CUDA(cudaMemcpyAsync(ctx->dobs_buf, dobs_t, (size_t)E * ctx->od * sizeof(float), kin, ctx->stream));
@@ -914,8 +953,8 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
       // the replayed exit must equal the stored checkpoint bitwise (tape.hpp:234-241)
       const StateView tl = view(ctx->tail, ctx->tail_attr, ctx->Ntot);
       if (ctx->inj_step == t)  // dm_debug_inject: a non-deterministic forward
-        k_debug_flip<<<(ctx->P.N + 255) / 256, 256, 0, ctx->stream>>>(ctx->P, tl, ctx->inj_env, ctx->inj_particle);
-      k_replay_check<<<ctx->grid_tiles, 256, 0, ctx->stream>>>(ctx->P, tl, store_view(ctx, (s0 + ck) / ck),
+        dm_launch((ctx->P.N + 255) / 256, 256, 0, ctx->stream, ctx->pdl, k_debug_flip, ctx->P, tl, ctx->inj_env, ctx->inj_particle);
+      dm_launch(ctx->grid_tiles, 256, 0, ctx->stream, ctx->pdl, k_replay_check, ctx->P, tl, store_view(ctx, (s0 + ck) / ck),
                                                                 ctx->law == kFluid, s0 + ck == s_end ? cut_t : nullptr,
                                                                 ctx->replay_bad);
       ctx->launches += 1 + (ctx->inj_step == t);
@@ -929,7 +968,7 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
       const StateView Se = kept ? store_view(ctx, s_end / ck) : view(ctx->tail, ctx->tail_attr, ctx->Ntot);
       if (dobs_t) {
         PROF_BEGIN(ctx, 7);
-        k_obs_adj<<<E, 256, 0, ctx->stream>>>(ctx->P, Se, step_cvo(ctx, t), (float)ctx->cfg.spill_half,
+        dm_launch(E, 256, 0, ctx->stream, ctx->pdl, k_obs_adj, ctx->P, Se, step_cvo(ctx, t), (float)ctx->cfg.spill_half,
                                               (float)ctx->cfg.spill_temp, ctx->cfg.obs_groups, ctx->dobs_buf, ctx->od,
                                               ctx->adj[cur], N, ctx->gcvo + (size_t)t * E * Kc * 9, spc_t,
                                               spc_t ? ctx->gspc + (size_t)t * E * 2 : nullptr);
@@ -937,7 +976,7 @@ int backward_step(DmContext* ctx, const float* dobs_t, float* dcvo_t, float* dac
         ++ctx->launches;
       }
       if (dcloud_t) {
-        k_cloud_adj<<<ctx->grid_tiles, 256, 0, ctx->stream>>>(ctx->P, Se.attr, ctx->cloud_stride, ctx->cloud_n,
+        dm_launch(ctx->grid_tiles, 256, 0, ctx->stream, ctx->pdl, k_cloud_adj, ctx->P, Se.attr, ctx->cloud_stride, ctx->cloud_n,
                                                                ctx->dcloud_buf, nullptr, ctx->adj[cur], N);
         ++ctx->launches;
       }
@@ -979,8 +1018,8 @@ int backward_end(DmContext* ctx, float* dx0, float* dv0, float* dF0, float* dC0,
   const size_t N = ctx->Ntot;
   float* out = ctx->adj[cur ^ 1];
   const StateView S0 = store_view(ctx, 0);
-  k_soa_to_aos<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>((int)N, ctx->P.N, ctx->adj[cur], S0.attr, N, 1, 0, out,
-                                                                     out + 3 * N, out + 6 * N, out + 15 * N);
+  dm_launch((unsigned)((N + 255) / 256), 256, 0, ctx->stream, ctx->pdl, k_soa_to_aos, (int)N, ctx->P.N, ctx->adj[cur], S0.attr, N, 1, 0, out,
+                                                                     out + 3 * N, out + 6 * N, out + 15 * N, 0);
   ++ctx->launches;
   if (dx0) DM_CUDA(cudaMemcpyAsync(dx0, out, 3 * N * sizeof(float), kout, ctx->stream));
   if (dv0) DM_CUDA(cudaMemcpyAsync(dv0, out + 3 * N, 3 * N * sizeof(float), kout, ctx->stream));
@@ -988,7 +1027,7 @@ int backward_end(DmContext* ctx, float* dx0, float* dv0, float* dF0, float* dC0,
   if (dC0) DM_CUDA(cudaMemcpyAsync(dC0, out + 15 * N, 9 * N * sizeof(float), kout, ctx->stream));
   if (dE) {
     double* d = kout == cudaMemcpyDeviceToDevice ? dE : ctx->dE_dev;
-    k_dE<<<(E * ctx->nmat + 127) / 128, 128, 0, ctx->stream>>>(E, ctx->nmat, ctx->gmu, ctx->glam, ctx->P, d);
+    dm_launch((E * ctx->nmat + 127) / 128, 128, 0, ctx->stream, ctx->pdl, k_dE, E, ctx->nmat, ctx->gmu, ctx->glam, ctx->P, d);
     ++ctx->launches;
     if (d != dE) DM_CUDA(cudaMemcpyAsync(dE, d, (size_t)E * ctx->nmat * sizeof(double), kout, ctx->stream));
   }
@@ -1179,7 +1218,7 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   const size_t NN = (size_t)P.E * P.dims[0] * P.dims[1] * P.dims[2];
   ok = ok && dalloc(ctx, &ctx->gmp, NN) && dalloc(ctx, &ctx->gv, NN) && dalloc(ctx, &ctx->gmb, NN);
   ok = ok && dalloc(ctx, &ctx->blocks, TT * kExt3) && dalloc(ctx, &ctx->ablocks, TT * kExt3) &&
-       dalloc(ctx, &ctx->tile_acc, TT * kNacc) && dalloc(ctx, &ctx->flags, 1) && dalloc(ctx, &ctx->wq, 4);
+       dalloc(ctx, &ctx->tile_acc, TT * kNacc) && dalloc(ctx, &ctx->flags, 1) && dalloc(ctx, &ctx->wq_ring, kWqRing);
   ok = ok && dalloc(ctx, &ctx->cvo_tape, (size_t)cfg->max_steps * P.E * Kc * 9) &&
        dalloc(ctx, &ctx->act_tape, (size_t)cfg->max_steps * P.E * Gc) &&
        dalloc(ctx, &ctx->obs_tape, (size_t)cfg->max_steps * P.E * ctx->od) &&
@@ -1218,6 +1257,7 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   }
   cudaMemsetAsync(ctx->store_attr, 0, N * sizeof(uint32_t), ctx->stream);
   cudaMemsetAsync(ctx->tile_acc, 0, TT * kNacc * sizeof(float), ctx->stream);
+  cudaMemsetAsync(ctx->wq_ring, 0, kWqRing * sizeof(int), ctx->stream);
   {
     // sort records for every substep of the tape, when device memory allows
     // (DIFFMPM_NO_SORT_RECORDS=1 disables them)
@@ -1265,6 +1305,10 @@ DmContext* dm_create(const DmConfig* cfg, const DmMaterial* mats, int num_materi
   // then the critical path); DIFFMPM_COOP_CG=2/4 forces it
   ctx->coop_cg = N < (size_t)kGridCoopParticlesPerWarp * ctx->grid_tiles * kWarps ? 4 : 2;
   if (const char* f = std::getenv("DIFFMPM_COOP_CG")) ctx->coop_cg = f[0] == '2' ? 2 : 4;
+  // launch chaining for small batches (r02 A/B: cfg1 +18 %, cfg2 +5 %, 128 envs
+  // neutral, 1,024 envs -2 %)
+  ctx->pdl = ctx->coop;
+  if (const char* f = std::getenv("DIFFMPM_PDL")) ctx->pdl = f[0] == '1';
   if (reset_flags(ctx) != DM_OK) return ctx;
   return ctx;
 }
@@ -1276,7 +1320,7 @@ void dm_destroy(DmContext* ctx) {
                   ctx->scratch_attr[0], ctx->scratch_attr[1], ctx->adj[0], ctx->adj[1], ctx->part, ctx->keys,
                   ctx->perm_all,  ctx->ptile, ctx->tstart_all, ctx->tcount_all, ctx->abase_all, ctx->acount_all,
                   ctx->active_all, ctx->work_all, ctx->ord_all, ctx->nact_all, ctx->tail, ctx->tail_attr, ctx->gvb_pool, ctx->gmpb_pool,
-                  ctx->blocks,    ctx->ablocks,    ctx->tile_acc,   ctx->gmp, ctx->gv, ctx->gmb,   ctx->flags, ctx->wq, ctx->cvo_tape,  ctx->act_tape,
+                  ctx->blocks,    ctx->ablocks,    ctx->tile_acc,   ctx->gmp, ctx->gv, ctx->gmb,   ctx->flags, ctx->wq_ring, ctx->cvo_tape,  ctx->act_tape,
                   ctx->obs_tape,  ctx->dobs_buf, ctx->gcvo,       ctx->gact,       ctx->gmu,        ctx->glam,
                   ctx->obs_cvo,   ctx->obs_out,  ctx->f32_stage,  ctx->dE_dev,     ctx->vmax_hist,  ctx->replay_bad,
                   ctx->vref_all,  ctx->spc_tape, ctx->gspc,       ctx->cut_tape,   ctx->dcloud_buf};
@@ -1352,7 +1396,7 @@ int reset_lattice_impl(DmContext* ctx, const DmLatticeReset* spec, unsigned long
     DM_CUDA(cudaMemcpyAsync(S0.f, cur.f, state_floats(ctx) * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream));
     DM_CUDA(cudaMemcpyAsync(S0.attr, cur.attr, ctx->Ntot * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream));
     if (ctx->law == kFluid) {  // the kept envs' F becomes a general initial state
-      k_fiso_expand<<<ctx->grid_tiles, 256, 0, ctx->stream>>>(ctx->Ntot, S0);
+      dm_launch(ctx->grid_tiles, 256, 0, ctx->stream, ctx->pdl, k_fiso_expand, ctx->Ntot, S0);
       ++ctx->launches;
     }
   }
@@ -1372,8 +1416,8 @@ int reset_lattice_impl(DmContext* ctx, const DmLatticeReset* spec, unsigned long
   R.material = spec->material;
   R.group = spec->group;
   double* od = odelta ? (dev ? odelta : d_delta) : nullptr;
-  k_reset_lattice<<<ctx->grid_tiles, 256, 0, ctx->stream>>>(R, E, N, seed, env_offset, m, g, od, d_flag, S0);
-  k_reset_normals_seq<<<(E + 127) / 128, 128, 0, ctx->stream>>>(R, E, N, seed, env_offset, d_flag, S0);
+  dm_launch(ctx->grid_tiles, 256, 0, ctx->stream, ctx->pdl, k_reset_lattice, R, E, N, seed, env_offset, m, g, od, d_flag, S0);
+  dm_launch((E + 127) / 128, 128, 0, ctx->stream, ctx->pdl, k_reset_normals_seq, R, E, N, seed, env_offset, d_flag, S0);
   ctx->launches += 2;
   if (odelta && !dev)
     DM_CUDA(cudaMemcpyAsync(odelta, d_delta, (size_t)E * 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1498,9 +1542,9 @@ static int observe_impl(DmContext* ctx, const float* cvo, float* obs, cudaMemcpy
   else
     P.K = 0;  // no pose: no spill statistic
   float* o = ctx->obs_out;
-  k_obs<<<E, 256, 0, ctx->stream>>>(P, fwd_state(ctx, ctx->steps * ctx->cfg.substeps), ctx->obs_cvo,
+  dm_launch(E, 256, 0, ctx->stream, ctx->pdl, k_obs, P, fwd_state(ctx, ctx->steps * ctx->cfg.substeps), ctx->obs_cvo,
                                     (float)ctx->cfg.spill_half, (float)ctx->cfg.spill_temp, ctx->cfg.obs_groups, o,
-                                    ctx->od);
+                                    ctx->od, (const float*)nullptr);
   ++ctx->launches;
   DM_CUDA(cudaMemcpyAsync(obs, o, (size_t)E * ctx->od * sizeof(float), kout, ctx->stream));
   if (kout != cudaMemcpyDeviceToDevice) DM_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -168,12 +168,35 @@ __device__ __forceinline__ void report(DevFlags* fl, int env, int sub, int stage
 }
 
 // Dynamic tile scheduling: warps take active-tile indices from a per-launch
-// counter (zeroed before the launch), so the load balances to within one
+// counter (a wq ring slot zeroed by the previous tile kernel), so the load balances to within one
 // tile; lane 0 grabs and broadcasts.
 __device__ __forceinline__ int grab_tile(int* ctr, int lane, int n = 1) {
   int a = 0;
   if (lane == 0) a = atomicAdd(ctr, n);
   return __shfl_sync(0xffffffffu, a, 0);
+}
+
+// ---- launch chaining (programmatic dependent launch) ----
+// Every kernel opens with dm_pdl(): it waits until the previous grid in the
+// stream has completed and its writes are visible, then lets the next kernel
+// be scheduled, so the next launch's setup and CTA rasterisation overlap this
+// grid's tail instead of following it (small batches: ~2 us per boundary).
+// Launched without the PDL attribute (DIFFMPM_NO_PDL=1) both are no-ops.
+__device__ __forceinline__ void dm_pdl() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+// Tile-scheduling counters: a ring of kWqRing ints (one per tile-kernel
+// launch, the ring aligned to its size).  Each tile kernel zeroes the next
+// slot for the next tile kernel, so no memset node sits between launches
+// (which would also break the PDL chain).
+constexpr int kWqRing = 32;
+constexpr int kOrdBuckets = 16;  // k_order_hist / k_order_scatter buckets
+__device__ __forceinline__ void wq_clear_next(int* wq) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const uintptr_t m = kWqRing * sizeof(int) - 1, u = reinterpret_cast<uintptr_t>(wq);
+    *reinterpret_cast<int*>((u & ~m) | ((u + sizeof(int)) & m)) = 0;
+  }
 }
 
 // Local base inside the tile, in [0, 4).  Always in range for valid particles
@@ -319,7 +342,11 @@ template <class CT>
 __global__ void __launch_bounds__(1024, 2) k_bin(DevParams P, StateView S, int* keys, int* perm, int* tile_start,
                                              int* tile_count, int4* active, int* env_abase, int* env_acount,
                                              DevFlags* flags, int* nact, int substep, int check_vmax,
-                                             float4* __restrict__ vref) {
+                                             float4* __restrict__ vref, int* __restrict__ ord) {
+  dm_pdl();
+  wq_clear_next(nact);  // nact: a zeroed ring slot here (k_order_hist stores the total in the slot's nact)
+  // the bucket counters of k_order_hist / k_order_scatter (no memset node)
+  if (blockIdx.x == 0 && threadIdx.x < 2 * kOrdBuckets) ord[threadIdx.x] = 0;
   extern __shared__ __align__(16) unsigned char bin_smem[];
   CT* cnt = reinterpret_cast<CT*>(bin_smem);  // [nw][Tn]
   __shared__ int s_part[1024 / 32 + 1][2];
@@ -483,18 +510,20 @@ __global__ void __launch_bounds__(1024, 2) k_bin(DevParams P, StateView S, int* 
 // every tile's result is order-independent, and the replay and the adjoint of
 // a substep share their slot's list, so the work index also names the tile's
 // stored grid blocks consistently.  ord[0..15]: bucket counts, ord[16..31]:
-// bucket cursors (zeroed before k_order_hist).
-constexpr int kOrdBuckets = 16;
+// bucket cursors (zeroed by k_bin).
 __device__ __forceinline__ int ord_bucket(int count) {
   const int b = count >> 6;
   return kOrdBuckets - 1 - (b < kOrdBuckets - 1 ? b : kOrdBuckets - 1);  // 0 = largest
 }
 
-__global__ void __launch_bounds__(256) k_order_hist(const int4* __restrict__ active, const int* nact, int* ord) {
+__global__ void __launch_bounds__(256) k_order_hist(const int4* __restrict__ active, const int* acc, int* ord,
+                                                    int* __restrict__ nact) {
+  dm_pdl();
   __shared__ int h[kOrdBuckets];
   if (threadIdx.x < kOrdBuckets) h[threadIdx.x] = 0;
   __syncthreads();
-  const int n = *(const volatile int*)nact;
+  const int n = *(const volatile int*)acc;  // k_bin's ring-slot total -> the slot's nact
+  if (blockIdx.x == 0 && threadIdx.x == 0) *nact = n;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     atomicAdd(&h[ord_bucket(active[i].w)], 1);
   __syncthreads();
@@ -503,6 +532,7 @@ __global__ void __launch_bounds__(256) k_order_hist(const int4* __restrict__ act
 
 __global__ void __launch_bounds__(256) k_order_scatter(const int4* __restrict__ active, const int* nact,
                                                        int* ord, int4* __restrict__ work) {
+  dm_pdl();
   __shared__ int h[kOrdBuckets], base[kOrdBuckets];
   if (threadIdx.x < kOrdBuckets) h[threadIdx.x] = 0;
   __syncthreads();
@@ -532,6 +562,105 @@ __global__ void __launch_bounds__(256) k_order_scatter(const int4* __restrict__ 
     if (b[k] >= 0) work[base[b[k]] + r[k]] = d[k];
 }
 
+// ============================ sort records ============================
+// The forward's binning of substep s (perm, dense tile counts, the active
+// and work lists, per-env ranges, vref) copied into the rollout's record s,
+// so the backward's segment replay reuses it instead of binning again (the
+// replay's state is bit-identical, so is its sort).  Lists longer than the
+// record's capacity set ovf (that substep is re-binned in the replay).
+struct SortRec {
+  int* perm;
+  int* tile_count;
+  int4* active;
+  int4* work;
+  int* abase;
+  int* acount;
+  int* nact;
+  float4* vref;
+  int* ovf;
+};
+// The sort record's copy of the capacity-limited binning tables, done by
+// the cell-sort kernel's threads (grid-stride) instead of a k_rec_save
+// launch; rec.nact == nullptr: no record for this substep.
+struct RecSrc {
+  const int4* active;
+  const int4* work;
+  const int* abase;
+  const int* acount;
+  const int* nact;
+  const float4* vref;
+  int cap, E;
+};
+__device__ __forceinline__ void rec_copy(const SortRec& r, const RecSrc& q) {
+  if (!r.nact) return;
+  const int n = *(const volatile int*)q.nact;
+  const bool fits = n <= q.cap;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t i0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i0 == 0) {
+    *r.nact = n;
+    *r.ovf = fits ? 0 : 1;
+  }
+  if (fits)
+    for (size_t i = i0; i < (size_t)n; i += stride) {
+      r.active[i] = q.active[i];
+      r.work[i] = q.work[i];
+    }
+  for (size_t i = i0; i < (size_t)q.E; i += stride) {
+    r.abase[i] = q.abase[i];
+    r.acount[i] = q.acount[i];
+    r.vref[i] = q.vref[i];
+  }
+}
+
+// Small batches (a few thousand active tiles at most): both passes in one
+// CTA -- bucket counts, scan, scatter -- one launch instead of two.  Same
+// bucket order as k_order_hist + k_order_scatter (the order inside a bucket
+// is not fixed by either; every tile's result is independent of it).
+// With a sort record (rec.nact != nullptr) it also writes the record's
+// copies of the lists and per-env tables (off the cell sort's critical path).
+__global__ void __launch_bounds__(1024) k_order_small(const int4* __restrict__ active, const int* acc,
+                                                      int* __restrict__ nact, int4* __restrict__ work, SortRec rec,
+                                                      RecSrc rs) {
+  dm_pdl();
+  __shared__ int h[kOrdBuckets], cur[kOrdBuckets];
+  if (threadIdx.x < kOrdBuckets) h[threadIdx.x] = 0;
+  __syncthreads();
+  const int n = *(const volatile int*)acc;  // k_bin's ring-slot total -> the slot's nact
+  const bool keep = rec.nact && n <= rs.cap;
+  if (threadIdx.x == 0) {
+    *nact = n;
+    if (rec.nact) {
+      *rec.nact = n;
+      *rec.ovf = keep ? 0 : 1;
+    }
+  }
+  if (rec.nact)
+    for (int i = threadIdx.x; i < rs.E; i += blockDim.x) {
+      rec.abase[i] = rs.abase[i];
+      rec.acount[i] = rs.acount[i];
+      rec.vref[i] = rs.vref[i];
+    }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int4 d = active[i];
+    atomicAdd(&h[ord_bucket(d.w)], 1);
+    if (keep) rec.active[i] = d;
+  }
+  __syncthreads();
+  if (threadIdx.x < kOrdBuckets) {
+    int start = 0;
+    for (int q = 0; q < (int)threadIdx.x; ++q) start += h[q];
+    cur[threadIdx.x] = start;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int4 d = active[i];
+    const int pos = atomicAdd(&cur[ord_bucket(d.w)], 1);
+    work[pos] = d;
+    if (keep) rec.work[pos] = d;
+  }
+}
+
 // Second sort level: within every active tile, a stable counting sort by the
 // cell inside the tile (64 buckets).  Final key = tile * 64 + cell; particles
 // of one cell become contiguous so the stencil scatters can accumulate runs in
@@ -541,7 +670,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_cellsort(DevParams P, StateView
                                                           const int* __restrict__ tile_start,
                                                           const int* __restrict__ tile_count,
                                                           const int4* __restrict__ active, const int* nact,
-                                                          DevFlags* flags, int* __restrict__ wq) {
+                                                          DevFlags* flags, int* __restrict__ wq, SortRec rec, RecSrc rsrc) {
+  dm_pdl();
+  wq_clear_next(wq);
+  rec_copy(rec, rsrc);
   __shared__ int c64[kWarps][64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int* cnt = c64[warp];
@@ -1039,7 +1171,10 @@ __device__ __forceinline__ V coop_sum(V v) {
 __global__ void __launch_bounds__(kWarps * 32) k_cellsort_coop(DevParams P, const int* __restrict__ ptile,
                                                                int* __restrict__ perm, const int* __restrict__ keys,
                                                                const int4* __restrict__ active, const int* nact,
-                                                               DevFlags* flags, int* __restrict__ wq) {
+                                                               DevFlags* flags, int* __restrict__ wq, SortRec rec, RecSrc rsrc) {
+  dm_pdl();
+  wq_clear_next(wq);
+  rec_copy(rec, rsrc);
   __shared__ int c64[kWarps][64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_active = *(const volatile int*)nact;
@@ -1158,6 +1293,8 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2G_MINB) k_p2g(DevParams P, S
                                                      const float* __restrict__ act, float4* __restrict__ blocks,
                                                      DevFlags* flags, const int* nact, int substep, int* __restrict__ wq,
                                                      const float4* __restrict__ vref) {
+  dm_pdl();
+  wq_clear_next(wq);
   extern __shared__ float4 dsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_active = *(const volatile int*)nact;
@@ -1375,6 +1512,8 @@ __global__ void __launch_bounds__(kWarps * 32, DM_GRID_MINB) k_grid(DevParams P,
                                                       const float4* __restrict__ blocks, float4* __restrict__ gmp,
                                                       float4* __restrict__ gv, const int* nact, int* __restrict__ wq,
                                                       const float4* __restrict__ vref) {
+  dm_pdl();
+  wq_clear_next(wq);
   __shared__ short own[kWarps][kExt3];
   __shared__ NodeMasks nm;
   __shared__ int nbt[kWarps][27];  // the tile's neighbour block indices (neighbour_mask)
@@ -1443,6 +1582,8 @@ __global__ void __launch_bounds__(kWarps * 32, kG2pBlocks(LAW)) k_g2p(DevParams 
                                                      int substep, const float4* __restrict__ gmp,
                                                      float4* __restrict__ out_gv, float4* __restrict__ out_gmp, int* __restrict__ wq,
                                                      int dump_cap, const float4* __restrict__ vref) {
+  dm_pdl();
+  wq_clear_next(wq);
   __shared__ __align__(128) float4 vg[kWarps][2][kExt3];
   __shared__ uint64_t vbar[kWarps][2];  // TMA completion of vg[w][b]
   // fluid, isotropic F: a ring of kG2pRing chunk slots per warp (x, F word,
@@ -1625,6 +1766,8 @@ __global__ void __launch_bounds__(kWarps * 32, DM_G2PADJ_MINB) k_g2p_adj(DevPara
                                                          float4* __restrict__ ablocks, float* __restrict__ part,
                                                          float* __restrict__ tile_acc, const int* nact, int* __restrict__ wq,
                                                          const float4* __restrict__ vref) {
+  dm_pdl();
+  wq_clear_next(wq);
   extern __shared__ __align__(128) float4 dsm[];
   __shared__ uint64_t vbar[kWarps];  // COOP: bulk-copy completion of the warp's vw
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1794,6 +1937,8 @@ __global__ void __launch_bounds__(kWarps * 32, DM_GRIDADJ_MINB) k_grid_adj(DevPa
                                                           const float4* __restrict__ gmpb, float4* __restrict__ gmb,
                                                           float* __restrict__ tile_acc, const int* nact, int* __restrict__ wq,
                                                           const float4* __restrict__ vref) {
+  dm_pdl();
+  wq_clear_next(wq);
   __shared__ short own[kWarps][kExt3];
   __shared__ NodeMasks nm;
   __shared__ int nbt[kWarps][27];  // the tile's neighbour block indices (neighbour_mask)
@@ -1883,6 +2028,8 @@ __global__ void __launch_bounds__(kWarps * 32, DM_P2GADJ_MINB) k_p2g_adj(DevPara
                                                          const float* __restrict__ part,
                                                          float* __restrict__ adj_out, size_t astride,
                                                          float* __restrict__ tile_acc, const int* nact, int* __restrict__ wq) {
+  dm_pdl();
+  wq_clear_next(wq);
   __shared__ __align__(128) float4 mb[kWarps][kExt3];
   __shared__ uint64_t mbar[kWarps];  // COOP: TMA completion of mb[w]
   __shared__ float stg[kWarps][kP2gAdjStage * 32];  // next chunk: [field][lane]
@@ -2078,6 +2225,7 @@ __global__ void __launch_bounds__(kNacc * kRedSlices) k_env_reduce(DevParams P, 
                              const int* __restrict__ env_acount, const float* __restrict__ tile_acc,
                              double* __restrict__ gcvo_t, double* __restrict__ gact_t, double* __restrict__ gmu,
                              double* __restrict__ glam) {
+  dm_pdl();
   __shared__ double part[kRedSlices][kNacc];
   __shared__ double sacc[kNacc];
   const int e = blockIdx.x, f = threadIdx.x % kNacc, g = threadIdx.x / kNacc;
@@ -2144,6 +2292,7 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 __global__ void __launch_bounds__(256) k_obs(DevParams P, StateView S, const float* __restrict__ cvo, float spill_half,
                                              float spill_temp, int ngr, float* __restrict__ obs, int od,
                                              const float* __restrict__ spc = nullptr) {
+  dm_pdl();
   __shared__ double sh[8];
   const int e = blockIdx.x;
   const size_t base = (size_t)e * P.N;
@@ -2236,6 +2385,7 @@ __global__ void __launch_bounds__(256) k_obs_adj(DevParams P, StateView S, const
                                                  const float* __restrict__ dobs, int od, float* __restrict__ adj,
                                                  size_t astride, double* __restrict__ gcvo_t,
                                                  const float* __restrict__ spc = nullptr, double* __restrict__ gspc_t = nullptr) {
+  dm_pdl();
   __shared__ double sh[8];
   const int e = blockIdx.x;
   const size_t base = (size_t)e * P.N;
@@ -2326,6 +2476,7 @@ __global__ void __launch_bounds__(256) k_obs_adj(DevParams P, StateView S, const
 // Fills D = D(0,0) I for every particle of a fluid G2P-produced state (makes
 // it a general state again: used when it becomes a new initial state).
 __global__ void k_fiso_expand(size_t Ntot, StateView S) {
+  dm_pdl();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < Ntot; i += (size_t)gridDim.x * blockDim.x) {
     const float sF = S.c(6, i);
 #pragma unroll
@@ -2365,6 +2516,7 @@ struct ResetSpec {
 __global__ void k_reset_lattice(ResetSpec R, int E, int N, unsigned long long seed, int env_offset,
                                 const unsigned char* __restrict__ mask, const int* __restrict__ pgroup,
                                 double* __restrict__ odelta, int* __restrict__ seq_flag, StateView S) {
+  dm_pdl();
   const size_t tot = (size_t)E * N;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
     const int e = (int)(i / N), p = (int)(i % N);
@@ -2421,6 +2573,7 @@ __global__ void k_reset_lattice(ResetSpec R, int E, int N, unsigned long long se
 // u1 <= 0, shifting the stream) for the flagged envs; one thread per env.
 __global__ void k_reset_normals_seq(ResetSpec R, int E, int N, unsigned long long seed, int env_offset,
                                     const int* __restrict__ seq_flag, StateView S) {
+  dm_pdl();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E || !seq_flag[e]) return;
   const unsigned long long key =
@@ -2439,6 +2592,7 @@ __global__ void k_reset_normals_seq(ResetSpec R, int E, int N, unsigned long lon
 __global__ void k_aos_to_soa(int Ntot, const float* __restrict__ x, const float* __restrict__ v,
                              const float* __restrict__ F, const float* __restrict__ C, const int* __restrict__ mat,
                              const int* __restrict__ grp, int N, StateView S) {
+  dm_pdl();
   const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (i >= (size_t)Ntot) return;
 #pragma unroll
@@ -2462,6 +2616,7 @@ __global__ void k_aos_to_soa(int Ntot, const float* __restrict__ x, const float*
 __global__ void k_soa_to_aos(int Ntot, int N, const float* __restrict__ f, const uint32_t* __restrict__ attr,
                              size_t stride, int state_layout, int fiso, float* __restrict__ x, float* __restrict__ v, float* __restrict__ F,
                              float* __restrict__ C, int eye = 0) {
+  dm_pdl();
   const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (i >= (size_t)Ntot) return;
   const size_t e = i / N;
@@ -2487,6 +2642,7 @@ __global__ void k_aos_to_soa_perm(int Ntot, int N, const float* __restrict__ x, 
                                   const float* __restrict__ F, const float* __restrict__ C,
                                   const uint32_t* __restrict__ attr, float* __restrict__ f, size_t stride,
                                   int ftrace = 0) {
+  dm_pdl();
   const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (i >= (size_t)Ntot) return;
   const size_t e = i / N;
@@ -2508,6 +2664,7 @@ __global__ void k_aos_to_soa_perm(int Ntot, int N, const float* __restrict__ x, 
 // fp64 -> fp32 cotangent conversion (stays on the device; the host entry
 // points copy the fp32 result out asynchronously).
 __global__ void k_f64_to_f32(size_t n, const double* __restrict__ src, float* __restrict__ dst) {
+  dm_pdl();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     dst[i] = (float)src[i];
 }
@@ -2516,6 +2673,7 @@ __global__ void k_f64_to_f32(size_t n, const double* __restrict__ src, float* __
 // map, mpm.hpp:33-35; the reference tape cannot produce it).
 __global__ void k_dE(int E, int nmat, const double* __restrict__ gmu, const double* __restrict__ glam, DevParams P,
                      double* __restrict__ out) {
+  dm_pdl();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= E * nmat) return;
   const int e = i / nmat, m = i % nmat;
@@ -2531,6 +2689,7 @@ __global__ void k_dE(int E, int nmat, const double* __restrict__ gmu, const doub
 // whose state was replaced by an in-tape reset (cut != 0) are skipped.
 __global__ void k_replay_check(DevParams P, StateView R, StateView St, int fluid_iso,
                                const unsigned char* __restrict__ cut, unsigned long long* __restrict__ bad) {
+  dm_pdl();
   const size_t tot = (size_t)P.E * P.N;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
     const int e = (int)(i / P.N);
@@ -2556,6 +2715,7 @@ __global__ void k_replay_check(DevParams P, StateView R, StateView St, int fluid
 // Test hook (dm_debug_inject): flips the lowest mantissa bit of x of the
 // particle with original index p in env e of state S.
 __global__ void k_debug_flip(DevParams P, StateView S, int e, int p) {
+  dm_pdl();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.N; i += gridDim.x * blockDim.x) {
     const size_t j = (size_t)e * P.N + i;
     if ((int)attr_index(S.attr[j]) == p) S.c(0, j) = __uint_as_float(__float_as_uint(S.c(0, j)) ^ 1u);
@@ -2568,6 +2728,7 @@ __global__ void k_debug_flip(DevParams P, StateView S, int e, int p) {
 // written to out[e * ostride + ooff + 3 (p / stride) + a].
 __global__ void k_cloud(DevParams P, StateView S, int stride, int ncloud, float* __restrict__ out, int ostride,
                         int ooff) {
+  dm_pdl();
   const size_t tot = (size_t)P.E * P.N;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
     const int p = (int)attr_index(S.attr[i]);
@@ -2584,6 +2745,7 @@ __global__ void k_cloud(DevParams P, StateView S, int stride, int ncloud, float*
 __global__ void k_cloud_adj(DevParams P, const uint32_t* __restrict__ attr, int stride, int ncloud,
                             const float* __restrict__ dcloud, const unsigned char* __restrict__ cut,
                             float* __restrict__ adj, size_t astride) {
+  dm_pdl();
   const size_t tot = (size_t)P.E * P.N;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
     const int e = (int)(i / P.N);
@@ -2601,6 +2763,7 @@ __global__ void k_cloud_adj(DevParams P, const uint32_t* __restrict__ attr, int 
 // F = I, C = 0 -- Task::reset copies the sample_box template).
 __global__ void k_task_reset(DevParams P, StateView S, const float* __restrict__ tmpl_x,
                              const unsigned char* __restrict__ mask, int material) {
+  dm_pdl();
   const size_t tot = (size_t)P.E * P.N;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
     const int e = (int)(i / P.N), p = (int)(i % P.N);
@@ -2622,6 +2785,7 @@ __global__ void k_task_reset(DevParams P, StateView S, const float* __restrict__
 // Zeroes the state cotangent of envs whose state was replaced by a reset
 // (the gradient does not flow across it, algo.hpp:171-178).
 __global__ void k_cut_adj(DevParams P, const unsigned char* __restrict__ cut, float* __restrict__ adj, size_t astride) {
+  dm_pdl();
   const size_t tot = (size_t)P.E * P.N;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
     if (!cut[i / P.N]) continue;
@@ -2630,27 +2794,11 @@ __global__ void k_cut_adj(DevParams P, const unsigned char* __restrict__ cut, fl
   }
 }
 
-// ============================ sort records ============================
-// The forward's binning of substep s (perm, dense tile counts, the active
-// and work lists, per-env ranges, vref) copied into the rollout's record s,
-// so the backward's segment replay reuses it instead of binning again (the
-// replay's state is bit-identical, so is its sort).  Lists longer than the
-// record's capacity set ovf (that substep is re-binned in the replay).
-struct SortRec {
-  int* perm;
-  int* tile_count;
-  int4* active;
-  int4* work;
-  int* abase;
-  int* acount;
-  int* nact;
-  float4* vref;
-  int* ovf;
-};
 __global__ void k_rec_save(size_t Ntot, size_t TT, int E, int cap, const int* __restrict__ perm,
                            const int* __restrict__ tile_count, const int4* __restrict__ active,
                            const int4* __restrict__ work, const int* __restrict__ abase, const int* __restrict__ acount,
                            const int* __restrict__ nact, const float4* __restrict__ vref, SortRec r) {
+  dm_pdl();
   const int n = *nact;
   const bool fits = n <= cap;
   const size_t stride = (size_t)gridDim.x * blockDim.x;

@@ -47,7 +47,7 @@ int restart_tape(DmContext* ctx) {
       DM_CUDA(cudaMemcpyAsync(S0.attr, cur.attr, ctx->Ntot * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream));
     }
     if (ctx->law == kFluid) {  // a G2P output stores D(0,0) only; the initial state is general
-      k_fiso_expand<<<ctx->grid_tiles, 256, 0, ctx->stream>>>(ctx->Ntot, S0);
+      dm_launch(ctx->grid_tiles, 256, 0, ctx->stream, ctx->pdl, k_fiso_expand, ctx->Ntot, S0);
       ++ctx->launches;
     }
   }
@@ -307,7 +307,7 @@ int dm_task_reset(DmTask* t, unsigned long long seed) {
     t->draw_reset(e);
   }
   DM_CUDA(cudaMemsetAsync(t->d_mask, 1, t->E, ctx->stream));
-  k_task_reset<<<ctx->grid_tiles, 256, 0, ctx->stream>>>(ctx->P, store_view(ctx, 0), t->d_tmpl, t->d_mask, 0);
+  dm_launch(ctx->grid_tiles, 256, 0, ctx->stream, ctx->pdl, k_task_reset, ctx->P, store_view(ctx, 0), t->d_tmpl, t->d_mask, 0);
   ++ctx->launches;
   ctx->steps = 0;
   ctx->cfl_checked = 0;
@@ -328,7 +328,7 @@ int dm_task_observe(DmTask* t, double* obs) {
   std::vector<float> o7((size_t)t->E * ctx->od), cl((size_t)t->E * t->ncloud * 3);
   int rc = observe_impl(ctx, nullptr, o7.data(), cudaMemcpyHostToDevice, cudaMemcpyDeviceToHost);
   if (rc != DM_OK) return task_ctx_err(t, rc);
-  k_cloud<<<ctx->grid_tiles, 256, 0, ctx->stream>>>(ctx->P, fwd_state(ctx, ctx->steps * ctx->cfg.substeps), t->stride,
+  dm_launch(ctx->grid_tiles, 256, 0, ctx->stream, ctx->pdl, k_cloud, ctx->P, fwd_state(ctx, ctx->steps * ctx->cfg.substeps), t->stride,
                                                     t->ncloud, t->d_cloud, t->ncloud * 3, 0);
   ++ctx->launches;
   DM_CUDA(cudaMemcpyAsync(cl.data(), t->d_cloud, cl.size() * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
@@ -437,7 +437,7 @@ int dm_task_step(DmTask* t, const double* actions, double* rewards, unsigned cha
   if (any) {  // the done envs' particles take the template (Task::reset); the tape is cut there
     DM_CUDA(cudaMemcpyAsync(t->d_mask, done.data(), E, cudaMemcpyHostToDevice, ctx->stream));
     DM_CUDA(cudaMemcpyAsync(ctx->cut_tape + (size_t)tt * E, done.data(), E, cudaMemcpyHostToDevice, ctx->stream));
-    k_task_reset<<<ctx->grid_tiles, 256, 0, ctx->stream>>>(ctx->P, fwd_state(ctx, ctx->steps * ctx->cfg.substeps),
+    dm_launch(ctx->grid_tiles, 256, 0, ctx->stream, ctx->pdl, k_task_reset, ctx->P, fwd_state(ctx, ctx->steps * ctx->cfg.substeps),
                                                            t->d_tmpl, t->d_mask, 0);
     ++ctx->launches;
     ctx->cut_any[tt] = 1;
