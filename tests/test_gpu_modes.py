@@ -101,3 +101,33 @@ def test_stress_cache_on_off_consistent():
     full = lambda r: np.concatenate([np.asarray(r[k], np.float64).ravel() for k in ("x", "v", "F", "C")])
     assert _rel(full(ra), full(rb)) <= 1e-4, _rel(full(ra), full(rb))
     assert _rel(ra["cvo"], rb["cvo"]) <= 1e-4
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_launch_chaining_bitwise(cfg):
+    """Programmatic dependent launch (DIFFMPM_PDL) and the one-CTA work-list
+    ordering change only when kernels start, never what they compute: a
+    rollout (forward, replay, adjoint) with launch chaining on equals the one
+    with it off bit for bit (cfg2: from the second control step on, the
+    work list is ordered by k_order_small -- the active-tile count is known
+    after the first)."""
+    sc = scenes.CONFIGS[2](seed=5, n_envs=2, n_ctrl=2) if cfg == 2 else scenes.CONFIGS[1](seed=5, n_sub=12)
+
+    def run(pdl):
+        old = os.environ.get("DIFFMPM_PDL")
+        os.environ["DIFFMPM_PDL"] = pdl
+        try:
+            b = api.from_scene(sc)
+            r = api.run_scene(b, sc)
+            b.close()
+        finally:
+            if old is None:
+                os.environ.pop("DIFFMPM_PDL", None)
+            else:
+                os.environ["DIFFMPM_PDL"] = old
+        return r
+
+    on, off = run("1"), run("0")
+    for k in off:
+        if isinstance(off[k], np.ndarray):
+            assert np.array_equal(on[k], off[k]), k
