@@ -183,8 +183,13 @@ __device__ __forceinline__ int grab_tile(int* ctr, int lane, int n = 1) {
 // grid's tail instead of following it (small batches: ~2 us per boundary).
 // Launched without the PDL attribute (DIFFMPM_NO_PDL=1) both are no-ops.
 __device__ __forceinline__ void dm_pdl() {
+#if DM_PDL_EARLY  // A/B: trigger first (the next-but-one kernel may then be scheduled too)
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#else
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#endif
 }
 // Tile-scheduling counters: a ring of kWqRing ints (one per tile-kernel
 // launch, the ring aligned to its size).  Each tile kernel zeroes the next
